@@ -1,0 +1,67 @@
+"""The five BASELINE.json workloads as data."""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+
+from .meshes import icosphere, graded_spheroid
+from .vectors import plane_wave_direction
+
+
+@dataclass(frozen=True)
+class WorkloadConfig:
+    cfg: int
+    name: str
+    mesh: str          # "icosphere:s" or "spheroid"
+    k: float
+    eps: float = 1e-4
+    max_leaf: int = 64
+    gmres_tol: float = 1e-4
+
+    @property
+    def alpha(self) -> complex:
+        """Burton-Miller coupling α = i/k."""
+        return 1j / self.k
+
+    @property
+    def direction(self) -> np.ndarray:
+        if self.cfg == 3:
+            return plane_wave_direction(3003)
+        if self.cfg == 4:
+            c = np.sqrt(0.5)
+            return np.array([c, c, 0.0])
+        return np.array([0.0, 0.0, 1.0])
+
+    @property
+    def x_seed(self) -> int:
+        return 1000 + self.cfg
+
+    @property
+    def rows_seed(self) -> int:
+        return 2000 + self.cfg
+
+
+CONFIGS = {
+    1: WorkloadConfig(1, "icosphere s=4, N=5120, kD=10", "icosphere:4", 10.0),
+    2: WorkloadConfig(2, "icosphere s=6, N=81920, kD=50", "icosphere:6", 50.0),
+    3: WorkloadConfig(3, "icosphere s=7, N=327680, kD=100", "icosphere:7", 100.0),
+    4: WorkloadConfig(4, "graded prolate spheroid, N~1.3M, kD=300", "spheroid", 300.0),
+    5: WorkloadConfig(5, "icosphere s=9, N=5242880, kD=1000", "icosphere:9", 1000.0),
+}
+
+
+@lru_cache(maxsize=4)
+def _mesh(spec: str):
+    if spec.startswith("icosphere:"):
+        return icosphere(int(spec.split(":")[1]), 0.5)
+    if spec == "spheroid":
+        return graded_spheroid()
+    raise ValueError(spec)
+
+
+def config_mesh(cfg: int):
+    """(vertices float64 (nv,3), triangles int32 (nt,3)) for a config."""
+    V, F = _mesh(CONFIGS[cfg].mesh)
+    return V.copy(), F.copy()
