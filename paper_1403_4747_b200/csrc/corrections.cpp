@@ -1,0 +1,81 @@
+// Near-field correction table C (host, fp64 → complex64 CSR in tree order).
+//
+// The device applies the 3-point rule Q3 to every element pair, either on the
+// fly (direct leaf pairs, near kernel) or folded into S2M (far pairs).  The
+// operator of Eq. (5) with the tier rule of reading C6 differs
+// from that only for pairs with ρ_ij = |x_i - c_j|/h_j < tier2_rho, so
+//   C_ij = A^tier_ij - A^Q3_ij   (ρ_ij < 3, including i = j)
+// where A^tier_ii = ½ + α H_ii (closed-form self term, reading C5) and the
+// Q3 value of the self pair is the (regular) 3-point sum on Δ_i.  The pair
+// search is a tree-independent radius search (uniform hash grid).
+#include <algorithm>
+#include <cmath>
+#include <unordered_map>
+
+#include "fda_internal.h"
+
+namespace fda {
+
+void build_corrections(const Geometry& g, const Params& p, Plan& plan) {
+  const int64_t n = g.n;
+  const double t1 = p.opt.tier1_rho, t2 = p.opt.tier2_rho;
+  double hmax = 0;
+  for (int64_t i = 0; i < n; ++i) hmax = std::max(hmax, g.hmax[i]);
+  const double cell = t2 * hmax;
+  Vec3 lo(1e300, 1e300, 1e300);
+  for (int64_t i = 0; i < n; ++i)
+    lo = {std::min(lo.x, g.centroid[i].x), std::min(lo.y, g.centroid[i].y), std::min(lo.z, g.centroid[i].z)};
+  auto cidx = [&](const Vec3& c, int64_t& a, int64_t& b, int64_t& d) {
+    a = (int64_t)std::floor((c.x - lo.x) / cell);
+    b = (int64_t)std::floor((c.y - lo.y) / cell);
+    d = (int64_t)std::floor((c.z - lo.z) / cell);
+  };
+  auto hkey = [](int64_t a, int64_t b, int64_t d) {
+    return (uint64_t)((a & 0x1fffff) | ((b & 0x1fffff) << 21) | ((d & 0x1fffff) << 42));
+  };
+  std::unordered_map<uint64_t, std::vector<int64_t>> grid;
+  for (int64_t j = 0; j < n; ++j) {
+    int64_t a, b, d;
+    cidx(g.centroid[j], a, b, d);
+    grid[hkey(a, b, d)].push_back(j);
+  }
+  std::vector<std::vector<std::pair<int64_t, cf>>> rows(n);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t i = 0; i < n; ++i) {
+    const Vec3& x = g.centroid[i];
+    int64_t a, b, d;
+    cidx(x, a, b, d);
+    auto& row = rows[i];
+    for (int64_t da = -1; da <= 1; ++da)
+      for (int64_t db = -1; db <= 1; ++db)
+        for (int64_t dd = -1; dd <= 1; ++dd) {
+          auto it = grid.find(hkey(a + da, b + db, d + dd));
+          if (it == grid.end()) continue;
+          for (int64_t j : it->second) {
+            double rho = (x - g.centroid[j]).norm() / g.hmax[j];
+            if (!(rho < t2)) continue;
+            cd q3 = entry_rule(3, x, g.normal[i], g.v0[j], g.v1[j], g.v2[j], g.normal[j], g.area[j], p.k, p.alpha);
+            cd exact;
+            if (j == i) exact = self_lhs(g.v0[i], g.v1[i], g.v2[i], p.k, p.alpha);
+            else exact = entry_rule(rho < t1 ? 1 : 2, x, g.normal[i], g.v0[j], g.v1[j], g.v2[j], g.normal[j],
+                                    g.area[j], p.k, p.alpha);
+            cd c = exact - q3;
+            row.push_back({j, cf((float)c.real(), (float)c.imag())});
+          }
+        }
+    std::sort(row.begin(), row.end(), [](const auto& u, const auto& v) { return u.first < v.first; });
+  }
+  plan.corr_ptr.assign(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) plan.corr_ptr[i + 1] = plan.corr_ptr[i] + (int64_t)rows[i].size();
+  plan.corr_col.resize(plan.corr_ptr[n]);
+  plan.corr_val.resize(plan.corr_ptr[n]);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t o = plan.corr_ptr[i];
+    for (size_t e = 0; e < rows[i].size(); ++e) {
+      plan.corr_col[o + e] = rows[i][e].first;
+      plan.corr_val[o + e] = rows[i][e].second;
+    }
+  }
+}
+
+}  // namespace fda

@@ -1,0 +1,572 @@
+// Device engine: uploads the build tables to HBM and runs the FDA matvec
+// (PAPER.md Algorithm Steps 2-4) and the GMRES solve (§5,
+// P:907-910) on one B200.
+//
+// Per matvec:
+//   main stream : gather → [memset states] → S2M → M2M (leaf level … top)
+//                 → M2L (every level) → L2L (top … leaf level) → L2T ─┐
+//   near stream :          near field (Q3 direct pairs + corrections) ─┴→ scatter
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "fda_internal.h"
+#include "kernels.cuh"
+
+namespace fda {
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      ctx->err = std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call; \
+      return FDA_E_CUDA;                                                           \
+    }                                                                              \
+  } while (0)
+
+struct XStage {
+  XTask* tasks = nullptr;
+  int64_t* src = nullptr;
+  int64_t* dst = nullptr;
+  int ntask = 0;
+  int max_rows = 0;
+};
+
+struct Dev {
+  int device = 0;
+  int n = 0, nleaf = 0;
+  cudaStream_t s_near = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev[8] = {};
+  cudaEvent_t ev_n0 = nullptr, ev_n1 = nullptr;
+  int32_t* perm = nullptr;
+  float4 *tgt_pos = nullptr, *tgt_nrm = nullptr;
+  SrcElem* src = nullptr;
+  float* src_w = nullptr;
+  int32_t *leaf_begin = nullptr, *leaf_end = nullptr, *near_ptr = nullptr, *near_idx = nullptr;
+  float4* near_off = nullptr;
+  int32_t *corr_ptr = nullptr, *corr_col = nullptr;
+  float2* corr_val = nullptr;
+  float2* pool = nullptr;
+  float2 *outb = nullptr, *inb = nullptr;
+  int64_t out_size = 0, in_size = 0;
+  LeafTask *s2m = nullptr, *l2t = nullptr;
+  int n_s2m = 0, n_l2t = 0, max_T = 0;
+  std::vector<XStage> m2m, m2l, l2l;
+  float2 *x_tree = nullptr, *y_near = nullptr, *y_far = nullptr;
+  double2 *xh = nullptr, *yh = nullptr;
+  double *cen = nullptr, *nrm = nullptr;
+  KernelParams kp{};
+  bool timed = false;
+  std::vector<void*> allocs;
+};
+
+template <class T>
+static fda_status upload(Context* ctx, Dev* d, T** dst, const T* src, size_t count) {
+  *dst = nullptr;
+  if (count == 0) count = 1;  // keep valid pointers for empty tables
+  CK(cudaMalloc((void**)dst, count * sizeof(T)));
+  d->allocs.push_back(*dst);
+  if (src) CK(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+  return FDA_OK;
+}
+template <class T>
+static fda_status alloc(Context* ctx, Dev* d, T** dst, size_t count) {
+  return upload<T>(ctx, d, dst, nullptr, count);
+}
+
+#define UP(...)                                 \
+  do {                                          \
+    fda_status s_ = upload(ctx, d, __VA_ARGS__); \
+    if (s_ != FDA_OK) return s_;                \
+  } while (0)
+#define AL(...)                                \
+  do {                                         \
+    fda_status s_ = alloc(ctx, d, __VA_ARGS__); \
+    if (s_ != FDA_OK) return s_;               \
+  } while (0)
+
+static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<Op>& ops, const std::vector<int64_t>& src_off,
+                               const std::vector<int64_t>& dst_off, XStage& st) {
+  const Plan& p = ctx->plan;
+  if (ops.empty()) return FDA_OK;
+  std::vector<size_t> ord(ops.size());
+  for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ops[a].mat < ops[b].mat; });
+  std::vector<int64_t> so, dof;
+  std::vector<XTask> tasks;
+  size_t i = 0;
+  while (i < ord.size()) {
+    const int64_t m = ops[ord[i]].mat;
+    size_t j = i;
+    while (j < ord.size() && ops[ord[j]].mat == m && j - i < (size_t)XT_NP) ++j;
+    XTask t;
+    t.mat_off = p.mats[m].offset;
+    t.rows = p.mats[m].rows;
+    t.cols = p.mats[m].cols;
+    t.op_begin = (int32_t)so.size();
+    t.op_count = (int32_t)(j - i);
+    for (size_t q = i; q < j; ++q) {
+      so.push_back(src_off[ops[ord[q]].src]);
+      dof.push_back(dst_off[ops[ord[q]].dst]);
+    }
+    st.max_rows = std::max(st.max_rows, t.rows);
+    if (t.cols > 320) { ctx->err = "translation matrix wider than 320 columns"; return FDA_E_INTERNAL; }
+    tasks.push_back(t);
+    i = j;
+  }
+  st.ntask = (int)tasks.size();
+  UP(&st.tasks, tasks.data(), tasks.size());
+  UP(&st.src, so.data(), so.size());
+  UP(&st.dst, dof.data(), dof.size());
+  return FDA_OK;
+}
+
+fda_status engine_create(Context* ctx) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    ctx->err = "no CUDA device available (the FDA matvec runs only on the GPU; use opt.device = -1 for a host-only build)";
+    return FDA_E_CUDA;
+  }
+  if (ctx->p.opt.device >= ndev) { ctx->err = "opt.device out of range"; return FDA_E_INVALID_ARG; }
+  Dev* d = new Dev();
+  ctx->dev = d;
+  d->device = ctx->p.opt.device;
+  CK(cudaSetDevice(d->device));
+  const Geometry& g = ctx->g;
+  const Tree& t = ctx->t;
+  const Plan& p = ctx->plan;
+  const int n = (int)g.n;
+  const int nleaf = (int)t.leaves.size();
+  d->n = n;
+  d->nleaf = nleaf;
+  d->kp.k = (float)ctx->p.k;
+  d->kp.alpha_re = (float)ctx->p.alpha.real();
+  d->kp.alpha_im = (float)ctx->p.alpha.imag();
+
+  // leaf-local element data (fp32 offsets from the owning leaf centre, computed in fp64)
+  std::vector<float4> tpos(n), tnrm(n);
+  std::vector<SrcElem> src(n);
+  std::vector<float> w(n);
+  std::vector<int32_t> lb(nleaf), le(nleaf), perm(n);
+  std::vector<double> cen(3 * (size_t)n), nrm(3 * (size_t)n);
+  const double inv12pi = 1.0 / (12.0 * M_PI);  // Q3 weight 1/3 and 1/(4π)
+  for (int i = 0; i < nleaf; ++i) {
+    const Box& B = t.boxes[t.leaves[i]];
+    if (B.end - B.begin > 128) { ctx->err = "leaf with more than 128 elements (depth cap hit)"; return FDA_E_INTERNAL; }
+    lb[i] = (int32_t)B.begin;
+    le[i] = (int32_t)B.end;
+    for (int64_t e = B.begin; e < B.end; ++e) {
+      Vec3 x = g.centroid[e] - B.center;
+      tpos[e] = make_float4((float)x.x, (float)x.y, (float)x.z, 0.f);
+      tnrm[e] = make_float4((float)g.normal[e].x, (float)g.normal[e].y, (float)g.normal[e].z, 0.f);
+      Vec3 q[3];
+      for (int k = 0; k < 3; ++k)
+        q[k] = g.v0[e] * Q3_BARY[k][0] + g.v1[e] * Q3_BARY[k][1] + g.v2[e] * Q3_BARY[k][2] - B.center;
+      src[e].a = make_float4((float)q[0].x, (float)q[0].y, (float)q[0].z, (float)g.normal[e].x);
+      src[e].b = make_float4((float)q[1].x, (float)q[1].y, (float)q[1].z, (float)g.normal[e].y);
+      src[e].c = make_float4((float)q[2].x, (float)q[2].y, (float)q[2].z, (float)g.normal[e].z);
+      w[e] = (float)(g.area[e] * inv12pi);
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    perm[i] = (int32_t)g.perm[i];
+    cen[3 * i] = g.centroid[i].x; cen[3 * i + 1] = g.centroid[i].y; cen[3 * i + 2] = g.centroid[i].z;
+    nrm[3 * i] = g.normal[i].x; nrm[3 * i + 1] = g.normal[i].y; nrm[3 * i + 2] = g.normal[i].z;
+  }
+  std::vector<int32_t> nptr(p.near_ptr.begin(), p.near_ptr.end()), nidx(p.near_idx.begin(), p.near_idx.end());
+  std::vector<float4> noff(p.near_idx.size());
+  for (int i = 0; i < nleaf; ++i) {
+    const Box& B = t.boxes[t.leaves[i]];
+    for (int64_t e = p.near_ptr[i]; e < p.near_ptr[i + 1]; ++e) {
+      const Box& C = t.boxes[t.leaves[p.near_idx[e]]];
+      Vec3 o = B.center - C.center;
+      noff[e] = make_float4((float)o.x, (float)o.y, (float)o.z, 0.f);
+    }
+  }
+  if (p.corr_col.size() >= (size_t)INT32_MAX || p.near_idx.size() >= (size_t)INT32_MAX) {
+    ctx->err = "table too large for 32-bit indices";
+    return FDA_E_INTERNAL;
+  }
+  std::vector<int32_t> cptr(p.corr_ptr.begin(), p.corr_ptr.end()), ccol(p.corr_col.begin(), p.corr_col.end());
+
+  UP(&d->perm, perm.data(), perm.size());
+  UP(&d->tgt_pos, tpos.data(), tpos.size());
+  UP(&d->tgt_nrm, tnrm.data(), tnrm.size());
+  UP(&d->src, src.data(), src.size());
+  UP(&d->src_w, w.data(), w.size());
+  UP(&d->leaf_begin, lb.data(), lb.size());
+  UP(&d->leaf_end, le.data(), le.size());
+  UP(&d->near_ptr, nptr.data(), nptr.size());
+  UP(&d->near_idx, nidx.data(), nidx.size());
+  UP(&d->near_off, noff.data(), noff.size());
+  UP(&d->corr_ptr, cptr.data(), cptr.size());
+  UP(&d->corr_col, ccol.data(), ccol.size());
+  UP(&d->corr_val, reinterpret_cast<const float2*>(p.corr_val.data()), p.corr_val.size());
+  UP(&d->pool, reinterpret_cast<const float2*>(p.pool.data()), p.pool.size());
+  UP(&d->cen, cen.data(), cen.size());
+  UP(&d->nrm, nrm.data(), nrm.size());
+  d->out_size = p.out_size;
+  d->in_size = p.in_size;
+  AL(&d->outb, (size_t)p.out_size);
+  AL(&d->inb, (size_t)p.in_size);
+  AL(&d->x_tree, (size_t)n);
+  AL(&d->y_near, (size_t)n);
+  AL(&d->y_far, (size_t)n);
+  AL(&d->xh, (size_t)n);
+  AL(&d->yh, (size_t)n);
+
+  // leaf tasks
+  std::vector<LeafTask> s2m, l2t;
+  for (int i = 0; i < nleaf; ++i) {
+    const Box& B = t.boxes[t.leaves[i]];
+    const int T = t.levels[B.level].rank;
+    if (p.leaf_S[i] >= 0) {
+      LeafTask lt{p.mats[p.leaf_S[i]].offset, p.out_offset[p.leaf_out[i]], (int32_t)B.begin,
+                  (int32_t)(B.end - B.begin), T, 0};
+      s2m.push_back(lt);
+      d->max_T = std::max(d->max_T, T);
+    }
+    LeafTask lt{-1, 0, (int32_t)B.begin, (int32_t)(B.end - B.begin), 0, 0};
+    if (p.leaf_T[i] >= 0) {
+      lt.mat_off = p.mats[p.leaf_T[i]].offset;
+      lt.state_off = p.in_offset[p.leaf_in[i]];
+      lt.T = T;
+      if (T > 320) { ctx->err = "rank above 320"; return FDA_E_INTERNAL; }
+    }
+    l2t.push_back(lt);
+  }
+  d->n_s2m = (int)s2m.size();
+  d->n_l2t = (int)l2t.size();
+  UP(&d->s2m, s2m.data(), s2m.size());
+  UP(&d->l2t, l2t.data(), l2t.size());
+
+  const int nlev = (int)t.levels.size();
+  d->m2m.resize(nlev); d->m2l.resize(nlev); d->l2l.resize(nlev);
+  for (int l = 0; l < nlev; ++l) {
+    fda_status s;
+    if ((s = build_xstage(ctx, d, p.m2m[l], p.out_offset, p.out_offset, d->m2m[l])) != FDA_OK) return s;
+    if ((s = build_xstage(ctx, d, p.m2l[l], p.out_offset, p.in_offset, d->m2l[l])) != FDA_OK) return s;
+    if ((s = build_xstage(ctx, d, p.l2l[l], p.in_offset, p.in_offset, d->l2l[l])) != FDA_OK) return s;
+  }
+  CK(cudaStreamCreateWithFlags(&d->s_near, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
+  for (auto& e : d->ev) CK(cudaEventCreate(&e));
+  CK(cudaEventCreate(&d->ev_n0));
+  CK(cudaEventCreate(&d->ev_n1));
+  CK(cudaDeviceSynchronize());
+  return FDA_OK;
+}
+
+void engine_destroy(Context* ctx) {
+  Dev* d = static_cast<Dev*>(ctx->dev);
+  if (!d) return;
+  cudaSetDevice(d->device);
+  cudaDeviceSynchronize();
+  for (void* a : d->allocs) cudaFree(a);
+  if (d->s_near) cudaStreamDestroy(d->s_near);
+  if (d->ev_fork) cudaEventDestroy(d->ev_fork);
+  if (d->ev_join) cudaEventDestroy(d->ev_join);
+  for (auto& e : d->ev) if (e) cudaEventDestroy(e);
+  if (d->ev_n0) cudaEventDestroy(d->ev_n0);
+  if (d->ev_n1) cudaEventDestroy(d->ev_n1);
+  delete d;
+  ctx->dev = nullptr;
+}
+
+// the device part of one matvec: x_tree → y_near, y_far (tree order)
+static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s) {
+  const bool prof = ctx->profiling;
+  CK(cudaEventRecord(d->ev_fork, s));
+  CK(cudaStreamWaitEvent(d->s_near, d->ev_fork, 0));
+  if (prof) CK(cudaEventRecord(d->ev_n0, d->s_near));
+  launch_near(d->nleaf, d->leaf_begin, d->leaf_end, d->near_ptr, d->near_idx, d->near_off, d->tgt_pos, d->tgt_nrm,
+              d->src, d->src_w, d->corr_ptr, d->corr_col, d->corr_val, d->x_tree, d->y_near, d->kp, d->s_near);
+  if (prof) CK(cudaEventRecord(d->ev_n1, d->s_near));
+  CK(cudaEventRecord(d->ev_join, d->s_near));
+
+  if (d->out_size) CK(cudaMemsetAsync(d->outb, 0, sizeof(float2) * d->out_size, s));
+  if (d->in_size) CK(cudaMemsetAsync(d->inb, 0, sizeof(float2) * d->in_size, s));
+  launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s);
+  if (prof) CK(cudaEventRecord(d->ev[2], s));
+  const int nlev = (int)d->m2m.size();
+  for (int l = nlev - 1; l >= 0; --l) {
+    const XStage& st = d->m2m[l];
+    launch_xlate(st.ntask, st.tasks, st.src, st.dst, d->pool, d->outb, d->outb, st.max_rows, s);
+  }
+  if (prof) CK(cudaEventRecord(d->ev[3], s));
+  for (int l = 0; l < nlev; ++l) {
+    const XStage& st = d->m2l[l];
+    launch_xlate(st.ntask, st.tasks, st.src, st.dst, d->pool, d->outb, d->inb, st.max_rows, s);
+  }
+  if (prof) CK(cudaEventRecord(d->ev[4], s));
+  for (int l = 0; l < nlev; ++l) {
+    const XStage& st = d->l2l[l];
+    launch_xlate(st.ntask, st.tasks, st.src, st.dst, d->pool, d->inb, d->inb, st.max_rows, s);
+  }
+  if (prof) CK(cudaEventRecord(d->ev[5], s));
+  launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
+  if (prof) CK(cudaEventRecord(d->ev[6], s));
+  CK(cudaStreamWaitEvent(s, d->ev_join, 0));
+  CK(cudaGetLastError());
+  return FDA_OK;
+}
+
+// device-pointer matvec in caller order (float2 in, float2 out)
+static fda_status matvec_dev(Context* ctx, Dev* d, const float2* x, float2* y, cudaStream_t s) {
+  const bool prof = ctx->profiling;
+  if (prof) CK(cudaEventRecord(d->ev[0], s));
+  launch_gather_f32(x, d->perm, d->x_tree, d->n, s);
+  if (prof) CK(cudaEventRecord(d->ev[1], s));
+  fda_status st = run_core(ctx, d, s);
+  if (st != FDA_OK) return st;
+  launch_scatter_f32(d->y_near, d->y_far, d->perm, y, d->n, s);
+  if (prof) CK(cudaEventRecord(d->ev[7], s));
+  d->timed = prof;
+  CK(cudaGetLastError());
+  return FDA_OK;
+}
+
+fda_status engine_matvec(Context* ctx, const void* x, void* y, int32_t flags, void* stream) {
+  Dev* d = static_cast<Dev*>(ctx->dev);
+  CK(cudaSetDevice(d->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (flags & FDA_DEVICE) return matvec_dev(ctx, d, static_cast<const float2*>(x), static_cast<float2*>(y), s);
+  // host complex128 in/out
+  const bool prof = ctx->profiling;
+  CK(cudaMemcpyAsync(d->xh, x, sizeof(double2) * d->n, cudaMemcpyHostToDevice, s));
+  if (prof) CK(cudaEventRecord(d->ev[0], s));
+  launch_gather_f64(d->xh, d->perm, d->x_tree, d->n, s);
+  if (prof) CK(cudaEventRecord(d->ev[1], s));
+  fda_status st = run_core(ctx, d, s);
+  if (st != FDA_OK) return st;
+  launch_scatter_f64(d->y_near, d->y_far, d->perm, d->yh, d->n, s);
+  if (prof) CK(cudaEventRecord(d->ev[7], s));
+  d->timed = prof;
+  CK(cudaMemcpyAsync(y, d->yh, sizeof(double2) * d->n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return FDA_OK;
+}
+
+fda_status engine_stage_times(Context* ctx, double* ms, int32_t* n) {
+  Dev* d = static_cast<Dev*>(ctx->dev);
+  if (!d->timed) { ctx->err = "no profiled matvec yet (call fda_set_profiling(ctx, 1) first)"; return FDA_E_STATE; }
+  CK(cudaEventSynchronize(d->ev[7]));
+  float v[8] = {0};
+  CK(cudaEventElapsedTime(&v[0], d->ev[0], d->ev[1]));
+  CK(cudaEventElapsedTime(&v[1], d->ev_n0, d->ev_n1));
+  CK(cudaEventElapsedTime(&v[2], d->ev[1], d->ev[2]));
+  CK(cudaEventElapsedTime(&v[3], d->ev[2], d->ev[3]));
+  CK(cudaEventElapsedTime(&v[4], d->ev[3], d->ev[4]));
+  CK(cudaEventElapsedTime(&v[5], d->ev[4], d->ev[5]));
+  CK(cudaEventElapsedTime(&v[6], d->ev[5], d->ev[6]));
+  CK(cudaEventElapsedTime(&v[7], d->ev[6], d->ev[7]));
+  int m = std::min(*n, 8);
+  for (int i = 0; i < m; ++i) ms[i] = v[i];
+  *n = m;
+  return FDA_OK;
+}
+
+fda_status engine_rhs_plane_wave(Context* ctx, const double dir[3], void* b, int32_t flags) {
+  Dev* d = static_cast<Dev*>(ctx->dev);
+  CK(cudaSetDevice(d->device));
+  double nn = std::sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
+  if (flags & FDA_DEVICE) {
+    launch_plane_wave(d->cen, d->nrm, d->perm, d->n, ctx->p.k, ctx->p.alpha.real(), ctx->p.alpha.imag(),
+                      dir[0] / nn, dir[1] / nn, dir[2] / nn, static_cast<float2*>(b), nullptr, 0);
+    CK(cudaGetLastError());
+    return FDA_OK;
+  }
+  launch_plane_wave(d->cen, d->nrm, d->perm, d->n, ctx->p.k, ctx->p.alpha.real(), ctx->p.alpha.imag(), dir[0] / nn,
+                    dir[1] / nn, dir[2] / nn, nullptr, d->yh, 0);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(b, d->yh, sizeof(double2) * d->n, cudaMemcpyDeviceToHost));
+  return FDA_OK;
+}
+
+// ------------------------------------------------------------------ GMRES
+namespace {
+struct Gm {
+  float2 *V = nullptr, *w = nullptr, *b = nullptr, *x = nullptr;
+  double2 *partial = nullptr, *hdev = nullptr;
+  double* np = nullptr;
+  int m = 0;
+};
+}  // namespace
+
+static const int kChunks = 128;
+
+static fda_status dotv(Context* ctx, Gm& gm, const float2* V, int nv, const float2* w, int64_t n, std::vector<cd>& h) {
+  launch_dots(V, n, nv, w, n, gm.partial, kChunks, 0);
+  CK(cudaGetLastError());
+  std::vector<double2> part((size_t)kChunks * nv);
+  CK(cudaMemcpy(part.data(), gm.partial, sizeof(double2) * part.size(), cudaMemcpyDeviceToHost));
+  h.assign(nv, 0.0);
+  for (int c = 0; c < kChunks; ++c)
+    for (int i = 0; i < nv; ++i) h[i] += cd(part[(size_t)c * nv + i].x, part[(size_t)c * nv + i].y);
+  return FDA_OK;
+}
+
+static fda_status norm(Context* ctx, Gm& gm, const float2* w, int64_t n, double& out) {
+  launch_norm2(w, n, gm.np, kChunks, 0);
+  CK(cudaGetLastError());
+  std::vector<double> part(kChunks);
+  CK(cudaMemcpy(part.data(), gm.np, sizeof(double) * kChunks, cudaMemcpyDeviceToHost));
+  double s = 0;
+  for (double v : part) s += v;
+  out = std::sqrt(s);
+  return FDA_OK;
+}
+
+static fda_status update(Context* ctx, Gm& gm, float2* w, const float2* V, int nv, const std::vector<cd>& h, int64_t n,
+                         double sign) {
+  std::vector<double2> hh(nv);
+  for (int i = 0; i < nv; ++i) hh[i] = make_double2(h[i].real(), h[i].imag());
+  CK(cudaMemcpy(gm.hdev, hh.data(), sizeof(double2) * nv, cudaMemcpyHostToDevice));
+  launch_update(w, V, n, nv, gm.hdev, n, sign, 0);
+  CK(cudaGetLastError());
+  return FDA_OK;
+}
+
+fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int32_t max_iter, int32_t restart,
+                        fda_solve_info* info, int32_t flags) {
+  Dev* d = static_cast<Dev*>(ctx->dev);
+  CK(cudaSetDevice(d->device));
+  CK(cudaDeviceSynchronize());
+  auto t0 = std::chrono::steady_clock::now();
+  const int64_t n = d->n;
+  const int m = restart > 0 ? std::min(restart, max_iter) : max_iter;
+  Gm gm;
+  gm.m = m;
+  std::vector<void*> mine;
+  auto A = [&](void** p, size_t bytes) -> fda_status {
+    CK(cudaMalloc(p, bytes));
+    mine.push_back(*p);
+    return FDA_OK;
+  };
+  fda_status st = FDA_OK;
+  auto cleanup = [&]() { for (void* p : mine) cudaFree(p); };
+  if ((st = A((void**)&gm.V, sizeof(float2) * n * (m + 1))) != FDA_OK ||
+      (st = A((void**)&gm.w, sizeof(float2) * n)) != FDA_OK || (st = A((void**)&gm.b, sizeof(float2) * n)) != FDA_OK ||
+      (st = A((void**)&gm.x, sizeof(float2) * n)) != FDA_OK ||
+      (st = A((void**)&gm.partial, sizeof(double2) * kChunks * (m + 1))) != FDA_OK ||
+      (st = A((void**)&gm.hdev, sizeof(double2) * (m + 1))) != FDA_OK ||
+      (st = A((void**)&gm.np, sizeof(double) * kChunks)) != FDA_OK) {
+    cleanup();
+    return st == FDA_E_CUDA ? FDA_E_NOMEM : st;
+  }
+#define GCK(expr)               \
+  do {                          \
+    st = (expr);                \
+    if (st != FDA_OK) {         \
+      cleanup();                \
+      return st;                \
+    }                           \
+  } while (0)
+  if (flags & FDA_DEVICE) {
+    CK(cudaMemcpy(gm.b, rhs, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+  } else {
+    CK(cudaMemcpy(d->xh, rhs, sizeof(double2) * n, cudaMemcpyHostToDevice));
+    launch_f64_to_f32(d->xh, gm.b, n, 0);
+  }
+  CK(cudaMemset(gm.x, 0, sizeof(float2) * n));
+  double bnorm = 0;
+  GCK(norm(ctx, gm, gm.b, n, bnorm));
+  int it = 0;
+  double res = 1.0;
+  bool conv = bnorm == 0.0;
+  std::vector<cd> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), h, h2;
+  while (!conv && it < max_iter) {
+    // r = b - A x   (x = 0 on the first cycle)
+    float2* v0 = gm.V;
+    double beta;
+    if (it == 0) {
+      CK(cudaMemcpy(v0, gm.b, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+      beta = bnorm;
+    } else {
+      GCK(matvec_dev(ctx, d, gm.x, gm.w, 0));
+      CK(cudaMemcpy(v0, gm.b, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+      launch_axpby(v0, gm.w, -1.0, 1.0, n, 0);
+      GCK(norm(ctx, gm, v0, n, beta));
+    }
+    launch_scale(v0, v0, 1.0 / beta, 0.0, n, 0);
+    std::fill(H.begin(), H.end(), cd(0));
+    std::fill(g.begin(), g.end(), cd(0));
+    g[0] = beta;
+    int jd = 0;
+    for (int j = 0; j < m && it < max_iter; ++j) {
+      float2* vj = gm.V + (int64_t)j * n;
+      GCK(matvec_dev(ctx, d, vj, gm.w, 0));
+      // classical Gram-Schmidt, twice (CGS2), fp64 dot accumulation
+      GCK(dotv(ctx, gm, gm.V, j + 1, gm.w, n, h));
+      GCK(update(ctx, gm, gm.w, gm.V, j + 1, h, n, -1.0));
+      GCK(dotv(ctx, gm, gm.V, j + 1, gm.w, n, h2));
+      GCK(update(ctx, gm, gm.w, gm.V, j + 1, h2, n, -1.0));
+      for (int i = 0; i <= j; ++i) H[(size_t)j * (m + 1) + i] = h[i] + h2[i];
+      double hn;
+      GCK(norm(ctx, gm, gm.w, n, hn));
+      H[(size_t)j * (m + 1) + j + 1] = hn;
+      if (hn > 0) launch_scale(gm.V + (int64_t)(j + 1) * n, gm.w, 1.0 / hn, 0.0, n, 0);
+      // Givens rotations (complex): [c̄ s̄; -s c]
+      for (int i = 0; i < j; ++i) {
+        cd a = H[(size_t)j * (m + 1) + i], bb = H[(size_t)j * (m + 1) + i + 1];
+        H[(size_t)j * (m + 1) + i] = std::conj(cs[i]) * a + std::conj(sn[i]) * bb;
+        H[(size_t)j * (m + 1) + i + 1] = -sn[i] * a + cs[i] * bb;
+      }
+      cd a = H[(size_t)j * (m + 1) + j], bb = H[(size_t)j * (m + 1) + j + 1];
+      double den = std::sqrt(std::norm(a) + std::norm(bb));
+      cs[j] = a / den;
+      sn[j] = bb / den;
+      H[(size_t)j * (m + 1) + j] = den;
+      H[(size_t)j * (m + 1) + j + 1] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = std::conj(cs[j]) * g[j];
+      ++it;
+      jd = j + 1;
+      res = std::abs(g[j + 1]) / bnorm;
+      if (res <= tol) { conv = true; break; }
+    }
+    // y = R⁻¹ g ; x += V y
+    std::vector<cd> y(jd);
+    for (int i = jd - 1; i >= 0; --i) {
+      cd s = g[i];
+      for (int k = i + 1; k < jd; ++k) s -= H[(size_t)k * (m + 1) + i] * y[k];
+      y[i] = s / H[(size_t)i * (m + 1) + i];
+    }
+    GCK(update(ctx, gm, gm.x, gm.V, jd, y, n, +1.0));
+    if (restart <= 0) break;
+  }
+  // true residual
+  double true_res = 0;
+  if (bnorm > 0) {
+    GCK(matvec_dev(ctx, d, gm.x, gm.w, 0));
+    launch_axpby(gm.w, gm.b, 1.0, -1.0, n, 0);  // w = b - A x
+    double rn;
+    GCK(norm(ctx, gm, gm.w, n, rn));
+    true_res = rn / bnorm;
+  }
+  if (flags & FDA_DEVICE) {
+    CK(cudaMemcpy(u, gm.x, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+  } else {
+    launch_f32_to_f64(gm.x, d->yh, n, 0);
+    CK(cudaMemcpy(u, d->yh, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+  }
+  CK(cudaDeviceSynchronize());
+  cleanup();
+  if (info) {
+    info->iterations = it;
+    info->converged = conv ? 1 : 0;
+    info->rel_residual = res;
+    info->true_residual = true_res;
+    info->t_solve_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return conv ? FDA_OK : FDA_E_NOT_CONVERGED;
+}
+
+}  // namespace fda

@@ -1,0 +1,305 @@
+// C ABI of the FDA library (include/fda.h): argument checking, build
+// orchestration (PAPER.md Algorithm Step 1, and §4 tables) and
+// host-table export for host-logic tests.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <omp.h>
+
+#include "fda_internal.h"
+
+using namespace fda;
+
+template <class T>
+static fda_status put(const std::vector<T>& v, void* dst, int64_t* count, int32_t* eb) {
+  *count = (int64_t)v.size();
+  *eb = (int32_t)sizeof(T);
+  if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(T));
+  return FDA_OK;
+}
+
+
+extern "C" {
+
+fda_status fda_options_default(fda_options* opt) {
+  if (!opt) return FDA_E_INVALID_ARG;
+  std::memset(opt, 0, sizeof(*opt));
+  opt->max_leaf = 64;
+  opt->p_eq = 8;
+  opt->p_chk_lf = 8;
+  opt->p_chk_hf = 12;
+  opt->eq_scale = 1.05;
+  opt->chk_scale_lf = 2.95;
+  opt->tier1_rho = 1.5;
+  opt->tier2_rho = 3.0;
+  opt->direct_all = 0;
+  opt->device = 0;
+  opt->build_threads = 0;
+  opt->use_graph = 1;
+  opt->verbose = 0;
+  return FDA_OK;
+}
+
+const char* fda_status_string(fda_status s) {
+  switch (s) {
+    case FDA_OK: return "FDA_OK";
+    case FDA_E_INVALID_ARG: return "FDA_E_INVALID_ARG";
+    case FDA_E_MESH: return "FDA_E_MESH";
+    case FDA_E_NOMEM: return "FDA_E_NOMEM";
+    case FDA_E_CUDA: return "FDA_E_CUDA";
+    case FDA_E_NCCL: return "FDA_E_NCCL";
+    case FDA_E_NOT_CONVERGED: return "FDA_E_NOT_CONVERGED";
+    case FDA_E_STATE: return "FDA_E_STATE";
+    case FDA_E_INTERNAL: return "FDA_E_INTERNAL";
+  }
+  return "unknown";
+}
+
+static thread_local std::string g_build_error;
+
+const char* fda_last_error(const fda_ctx* ctx) {
+  if (!ctx) return g_build_error.c_str();
+  return ctx->err.c_str();
+}
+
+fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangles, int64_t nt, double k,
+                     fda_cplx alpha, double eps, const fda_options* opt, fda_ctx** out) {
+  g_build_error.clear();
+  if (!out || !vertices || !triangles) { g_build_error = "null pointer argument"; return FDA_E_INVALID_ARG; }
+  *out = nullptr;
+  if (!(k > 0) || !std::isfinite(k)) { g_build_error = "k must be > 0"; return FDA_E_INVALID_ARG; }
+  if (!(eps > 0 && eps <= 0.1)) { g_build_error = "eps must lie in (0, 0.1]"; return FDA_E_INVALID_ARG; }
+  if (alpha.im == 0.0 || !std::isfinite(alpha.re) || !std::isfinite(alpha.im)) {
+    g_build_error = "alpha must have a non-zero imaginary part (Burton-Miller coupling, i/k recommended)";
+    return FDA_E_INVALID_ARG;
+  }
+  if (nt < 1) { g_build_error = "nt must be >= 1"; return FDA_E_INVALID_ARG; }
+  auto t0 = std::chrono::steady_clock::now();
+  fda_ctx* ctx = new (std::nothrow) fda_ctx();
+  if (!ctx) return FDA_E_NOMEM;
+  ctx->p.k = k;
+  ctx->p.alpha = cd(alpha.re, alpha.im);
+  ctx->p.eps = eps;
+  if (opt) ctx->p.opt = *opt; else fda_options_default(&ctx->p.opt);
+  fda_options& o = ctx->p.opt;
+  if (o.max_leaf < 1 || o.p_eq < 2 || o.p_chk_lf < 2 || o.p_chk_hf < 2 || !(o.eq_scale > 0) ||
+      !(o.chk_scale_lf > o.eq_scale) || !(o.tier1_rho >= 0) || !(o.tier2_rho >= o.tier1_rho)) {
+    g_build_error = "invalid fda_options";
+    delete ctx;
+    return FDA_E_INVALID_ARG;
+  }
+  int saved_threads = omp_get_max_threads();
+  if (o.build_threads > 0) omp_set_num_threads(o.build_threads);
+  fda_status st = FDA_OK;
+  try {
+    st = build_geometry(vertices, nv, triangles, nt, ctx->g, ctx->err);
+    if (st == FDA_OK) {
+      build_tree(ctx->g, ctx->p, ctx->t);
+      build_lists(ctx->g, ctx->p, ctx->t, ctx->plan);
+      Plan& pl = ctx->plan;
+      const int nlev = (int)ctx->t.levels.size();
+      std::vector<bool> need(nlev, false);
+      for (int l = 0; l < nlev; ++l)
+        need[l] = pl.out_level_begin[l + 1] > pl.out_level_begin[l] || pl.in_level_begin[l + 1] > pl.in_level_begin[l];
+      build_clouds_and_svd(ctx->p, ctx->t, need);
+      // state offsets (complex entries)
+      pl.out_offset.resize(pl.out_states.size());
+      pl.in_offset.resize(pl.in_states.size());
+      int64_t off = 0;
+      for (size_t s = 0; s < pl.out_states.size(); ++s) {
+        pl.out_offset[s] = off;
+        off += ctx->t.levels[ctx->t.boxes[pl.out_states[s].box].level].rank;
+      }
+      pl.out_size = off;
+      off = 0;
+      for (size_t s = 0; s < pl.in_states.size(); ++s) {
+        pl.in_offset[s] = off;
+        off += ctx->t.levels[ctx->t.boxes[pl.in_states[s].box].level].rank;
+      }
+      pl.in_size = off;
+      build_operators(ctx->g, ctx->p, ctx->t, pl);
+      build_corrections(ctx->g, ctx->p, pl);
+    }
+  } catch (const std::bad_alloc&) {
+    ctx->err = "host allocation failed during build";
+    st = FDA_E_NOMEM;
+  } catch (const std::exception& e) {
+    ctx->err = std::string("build failed: ") + e.what();
+    st = FDA_E_INTERNAL;
+  }
+  if (o.build_threads > 0) omp_set_num_threads(saved_threads);
+  if (st == FDA_OK && o.device >= 0) st = engine_create(ctx);
+  if (st != FDA_OK) {
+    g_build_error = ctx->err;
+    engine_destroy(ctx);
+    delete ctx;
+    return st;
+  }
+  // statistics
+  fda_build_info& I = ctx->info;
+  const Plan& pl = ctx->plan;
+  const Tree& t = ctx->t;
+  I.n_elements = nt;
+  I.n_levels = (int32_t)t.levels.size();
+  I.n_hf_levels = 0;
+  for (int l = 0; l < I.n_levels && l < 32; ++l) {
+    I.rank[l] = t.levels[l].rank;
+    I.dirs[l] = t.levels[l].ndir;
+    I.width[l] = t.levels[l].width;
+    if (t.levels[l].hf) ++I.n_hf_levels;
+  }
+  I.n_boxes = (int64_t)t.boxes.size();
+  I.n_leaves = (int64_t)t.leaves.size();
+  I.n_out_states = (int64_t)pl.out_states.size();
+  I.n_in_states = (int64_t)pl.in_states.size();
+  for (auto& v : pl.m2l) I.n_m2l_pairs += (int64_t)v.size();
+  for (auto& v : pl.m2m) I.n_m2m_ops += (int64_t)v.size();
+  for (auto& v : pl.l2l) I.n_l2l_ops += (int64_t)v.size();
+  I.n_direct_leaf_pairs = (int64_t)pl.near_idx.size();
+  for (size_t i = 0; i + 1 < pl.near_ptr.size(); ++i) {
+    const Box& B = t.boxes[t.leaves[i]];
+    for (int64_t e = pl.near_ptr[i]; e < pl.near_ptr[i + 1]; ++e) {
+      const Box& C = t.boxes[t.leaves[pl.near_idx[e]]];
+      I.n_direct_element_pairs += (B.end - B.begin) * (C.end - C.begin);
+    }
+  }
+  I.n_corrections = (int64_t)pl.corr_col.size();
+  I.n_matrices = (int64_t)pl.mats.size();
+  I.table_bytes = (int64_t)pl.pool.size() * 8 + (int64_t)pl.corr_val.size() * 12;
+  I.t_build_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = ctx;
+  return FDA_OK;
+}
+
+fda_status fda_matvec(fda_ctx* ctx, const void* x, void* y, int32_t flags, void* stream) {
+  if (!ctx) return FDA_E_INVALID_ARG;
+  if (!x || !y || x == y) { ctx->err = "x and y must be non-null and must not alias"; return FDA_E_INVALID_ARG; }
+  if (!ctx->dev) { ctx->err = "context was built host-only (opt.device = -1): no device matvec"; return FDA_E_STATE; }
+  return engine_matvec(ctx, x, y, flags, stream);
+}
+
+fda_status fda_rhs_plane_wave(fda_ctx* ctx, const double dir[3], void* b, int32_t flags) {
+  if (!ctx || !dir || !b) return FDA_E_INVALID_ARG;
+  double nrm = std::sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
+  if (!(nrm > 0)) { ctx->err = "plane-wave direction must be non-zero"; return FDA_E_INVALID_ARG; }
+  if (!ctx->dev) { ctx->err = "context was built host-only"; return FDA_E_STATE; }
+  return engine_rhs_plane_wave(ctx, dir, b, flags);
+}
+
+fda_status bm_solve(fda_ctx* ctx, const void* rhs, void* u, double tol, int32_t max_iter, int32_t restart,
+                    fda_solve_info* info, int32_t flags) {
+  if (!ctx) return FDA_E_INVALID_ARG;
+  if (!rhs || !u || rhs == u) { ctx->err = "rhs and u must be non-null and must not alias"; return FDA_E_INVALID_ARG; }
+  if (!(tol > 0) || max_iter < 1 || restart < 0) { ctx->err = "tol > 0, max_iter >= 1, restart >= 0"; return FDA_E_INVALID_ARG; }
+  if (!ctx->dev) { ctx->err = "context was built host-only"; return FDA_E_STATE; }
+  return engine_solve(ctx, rhs, u, tol, max_iter, restart, info, flags);
+}
+
+fda_status fda_stats(const fda_ctx* ctx, fda_build_info* info) {
+  if (!ctx || !info) return FDA_E_INVALID_ARG;
+  *info = ctx->info;
+  return FDA_OK;
+}
+
+fda_status fda_set_profiling(fda_ctx* ctx, int32_t on) {
+  if (!ctx) return FDA_E_INVALID_ARG;
+  ctx->profiling = on != 0;
+  return FDA_OK;
+}
+
+fda_status fda_stage_times(fda_ctx* ctx, double* ms, int32_t* n) {
+  if (!ctx || !ms || !n) return FDA_E_INVALID_ARG;
+  if (!ctx->dev) return FDA_E_STATE;
+  return engine_stage_times(ctx, ms, n);
+}
+
+fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int64_t* count, int32_t* eb) {
+  if (!ctx || !name || !count || !eb) return FDA_E_INVALID_ARG;
+  const Plan& p = ctx->plan;
+  const Tree& t = ctx->t;
+  const Geometry& g = ctx->g;
+  std::string nm(name);
+  auto ops = [&](const std::vector<std::vector<Op>>& v) {
+    std::vector<int64_t> o;
+    for (size_t l = 0; l < v.size(); ++l)
+      for (auto& op : v[l]) { o.push_back((int64_t)l); o.push_back(op.src); o.push_back(op.dst); o.push_back(op.mat); }
+    return o;
+  };
+  if (nm == "perm") return put(g.perm, dst, count, eb);
+  if (nm == "verts") {
+    std::vector<double> v;
+    for (int64_t i = 0; i < g.n; ++i)
+      for (const Vec3* q : {&g.v0[i], &g.v1[i], &g.v2[i]}) { v.push_back(q->x); v.push_back(q->y); v.push_back(q->z); }
+    return put(v, dst, count, eb);
+  }
+  if (nm == "leaf_range") {
+    std::vector<int64_t> v;
+    for (int64_t b : t.leaves) { v.push_back(t.boxes[b].begin); v.push_back(t.boxes[b].end); }
+    return put(v, dst, count, eb);
+  }
+  if (nm == "leaf_S") return put(p.leaf_S, dst, count, eb);
+  if (nm == "leaf_T") return put(p.leaf_T, dst, count, eb);
+  if (nm == "leaf_out") return put(p.leaf_out, dst, count, eb);
+  if (nm == "leaf_in") return put(p.leaf_in, dst, count, eb);
+  if (nm == "out_offset") return put(p.out_offset, dst, count, eb);
+  if (nm == "in_offset") return put(p.in_offset, dst, count, eb);
+  if (nm == "sizes") return put(std::vector<int64_t>{p.out_size, p.in_size}, dst, count, eb);
+  if (nm == "m2m") return put(ops(p.m2m), dst, count, eb);
+  if (nm == "m2l") return put(ops(p.m2l), dst, count, eb);
+  if (nm == "l2l") return put(ops(p.l2l), dst, count, eb);
+  if (nm == "mats") {
+    std::vector<int64_t> v;
+    for (auto& m : p.mats) { v.push_back(m.offset); v.push_back(m.rows); v.push_back(m.cols); }
+    return put(v, dst, count, eb);
+  }
+  if (nm == "specs") {
+    std::vector<int64_t> v;
+    for (auto& s : p.specs) {
+      for (int64_t x : {(int64_t)s.kind, (int64_t)s.level, (int64_t)s.octant, (int64_t)s.dir, s.leaf, s.dx, s.dy, s.dz}) v.push_back(x);
+    }
+    return put(v, dst, count, eb);
+  }
+  if (nm == "pool") return put(p.pool, dst, count, eb);
+  if (nm == "near_ptr") return put(p.near_ptr, dst, count, eb);
+  if (nm == "near_idx") return put(p.near_idx, dst, count, eb);
+  if (nm == "corr_ptr") return put(p.corr_ptr, dst, count, eb);
+  if (nm == "corr_col") return put(p.corr_col, dst, count, eb);
+  if (nm == "corr_val") return put(p.corr_val, dst, count, eb);
+  if (nm == "out_states" || nm == "in_states") {
+    const auto& S = nm == "out_states" ? p.out_states : p.in_states;
+    std::vector<int64_t> v;
+    for (auto& s : S) { v.push_back(s.box); v.push_back(s.dir); }
+    return put(v, dst, count, eb);
+  }
+  if (nm == "boxes") {  // level, ix, iy, iz, parent, begin, end, leaf
+    std::vector<int64_t> v;
+    for (auto& b : t.boxes)
+      for (int64_t x : {(int64_t)b.level, b.ix, b.iy, b.iz, b.parent, b.begin, b.end, (int64_t)b.leaf}) v.push_back(x);
+    return put(v, dst, count, eb);
+  }
+  if (nm == "box_center") {
+    std::vector<double> v;
+    for (auto& b : t.boxes) { v.push_back(b.center.x); v.push_back(b.center.y); v.push_back(b.center.z); }
+    return put(v, dst, count, eb);
+  }
+  if (nm == "levels") {  // width, hf, nf, rank
+    std::vector<double> v;
+    for (auto& L : t.levels) { v.push_back(L.width); v.push_back(L.hf); v.push_back(L.nf); v.push_back(L.rank); }
+    return put(v, dst, count, eb);
+  }
+  if (nm == "root") {
+    return put(std::vector<double>{t.root_center.x, t.root_center.y, t.root_center.z, t.root_width, t.lambda},
+               dst, count, eb);
+  }
+  const_cast<fda_ctx*>(ctx)->err = "unknown table name: " + nm;
+  return FDA_E_INVALID_ARG;
+}
+
+void fda_free(fda_ctx* ctx) {
+  if (!ctx) return;
+  engine_destroy(ctx);
+  delete ctx;
+}
+
+}  // extern "C"

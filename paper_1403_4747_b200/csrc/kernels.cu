@@ -1,0 +1,445 @@
+// Device kernels of the FDA Burton–Miller matvec (sm_100a, complex64 data,
+// fp32 arithmetic; fp64 accumulation in the GMRES reductions).
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "kernels.cuh"
+
+namespace fda {
+
+// ------------------------------------------------------------------ permutes
+// a1 gather: x_tree[i] = x_caller[perm[i]]  (HBM-bound, 16 B/element)
+__global__ void k_gather_f32(const float2* __restrict__ xc, const int32_t* __restrict__ perm,
+                             float2* __restrict__ xt, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) xt[i] = xc[perm[i]];
+}
+__global__ void k_gather_f64(const double2* __restrict__ xc, const int32_t* __restrict__ perm,
+                             float2* __restrict__ xt, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    double2 v = xc[perm[i]];
+    xt[i] = make_float2((float)v.x, (float)v.y);
+  }
+}
+// a8 scatter: y_caller[perm[i]] = y_near[i] + y_far[i]
+__global__ void k_scatter_f32(const float2* __restrict__ yn, const float2* __restrict__ yf,
+                              const int32_t* __restrict__ perm, float2* __restrict__ yc, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    float2 a = yn[i], b = yf[i];
+    yc[perm[i]] = make_float2(a.x + b.x, a.y + b.y);
+  }
+}
+__global__ void k_scatter_f64(const float2* __restrict__ yn, const float2* __restrict__ yf,
+                              const int32_t* __restrict__ perm, double2* __restrict__ yc, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    float2 a = yn[i], b = yf[i];
+    yc[perm[i]] = make_double2((double)a.x + (double)b.x, (double)a.y + (double)b.y);
+  }
+}
+
+void launch_gather_f32(const float2* x, const int32_t* perm, float2* xt, int n, cudaStream_t s) {
+  k_gather_f32<<<(n + 255) / 256, 256, 0, s>>>(x, perm, xt, n);
+}
+void launch_gather_f64(const double2* x, const int32_t* perm, float2* xt, int n, cudaStream_t s) {
+  k_gather_f64<<<(n + 255) / 256, 256, 0, s>>>(x, perm, xt, n);
+}
+void launch_scatter_f32(const float2* yn, const float2* yf, const int32_t* perm, float2* yc, int n, cudaStream_t s) {
+  k_scatter_f32<<<(n + 255) / 256, 256, 0, s>>>(yn, yf, perm, yc, n);
+}
+void launch_scatter_f64(const float2* yn, const float2* yf, const int32_t* perm, double2* yc, int n, cudaStream_t s) {
+  k_scatter_f64<<<(n + 255) / 256, 256, 0, s>>>(yn, yf, perm, yc, n);
+}
+
+// ------------------------------------------------------------------ near field (a7)
+// y_i = Σ_{j ∈ direct(i)} A^{Q3}_ij x_j + Σ_{j: ρ_ij<3} C_ij x_j
+// A^{Q3}_ij = (A_j/3) Σ_q [∂G/∂n_y + α ∂²G/∂n_x∂n_y](x_i, y_jq)   (Eq. 5)
+// One CTA per target leaf; the source elements of all direct leaves are staged
+// through shared memory in chunks; P = ⌊NT/n_B⌋ threads share one target and
+// split the sources; partial sums are reduced in shared memory.
+constexpr int NEAR_NT = 128;
+constexpr int NEAR_MAXS = 256;
+constexpr int NEAR_MAXL = 256;
+
+__device__ __forceinline__ void lhs_eval(float3 x, float3 nx, float3 y, float3 ny, float cn, float2 w,
+                                         const KernelParams& kp, float2& acc) {
+  const float dx = x.x - y.x, dy = x.y - y.y, dz = x.z - y.z;
+  const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  const float ir = rsqrtf(r2);
+  const float r = r2 * ir;
+  const float q = kp.k * r;
+  const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * ir;   // ∂r/∂n_x
+  const float b = -fmaf(dx, ny.x, fmaf(dy, ny.y, dz * ny.z)) * ir;  // ∂r/∂n_y
+  const float ab = a * b;
+  // e^{iq} with explicit range reduction to [-π, π] before the SFU sin/cos
+  float t = q * (0.5f / CUDART_PI_F);
+  t -= rintf(t);
+  float sn, cs;
+  __sincosf(t * (2.0f * CUDART_PI_F), &sn, &cs);
+  const float ir2 = ir * ir;
+  const float Er = ir2 * cs, Ei = ir2 * sn;  // E = e^{iq}/r² (1/4π folded into w)
+  // D = E (iq - 1) b ;  H = (E/r) [ (3 - q²) ab + c - i q (3ab + c) ]
+  const float u1 = fmaf(3.0f - q * q, ab, cn);
+  const float u2 = -q * fmaf(3.0f, ab, cn);
+  const float P = fmaf(ir, kp.alpha_re * u1 - kp.alpha_im * u2, -b);
+  const float Q = fmaf(ir, kp.alpha_re * u2 + kp.alpha_im * u1, q * b);
+  const float Kr = Er * P - Ei * Q;
+  const float Ki = Er * Q + Ei * P;
+  acc.x = fmaf(Kr, w.x, fmaf(-Ki, w.y, acc.x));
+  acc.y = fmaf(Kr, w.y, fmaf(Ki, w.x, acc.y));
+}
+
+__global__ void __launch_bounds__(NEAR_NT) k_near(
+    const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end,
+    const int32_t* __restrict__ near_ptr, const int32_t* __restrict__ near_idx,
+    const float4* __restrict__ near_off, const float4* __restrict__ tgt_pos, const float4* __restrict__ tgt_nrm,
+    const SrcElem* __restrict__ src, const float* __restrict__ src_w, const int32_t* __restrict__ corr_ptr,
+    const int32_t* __restrict__ corr_col, const float2* __restrict__ corr_val, const float2* __restrict__ x,
+    float2* __restrict__ y, KernelParams kp) {
+  __shared__ float4 sa[NEAR_MAXS], sb[NEAR_MAXS], sc[NEAR_MAXS];
+  __shared__ float2 sx[NEAR_MAXS];
+  __shared__ int spre[NEAR_MAXL + 1];
+  __shared__ float2 sred[NEAR_NT];
+  const int leaf = blockIdx.x;
+  const int tb = leaf_begin[leaf];
+  const int nt = leaf_end[leaf] - tb;
+  const int P = max(1, NEAR_NT / nt);
+  const int tid = threadIdx.x;
+  const int ti = tid % nt, part = tid / nt;
+  const bool active = part < P && ti < nt;
+  float3 xt = make_float3(0.f, 0.f, 0.f), nx = xt;
+  if (active) {
+    float4 p = tgt_pos[tb + ti], q = tgt_nrm[tb + ti];
+    xt = make_float3(p.x, p.y, p.z);
+    nx = make_float3(q.x, q.y, q.z);
+  }
+  float2 acc = make_float2(0.f, 0.f);
+  const int lb = near_ptr[leaf], le = near_ptr[leaf + 1];
+  for (int e0 = lb; e0 < le; e0 += NEAR_MAXL) {
+    const int ne = min(NEAR_MAXL, le - e0);
+    __syncthreads();
+    if (tid == 0) {
+      int s = 0;
+      for (int j = 0; j < ne; ++j) {
+        spre[j] = s;
+        int c = near_idx[e0 + j];
+        s += leaf_end[c] - leaf_begin[c];
+      }
+      spre[ne] = s;
+    }
+    __syncthreads();
+    const int total = spre[ne];
+    for (int base = 0; base < total; base += NEAR_MAXS) {
+      const int ns = min(NEAR_MAXS, total - base);
+      for (int slot = tid; slot < ns; slot += NEAR_NT) {
+        const int g = base + slot;
+        int lo = 0, hi = ne - 1;  // last j with spre[j] <= g
+        while (lo < hi) {
+          int mid = (lo + hi + 1) >> 1;
+          if (spre[mid] <= g) lo = mid; else hi = mid - 1;
+        }
+        const int c = near_idx[e0 + lo];
+        const int el = leaf_begin[c] + (g - spre[lo]);
+        const float4 off = near_off[e0 + lo];  // c_B - c_C
+        SrcElem se = src[el];
+        se.a.x -= off.x; se.a.y -= off.y; se.a.z -= off.z;
+        se.b.x -= off.x; se.b.y -= off.y; se.b.z -= off.z;
+        se.c.x -= off.x; se.c.y -= off.y; se.c.z -= off.z;
+        sa[slot] = se.a; sb[slot] = se.b; sc[slot] = se.c;
+        const float2 xv = x[el];
+        const float wv = src_w[el];
+        sx[slot] = make_float2(xv.x * wv, xv.y * wv);
+      }
+      __syncthreads();
+      if (active) {
+        for (int s = part; s < ns; s += P) {
+          const float4 A = sa[s], B = sb[s], C = sc[s];
+          const float2 w = sx[s];
+          const float3 ny = make_float3(A.w, B.w, C.w);
+          const float cn = fmaf(nx.x, ny.x, fmaf(nx.y, ny.y, nx.z * ny.z));
+          lhs_eval(xt, nx, make_float3(A.x, A.y, A.z), ny, cn, w, kp, acc);
+          lhs_eval(xt, nx, make_float3(B.x, B.y, B.z), ny, cn, w, kp, acc);
+          lhs_eval(xt, nx, make_float3(C.x, C.y, C.z), ny, cn, w, kp, acc);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // correction SpMV, rows split over the P parts
+  if (active) {
+    const int i = tb + ti;
+    const int cb = corr_ptr[i], ce = corr_ptr[i + 1];
+    for (int e = cb + part; e < ce; e += P) {
+      const float2 v = corr_val[e];
+      const float2 xv = x[corr_col[e]];
+      acc.x = fmaf(v.x, xv.x, fmaf(-v.y, xv.y, acc.x));
+      acc.y = fmaf(v.x, xv.y, fmaf(v.y, xv.x, acc.y));
+    }
+  }
+  sred[tid] = active ? acc : make_float2(0.f, 0.f);
+  __syncthreads();
+  if (tid < nt) {
+    float2 s = make_float2(0.f, 0.f);
+    for (int p = 0; p < P; ++p) {
+      float2 v = sred[p * nt + tid];
+      s.x += v.x; s.y += v.y;
+    }
+    y[tb + tid] = s;
+  }
+}
+
+void launch_near(int nleaf, const int32_t* leaf_begin, const int32_t* leaf_end, const int32_t* near_ptr,
+                 const int32_t* near_idx, const float4* near_off, const float4* tgt_pos, const float4* tgt_nrm,
+                 const SrcElem* src, const float* src_w, const int32_t* corr_ptr, const int32_t* corr_col,
+                 const float2* corr_val, const float2* x, float2* y, KernelParams kp, cudaStream_t s) {
+  if (nleaf <= 0) return;
+  k_near<<<nleaf, NEAR_NT, 0, s>>>(leaf_begin, leaf_end, near_ptr, near_idx, near_off, tgt_pos, tgt_nrm, src,
+                                   src_w, corr_ptr, corr_col, corr_val, x, y, kp);
+}
+
+// ------------------------------------------------------------------ S2M (a2) / L2T (a6)
+// S2M: m̃_B = S̃_B x_B (T × n_B, column-major); one CTA per leaf, thread = row.
+__global__ void k_s2m(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
+                      const float2* __restrict__ x, float2* __restrict__ out) {
+  __shared__ float2 sx[128];
+  const LeafTask t = tasks[blockIdx.x];
+  for (int j = threadIdx.x; j < t.elem_count; j += blockDim.x) sx[j] = x[t.elem_begin + j];
+  __syncthreads();
+  const float2* M = pool + t.mat_off;
+  for (int r = threadIdx.x; r < t.T; r += blockDim.x) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int j = 0; j < t.elem_count; ++j) {
+      const float2 m = M[(int64_t)j * t.T + r];
+      const float2 v = sx[j];
+      acc.x = fmaf(m.x, v.x, fmaf(-m.y, v.y, acc.x));
+      acc.y = fmaf(m.x, v.y, fmaf(m.y, v.x, acc.y));
+    }
+    out[t.state_off + r] = acc;
+  }
+}
+
+// L2T: y_B = T̃_B ℓ̃_B (n_B × T column-major); thread = target element.
+__global__ void k_l2t(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
+                      const float2* __restrict__ in, float2* __restrict__ y) {
+  __shared__ float2 sl[320];
+  const LeafTask t = tasks[blockIdx.x];
+  if (t.mat_off < 0) {
+    for (int i = threadIdx.x; i < t.elem_count; i += blockDim.x) y[t.elem_begin + i] = make_float2(0.f, 0.f);
+    return;
+  }
+  for (int c = threadIdx.x; c < t.T; c += blockDim.x) sl[c] = in[t.state_off + c];
+  __syncthreads();
+  const float2* M = pool + t.mat_off;
+  for (int i = threadIdx.x; i < t.elem_count; i += blockDim.x) {
+    float2 acc = make_float2(0.f, 0.f);
+    for (int c = 0; c < t.T; ++c) {
+      const float2 m = M[(int64_t)c * t.elem_count + i];
+      const float2 v = sl[c];
+      acc.x = fmaf(m.x, v.x, fmaf(-m.y, v.y, acc.x));
+      acc.y = fmaf(m.x, v.y, fmaf(m.y, v.x, acc.y));
+    }
+    y[t.elem_begin + i] = acc;
+  }
+}
+
+void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const float2* x, float2* out, int max_rows,
+                cudaStream_t s) {
+  if (ntask <= 0) return;
+  int bd = ((max_rows + 31) / 32) * 32;
+  bd = bd < 32 ? 32 : (bd > 256 ? 256 : bd);
+  k_s2m<<<ntask, bd, 0, s>>>(tasks, pool, x, out);
+}
+void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s) {
+  if (ntask <= 0) return;
+  k_l2t<<<ntask, 64, 0, s>>>(tasks, pool, in, y);
+}
+
+// ------------------------------------------------------------------ translations (a3 M2M, a4 M2L, a5 L2L)
+// dst[op] += M · src[op] for a group of ≤ XT_NP ops sharing M.  The sources
+// are staged in shared memory; each thread owns one output row and keeps
+// XT_NP complex accumulators, so every M element loaded (coalesced along the
+// rows) feeds XT_NP complex FMAs.  Results are accumulated with fp32 atomics
+// (several groups may target the same state).
+__global__ void k_xlate(const XTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
+                        const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
+                        const float2* __restrict__ src, float2* __restrict__ dst) {
+  extern __shared__ float2 sS[];  // [cols][XT_NP]
+  const XTask t = tasks[blockIdx.x];
+  const int np = t.op_count;
+  for (int idx = threadIdx.x; idx < t.cols * XT_NP; idx += blockDim.x) {
+    const int k = idx / XT_NP, p = idx % XT_NP;
+    sS[idx] = p < np ? src[src_off[t.op_begin + p] + k] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  const float2* M = pool + t.mat_off;
+  for (int r = threadIdx.x; r < t.rows; r += blockDim.x) {
+    float2 acc[XT_NP];
+#pragma unroll
+    for (int p = 0; p < XT_NP; ++p) acc[p] = make_float2(0.f, 0.f);
+    for (int k = 0; k < t.cols; ++k) {
+      const float2 m = M[(int64_t)k * t.rows + r];
+      const float4* s4 = reinterpret_cast<const float4*>(sS + k * XT_NP);
+#pragma unroll
+      for (int p2 = 0; p2 < XT_NP / 2; ++p2) {
+        const float4 v = s4[p2];
+        acc[2 * p2].x = fmaf(m.x, v.x, fmaf(-m.y, v.y, acc[2 * p2].x));
+        acc[2 * p2].y = fmaf(m.x, v.y, fmaf(m.y, v.x, acc[2 * p2].y));
+        acc[2 * p2 + 1].x = fmaf(m.x, v.z, fmaf(-m.y, v.w, acc[2 * p2 + 1].x));
+        acc[2 * p2 + 1].y = fmaf(m.x, v.w, fmaf(m.y, v.z, acc[2 * p2 + 1].y));
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < XT_NP; ++p) {
+      if (p < np) {
+        float2* d = dst + dst_off[t.op_begin + p] + r;
+        atomicAdd(&d->x, acc[p].x);
+        atomicAdd(&d->y, acc[p].y);
+      }
+    }
+  }
+}
+
+void launch_xlate(int ntask, const XTask* tasks, const int64_t* src_off, const int64_t* dst_off, const float2* pool,
+                  const float2* src, float2* dst, int max_rows, cudaStream_t s) {
+  if (ntask <= 0) return;
+  int bd = ((max_rows + 31) / 32) * 32;
+  bd = bd < 32 ? 32 : (bd > 256 ? 256 : bd);
+  size_t smem = (size_t)320 * XT_NP * sizeof(float2);  // cols ≤ 320
+  k_xlate<<<ntask, bd, smem, s>>>(tasks, src_off, dst_off, pool, src, dst);
+}
+
+// ------------------------------------------------------------------ GMRES helpers (a9)
+// partial[c * nv + i] = Σ_{n ∈ chunk c} conj(V_i[n]) w[n]   (fp64 accumulation)
+__global__ void k_dots(const float2* __restrict__ V, int64_t ldv, int nv, const float2* __restrict__ w, int64_t n,
+                       double2* __restrict__ partial, int64_t chunk) {
+  __shared__ double2 red[256];
+  const int i = blockIdx.y, c = blockIdx.x;
+  const int64_t b = (int64_t)c * chunk, e = min(n, b + chunk);
+  const float2* v = V + (int64_t)i * ldv;
+  double sr = 0, si = 0;
+  for (int64_t j = b + threadIdx.x; j < e; j += blockDim.x) {
+    float2 a = v[j], x = w[j];
+    sr += (double)a.x * x.x + (double)a.y * x.y;
+    si += (double)a.x * x.y - (double)a.y * x.x;
+  }
+  red[threadIdx.x] = make_double2(sr, si);
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      red[threadIdx.x].x += red[threadIdx.x + s].x;
+      red[threadIdx.x].y += red[threadIdx.x + s].y;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[(int64_t)c * nv + i] = red[0];
+}
+
+void launch_dots(const float2* V, int64_t ldv, int nv, const float2* w, int64_t n, double2* partial, int nchunks,
+                 cudaStream_t s) {
+  int64_t chunk = (n + nchunks - 1) / nchunks;
+  dim3 grid(nchunks, nv);
+  k_dots<<<grid, 256, 0, s>>>(V, ldv, nv, w, n, partial, chunk);
+}
+
+// w[n] += sign * Σ_i V_i[n] h_i
+__global__ void k_update(float2* __restrict__ w, const float2* __restrict__ V, int64_t ldv, int nv,
+                         const double2* __restrict__ h, int64_t n, double sign) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double ar = 0, ai = 0;
+  for (int i = 0; i < nv; ++i) {
+    float2 v = V[(int64_t)i * ldv + j];
+    double2 c = h[i];
+    ar += (double)v.x * c.x - (double)v.y * c.y;
+    ai += (double)v.x * c.y + (double)v.y * c.x;
+  }
+  float2 x = w[j];
+  w[j] = make_float2((float)(x.x + sign * ar), (float)(x.y + sign * ai));
+}
+void launch_update(float2* w, const float2* V, int64_t ldv, int nv, const double2* h, int64_t n, double sign,
+                   cudaStream_t s) {
+  k_update<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w, V, ldv, nv, h, n, sign);
+}
+
+__global__ void k_norm2(const float2* __restrict__ w, int64_t n, double* __restrict__ partial, int64_t chunk) {
+  __shared__ double red[256];
+  const int c = blockIdx.x;
+  const int64_t b = (int64_t)c * chunk, e = min(n, b + chunk);
+  double s = 0;
+  for (int64_t j = b + threadIdx.x; j < e; j += blockDim.x) {
+    float2 x = w[j];
+    s += (double)x.x * x.x + (double)x.y * x.y;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[c] = red[0];
+}
+void launch_norm2(const float2* w, int64_t n, double* partial, int nchunks, cudaStream_t s) {
+  int64_t chunk = (n + nchunks - 1) / nchunks;
+  k_norm2<<<nchunks, 256, 0, s>>>(w, n, partial, chunk);
+}
+
+__global__ void k_scale(float2* dst, const float2* src, double sre, double sim, int64_t n) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float2 x = src[j];
+  dst[j] = make_float2((float)(x.x * sre - x.y * sim), (float)(x.x * sim + x.y * sre));
+}
+void launch_scale(float2* dst, const float2* src, double sre, double sim, int64_t n, cudaStream_t s) {
+  k_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dst, src, sre, sim, n);
+}
+
+__global__ void k_axpby(float2* y, const float2* x, double a, double b, int64_t n) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float2 u = x[j], v = y[j];
+  y[j] = make_float2((float)(a * u.x + b * v.x), (float)(a * u.y + b * v.y));
+}
+void launch_axpby(float2* y, const float2* x, double a, double b, int64_t n, cudaStream_t s) {
+  k_axpby<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(y, x, a, b, n);
+}
+
+// b_i = e^{ik d·x_i} (1 + iαk d·n_i)   (Eq. 4 right side, ∂u/∂n = 0, reading C22)
+__global__ void k_plane_wave(const double* __restrict__ cen, const double* __restrict__ nrm,
+                             const int32_t* __restrict__ perm, int n, double k, double are, double aim, double dx,
+                             double dy, double dz, float2* b32, double2* b64) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ph = k * (dx * cen[3 * i] + dy * cen[3 * i + 1] + dz * cen[3 * i + 2]);
+  double dn = dx * nrm[3 * i] + dy * nrm[3 * i + 1] + dz * nrm[3 * i + 2];
+  double s, c;
+  sincos(ph, &s, &c);
+  // 1 + i α k dn  with α = are + i aim
+  double fr = 1.0 - aim * k * dn, fi = are * k * dn;
+  double br = c * fr - s * fi, bi = c * fi + s * fr;
+  int j = perm[i];
+  if (b32) b32[j] = make_float2((float)br, (float)bi);
+  if (b64) b64[j] = make_double2(br, bi);
+}
+void launch_plane_wave(const double* cen, const double* nrm, const int32_t* perm, int n, double k, double are,
+                       double aim, double dx, double dy, double dz, float2* b32, double2* b64, cudaStream_t s) {
+  k_plane_wave<<<(n + 255) / 256, 256, 0, s>>>(cen, nrm, perm, n, k, are, aim, dx, dy, dz, b32, b64);
+}
+
+__global__ void k_f64_to_f32(const double2* a, float2* b, int64_t n) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) b[j] = make_float2((float)a[j].x, (float)a[j].y);
+}
+__global__ void k_f32_to_f64(const float2* a, double2* b, int64_t n) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) b[j] = make_double2(a[j].x, a[j].y);
+}
+void launch_f64_to_f32(const double2* a, float2* b, int64_t n, cudaStream_t s) {
+  k_f64_to_f32<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, n);
+}
+void launch_f32_to_f64(const float2* a, double2* b, int64_t n, cudaStream_t s) {
+  k_f32_to_f64<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, n);
+}
+
+}  // namespace fda

@@ -1,0 +1,67 @@
+// Device kernels of the FDA matvec (sm_100a).  See DESIGN.md §5 for the
+// roofline of each kernel and its algorithmic bytes / evaluations per unit.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fda {
+
+// per source element, positions local to the source leaf centre:
+//   a = (q0.x, q0.y, q0.z, n.x), b = (q1.xyz, n.y), c = (q2.xyz, n.z)
+struct __align__(16) SrcElem {
+  float4 a, b, c;
+};
+
+struct KernelParams {
+  float k;          // wavenumber
+  float alpha_re;   // Burton–Miller coupling α
+  float alpha_im;
+};
+
+// one block of the grouped translation kernel: dst[op] += M · src[op] for
+// up to XT_NP ops sharing the matrix M (rows × cols, column-major)
+constexpr int XT_NP = 16;
+struct XTask {
+  int64_t mat_off;
+  int32_t rows, cols;
+  int32_t op_begin, op_count;
+};
+
+// leaf-level ops (S2M / L2T)
+struct LeafTask {
+  int64_t mat_off;   // -1: no matrix (L2T writes zeros)
+  int64_t state_off;
+  int32_t elem_begin, elem_count;
+  int32_t T;
+  int32_t pad;
+};
+
+void launch_gather_f32(const float2* x_caller, const int32_t* perm, float2* x_tree, int n, cudaStream_t s);
+void launch_gather_f64(const double2* x_caller, const int32_t* perm, float2* x_tree, int n, cudaStream_t s);
+void launch_scatter_f32(const float2* y_near, const float2* y_far, const int32_t* perm, float2* y_caller, int n,
+                        cudaStream_t s);
+void launch_scatter_f64(const float2* y_near, const float2* y_far, const int32_t* perm, double2* y_caller, int n,
+                        cudaStream_t s);
+void launch_near(int nleaf, const int32_t* leaf_begin, const int32_t* leaf_end, const int32_t* near_ptr,
+                 const int32_t* near_idx, const float4* near_off, const float4* tgt_pos, const float4* tgt_nrm,
+                 const SrcElem* src, const float* src_w, const int32_t* corr_ptr, const int32_t* corr_col,
+                 const float2* corr_val, const float2* x, float2* y, KernelParams kp, cudaStream_t s);
+void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const float2* x, float2* out, int max_rows,
+                cudaStream_t s);
+void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s);
+void launch_xlate(int ntask, const XTask* tasks, const int64_t* src_off, const int64_t* dst_off, const float2* pool,
+                  const float2* src, float2* dst, int max_rows, cudaStream_t s);
+// GMRES / BLAS-1 helpers (fp64 accumulation)
+void launch_dots(const float2* V, int64_t ldv, int nv, const float2* w, int64_t n, double2* partial, int nchunks,
+                 cudaStream_t s);
+void launch_update(float2* w, const float2* V, int64_t ldv, int nv, const double2* h, int64_t n, double sign,
+                   cudaStream_t s);
+void launch_norm2(const float2* w, int64_t n, double* partial, int nchunks, cudaStream_t s);
+void launch_scale(float2* dst, const float2* src, double sre, double sim, int64_t n, cudaStream_t s);
+void launch_axpby(float2* y, const float2* x, double a, double b, int64_t n, cudaStream_t s);  // y = a*x + b*y (real)
+void launch_plane_wave(const double* cen, const double* nrm, const int32_t* perm, int n, double k, double are,
+                       double aim, double dx, double dy, double dz, float2* b32, double2* b64, cudaStream_t s);
+void launch_f64_to_f32(const double2* a, float2* b, int64_t n, cudaStream_t s);
+void launch_f32_to_f64(const float2* a, double2* b, int64_t n, cudaStream_t s);
+
+}  // namespace fda

@@ -1,0 +1,244 @@
+// Equivalent / check clouds, truncated SVDs and the compressed translation
+// tables (host, fp64 → complex64).
+//
+// PAPER.md §3.1 and §4.1.2-§4.3:
+//   G_up = G(OUT_CHECK, OUT_EQUIV) = U Σ V^H, truncated at σ_i < ε σ_0 (C15)
+//   G_dn = G_up^T  (incoming clouds are the point reflection of the outgoing
+//                   ones, reading C12)  ⇒ U_dn = conj(V), V_dn = conj(U)
+//   S̃ = Σ̃⁻¹ Ũ^H E_up   T × n_B   per leaf
+//   M̃ = Σ̃_l⁻¹ Ũ_l^H E_up Ṽ_{l+1}  per (level, octant, direction)
+//   K̃ = Ũ_dn^H K Ṽ_up          (Eq. eq_cmpm2l) per (level, rotated offset)
+//   L̃ = Ũ_dn,l+1^H E_dn Ṽ_dn,l Σ̃_l⁻¹
+//   T̃ = E_dn Ṽ_dn Σ̃⁻¹   n_B × T   per leaf
+// Clouds (readings C12-C14): OUT_EQUIV = cube grid (p_eq per edge, side
+// 1.05 w); LF OUT_CHECK = cube grid (p_chk_lf, side 2.95 w); HF OUT_CHECK = the
+// p_chk_hf cube grid mapped onto a +z frustum, ρ(c) = d_min (d_max/d_min)^{(c+1)/2},
+// half-width ρ tan θ_w + (√3/2) w, θ_w = atan(√2/n_f), d_min = max(2w, w²/λ),
+// d_max = root diagonal; the cloud of direction u is the reference cloud
+// rotated by R_u^T (rotation invariance).
+#include <algorithm>
+#include <cmath>
+
+#include "fda_internal.h"
+
+namespace fda {
+
+static std::vector<Vec3> cube_grid(int p, double side) {
+  std::vector<Vec3> pts;
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j)
+      for (int k = 0; k < p; ++k) {
+        bool surf = i == 0 || j == 0 || k == 0 || i == p - 1 || j == p - 1 || k == p - 1;
+        if (!surf) continue;
+        auto c = [&](int t) { return -0.5 * side + side * t / (p - 1); };
+        pts.push_back({c(i), c(j), c(k)});
+      }
+  return pts;
+}
+
+static std::vector<Vec3> frustum(int p, double w, double lambda, int nf, double root_width) {
+  std::vector<Vec3> pts;
+  double dmin = std::max(2.0 * w, w * w / lambda);
+  double dmax = std::max(std::sqrt(3.0) * root_width, 2.0 * dmin);
+  double tanth = std::sqrt(2.0) / nf;
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j)
+      for (int k = 0; k < p; ++k) {
+        bool surf = i == 0 || j == 0 || k == 0 || i == p - 1 || j == p - 1 || k == p - 1;
+        if (!surf) continue;
+        double a = -1.0 + 2.0 * i / (p - 1), b = -1.0 + 2.0 * j / (p - 1), c = -1.0 + 2.0 * k / (p - 1);
+        double rho = dmin * std::pow(dmax / dmin, 0.5 * (c + 1.0));
+        double hw = rho * tanth + 0.5 * std::sqrt(3.0) * w;
+        pts.push_back({a * hw, b * hw, rho});
+      }
+  return pts;
+}
+
+void build_clouds_and_svd(const Params& p, Tree& t, const std::vector<bool>& need) {
+  for (size_t l = 0; l < t.levels.size(); ++l) {
+    Level& L = t.levels[l];
+    if (!need[l]) { L.rank = 0; continue; }
+    L.eq = cube_grid(p.opt.p_eq, p.opt.eq_scale * L.width);
+    if (L.hf) L.chk = frustum(p.opt.p_chk_hf, L.width, t.lambda, L.nf, t.root_width);
+    else L.chk = cube_grid(p.opt.p_chk_lf, p.opt.chk_scale_lf * L.width);
+    const int m = (int)L.chk.size(), n = (int)L.eq.size();
+    std::vector<cd> A((size_t)m * n);
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < m; ++i) A[(size_t)j * m + i] = G(L.chk[i], L.eq[j], p.k);
+    std::vector<double> S;
+    std::vector<cd> V;
+    svd_jacobi(m, n, A, S, V);
+    int T = 0;
+    while (T < n && S[T] >= p.eps * S[0]) ++T;
+    L.rank = T;
+    L.S.assign(S.begin(), S.begin() + T);
+    L.U.assign(A.begin(), A.begin() + (size_t)T * m);
+    L.V.assign(V.begin(), V.begin() + (size_t)T * n);
+  }
+}
+
+// frame rotation of an out-state (dir u) or in-state (dir w: frame of anti(w))
+static Mat3 out_frame(const Level& L, int dir) {
+  if (dir < 0) return rotation_to_z(Vec3(0, 0, 1));
+  return rotation_to_z(dir_center(dir, L.nf));
+}
+static Mat3 in_frame(const Level& L, int dir) {
+  if (dir < 0) return rotation_to_z(Vec3(0, 0, 1));
+  return rotation_to_z(dir_center(anti_dir(dir, L.nf), L.nf));
+}
+static Vec3 octant_offset(int o, double wc) {
+  return Vec3(((o & 1) ? 0.5 : -0.5) * wc, ((o >> 1) & 1 ? 0.5 : -0.5) * wc, ((o >> 2) & 1 ? 0.5 : -0.5) * wc);
+}
+
+static void store(Plan& plan, int64_t id, int rows, int cols, const std::vector<cd>& M) {
+  cf* dst = plan.pool.data() + plan.mats[id].offset;
+  for (size_t i = 0; i < (size_t)rows * cols; ++i) dst[i] = cf((float)M[i].real(), (float)M[i].imag());
+}
+
+void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
+  const int64_t nm = (int64_t)plan.specs.size();
+  plan.mats.resize(nm);
+  // leaf index of a leaf box
+  std::vector<int64_t> leaf_of_box(t.boxes.size(), -1);
+  for (size_t i = 0; i < plan.leaf_box.size(); ++i) leaf_of_box[plan.leaf_box[i]] = (int64_t)i;
+  int64_t off = 0;
+  for (int64_t id = 0; id < nm; ++id) {
+    const MatSpec& s = plan.specs[id];
+    int rows = 0, cols = 0;
+    switch (s.kind) {
+      case MK_S2M: {
+        const Box& B = t.boxes[s.leaf];
+        rows = t.levels[s.level].rank; cols = (int)(B.end - B.begin);
+      } break;
+      case MK_L2T: {
+        const Box& B = t.boxes[s.leaf];
+        rows = (int)(B.end - B.begin); cols = t.levels[s.level].rank;
+      } break;
+      case MK_M2M: rows = t.levels[s.level].rank; cols = t.levels[s.level + 1].rank; break;
+      case MK_L2L: rows = t.levels[s.level + 1].rank; cols = t.levels[s.level].rank; break;
+      case MK_M2L: rows = cols = t.levels[s.level].rank; break;
+    }
+    plan.mats[id] = {off, rows, cols};
+    off += (int64_t)rows * cols;
+  }
+  plan.pool.assign(off, cf(0, 0));
+
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t id = 0; id < nm; ++id) {
+    const MatSpec& s = plan.specs[id];
+    const Level& L = t.levels[s.level];
+    const int m = (int)L.chk.size(), n = (int)L.eq.size(), T = L.rank;
+    std::vector<cd> E, X, M;
+    switch (s.kind) {
+      case MK_S2M: {
+        // E_up[c, j] = Σ_q (A_j/3) ∂G/∂n_y(chk_c, y_jq)   (Eq. 10)
+        const Box& B = t.boxes[s.leaf];
+        const int nb = (int)(B.end - B.begin);
+        E.resize((size_t)m * nb);
+        for (int j = 0; j < nb; ++j) {
+          const int64_t e = B.begin + j;
+          for (int c = 0; c < m; ++c) {
+            Vec3 xc = B.center + L.chk[c];
+            cd acc = 0.0;
+            for (int q = 0; q < 3; ++q) {
+              Vec3 y = g.v0[e] * Q3_BARY[q][0] + g.v1[e] * Q3_BARY[q][1] + g.v2[e] * Q3_BARY[q][2];
+              acc += dGdny(xc, y, g.normal[e], p.k);
+            }
+            E[(size_t)j * m + c] = acc * (g.area[e] / 3.0);
+          }
+        }
+        M.resize((size_t)T * nb);
+        zgemm_cm(T, nb, m, L.U.data(), m, E.data(), m, M.data(), T, true);
+        for (int j = 0; j < nb; ++j)
+          for (int r = 0; r < T; ++r) M[(size_t)j * T + r] /= L.S[r];
+        store(plan, id, T, nb, M);
+      } break;
+      case MK_L2T: {
+        // E_dn[i, j] = G(x_i, y_j) + α ∂G/∂n_x(x_i, y_j), y_j = IN_EQUIV = c_B - chk_j  (Eq. 12)
+        const Box& B = t.boxes[s.leaf];
+        const int nb = (int)(B.end - B.begin);
+        E.resize((size_t)nb * m);
+        for (int j = 0; j < m; ++j) {
+          Vec3 y = B.center - L.chk[j];
+          for (int i = 0; i < nb; ++i) {
+            const int64_t e = B.begin + i;
+            E[(size_t)j * nb + i] = G(g.centroid[e], y, p.k) + p.alpha * dGdnx(g.centroid[e], g.normal[e], y, p.k);
+          }
+        }
+        // T̃ = E_dn conj(U) Σ̃⁻¹
+        std::vector<cd> Uc(L.U.size());
+        for (size_t i = 0; i < Uc.size(); ++i) Uc[i] = std::conj(L.U[i]);
+        M.resize((size_t)nb * T);
+        zgemm_cm(nb, T, m, E.data(), nb, Uc.data(), m, M.data(), nb, false);
+        for (int c = 0; c < T; ++c)
+          for (int i = 0; i < nb; ++i) M[(size_t)c * nb + i] /= L.S[c];
+        store(plan, id, nb, T, M);
+      } break;
+      case MK_M2M: {
+        const Level& Lc = t.levels[s.level + 1];
+        const int nc = (int)Lc.eq.size(), Tc = Lc.rank;
+        Mat3 Rp = out_frame(L, s.dir);
+        int cdir = (Lc.hf && s.dir >= 0) ? child_dir(s.dir, L.nf) : -1;
+        Mat3 Rc = out_frame(Lc, cdir);
+        Vec3 oc = octant_offset(s.octant, Lc.width);
+        E.resize((size_t)m * nc);
+        for (int j = 0; j < nc; ++j) {
+          Vec3 y = oc + Rc.apply_t(Lc.eq[j]);
+          for (int i = 0; i < m; ++i) E[(size_t)j * m + i] = G(Rp.apply_t(L.chk[i]), y, p.k);
+        }
+        X.resize((size_t)m * Tc);
+        zgemm_cm(m, Tc, nc, E.data(), m, Lc.V.data(), nc, X.data(), m, false);
+        M.resize((size_t)T * Tc);
+        zgemm_cm(T, Tc, m, L.U.data(), m, X.data(), m, M.data(), T, true);
+        for (int j = 0; j < Tc; ++j)
+          for (int r = 0; r < T; ++r) M[(size_t)j * T + r] /= L.S[r];
+        store(plan, id, T, Tc, M);
+      } break;
+      case MK_L2L: {
+        const Level& Lc = t.levels[s.level + 1];
+        const int nc = (int)Lc.eq.size(), Tc = Lc.rank;
+        Mat3 Qp = in_frame(L, s.dir);
+        int cdir = (Lc.hf && s.dir >= 0) ? child_dir(s.dir, L.nf) : -1;
+        Mat3 Qc = in_frame(Lc, cdir);
+        Vec3 oc = octant_offset(s.octant, Lc.width);
+        // E_dn[i, j] = G(child IN_CHECK_i, parent IN_EQUIV_j)
+        E.resize((size_t)nc * m);
+        for (int j = 0; j < m; ++j) {
+          Vec3 y = Qp.apply_t(-L.chk[j]);
+          for (int i = 0; i < nc; ++i) E[(size_t)j * nc + i] = G(oc + Qc.apply_t(-Lc.eq[i]), y, p.k);
+        }
+        std::vector<cd> Uc(L.U.size());
+        for (size_t i = 0; i < Uc.size(); ++i) Uc[i] = std::conj(L.U[i]);
+        X.resize((size_t)nc * T);
+        zgemm_cm(nc, T, m, E.data(), nc, Uc.data(), m, X.data(), nc, false);
+        for (int c = 0; c < T; ++c)
+          for (int i = 0; i < nc; ++i) X[(size_t)c * nc + i] /= L.S[c];
+        // L̃ = V_c^T X  = (conj V_c)^H X
+        std::vector<cd> Vcc(Lc.V.size());
+        for (size_t i = 0; i < Vcc.size(); ++i) Vcc[i] = std::conj(Lc.V[i]);
+        M.resize((size_t)Tc * T);
+        zgemm_cm(Tc, T, nc, Vcc.data(), nc, X.data(), nc, M.data(), Tc, true);
+        store(plan, id, Tc, T, M);
+      } break;
+      case MK_M2L: {
+        // K[i, j] = G(IN_CHECK(D)_i, OUT_EQUIV(C)_j) with both clouds in the frame R_u
+        Mat3 R = out_frame(L, s.dir);
+        Vec3 d((double)s.dx * L.width, (double)s.dy * L.width, (double)s.dz * L.width);
+        E.resize((size_t)n * n);
+        for (int j = 0; j < n; ++j) {
+          Vec3 y = R.apply_t(L.eq[j]);
+          for (int i = 0; i < n; ++i) E[(size_t)j * n + i] = G(d + R.apply_t(-L.eq[i]), y, p.k);
+        }
+        X.resize((size_t)n * T);
+        zgemm_cm(n, T, n, E.data(), n, L.V.data(), n, X.data(), n, false);
+        std::vector<cd> Vc(L.V.size());
+        for (size_t i = 0; i < Vc.size(); ++i) Vc[i] = std::conj(L.V[i]);
+        M.resize((size_t)T * T);
+        zgemm_cm(T, T, n, Vc.data(), n, X.data(), n, M.data(), T, true);  // V^T (K V)
+        store(plan, id, T, T, M);
+      } break;
+    }
+  }
+}
+
+}  // namespace fda
