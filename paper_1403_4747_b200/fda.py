@@ -161,6 +161,15 @@ class FDA:
     def matvec(self, x, y=None, stream=None):
         """y = A x.  numpy complex128 → numpy complex128 (host path), or torch
         complex64 CUDA tensors (device path, asynchronous on ``stream``)."""
+        if _is_torch(x) and not x.is_cuda:
+            # host tensors (e.g. pinned complex128): host path with raw pointers
+            import torch
+            if not (x.dtype == torch.complex128 and x.is_contiguous() and x.numel() == self.n):
+                raise ValueError("host x must be a contiguous complex128 tensor of length n")
+            if y is None:
+                y = torch.empty_like(x)
+            self._check(self.lib.fda_matvec(self.ctx, x.data_ptr(), y.data_ptr(), FDA_HOST, None))
+            return y
         if _is_torch(x):
             import torch
             if not (x.is_cuda and x.dtype == torch.complex64 and x.is_contiguous() and x.numel() == self.n):

@@ -1,0 +1,171 @@
+"""GPU parity: the CUDA FDA matvec (through the C ABI) vs the fp64 oracle.
+
+Gate (BASELINE north_star): matvec relative L2 ≤ 1e-3 at ε = 1e-4; solved
+surface potential ≤ 2e-3.  The exact path (direct_all: every pair through the
+near kernel + corrections) must agree to fp32 rounding (≤ 2e-6).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from oracle import fast
+from fda_inputs import icosphere, octasphere, config_mesh, CONFIGS, random_density, sampled_rows
+
+pytestmark = pytest.mark.gpu
+
+MATVEC_TOL = 1e-3
+EXACT_TOL = 2e-6
+SOLVE_TOL = 2e-3
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1403_4747_b200 import FDA, load_library
+    load_library()
+    return FDA
+
+
+@pytest.fixture(scope="module")
+def cfg1(lib):
+    V, F = config_mesh(1)
+    c = CONFIGS[1]
+    el = O.element_geometry(V, F)
+    A = fast.dense(el, c.k, c.alpha, "lhs")
+    f = lib(V, F, c.k, c.alpha, 1e-4)
+    return V, F, c, el, A, f
+
+
+def test_config1_matvec_parity(cfg1):
+    V, F, c, el, A, f = cfg1
+    x = random_density(len(F), c.x_seed)
+    y = f.matvec(x)
+    yo = A @ x
+    err = _rel(y, yo)
+    print(f"config1 matvec rel-L2 = {err:.3e}")
+    assert err <= MATVEC_TOL
+    # element-wise: no single row is off by more than a few times the gate
+    row_err = np.abs(y - yo) / np.maximum(np.abs(yo), np.linalg.norm(yo) / np.sqrt(len(F)))
+    assert row_err.max() < 20 * MATVEC_TOL
+
+
+def test_device_path_equals_host_path(cfg1):
+    import torch
+    V, F, c, el, A, f = cfg1
+    x = random_density(len(F), 77)
+    yh = f.matvec(x)
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda()
+    yd = f.matvec(xd)
+    torch.cuda.synchronize()
+    assert _rel(yd.cpu().numpy().astype(np.complex128), yh) < 1e-6
+
+
+def test_linearity_and_zero(cfg1):
+    V, F, c, el, A, f = cfg1
+    z = f.matvec(np.zeros(len(F), complex))
+    assert np.all(z == 0)
+    x1, x2 = random_density(len(F), 1), random_density(len(F), 2)
+    a, b = 0.3 - 1.1j, 2.0 + 0.5j
+    lhs = f.matvec(a * x1 + b * x2)
+    rhs = a * f.matvec(x1) + b * f.matvec(x2)
+    assert _rel(lhs, rhs) < 1e-5
+
+
+def test_direct_all_exact_operator(lib, cfg1):
+    """Every pair through the near kernel (Q3) + the correction table: the
+    same operator as the oracle up to fp32 rounding (3.9e-7)."""
+    V, F, c, el, A, _ = cfg1
+    f = lib(V, F, c.k, c.alpha, 1e-4, direct_all=1)
+    x = random_density(len(F), c.x_seed)
+    err = _rel(f.matvec(x), A @ x)
+    print(f"config1 exact-path rel-L2 = {err:.3e}")
+    assert err <= EXACT_TOL
+
+
+@pytest.mark.parametrize("mesh,k,ml", [("ico0", 2.0, 64), ("octa0", 1.0, 64), ("ico2", 10.0, 7),
+                                       ("ico3", 25.0, 5), ("octa3", np.pi, 64)])
+def test_small_and_ragged_meshes(lib, mesh, k, ml):
+    """Edge cases: a single leaf (20 / 8 elements, all direct), ragged leaves
+    (max_leaf 5 / 7), the paper's octahedral N=512 mesh."""
+    V, F = {"ico0": lambda: icosphere(0, 0.5), "octa0": lambda: octasphere(0, 1.0),
+            "ico2": lambda: icosphere(2, 0.5), "ico3": lambda: icosphere(3, 0.5),
+            "octa3": lambda: octasphere(3, 1.0)}[mesh]()
+    el = O.element_geometry(V, F)
+    f = lib(V, F, k, 1j / k, 1e-4, max_leaf=ml)
+    x = random_density(len(F), 5)
+    yo = fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k)
+    err = _rel(f.matvec(x), yo)
+    print(f"{mesh} k={k} leaf={ml}: rel-L2 {err:.3e}")
+    assert err <= MATVEC_TOL
+
+
+def test_hf_small_parity(lib):
+    """Three HF levels (384/96/24 wedges), 5,120 elements, kD = 40."""
+    V, F = icosphere(4, 0.5)
+    k = 40.0
+    f = lib(V, F, k, 1j / k, 1e-4, max_leaf=16)
+    assert f.stats()["n_hf_levels"] >= 3
+    el = O.element_geometry(V, F)
+    x = random_density(len(F), 9)
+    yo = fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k)
+    err = _rel(f.matvec(x), yo)
+    print(f"HF small rel-L2 = {err:.3e}")
+    assert err <= MATVEC_TOL
+
+
+def test_config2_sampled_rows(lib):
+    """Config 2 (the bench workload, same build options as bench.py):
+    N = 81,920, kD = 50, one HF level; 2,000 seeded rows of the oracle."""
+    V, F = config_mesh(2)
+    c = CONFIGS[2]
+    f = lib(V, F, c.k, c.alpha, c.eps)
+    x = random_density(len(F), c.x_seed)
+    y = f.matvec(x)
+    rows = sampled_rows(len(F), 2000, c.rows_seed)
+    el = O.element_geometry(V, F)
+    yo = fast.matvec_rows(el, rows, x, c.k, c.alpha)
+    err = _rel(y[rows], yo)
+    print(f"config2 sampled-row rel-L2 = {err:.3e}; stats {f.stats()['n_m2l_pairs']} M2L pairs")
+    assert err <= MATVEC_TOL
+
+
+def test_plane_wave_rhs(cfg1):
+    V, F, c, el, A, f = cfg1
+    b = f.rhs_plane_wave(c.direction)
+    bo = O.plane_wave_rhs(el.centroid, el.normal, c.k, c.alpha, c.direction)
+    assert _rel(b, bo) < 1e-6
+
+
+def test_bm_solve_config1(cfg1):
+    """GMRES on the FDA operator (tol 1e-4) vs the dense LU solution of the
+    oracle system; and the rigid-sphere series as a discretisation sanity
+    check (6.1e-3)."""
+    V, F, c, el, A, f = cfg1
+    b = O.plane_wave_rhs(el.centroid, el.normal, c.k, c.alpha, c.direction)
+    u_ref = O.lu_solve(A, b)
+    u, info = f.solve(b, tol=c.gmres_tol, max_iter=100)
+    err = _rel(u, u_ref)
+    print(f"config1 solve: {info}, rel-L2 vs dense LU {err:.3e}")
+    assert info["converged"] and info["iterations"] < 60
+    assert err <= SOLVE_TOL
+    assert info["true_residual"] < 5 * c.gmres_tol
+    ser = O.rigid_sphere_total(el.centroid, c.k, 0.5, c.direction)
+    assert _rel(u, ser) < 1.5e-2
+    # restarted GMRES reaches the same solution
+    u2, info2 = f.solve(b, tol=c.gmres_tol, max_iter=200, restart=10)
+    assert info2["converged"] and _rel(u2, u_ref) <= SOLVE_TOL
+
+
+def test_stage_times(cfg1):
+    V, F, c, el, A, f = cfg1
+    f.set_profiling(True)
+    f.matvec(random_density(len(F), 3))
+    t = f.stage_times()
+    f.set_profiling(False)
+    assert set(t) == {"gather", "near", "s2m", "m2m", "m2l", "l2l", "l2t", "scatter"}
+    assert all(v >= 0 for v in t.values()) and t["near"] > 0

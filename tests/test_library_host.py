@@ -1,0 +1,167 @@
+"""Host-logic tests of libfda.so (no GPU): the C ABI loads and exports every
+symbol of include/fda.h, argument/mesh errors, tree/list/direction
+invariants (readings C7-C11, C18), and the host build tables reproduce the
+oracle when applied in complex128 (tests/host_exec.py)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+from oracle import fast
+from fda_inputs import icosphere, octasphere, config_mesh, CONFIGS, random_density
+from paper_1403_4747_b200 import FDA, FdaError, EXPORTS, load_library
+from paper_1403_4747_b200.build import build as build_lib
+from host_exec import apply_tables
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    build_lib()
+    return load_library()
+
+
+def test_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "fda.h")).read()
+    declared = set(re.findall(r"^\s*(?:fda_status|const char\*|void)\s+(\w+)\(", hdr, re.M))
+    assert declared == set(EXPORTS), declared ^ set(EXPORTS)
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_1403_4747_b200", "libfda.so"))
+    for name in declared:
+        assert hasattr(lib, name), name
+
+
+def test_argument_and_mesh_errors():
+    V, F = icosphere(1, 0.5)
+    with pytest.raises(FdaError) as e:
+        FDA(V, F, -1.0, 1j, 1e-4, device=-1)
+    assert e.value.status == 1
+    with pytest.raises(FdaError) as e:
+        FDA(V, F, 1.0, 1j, 0.5, device=-1)
+    assert e.value.status == 1
+    with pytest.raises(FdaError) as e:
+        FDA(V, F, 1.0, 0.0, 1e-4, device=-1)          # Im α = 0
+    assert e.value.status == 1
+    with pytest.raises(FdaError) as e:
+        FDA(V, F[:-1], 1.0, 1j, 1e-4, device=-1)      # open mesh
+    assert e.value.status == 2
+    with pytest.raises(FdaError) as e:
+        FDA(V, F[:, ::-1], 1.0, 1j, 1e-4, device=-1)  # inward orientation
+    assert e.value.status == 2
+    F2 = F.copy()
+    F2[0, 1] = F2[0, 0]
+    with pytest.raises(FdaError) as e:
+        FDA(V, F2, 1.0, 1j, 1e-4, device=-1)
+    assert e.value.status == 2
+    F3 = F.copy()
+    F3[0, 0] = len(V) + 5
+    with pytest.raises(FdaError) as e:
+        FDA(V, F3, 1.0, 1j, 1e-4, device=-1)
+    assert e.value.status == 1
+
+
+def test_host_only_context_refuses_matvec():
+    V, F = icosphere(1, 0.5)
+    f = FDA(V, F, 3.0, 1j / 3, 1e-4, device=-1)
+    with pytest.raises(FdaError) as e:
+        f.matvec(np.zeros(len(F), complex))
+    assert e.value.status == 7
+
+
+def test_config1_tree_and_list_counts():
+    """272 leaves, 14,432 M2L pairs, 1.457e6
+    direct element pairs; ≈74 corrections per row (A.7)."""
+    V, F = config_mesh(1)
+    c = CONFIGS[1]
+    f = FDA(V, F, c.k, c.alpha, 1e-4, device=-1)
+    s = f.stats()
+    assert s["n_leaves"] == 272
+    assert s["n_m2l_pairs"] == 14432
+    assert abs(s["n_direct_element_pairs"] / 1.457e6 - 1) < 0.01
+    assert 70 < s["n_corrections"] / len(F) < 78
+
+
+def _coverage(f):
+    """Brute-force pair coverage: for every ordered element pair, the number
+    of M2L pairs between ancestors plus direct leaf pairs containing it."""
+    n = f.n
+    boxes = f.table("boxes").reshape(-1, 8)
+    lr = f.table("leaf_range").reshape(-1, 2)
+    cov = np.zeros((n, n), dtype=np.int32)
+    nptr, nidx = f.table("near_ptr"), f.table("near_idx")
+    for i in range(lr.shape[0]):
+        for j in nidx[nptr[i]:nptr[i + 1]]:
+            cov[lr[i, 0]:lr[i, 1], lr[j, 0]:lr[j, 1]] += 1
+    outs = f.table("out_states").reshape(-1, 2)
+    ins = f.table("in_states").reshape(-1, 2)
+    for (_, s, d, _) in f.table("m2l").reshape(-1, 4):
+        C, B = boxes[outs[s, 0]], boxes[ins[d, 0]]
+        cov[B[5]:B[6], C[5]:C[6]] += 1
+    return cov
+
+
+@pytest.mark.parametrize("s,k,ml", [(3, 60.0, 8), (3, 120.0, 4), (2, 10.0, 4)])
+def test_pair_coverage_exact(s, k, ml):
+    """Every ordered element pair is covered exactly once (reading C11;
+    SURVEY A.13)."""
+    V, F = icosphere(s, 0.5)
+    f = FDA(V, F, k, 1j / k, 1e-3, device=-1, max_leaf=ml)
+    assert (_coverage(f) == 1).all()
+
+
+def test_direct_all_covers_everything_directly():
+    V, F = icosphere(2, 0.5)
+    f = FDA(V, F, 10.0, 0.1j, 1e-4, device=-1, direct_all=1, max_leaf=8)
+    assert f.stats()["n_m2l_pairs"] == 0
+    assert (_coverage(f) == 1).all()
+
+
+def test_config1_tables_match_oracle():
+    """LF-only FDA (config 1 is pure kernel-independent FMM, SURVEY §0.1 item
+    6) applied from the exported tables vs the dense oracle."""
+    V, F = config_mesh(1)
+    c = CONFIGS[1]
+    f = FDA(V, F, c.k, c.alpha, 1e-4, device=-1)
+    x = random_density(len(F), c.x_seed)
+    y = apply_tables(f, x)
+    el = O.element_geometry(V, F)
+    yo = fast.matvec_rows(el, np.arange(len(F)), x, c.k, c.alpha)
+    assert np.linalg.norm(y - yo) / np.linalg.norm(yo) < 1e-4
+    # direct path alone (near + corrections, no far field) is NOT the operator
+    yn = apply_tables(f, x, far=False)
+    assert np.linalg.norm(yn - yo) / np.linalg.norm(yo) > 1e-3
+
+
+def test_hf_tables_match_oracle():
+    """Three HF levels (384/96/24 wedges) on a 5,120-element sphere, kD = 40."""
+    V, F = icosphere(4, 0.5)
+    k = 40.0
+    f = FDA(V, F, k, 1j / k, 1e-4, device=-1, max_leaf=16)
+    s = f.stats()
+    assert s["n_hf_levels"] >= 3 and s["dirs"][:3] == [384, 96, 24]
+    x = random_density(len(F), 11)
+    y = apply_tables(f, x)
+    el = O.element_geometry(V, F)
+    rows = np.arange(0, len(F), 3)
+    yo = fast.matvec_rows(el, rows, x, k, 1j / k)
+    err = np.linalg.norm(y[rows] - yo) / np.linalg.norm(yo)
+    assert err < 1e-3, err
+
+
+def test_eps_convergence():
+    """FDA error falls with ε (the invariant of BASELINE north_star): the
+    tables at ε = 1e-2, 1e-3, 1e-4 give decreasing errors."""
+    V, F = icosphere(3, 0.5)
+    k = 30.0
+    el = O.element_geometry(V, F)
+    x = random_density(len(F), 3)
+    yo = fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k)
+    errs = []
+    for eps in (1e-2, 1e-3, 1e-4):
+        f = FDA(V, F, k, 1j / k, eps, device=-1, max_leaf=8)
+        y = apply_tables(f, x)
+        errs.append(np.linalg.norm(y - yo) / np.linalg.norm(yo))
+    assert errs[0] > errs[1] > errs[2] and errs[2] < 1e-3, errs
