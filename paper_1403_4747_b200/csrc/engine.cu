@@ -29,11 +29,10 @@ namespace fda {
   } while (0)
 
 struct XStage {
-  XTask* tasks = nullptr;
+  XTask* tasks[XV] = {};
+  int ntask[XV] = {};
   int64_t* src = nullptr;
   int64_t* dst = nullptr;
-  int ntask = 0;
-  int max_rows = 0;
 };
 
 struct Dev {
@@ -48,6 +47,8 @@ struct Dev {
   SrcElem* src = nullptr;
   float* src_w = nullptr;
   int32_t *leaf_begin = nullptr, *leaf_end = nullptr, *near_ptr = nullptr, *near_idx = nullptr;
+  int32_t* near_order = nullptr;   // leaves by descending near-field work (LPT block order)
+  bool alpha_pure_imag = false;
   float4* near_off = nullptr;
   int32_t *corr_ptr = nullptr, *corr_col = nullptr;
   float2* corr_val = nullptr;
@@ -56,7 +57,11 @@ struct Dev {
   int64_t out_size = 0, in_size = 0;
   LeafTask *s2m = nullptr, *l2t = nullptr;
   int n_s2m = 0, n_l2t = 0, max_T = 0;
-  std::vector<XStage> m2m, m2l, l2l;
+  std::vector<XStage> m2m, l2l;
+  XStage m2l;                      // all levels at once (M2L levels are independent)
+  cudaStream_t s_cap = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  bool use_graph = false;
   float2 *x_tree = nullptr, *y_near = nullptr, *y_far = nullptr;
   double2 *xh = nullptr, *yh = nullptr;
   double *cen = nullptr, *nrm = nullptr;
@@ -90,40 +95,90 @@ static fda_status alloc(Context* ctx, Dev* d, T** dst, size_t count) {
     if (s_ != FDA_OK) return s_;               \
   } while (0)
 
+// Group the ops of one stage (one level, or all M2L levels at once) by matrix
+// and cut each group into tiles of the kernel variant (rows × ops per CTA)
+// that pads the group least.  Stages with fewer CTAs than ~4 waves are split
+// along K (cols) so that small, latency-bound stages still fill the GPU.
 static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<Op>& ops, const std::vector<int64_t>& src_off,
                                const std::vector<int64_t>& dst_off, XStage& st) {
   const Plan& p = ctx->plan;
   if (ops.empty()) return FDA_OK;
   std::vector<size_t> ord(ops.size());
   for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
-  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return ops[a].mat < ops[b].mat; });
+  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+    return ops[a].mat != ops[b].mat ? ops[a].mat < ops[b].mat : ops[a].dst < ops[b].dst;
+  });
   std::vector<int64_t> so, dof;
-  std::vector<XTask> tasks;
+  std::vector<XTask> tasks[XV];
   size_t i = 0;
   while (i < ord.size()) {
     const int64_t m = ops[ord[i]].mat;
     size_t j = i;
-    while (j < ord.size() && ops[ord[j]].mat == m && j - i < (size_t)XT_NP) ++j;
-    XTask t;
-    t.mat_off = p.mats[m].offset;
-    t.rows = p.mats[m].rows;
-    t.cols = p.mats[m].cols;
-    t.op_begin = (int32_t)so.size();
-    t.op_count = (int32_t)(j - i);
+    while (j < ord.size() && ops[ord[j]].mat == m) ++j;
+    const int rows = p.mats[m].rows, cols = p.mats[m].cols;
+    const int64_t nops = (int64_t)(j - i);
+    int best = 1;
+    int64_t best_cost = -1;
+    for (int v = 0; v < XV; ++v) {
+      const int64_t R = xvar_rows(v), O = xvar_ops(v);
+      const int64_t cost = ((rows + R - 1) / R) * R * ((nops + O - 1) / O) * O;
+      if (best_cost < 0 || cost < best_cost) { best = v; best_cost = cost; }
+    }
+    const int R = xvar_rows(best), O = xvar_ops(best);
+    const int32_t base = (int32_t)so.size();
     for (size_t q = i; q < j; ++q) {
       so.push_back(src_off[ops[ord[q]].src]);
       dof.push_back(dst_off[ops[ord[q]].dst]);
     }
-    st.max_rows = std::max(st.max_rows, t.rows);
-    if (t.cols > 320) { ctx->err = "translation matrix wider than 320 columns"; return FDA_E_INTERNAL; }
-    tasks.push_back(t);
+    for (int64_t c0 = 0; c0 < nops; c0 += O)
+      for (int r0 = 0; r0 < rows; r0 += R) {
+        XTask t;
+        t.mat_off = p.mats[m].offset;
+        t.rows = rows;
+        t.cols = cols;
+        t.row0 = r0;
+        t.op_begin = base + (int32_t)c0;
+        t.op_count = (int32_t)std::min<int64_t>(O, nops - c0);
+        t.k_begin = 0;
+        t.k_end = cols;
+        t.pad = 0;
+        tasks[best].push_back(t);
+      }
     i = j;
   }
-  st.ntask = (int)tasks.size();
-  UP(&st.tasks, tasks.data(), tasks.size());
+  int64_t total = 0;
+  for (int v = 0; v < XV; ++v) total += (int64_t)tasks[v].size();
+  const int64_t target = 4 * 148 * 4;  // ≈ 4 waves of 4 resident CTAs per SM
+  if (total < target) {
+    const int64_t split = (target + total - 1) / total;
+    for (int v = 0; v < XV; ++v) {
+      std::vector<XTask> out;
+      for (const XTask& t : tasks[v]) {
+        const int nk = (t.cols + XK - 1) / XK;
+        const int sp = (int)std::min<int64_t>(split, nk);
+        const int per = (nk + sp - 1) / sp;
+        for (int c = 0; c < nk; c += per) {
+          XTask u = t;
+          u.k_begin = c * XK;
+          u.k_end = std::min(t.cols, (c + per) * XK);
+          out.push_back(u);
+        }
+      }
+      tasks[v].swap(out);
+    }
+  }
+  for (int v = 0; v < XV; ++v) {
+    st.ntask[v] = (int)tasks[v].size();
+    if (st.ntask[v]) UP(&st.tasks[v], tasks[v].data(), tasks[v].size());
+  }
   UP(&st.src, so.data(), so.size());
   UP(&st.dst, dof.data(), dof.size());
   return FDA_OK;
+}
+
+static void launch_stage(const XStage& st, const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
+  for (int v = 0; v < XV; ++v)
+    if (st.ntask[v]) launch_xlate(v, st.ntask[v], st.tasks[v], st.src, st.dst, pool, src, dst, s);
 }
 
 fda_status engine_create(Context* ctx) {
@@ -194,6 +249,21 @@ fda_status engine_create(Context* ctx) {
     return FDA_E_INTERNAL;
   }
   std::vector<int32_t> cptr(p.corr_ptr.begin(), p.corr_ptr.end()), ccol(p.corr_col.begin(), p.corr_col.end());
+  // LPT order of the near-field CTAs: estimated work = targets × (3·sources + corrections)
+  std::vector<int64_t> work(nleaf, 0);
+  for (int i = 0; i < nleaf; ++i) {
+    const Box& B = t.boxes[t.leaves[i]];
+    int64_t srcs = 0;
+    for (int64_t e = p.near_ptr[i]; e < p.near_ptr[i + 1]; ++e) {
+      const Box& C = t.boxes[t.leaves[p.near_idx[e]]];
+      srcs += C.end - C.begin;
+    }
+    work[i] = (B.end - B.begin) * 3 * srcs + (p.corr_ptr[B.end] - p.corr_ptr[B.begin]);
+  }
+  std::vector<int32_t> order(nleaf);
+  for (int i = 0; i < nleaf; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
+  d->alpha_pure_imag = ctx->p.alpha.real() == 0.0;
 
   UP(&d->perm, perm.data(), perm.size());
   UP(&d->tgt_pos, tpos.data(), tpos.size());
@@ -204,6 +274,7 @@ fda_status engine_create(Context* ctx) {
   UP(&d->leaf_end, le.data(), le.size());
   UP(&d->near_ptr, nptr.data(), nptr.size());
   UP(&d->near_idx, nidx.data(), nidx.size());
+  UP(&d->near_order, order.data(), order.size());
   UP(&d->near_off, noff.data(), noff.size());
   UP(&d->corr_ptr, cptr.data(), cptr.size());
   UP(&d->corr_col, ccol.data(), ccol.size());
@@ -247,14 +318,21 @@ fda_status engine_create(Context* ctx) {
   UP(&d->l2t, l2t.data(), l2t.size());
 
   const int nlev = (int)t.levels.size();
-  d->m2m.resize(nlev); d->m2l.resize(nlev); d->l2l.resize(nlev);
+  d->m2m.resize(nlev); d->l2l.resize(nlev);
+  std::vector<Op> all_m2l;
   for (int l = 0; l < nlev; ++l) {
     fda_status s;
     if ((s = build_xstage(ctx, d, p.m2m[l], p.out_offset, p.out_offset, d->m2m[l])) != FDA_OK) return s;
-    if ((s = build_xstage(ctx, d, p.m2l[l], p.out_offset, p.in_offset, d->m2l[l])) != FDA_OK) return s;
     if ((s = build_xstage(ctx, d, p.l2l[l], p.in_offset, p.in_offset, d->l2l[l])) != FDA_OK) return s;
+    all_m2l.insert(all_m2l.end(), p.m2l[l].begin(), p.m2l[l].end());
+  }
+  {
+    fda_status s;
+    if ((s = build_xstage(ctx, d, all_m2l, p.out_offset, p.in_offset, d->m2l)) != FDA_OK) return s;
   }
   CK(cudaStreamCreateWithFlags(&d->s_near, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&d->s_cap, cudaStreamNonBlocking));
+  d->use_graph = ctx->p.opt.use_graph != 0;
   CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
   for (auto& e : d->ev) CK(cudaEventCreate(&e));
@@ -270,7 +348,9 @@ void engine_destroy(Context* ctx) {
   cudaSetDevice(d->device);
   cudaDeviceSynchronize();
   for (void* a : d->allocs) cudaFree(a);
+  if (d->graph_exec) cudaGraphExecDestroy(d->graph_exec);
   if (d->s_near) cudaStreamDestroy(d->s_near);
+  if (d->s_cap) cudaStreamDestroy(d->s_cap);
   if (d->ev_fork) cudaEventDestroy(d->ev_fork);
   if (d->ev_join) cudaEventDestroy(d->ev_join);
   for (auto& e : d->ev) if (e) cudaEventDestroy(e);
@@ -282,15 +362,20 @@ void engine_destroy(Context* ctx) {
 
 // the device part of one matvec: x_tree → y_near, y_far (tree order)
 static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s) {
+  // profiling mode serialises the near field on the main stream so that every
+  // stage time is the isolated duration of its kernels
   const bool prof = ctx->profiling;
+  cudaStream_t sn = prof ? s : d->s_near;
   CK(cudaEventRecord(d->ev_fork, s));
-  CK(cudaStreamWaitEvent(d->s_near, d->ev_fork, 0));
-  if (prof) CK(cudaEventRecord(d->ev_n0, d->s_near));
-  launch_near(d->nleaf, d->leaf_begin, d->leaf_end, d->near_ptr, d->near_idx, d->near_off, d->tgt_pos, d->tgt_nrm,
-              d->src, d->src_w, d->corr_ptr, d->corr_col, d->corr_val, d->x_tree, d->y_near, d->kp, d->s_near);
-  if (prof) CK(cudaEventRecord(d->ev_n1, d->s_near));
-  CK(cudaEventRecord(d->ev_join, d->s_near));
+  CK(cudaStreamWaitEvent(sn, d->ev_fork, 0));
+  if (prof) CK(cudaEventRecord(d->ev_n0, sn));
+  launch_near(d->nleaf, d->near_order, d->leaf_begin, d->leaf_end, d->near_ptr, d->near_idx, d->near_off,
+              d->tgt_pos, d->tgt_nrm, d->src, d->src_w, d->corr_ptr, d->corr_col, d->corr_val, d->x_tree, d->y_near,
+              d->kp, d->alpha_pure_imag, sn);
+  if (prof) CK(cudaEventRecord(d->ev_n1, sn));
+  CK(cudaEventRecord(d->ev_join, sn));
 
+  if (prof) CK(cudaEventRecord(d->ev[1], s));
   if (d->out_size) CK(cudaMemsetAsync(d->outb, 0, sizeof(float2) * d->out_size, s));
   if (d->in_size) CK(cudaMemsetAsync(d->inb, 0, sizeof(float2) * d->in_size, s));
   launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s);
@@ -298,17 +383,14 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s) {
   const int nlev = (int)d->m2m.size();
   for (int l = nlev - 1; l >= 0; --l) {
     const XStage& st = d->m2m[l];
-    launch_xlate(st.ntask, st.tasks, st.src, st.dst, d->pool, d->outb, d->outb, st.max_rows, s);
+    launch_stage(st, d->pool, d->outb, d->outb, s);
   }
   if (prof) CK(cudaEventRecord(d->ev[3], s));
-  for (int l = 0; l < nlev; ++l) {
-    const XStage& st = d->m2l[l];
-    launch_xlate(st.ntask, st.tasks, st.src, st.dst, d->pool, d->outb, d->inb, st.max_rows, s);
-  }
+  launch_stage(d->m2l, d->pool, d->outb, d->inb, s);
   if (prof) CK(cudaEventRecord(d->ev[4], s));
   for (int l = 0; l < nlev; ++l) {
     const XStage& st = d->l2l[l];
-    launch_xlate(st.ntask, st.tasks, st.src, st.dst, d->pool, d->inb, d->inb, st.max_rows, s);
+    launch_stage(st, d->pool, d->inb, d->inb, s);
   }
   if (prof) CK(cudaEventRecord(d->ev[5], s));
   launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
@@ -318,13 +400,39 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s) {
   return FDA_OK;
 }
 
+// run_core through a CUDA graph (captured once: all its buffers are internal,
+// so the same graph serves every call); profiled calls run it eagerly.
+static fda_status core(Context* ctx, Dev* d, cudaStream_t s) {
+  if (ctx->profiling || !d->use_graph) return run_core(ctx, d, s);
+  if (!d->graph_exec) {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(d->s_cap, cudaStreamCaptureModeThreadLocal));
+    fda_status st = run_core(ctx, d, d->s_cap);
+    cudaError_t e = cudaStreamEndCapture(d->s_cap, &g);
+    if (st != FDA_OK) return st;
+    if (e != cudaSuccess) {
+      ctx->err = std::string("graph capture failed: ") + cudaGetErrorString(e);
+      return FDA_E_CUDA;
+    }
+    e = cudaGraphInstantiate(&d->graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      d->graph_exec = nullptr;
+      ctx->err = std::string("graph instantiate failed: ") + cudaGetErrorString(e);
+      return FDA_E_CUDA;
+    }
+  }
+  CK(cudaGraphLaunch(d->graph_exec, s));
+  return FDA_OK;
+}
+
 // device-pointer matvec in caller order (float2 in, float2 out)
 static fda_status matvec_dev(Context* ctx, Dev* d, const float2* x, float2* y, cudaStream_t s) {
   const bool prof = ctx->profiling;
   if (prof) CK(cudaEventRecord(d->ev[0], s));
   launch_gather_f32(x, d->perm, d->x_tree, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[1], s));
-  fda_status st = run_core(ctx, d, s);
+  fda_status st = core(ctx, d, s);
   if (st != FDA_OK) return st;
   launch_scatter_f32(d->y_near, d->y_far, d->perm, y, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[7], s));
@@ -344,7 +452,7 @@ fda_status engine_matvec(Context* ctx, const void* x, void* y, int32_t flags, vo
   if (prof) CK(cudaEventRecord(d->ev[0], s));
   launch_gather_f64(d->xh, d->perm, d->x_tree, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[1], s));
-  fda_status st = run_core(ctx, d, s);
+  fda_status st = core(ctx, d, s);
   if (st != FDA_OK) return st;
   launch_scatter_f64(d->y_near, d->y_far, d->perm, d->yh, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[7], s));
@@ -359,7 +467,7 @@ fda_status engine_stage_times(Context* ctx, double* ms, int32_t* n) {
   if (!d->timed) { ctx->err = "no profiled matvec yet (call fda_set_profiling(ctx, 1) first)"; return FDA_E_STATE; }
   CK(cudaEventSynchronize(d->ev[7]));
   float v[8] = {0};
-  CK(cudaEventElapsedTime(&v[0], d->ev[0], d->ev[1]));
+  CK(cudaEventElapsedTime(&v[0], d->ev[0], d->ev_n0));
   CK(cudaEventElapsedTime(&v[1], d->ev_n0, d->ev_n1));
   CK(cudaEventElapsedTime(&v[2], d->ev[1], d->ev[2]));
   CK(cudaEventElapsedTime(&v[3], d->ev[2], d->ev[3]));
@@ -391,46 +499,31 @@ fda_status engine_rhs_plane_wave(Context* ctx, const double dir[3], void* b, int
 }
 
 // ------------------------------------------------------------------ GMRES
+// bm_solve: GMRES (§5; reading C20) on device vectors in
+// caller order.  Arnoldi with classical Gram-Schmidt applied twice (CGS2),
+// fp64 accumulation of every inner product, coefficients kept on the device;
+// one small device→host copy per iteration feeds the Givens rotations.
 namespace {
 struct Gm {
   float2 *V = nullptr, *w = nullptr, *b = nullptr, *x = nullptr;
-  double2 *partial = nullptr, *hdev = nullptr;
-  double* np = nullptr;
+  double2 *partial = nullptr, *hbuf = nullptr;   // hbuf: [h1 (m+1) | h2 (m+1) | y (m+1)]
+  double *np = nullptr, *nrm = nullptr;
   int m = 0;
 };
 }  // namespace
 
 static const int kChunks = 128;
 
-static fda_status dotv(Context* ctx, Gm& gm, const float2* V, int nv, const float2* w, int64_t n, std::vector<cd>& h) {
-  launch_dots(V, n, nv, w, n, gm.partial, kChunks, 0);
-  CK(cudaGetLastError());
-  std::vector<double2> part((size_t)kChunks * nv);
-  CK(cudaMemcpy(part.data(), gm.partial, sizeof(double2) * part.size(), cudaMemcpyDeviceToHost));
-  h.assign(nv, 0.0);
-  for (int c = 0; c < kChunks; ++c)
-    for (int i = 0; i < nv; ++i) h[i] += cd(part[(size_t)c * nv + i].x, part[(size_t)c * nv + i].y);
-  return FDA_OK;
+// h[0..nv) = V[0..nv)^H w  → device
+static void dots_dev(Gm& gm, int nv, const float2* w, int64_t n, double2* h) {
+  launch_dots(gm.V, n, nv, w, n, gm.partial, kChunks, 0);
+  launch_reduce_partials(gm.partial, nv, kChunks, h, 0);
 }
 
-static fda_status norm(Context* ctx, Gm& gm, const float2* w, int64_t n, double& out) {
+static fda_status norm_host(Context* ctx, Gm& gm, const float2* w, int64_t n, double& out) {
   launch_norm2(w, n, gm.np, kChunks, 0);
-  CK(cudaGetLastError());
-  std::vector<double> part(kChunks);
-  CK(cudaMemcpy(part.data(), gm.np, sizeof(double) * kChunks, cudaMemcpyDeviceToHost));
-  double s = 0;
-  for (double v : part) s += v;
-  out = std::sqrt(s);
-  return FDA_OK;
-}
-
-static fda_status update(Context* ctx, Gm& gm, float2* w, const float2* V, int nv, const std::vector<cd>& h, int64_t n,
-                         double sign) {
-  std::vector<double2> hh(nv);
-  for (int i = 0; i < nv; ++i) hh[i] = make_double2(h[i].real(), h[i].imag());
-  CK(cudaMemcpy(gm.hdev, hh.data(), sizeof(double2) * nv, cudaMemcpyHostToDevice));
-  launch_update(w, V, n, nv, gm.hdev, n, sign, 0);
-  CK(cudaGetLastError());
+  launch_reduce_norm(gm.np, kChunks, gm.nrm, 0);
+  CK(cudaMemcpy(&out, gm.nrm, sizeof(double), cudaMemcpyDeviceToHost));
   return FDA_OK;
 }
 
@@ -445,55 +538,72 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
   Gm gm;
   gm.m = m;
   std::vector<void*> mine;
-  auto A = [&](void** p, size_t bytes) -> fda_status {
-    CK(cudaMalloc(p, bytes));
-    mine.push_back(*p);
-    return FDA_OK;
+  auto cleanup = [&]() {
+    for (void* p : mine) cudaFree(p);
   };
-  fda_status st = FDA_OK;
-  auto cleanup = [&]() { for (void* p : mine) cudaFree(p); };
-  if ((st = A((void**)&gm.V, sizeof(float2) * n * (m + 1))) != FDA_OK ||
-      (st = A((void**)&gm.w, sizeof(float2) * n)) != FDA_OK || (st = A((void**)&gm.b, sizeof(float2) * n)) != FDA_OK ||
-      (st = A((void**)&gm.x, sizeof(float2) * n)) != FDA_OK ||
-      (st = A((void**)&gm.partial, sizeof(double2) * kChunks * (m + 1))) != FDA_OK ||
-      (st = A((void**)&gm.hdev, sizeof(double2) * (m + 1))) != FDA_OK ||
-      (st = A((void**)&gm.np, sizeof(double) * kChunks)) != FDA_OK) {
+  auto A = [&](void** p, size_t bytes) -> bool {
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    mine.push_back(*p);
+    return true;
+  };
+  if (!A((void**)&gm.V, sizeof(float2) * n * (m + 1)) || !A((void**)&gm.w, sizeof(float2) * n) ||
+      !A((void**)&gm.b, sizeof(float2) * n) || !A((void**)&gm.x, sizeof(float2) * n) ||
+      !A((void**)&gm.partial, sizeof(double2) * kChunks * (m + 1)) ||
+      !A((void**)&gm.hbuf, sizeof(double2) * 3 * (m + 1)) || !A((void**)&gm.np, sizeof(double) * kChunks) ||
+      !A((void**)&gm.nrm, sizeof(double))) {
     cleanup();
-    return st == FDA_E_CUDA ? FDA_E_NOMEM : st;
+    ctx->err = "device allocation for the GMRES workspace failed";
+    return FDA_E_NOMEM;
   }
-#define GCK(expr)               \
-  do {                          \
-    st = (expr);                \
-    if (st != FDA_OK) {         \
-      cleanup();                \
-      return st;                \
-    }                           \
+  fda_status st = FDA_OK;
+#define GCK(expr)       \
+  do {                  \
+    st = (expr);        \
+    if (st != FDA_OK) { \
+      cleanup();        \
+      return st;        \
+    }                   \
   } while (0)
+#define GCU(call)                                                                  \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      ctx->err = std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call; \
+      cleanup();                                                                   \
+      return FDA_E_CUDA;                                                           \
+    }                                                                              \
+  } while (0)
+  double2* h1 = gm.hbuf;
+  double2* h2 = gm.hbuf + (m + 1);
+  double2* yd = gm.hbuf + 2 * (m + 1);
   if (flags & FDA_DEVICE) {
-    CK(cudaMemcpy(gm.b, rhs, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+    GCU(cudaMemcpy(gm.b, rhs, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
   } else {
-    CK(cudaMemcpy(d->xh, rhs, sizeof(double2) * n, cudaMemcpyHostToDevice));
+    GCU(cudaMemcpy(d->xh, rhs, sizeof(double2) * n, cudaMemcpyHostToDevice));
     launch_f64_to_f32(d->xh, gm.b, n, 0);
   }
-  CK(cudaMemset(gm.x, 0, sizeof(float2) * n));
+  GCU(cudaMemset(gm.x, 0, sizeof(float2) * n));
   double bnorm = 0;
-  GCK(norm(ctx, gm, gm.b, n, bnorm));
+  GCK(norm_host(ctx, gm, gm.b, n, bnorm));
   int it = 0;
   double res = 1.0;
   bool conv = bnorm == 0.0;
-  std::vector<cd> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), h, h2;
+  std::vector<cd> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1);
+  std::vector<double2> hh(2 * (m + 1) + 1);
   while (!conv && it < max_iter) {
-    // r = b - A x   (x = 0 on the first cycle)
     float2* v0 = gm.V;
     double beta;
     if (it == 0) {
-      CK(cudaMemcpy(v0, gm.b, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+      GCU(cudaMemcpy(v0, gm.b, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
       beta = bnorm;
-    } else {
+    } else {  // restart: r = b - A x
       GCK(matvec_dev(ctx, d, gm.x, gm.w, 0));
-      CK(cudaMemcpy(v0, gm.b, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+      GCU(cudaMemcpy(v0, gm.b, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
       launch_axpby(v0, gm.w, -1.0, 1.0, n, 0);
-      GCK(norm(ctx, gm, v0, n, beta));
+      GCK(norm_host(ctx, gm, v0, n, beta));
     }
     launch_scale(v0, v0, 1.0 / beta, 0.0, n, 0);
     std::fill(H.begin(), H.end(), cd(0));
@@ -503,16 +613,21 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
     for (int j = 0; j < m && it < max_iter; ++j) {
       float2* vj = gm.V + (int64_t)j * n;
       GCK(matvec_dev(ctx, d, vj, gm.w, 0));
-      // classical Gram-Schmidt, twice (CGS2), fp64 dot accumulation
-      GCK(dotv(ctx, gm, gm.V, j + 1, gm.w, n, h));
-      GCK(update(ctx, gm, gm.w, gm.V, j + 1, h, n, -1.0));
-      GCK(dotv(ctx, gm, gm.V, j + 1, gm.w, n, h2));
-      GCK(update(ctx, gm, gm.w, gm.V, j + 1, h2, n, -1.0));
-      for (int i = 0; i <= j; ++i) H[(size_t)j * (m + 1) + i] = h[i] + h2[i];
+      dots_dev(gm, j + 1, gm.w, n, h1);
+      launch_update(gm.w, gm.V, n, j + 1, h1, n, -1.0, 0);
+      dots_dev(gm, j + 1, gm.w, n, h2);
+      launch_update(gm.w, gm.V, n, j + 1, h2, n, -1.0, 0);
+      launch_norm2(gm.w, n, gm.np, kChunks, 0);
+      launch_reduce_norm(gm.np, kChunks, gm.nrm, 0);
+      launch_scale_by_inv(gm.V + (int64_t)(j + 1) * n, gm.w, gm.nrm, n, 0);
+      // one copy: h1, h2 and the norm
+      GCU(cudaMemcpy(hh.data(), h1, sizeof(double2) * (j + 1), cudaMemcpyDeviceToHost));
+      GCU(cudaMemcpy(hh.data() + (m + 1), h2, sizeof(double2) * (j + 1), cudaMemcpyDeviceToHost));
       double hn;
-      GCK(norm(ctx, gm, gm.w, n, hn));
+      GCU(cudaMemcpy(&hn, gm.nrm, sizeof(double), cudaMemcpyDeviceToHost));
+      for (int i = 0; i <= j; ++i)
+        H[(size_t)j * (m + 1) + i] = cd(hh[i].x + hh[m + 1 + i].x, hh[i].y + hh[m + 1 + i].y);
       H[(size_t)j * (m + 1) + j + 1] = hn;
-      if (hn > 0) launch_scale(gm.V + (int64_t)(j + 1) * n, gm.w, 1.0 / hn, 0.0, n, 0);
       // Givens rotations (complex): [c̄ s̄; -s c]
       for (int i = 0; i < j; ++i) {
         cd a = H[(size_t)j * (m + 1) + i], bb = H[(size_t)j * (m + 1) + i + 1];
@@ -530,34 +645,39 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
       ++it;
       jd = j + 1;
       res = std::abs(g[j + 1]) / bnorm;
-      if (res <= tol) { conv = true; break; }
+      if (res <= tol || hn == 0.0) { conv = res <= tol; break; }
     }
     // y = R⁻¹ g ; x += V y
-    std::vector<cd> y(jd);
+    std::vector<double2> y(jd);
+    std::vector<cd> yc(jd);
     for (int i = jd - 1; i >= 0; --i) {
       cd s = g[i];
-      for (int k = i + 1; k < jd; ++k) s -= H[(size_t)k * (m + 1) + i] * y[k];
-      y[i] = s / H[(size_t)i * (m + 1) + i];
+      for (int k = i + 1; k < jd; ++k) s -= H[(size_t)k * (m + 1) + i] * yc[k];
+      yc[i] = s / H[(size_t)i * (m + 1) + i];
+      y[i] = make_double2(yc[i].real(), yc[i].imag());
     }
-    GCK(update(ctx, gm, gm.x, gm.V, jd, y, n, +1.0));
+    if (jd > 0) {
+      GCU(cudaMemcpy(yd, y.data(), sizeof(double2) * jd, cudaMemcpyHostToDevice));
+      launch_update(gm.x, gm.V, n, jd, yd, n, +1.0, 0);
+    }
     if (restart <= 0) break;
   }
-  // true residual
+  // true residual ‖b - A x‖ / ‖b‖ (one extra matvec)
   double true_res = 0;
   if (bnorm > 0) {
     GCK(matvec_dev(ctx, d, gm.x, gm.w, 0));
     launch_axpby(gm.w, gm.b, 1.0, -1.0, n, 0);  // w = b - A x
     double rn;
-    GCK(norm(ctx, gm, gm.w, n, rn));
+    GCK(norm_host(ctx, gm, gm.w, n, rn));
     true_res = rn / bnorm;
   }
   if (flags & FDA_DEVICE) {
-    CK(cudaMemcpy(u, gm.x, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+    GCU(cudaMemcpy(u, gm.x, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
   } else {
     launch_f32_to_f64(gm.x, d->yh, n, 0);
-    CK(cudaMemcpy(u, d->yh, sizeof(double2) * n, cudaMemcpyDeviceToHost));
+    GCU(cudaMemcpy(u, d->yh, sizeof(double2) * n, cudaMemcpyDeviceToHost));
   }
-  CK(cudaDeviceSynchronize());
+  GCU(cudaDeviceSynchronize());
   cleanup();
   if (info) {
     info->iterations = it;

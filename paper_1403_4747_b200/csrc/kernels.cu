@@ -63,36 +63,53 @@ constexpr int NEAR_NT = 128;
 constexpr int NEAR_MAXS = 256;
 constexpr int NEAR_MAXL = 256;
 
+// One Q3 point of the LHS kernel, accumulated into acc:
+//   acc += [∂G/∂n_y + α ∂²G/∂n_x∂n_y](x, y) · w      (w = x_j A_j/(12π))
+// With q = kr, a = ∂r/∂n_x, b = ∂r/∂n_y, c = n_x·n_y:
+//   4π r² e^{-iq} ∂G/∂n_y          = (iq - 1) b
+//   4π r² e^{-iq} ∂²G/∂n_x∂n_y     = (1/r) [ (3 - q²) ab + c - iq (3ab + c) ]
+// PURE_IMAG specialises α = i·alpha_im (α = i/k).
+template <bool PURE_IMAG>
 __device__ __forceinline__ void lhs_eval(float3 x, float3 nx, float3 y, float3 ny, float cn, float2 w,
                                          const KernelParams& kp, float2& acc) {
   const float dx = x.x - y.x, dy = x.y - y.y, dz = x.z - y.z;
   const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
   const float ir = rsqrtf(r2);
-  const float r = r2 * ir;
-  const float q = kp.k * r;
+  const float q = kp.k * (r2 * ir);
   const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * ir;   // ∂r/∂n_x
   const float b = -fmaf(dx, ny.x, fmaf(dy, ny.y, dz * ny.z)) * ir;  // ∂r/∂n_y
   const float ab = a * b;
-  // e^{iq} with explicit range reduction to [-π, π] before the SFU sin/cos
-  float t = q * (0.5f / CUDART_PI_F);
-  t -= rintf(t);
   float sn, cs;
-  __sincosf(t * (2.0f * CUDART_PI_F), &sn, &cs);
+  __sincosf(q, &sn, &cs);  // SFU sin/cos; |q| ≤ k·(near range), argument error ≤ ulp(q/2π)
+  const float g = fmaf(3.0f, ab, cn);           // 3ab + c
+  const float u1 = fmaf(fmaf(-q, q, 3.0f), ab, cn);  // (3 - q²) ab + c
+  float P, Q;
+  if (PURE_IMAG) {
+    const float s = kp.alpha_im * ir;
+    P = fmaf(s * q, g, -b);          // -b - α_i ir u2,  u2 = -q g
+    Q = fmaf(s, u1, q * b);          //  q b + α_i ir u1
+  } else {
+    const float u2 = -q * g;
+    P = fmaf(ir, kp.alpha_re * u1 - kp.alpha_im * u2, -b);
+    Q = fmaf(ir, kp.alpha_re * u2 + kp.alpha_im * u1, q * b);
+  }
   const float ir2 = ir * ir;
-  const float Er = ir2 * cs, Ei = ir2 * sn;  // E = e^{iq}/r² (1/4π folded into w)
-  // D = E (iq - 1) b ;  H = (E/r) [ (3 - q²) ab + c - i q (3ab + c) ]
-  const float u1 = fmaf(3.0f - q * q, ab, cn);
-  const float u2 = -q * fmaf(3.0f, ab, cn);
-  const float P = fmaf(ir, kp.alpha_re * u1 - kp.alpha_im * u2, -b);
-  const float Q = fmaf(ir, kp.alpha_re * u2 + kp.alpha_im * u1, q * b);
+  const float Er = ir2 * cs, Ei = ir2 * sn;
   const float Kr = Er * P - Ei * Q;
   const float Ki = Er * Q + Ei * P;
   acc.x = fmaf(Kr, w.x, fmaf(-Ki, w.y, acc.x));
   acc.y = fmaf(Kr, w.y, fmaf(Ki, w.x, acc.y));
 }
 
+// y_i = Σ_{j ∈ direct(i)} A^{Q3}_ij x_j + Σ_{j: ρ_ij<3} C_ij x_j   (a7)
+// A^{Q3}_ij = (A_j/3) Σ_q [∂G/∂n_y + α ∂²G/∂n_x∂n_y](x_i, y_jq)   (Eq. 5)
+// One CTA per target leaf (leaves launched in descending-work order); the
+// source elements of all direct leaves are staged through shared memory in
+// chunks; P = ⌊NT/n_B⌋ threads share one target and split the sources;
+// partial sums are reduced in shared memory.
+template <bool PURE_IMAG>
 __global__ void __launch_bounds__(NEAR_NT) k_near(
-    const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end,
+    const int32_t* __restrict__ order, const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end,
     const int32_t* __restrict__ near_ptr, const int32_t* __restrict__ near_idx,
     const float4* __restrict__ near_off, const float4* __restrict__ tgt_pos, const float4* __restrict__ tgt_nrm,
     const SrcElem* __restrict__ src, const float* __restrict__ src_w, const int32_t* __restrict__ corr_ptr,
@@ -102,7 +119,7 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
   __shared__ float2 sx[NEAR_MAXS];
   __shared__ int spre[NEAR_MAXL + 1];
   __shared__ float2 sred[NEAR_NT];
-  const int leaf = blockIdx.x;
+  const int leaf = order[blockIdx.x];
   const int tb = leaf_begin[leaf];
   const int nt = leaf_end[leaf] - tb;
   const int P = max(1, NEAR_NT / nt);
@@ -120,14 +137,25 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
   for (int e0 = lb; e0 < le; e0 += NEAR_MAXL) {
     const int ne = min(NEAR_MAXL, le - e0);
     __syncthreads();
-    if (tid == 0) {
-      int s = 0;
-      for (int j = 0; j < ne; ++j) {
-        spre[j] = s;
-        int c = near_idx[e0 + j];
-        s += leaf_end[c] - leaf_begin[c];
+    if (tid < 32) {  // warp-parallel exclusive scan of the source-leaf sizes
+      int carry = 0;
+      for (int j0 = 0; j0 < ne; j0 += 32) {
+        const int j = j0 + tid;
+        int v = 0;
+        if (j < ne) {
+          const int c = near_idx[e0 + j];
+          v = leaf_end[c] - leaf_begin[c];
+        }
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (tid >= o) incl += t;
+        }
+        if (j < ne) spre[j] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
       }
-      spre[ne] = s;
+      if (tid == 0) spre[ne] = carry;
     }
     __syncthreads();
     const int total = spre[ne];
@@ -154,14 +182,15 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
       }
       __syncthreads();
       if (active) {
+#pragma unroll 2
         for (int s = part; s < ns; s += P) {
           const float4 A = sa[s], B = sb[s], C = sc[s];
           const float2 w = sx[s];
           const float3 ny = make_float3(A.w, B.w, C.w);
           const float cn = fmaf(nx.x, ny.x, fmaf(nx.y, ny.y, nx.z * ny.z));
-          lhs_eval(xt, nx, make_float3(A.x, A.y, A.z), ny, cn, w, kp, acc);
-          lhs_eval(xt, nx, make_float3(B.x, B.y, B.z), ny, cn, w, kp, acc);
-          lhs_eval(xt, nx, make_float3(C.x, C.y, C.z), ny, cn, w, kp, acc);
+          lhs_eval<PURE_IMAG>(xt, nx, make_float3(A.x, A.y, A.z), ny, cn, w, kp, acc);
+          lhs_eval<PURE_IMAG>(xt, nx, make_float3(B.x, B.y, B.z), ny, cn, w, kp, acc);
+          lhs_eval<PURE_IMAG>(xt, nx, make_float3(C.x, C.y, C.z), ny, cn, w, kp, acc);
         }
       }
       __syncthreads();
@@ -190,13 +219,18 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
   }
 }
 
-void launch_near(int nleaf, const int32_t* leaf_begin, const int32_t* leaf_end, const int32_t* near_ptr,
-                 const int32_t* near_idx, const float4* near_off, const float4* tgt_pos, const float4* tgt_nrm,
-                 const SrcElem* src, const float* src_w, const int32_t* corr_ptr, const int32_t* corr_col,
-                 const float2* corr_val, const float2* x, float2* y, KernelParams kp, cudaStream_t s) {
+void launch_near(int nleaf, const int32_t* order, const int32_t* leaf_begin, const int32_t* leaf_end,
+                 const int32_t* near_ptr, const int32_t* near_idx, const float4* near_off, const float4* tgt_pos,
+                 const float4* tgt_nrm, const SrcElem* src, const float* src_w, const int32_t* corr_ptr,
+                 const int32_t* corr_col, const float2* corr_val, const float2* x, float2* y, KernelParams kp,
+                 bool alpha_pure_imag, cudaStream_t s) {
   if (nleaf <= 0) return;
-  k_near<<<nleaf, NEAR_NT, 0, s>>>(leaf_begin, leaf_end, near_ptr, near_idx, near_off, tgt_pos, tgt_nrm, src,
-                                   src_w, corr_ptr, corr_col, corr_val, x, y, kp);
+  if (alpha_pure_imag)
+    k_near<true><<<nleaf, NEAR_NT, 0, s>>>(order, leaf_begin, leaf_end, near_ptr, near_idx, near_off, tgt_pos,
+                                           tgt_nrm, src, src_w, corr_ptr, corr_col, corr_val, x, y, kp);
+  else
+    k_near<false><<<nleaf, NEAR_NT, 0, s>>>(order, leaf_begin, leaf_end, near_ptr, near_idx, near_off, tgt_pos,
+                                            tgt_nrm, src, src_w, corr_ptr, corr_col, corr_val, x, y, kp);
 }
 
 // ------------------------------------------------------------------ S2M (a2) / L2T (a6)
@@ -257,57 +291,106 @@ void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const floa
 }
 
 // ------------------------------------------------------------------ translations (a3 M2M, a4 M2L, a5 L2L)
-// dst[op] += M · src[op] for a group of ≤ XT_NP ops sharing M.  The sources
-// are staged in shared memory; each thread owns one output row and keeps
-// XT_NP complex accumulators, so every M element loaded (coalesced along the
-// rows) feeds XT_NP complex FMAs.  Results are accumulated with fp32 atomics
-// (several groups may target the same state).
-__global__ void k_xlate(const XTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
-                        const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
-                        const float2* __restrict__ src, float2* __restrict__ dst) {
-  extern __shared__ float2 sS[];  // [cols][XT_NP]
+// Grouped complex GEMM with gathered inputs and scattered accumulation:
+// for the ops of one task (all sharing M), D[:, p] = M[row0:row0+XR, :] S[:, p]
+// with S[:, p] = src[src_off[p] : +cols]; then dst[dst_off[p] + row] += D.
+// K is streamed in chunks of XK through shared memory (register prefetch of
+// the next chunk overlaps the FMAs of the current one); each thread keeps an
+// MR × MO complex register tile, so one k step costs MR + MO shared loads for
+// 4·MR·MO FFMA.  Several tasks may target one state: fp32 vector atomics.
+template <int MR, int MO>
+__global__ void __launch_bounds__(128) k_xlate(const XTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
+                                               const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
+                                               const float2* __restrict__ src, float2* __restrict__ dst) {
+  constexpr int R = 16 * MR, O = 8 * MO;
+  constexpr int ML = XK * R / 128, SL = XK * O / 128;  // loads per thread per chunk
+  __shared__ float2 sM[XK][R];
+  __shared__ float2 sS[XK][O + 1];
   const XTask t = tasks[blockIdx.x];
-  const int np = t.op_count;
-  for (int idx = threadIdx.x; idx < t.cols * XT_NP; idx += blockDim.x) {
-    const int k = idx / XT_NP, p = idx % XT_NP;
-    sS[idx] = p < np ? src[src_off[t.op_begin + p] + k] : make_float2(0.f, 0.f);
+  const int tid = threadIdx.x, tr = tid & 15, to = tid >> 4;
+  const float2* __restrict__ M = pool + t.mat_off;
+  const float2* sp[SL];
+  int sk[SL], spo[SL];
+#pragma unroll
+  for (int e = 0; e < SL; ++e) {
+    const int idx = tid + 128 * e;
+    const int p = idx / XK, kk = idx % XK;
+    spo[e] = p;
+    sk[e] = kk;
+    sp[e] = p < t.op_count ? src + src_off[t.op_begin + p] : nullptr;
   }
-  __syncthreads();
-  const float2* M = pool + t.mat_off;
-  for (int r = threadIdx.x; r < t.rows; r += blockDim.x) {
-    float2 acc[XT_NP];
+  float2 acc[MR][MO];
 #pragma unroll
-    for (int p = 0; p < XT_NP; ++p) acc[p] = make_float2(0.f, 0.f);
-    for (int k = 0; k < t.cols; ++k) {
-      const float2 m = M[(int64_t)k * t.rows + r];
-      const float4* s4 = reinterpret_cast<const float4*>(sS + k * XT_NP);
+  for (int i = 0; i < MR; ++i)
 #pragma unroll
-      for (int p2 = 0; p2 < XT_NP / 2; ++p2) {
-        const float4 v = s4[p2];
-        acc[2 * p2].x = fmaf(m.x, v.x, fmaf(-m.y, v.y, acc[2 * p2].x));
-        acc[2 * p2].y = fmaf(m.x, v.y, fmaf(m.y, v.x, acc[2 * p2].y));
-        acc[2 * p2 + 1].x = fmaf(m.x, v.z, fmaf(-m.y, v.w, acc[2 * p2 + 1].x));
-        acc[2 * p2 + 1].y = fmaf(m.x, v.w, fmaf(m.y, v.z, acc[2 * p2 + 1].y));
-      }
+    for (int j = 0; j < MO; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  float2 rm[ML], rs[SL];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < ML; ++e) {
+      const int idx = tid + 128 * e;
+      const int kk = idx / R, r = idx % R;
+      const int row = t.row0 + r, col = k0 + kk;
+      rm[e] = (row < t.rows && col < t.k_end) ? __ldg(M + (int64_t)col * t.rows + row) : make_float2(0.f, 0.f);
     }
 #pragma unroll
-    for (int p = 0; p < XT_NP; ++p) {
-      if (p < np) {
-        float2* d = dst + dst_off[t.op_begin + p] + r;
-        atomicAdd(&d->x, acc[p].x);
-        atomicAdd(&d->y, acc[p].y);
-      }
+    for (int e = 0; e < SL; ++e) {
+      const int col = k0 + sk[e];
+      rs[e] = (sp[e] != nullptr && col < t.k_end) ? sp[e][col] : make_float2(0.f, 0.f);
+    }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int e = 0; e < ML; ++e) {
+      const int idx = tid + 128 * e;
+      sM[idx / R][idx % R] = rm[e];
+    }
+#pragma unroll
+    for (int e = 0; e < SL; ++e) sS[sk[e]][spo[e]] = rs[e];
+  };
+  load(t.k_begin);
+  for (int k0 = t.k_begin; k0 < t.k_end; k0 += XK) {
+    store();
+    __syncthreads();
+    if (k0 + XK < t.k_end) load(k0 + XK);
+#pragma unroll
+    for (int kk = 0; kk < XK; ++kk) {
+      float2 m[MR], s[MO];
+#pragma unroll
+      for (int i = 0; i < MR; ++i) m[i] = sM[kk][tr + 16 * i];
+#pragma unroll
+      for (int j = 0; j < MO; ++j) s[j] = sS[kk][to + 8 * j];
+#pragma unroll
+      for (int i = 0; i < MR; ++i)
+#pragma unroll
+        for (int j = 0; j < MO; ++j) {
+          acc[i][j].x = fmaf(m[i].x, s[j].x, fmaf(-m[i].y, s[j].y, acc[i][j].x));
+          acc[i][j].y = fmaf(m[i].x, s[j].y, fmaf(m[i].y, s[j].x, acc[i][j].y));
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < MO; ++j) {
+    const int op = to + 8 * j;
+    if (op >= t.op_count) continue;
+    float2* d = dst + dst_off[t.op_begin + op];
+#pragma unroll
+    for (int i = 0; i < MR; ++i) {
+      const int row = t.row0 + tr + 16 * i;
+      if (row < t.rows) atomicAdd(d + row, acc[i][j]);
     }
   }
 }
 
-void launch_xlate(int ntask, const XTask* tasks, const int64_t* src_off, const int64_t* dst_off, const float2* pool,
-                  const float2* src, float2* dst, int max_rows, cudaStream_t s) {
+void launch_xlate(int variant, int ntask, const XTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                  const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
   if (ntask <= 0) return;
-  int bd = ((max_rows + 31) / 32) * 32;
-  bd = bd < 32 ? 32 : (bd > 256 ? 256 : bd);
-  size_t smem = (size_t)320 * XT_NP * sizeof(float2);  // cols ≤ 320
-  k_xlate<<<ntask, bd, smem, s>>>(tasks, src_off, dst_off, pool, src, dst);
+  switch (variant) {
+    case 0: k_xlate<2, 8><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+    case 1: k_xlate<4, 4><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+    default: k_xlate<8, 2><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+  }
 }
 
 // ------------------------------------------------------------------ GMRES helpers (a9)
@@ -383,6 +466,58 @@ __global__ void k_norm2(const float2* __restrict__ w, int64_t n, double* __restr
 void launch_norm2(const float2* w, int64_t n, double* partial, int nchunks, cudaStream_t s) {
   int64_t chunk = (n + nchunks - 1) / nchunks;
   k_norm2<<<nchunks, 256, 0, s>>>(w, n, partial, chunk);
+}
+
+__global__ void k_reduce_partials(const double2* __restrict__ partial, int nv, int nchunks, double2* __restrict__ out) {
+  const int i = blockIdx.x;
+  __shared__ double2 red[128];
+  double sr = 0, si = 0;
+  for (int c = threadIdx.x; c < nchunks; c += blockDim.x) {
+    double2 v = partial[(int64_t)c * nv + i];
+    sr += v.x;
+    si += v.y;
+  }
+  red[threadIdx.x] = make_double2(sr, si);
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) {
+      red[threadIdx.x].x += red[threadIdx.x + k].x;
+      red[threadIdx.x].y += red[threadIdx.x + k].y;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[i] = red[0];
+}
+void launch_reduce_partials(const double2* partial, int nv, int nchunks, double2* out, cudaStream_t s) {
+  k_reduce_partials<<<nv, 128, 0, s>>>(partial, nv, nchunks, out);
+}
+
+__global__ void k_reduce_norm(const double* __restrict__ partial, int nchunks, double* __restrict__ out) {
+  __shared__ double red[128];
+  double a = 0;
+  for (int c = threadIdx.x; c < nchunks; c += blockDim.x) a += partial[c];
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sqrt(red[0]);
+}
+void launch_reduce_norm(const double* partial, int nchunks, double* out, cudaStream_t s) {
+  k_reduce_norm<<<1, 128, 0, s>>>(partial, nchunks, out);
+}
+
+__global__ void k_scale_by_inv(float2* dst, const float2* src, const double* __restrict__ nrm, int64_t n) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double v = nrm[0];
+  const double inv = v > 0 ? 1.0 / v : 0.0;
+  float2 x = src[j];
+  dst[j] = make_float2((float)(x.x * inv), (float)(x.y * inv));
+}
+void launch_scale_by_inv(float2* dst, const float2* src, const double* nrm, int64_t n, cudaStream_t s) {
+  k_scale_by_inv<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dst, src, nrm, n);
 }
 
 __global__ void k_scale(float2* dst, const float2* src, double sre, double sim, int64_t n) {

@@ -18,14 +18,23 @@ struct KernelParams {
   float alpha_im;
 };
 
-// one block of the grouped translation kernel: dst[op] += M · src[op] for
-// up to XT_NP ops sharing the matrix M (rows × cols, column-major)
-constexpr int XT_NP = 16;
+// one CTA of the grouped translation kernel: a tile of XR rows × ≤ XO ops of
+// dst[op] += M · src[op], all ops sharing M (rows × cols, column-major).
+// 128 threads as 16 (rows) × 8 (ops); each thread owns MR × MO outputs.
+// Variants (MR, MO) = (2, 8) → 32 × 64, (4, 4) → 64 × 32, (8, 2) → 128 × 16;
+// the host picks per matrix the variant with the least padding.
+constexpr int XK = 16;   // k (column) chunk
+constexpr int XV = 3;    // number of variants
 struct XTask {
   int64_t mat_off;
   int32_t rows, cols;
+  int32_t row0;
   int32_t op_begin, op_count;
+  int32_t k_begin, k_end;   // column range (split-K: partial products are accumulated atomically)
+  int32_t pad;
 };
+inline int xvar_rows(int v) { return v == 0 ? 32 : (v == 1 ? 64 : 128); }
+inline int xvar_ops(int v) { return v == 0 ? 64 : (v == 1 ? 32 : 16); }
 
 // leaf-level ops (S2M / L2T)
 struct LeafTask {
@@ -42,21 +51,26 @@ void launch_scatter_f32(const float2* y_near, const float2* y_far, const int32_t
                         cudaStream_t s);
 void launch_scatter_f64(const float2* y_near, const float2* y_far, const int32_t* perm, double2* y_caller, int n,
                         cudaStream_t s);
-void launch_near(int nleaf, const int32_t* leaf_begin, const int32_t* leaf_end, const int32_t* near_ptr,
+void launch_near(int nleaf, const int32_t* order, const int32_t* leaf_begin, const int32_t* leaf_end, const int32_t* near_ptr,
                  const int32_t* near_idx, const float4* near_off, const float4* tgt_pos, const float4* tgt_nrm,
                  const SrcElem* src, const float* src_w, const int32_t* corr_ptr, const int32_t* corr_col,
-                 const float2* corr_val, const float2* x, float2* y, KernelParams kp, cudaStream_t s);
+                 const float2* corr_val, const float2* x, float2* y, KernelParams kp, bool alpha_pure_imag,
+                 cudaStream_t s);
 void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const float2* x, float2* out, int max_rows,
                 cudaStream_t s);
 void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s);
-void launch_xlate(int ntask, const XTask* tasks, const int64_t* src_off, const int64_t* dst_off, const float2* pool,
-                  const float2* src, float2* dst, int max_rows, cudaStream_t s);
+void launch_xlate(int variant, int ntask, const XTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                  const float2* pool, const float2* src, float2* dst, cudaStream_t s);
 // GMRES / BLAS-1 helpers (fp64 accumulation)
 void launch_dots(const float2* V, int64_t ldv, int nv, const float2* w, int64_t n, double2* partial, int nchunks,
                  cudaStream_t s);
 void launch_update(float2* w, const float2* V, int64_t ldv, int nv, const double2* h, int64_t n, double sign,
                    cudaStream_t s);
 void launch_norm2(const float2* w, int64_t n, double* partial, int nchunks, cudaStream_t s);
+// out[i] = Σ_c partial[c*nv + i]  (device-side reduction, no host round trip)
+void launch_reduce_partials(const double2* partial, int nv, int nchunks, double2* out, cudaStream_t s);
+void launch_reduce_norm(const double* partial, int nchunks, double* out, cudaStream_t s);   // out = sqrt(Σ)
+void launch_scale_by_inv(float2* dst, const float2* src, const double* nrm, int64_t n, cudaStream_t s);
 void launch_scale(float2* dst, const float2* src, double sre, double sim, int64_t n, cudaStream_t s);
 void launch_axpby(float2* y, const float2* x, double a, double b, int64_t n, cudaStream_t s);  // y = a*x + b*y (real)
 void launch_plane_wave(const double* cen, const double* nrm, const int32_t* perm, int n, double k, double are,
