@@ -294,81 +294,85 @@ void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const floa
 // Grouped complex GEMM with gathered inputs and scattered accumulation:
 // for the ops of one task (all sharing M), D[:, p] = M[row0:row0+XR, :] S[:, p]
 // with S[:, p] = src[src_off[p] : +cols]; then dst[dst_off[p] + row] += D.
-// K is streamed in chunks of XK through shared memory (register prefetch of
-// the next chunk overlaps the FMAs of the current one); each thread keeps an
+// K is streamed in chunks of XK through a two-stage cp.async shared-memory
+// pipeline (the copy of chunk k+1 overlaps the FMAs of chunk k); each thread keeps an
 // MR × MO complex register tile, so one k step costs MR + MO shared loads for
 // 4·MR·MO FFMA.  Several tasks may target one state: fp32 vector atomics.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 8 : 0;   // src-size 0 → zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
 template <int MR, int MO>
 __global__ void __launch_bounds__(128) k_xlate(const XTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
                                                const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
                                                const float2* __restrict__ src, float2* __restrict__ dst) {
   constexpr int R = 16 * MR, O = 8 * MO;
-  constexpr int ML = XK * R / 128, SL = XK * O / 128;  // loads per thread per chunk
-  __shared__ float2 sM[XK][R];
-  __shared__ float2 sS[XK][O + 1];
+  constexpr int ML = XK * R / 128, SL = XK * O / 128;  // cp.async per thread per chunk
+  __shared__ __align__(16) float2 sM[2][XK][R];
+  __shared__ __align__(16) float2 sS[2][XK][O + 1];
+  __shared__ int64_t soff[O];
   const XTask t = tasks[blockIdx.x];
   const int tid = threadIdx.x, tr = tid & 15, to = tid >> 4;
+  for (int p = tid; p < O; p += 128) soff[p] = p < t.op_count ? src_off[t.op_begin + p] : -1;
+  __syncthreads();
   const float2* __restrict__ M = pool + t.mat_off;
-  const float2* sp[SL];
-  int sk[SL], spo[SL];
-#pragma unroll
-  for (int e = 0; e < SL; ++e) {
-    const int idx = tid + 128 * e;
-    const int p = idx / XK, kk = idx % XK;
-    spo[e] = p;
-    sk[e] = kk;
-    sp[e] = p < t.op_count ? src + src_off[t.op_begin + p] : nullptr;
-  }
-  float2 acc[MR][MO];
-#pragma unroll
-  for (int i = 0; i < MR; ++i)
-#pragma unroll
-    for (int j = 0; j < MO; ++j) acc[i][j] = make_float2(0.f, 0.f);
-  float2 rm[ML], rs[SL];
-  auto load = [&](int k0) {
+  auto issue = [&](int buf, int k0) {
 #pragma unroll
     for (int e = 0; e < ML; ++e) {
       const int idx = tid + 128 * e;
       const int kk = idx / R, r = idx % R;
       const int row = t.row0 + r, col = k0 + kk;
-      rm[e] = (row < t.rows && col < t.k_end) ? __ldg(M + (int64_t)col * t.rows + row) : make_float2(0.f, 0.f);
+      const bool ok = row < t.rows && col < t.k_end;
+      cp_async8(&sM[buf][kk][r], ok ? (const void*)(M + (int64_t)col * t.rows + row) : (const void*)M, ok);
     }
 #pragma unroll
     for (int e = 0; e < SL; ++e) {
-      const int col = k0 + sk[e];
-      rs[e] = (sp[e] != nullptr && col < t.k_end) ? sp[e][col] : make_float2(0.f, 0.f);
-    }
-  };
-  auto store = [&]() {
-#pragma unroll
-    for (int e = 0; e < ML; ++e) {
       const int idx = tid + 128 * e;
-      sM[idx / R][idx % R] = rm[e];
+      const int p = idx / XK, kk = idx % XK;
+      const int col = k0 + kk;
+      const int64_t so = soff[p];
+      const bool ok = so >= 0 && col < t.k_end;
+      cp_async8(&sS[buf][kk][p], ok ? (const void*)(src + so + col) : (const void*)src, ok);
     }
-#pragma unroll
-    for (int e = 0; e < SL; ++e) sS[sk[e]][spo[e]] = rs[e];
+    cp_async_commit();
   };
-  load(t.k_begin);
+  float2 acc[MR][MO];
+#pragma unroll
+  for (int i = 0; i < MR; ++i)
+#pragma unroll
+    for (int j = 0; j < MO; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  issue(0, t.k_begin);
+  int buf = 0;
   for (int k0 = t.k_begin; k0 < t.k_end; k0 += XK) {
-    store();
+    if (k0 + XK < t.k_end) {
+      issue(buf ^ 1, k0 + XK);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_0();
+    }
     __syncthreads();
-    if (k0 + XK < t.k_end) load(k0 + XK);
 #pragma unroll
     for (int kk = 0; kk < XK; ++kk) {
-      float2 m[MR], s[MO];
+      float2 m[MR], sv[MO];
 #pragma unroll
-      for (int i = 0; i < MR; ++i) m[i] = sM[kk][tr + 16 * i];
+      for (int i = 0; i < MR; ++i) m[i] = sM[buf][kk][tr + 16 * i];
 #pragma unroll
-      for (int j = 0; j < MO; ++j) s[j] = sS[kk][to + 8 * j];
+      for (int j = 0; j < MO; ++j) sv[j] = sS[buf][kk][to + 8 * j];
 #pragma unroll
       for (int i = 0; i < MR; ++i)
 #pragma unroll
         for (int j = 0; j < MO; ++j) {
-          acc[i][j].x = fmaf(m[i].x, s[j].x, fmaf(-m[i].y, s[j].y, acc[i][j].x));
-          acc[i][j].y = fmaf(m[i].x, s[j].y, fmaf(m[i].y, s[j].x, acc[i][j].y));
+          acc[i][j].x = fmaf(m[i].x, sv[j].x, fmaf(-m[i].y, sv[j].y, acc[i][j].x));
+          acc[i][j].y = fmaf(m[i].x, sv[j].y, fmaf(m[i].y, sv[j].x, acc[i][j].y));
         }
     }
     __syncthreads();
+    buf ^= 1;
   }
 #pragma unroll
   for (int j = 0; j < MO; ++j) {
