@@ -70,7 +70,9 @@ typedef struct {
   int32_t build_threads; /* host threads for the build (0 = all)                         */
   int32_t use_graph;     /* capture the matvec as a CUDA graph (1)                       */
   int32_t verbose;       /* print build statistics to stderr                             */
-  int32_t reserved[7];
+  int32_t m2l_lowrank;   /* 1: second-stage SVD K̃ ≈ ÛV̂ where r < T/2 (PAPER §4.2) */
+  int32_t rhs_operator;  /* 1: also build the RHS pass B (fda_rhs_apply)        */
+  int32_t reserved[5];
 } fda_options;
 
 typedef struct {
@@ -128,6 +130,15 @@ fda_status fda_matvec(fda_ctx* ctx, const void* x, void* y, int32_t flags, void*
 /* b_i = u_inc(x_i) + α ∂u_inc/∂n(x_i) for u_inc = e^{ik d·x} (Eq. (4) right
  * side with ∂u/∂n = 0, reading C22).  dir need not be unit. */
 fda_status fda_rhs_plane_wave(fda_ctx* ctx, const double dir[3], void* b, int32_t flags);
+
+/* b = B v with B = -(α/2)I + S + αK' — the right-hand-side operator of Eq. (4)
+ * (P:176-181): (B v)_i = -(α/2) v_i + Σ_j ∫_Δj [G + α ∂G/∂n_x](x_i, y) dS_y v_j,
+ * applied by the second fast directional pass (G sources, the same target
+ * kernel and translation tables).  For a Neumann problem with
+ * ∂u/∂n = v (n into the body) the BM system is A u = B v.  Needs a context
+ * built with opt.rhs_operator = 1 (FDA_E_STATE otherwise).  Same vector
+ * conventions as fda_matvec. */
+fda_status fda_rhs_apply(fda_ctx* ctx, const void* v, void* b, int32_t flags, void* stream);
 
 /* Solve A u = rhs by GMRES (§5: tolerance on the relative
  * residual, no preconditioner; reading C20).  restart = 0: no restart.

@@ -19,7 +19,8 @@ OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libfda.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CXXFLAGS = ["-O2", "-fPIC", "-fopenmp", "-std=c++17", "-Wall", "-Wno-unused-function"]
+CXXFLAGS = ["-O3", "-fPIC", "-fopenmp", "-std=c++17", "-march=x86-64-v3", "-fcx-limited-range",
+            "-Wall", "-Wno-unused-function"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 

@@ -1,4 +1,5 @@
-// Near-field correction table C (host, fp64 → complex64 CSR in tree order).
+// Near-field correction tables C (LHS) and C_rhs (RHS operator, kind 1)
+// (host, fp64 → complex64 CSR in tree order).
 //
 // The device applies the 3-point rule Q3 to every element pair, either on the
 // fly (direct leaf pairs, near kernel) or folded into S2M (far pairs).  The
@@ -16,7 +17,7 @@
 
 namespace fda {
 
-void build_corrections(const Geometry& g, const Params& p, Plan& plan) {
+void build_corrections(const Geometry& g, const Params& p, Plan& plan, int kind) {
   const int64_t n = g.n;
   const double t1 = p.opt.tier1_rho, t2 = p.opt.tier2_rho;
   double hmax = 0;
@@ -54,26 +55,32 @@ void build_corrections(const Geometry& g, const Params& p, Plan& plan) {
           for (int64_t j : it->second) {
             double rho = (x - g.centroid[j]).norm() / g.hmax[j];
             if (!(rho < t2)) continue;
-            cd q3 = entry_rule(3, x, g.normal[i], g.v0[j], g.v1[j], g.v2[j], g.normal[j], g.area[j], p.k, p.alpha);
+            cd q3 = entry_rule(3, x, g.normal[i], g.v0[j], g.v1[j], g.v2[j], g.normal[j], g.area[j], p.k, p.alpha,
+                               kind);
             cd exact;
-            if (j == i) exact = self_lhs(g.v0[i], g.v1[i], g.v2[i], p.k, p.alpha);
+            if (j == i)
+              exact = kind == 0 ? self_lhs(g.v0[i], g.v1[i], g.v2[i], p.k, p.alpha)
+                                : self_rhs(g.v0[i], g.v1[i], g.v2[i], p.k, p.alpha);
             else exact = entry_rule(rho < t1 ? 1 : 2, x, g.normal[i], g.v0[j], g.v1[j], g.v2[j], g.normal[j],
-                                    g.area[j], p.k, p.alpha);
+                                    g.area[j], p.k, p.alpha, kind);
             cd c = exact - q3;
             row.push_back({j, cf((float)c.real(), (float)c.imag())});
           }
         }
     std::sort(row.begin(), row.end(), [](const auto& u, const auto& v) { return u.first < v.first; });
   }
-  plan.corr_ptr.assign(n + 1, 0);
-  for (int64_t i = 0; i < n; ++i) plan.corr_ptr[i + 1] = plan.corr_ptr[i] + (int64_t)rows[i].size();
-  plan.corr_col.resize(plan.corr_ptr[n]);
-  plan.corr_val.resize(plan.corr_ptr[n]);
+  auto& ptr = kind == 0 ? plan.corr_ptr : plan.corr_ptr_rhs;
+  auto& col = kind == 0 ? plan.corr_col : plan.corr_col_rhs;
+  auto& val = kind == 0 ? plan.corr_val : plan.corr_val_rhs;
+  ptr.assign(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) ptr[i + 1] = ptr[i] + (int64_t)rows[i].size();
+  col.resize(ptr[n]);
+  val.resize(ptr[n]);
   for (int64_t i = 0; i < n; ++i) {
-    int64_t o = plan.corr_ptr[i];
+    int64_t o = ptr[i];
     for (size_t e = 0; e < rows[i].size(); ++e) {
-      plan.corr_col[o + e] = rows[i][e].first;
-      plan.corr_val[o + e] = rows[i][e].second;
+      col[o + e] = rows[i][e].first;
+      val[o + e] = rows[i][e].second;
     }
   }
 }

@@ -28,7 +28,13 @@ namespace fda {
     }                                                                              \
   } while (0)
 
+// one translation op in offsets: dst[dof : +rows] (+)= M[mat] · src[so : +cols]
+struct XOp {
+  int64_t so, dof, mat;
+};
+
 struct XStage {
+  bool atomic = true;
   XTask* tasks[XV] = {};
   int ntask[XV] = {};
   int64_t* src = nullptr;
@@ -52,6 +58,10 @@ struct Dev {
   float4* near_off = nullptr;
   int32_t *corr_ptr = nullptr, *corr_col = nullptr;
   float2* corr_val = nullptr;
+  int32_t *corr_ptr_rhs = nullptr, *corr_col_rhs = nullptr;   // RHS operator (kind 1)
+  float2* corr_val_rhs = nullptr;
+  LeafTask* s2m_rhs = nullptr;
+  int n_s2m_rhs = 0;
   float2* pool = nullptr;
   float2 *outb = nullptr, *inb = nullptr;
   int64_t out_size = 0, in_size = 0;
@@ -59,8 +69,11 @@ struct Dev {
   int n_s2m = 0, n_l2t = 0, max_T = 0;
   std::vector<XStage> m2m, l2l;
   XStage m2l;                      // all levels at once (M2L levels are independent)
+  XStage m2l_a, m2l_b;             // §4.2 factored M2L: tmp = V̂ src ; in += Û tmp
+  float2* tmpb = nullptr;
+  int64_t tmp_size = 0;
   cudaStream_t s_cap = nullptr;
-  cudaGraphExec_t graph_exec = nullptr;
+  cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};
   bool use_graph = false;
   float2 *x_tree = nullptr, *y_near = nullptr, *y_far = nullptr;
   double2 *xh = nullptr, *yh = nullptr;
@@ -99,14 +112,14 @@ static fda_status alloc(Context* ctx, Dev* d, T** dst, size_t count) {
 // and cut each group into tiles of the kernel variant (rows × ops per CTA)
 // that pads the group least.  Stages with fewer CTAs than ~4 waves are split
 // along K (cols) so that small, latency-bound stages still fill the GPU.
-static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<Op>& ops, const std::vector<int64_t>& src_off,
-                               const std::vector<int64_t>& dst_off, XStage& st) {
+static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops, bool atomic, XStage& st) {
   const Plan& p = ctx->plan;
+  st.atomic = atomic;
   if (ops.empty()) return FDA_OK;
   std::vector<size_t> ord(ops.size());
   for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
   std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
-    return ops[a].mat != ops[b].mat ? ops[a].mat < ops[b].mat : ops[a].dst < ops[b].dst;
+    return ops[a].mat != ops[b].mat ? ops[a].mat < ops[b].mat : ops[a].dof < ops[b].dof;
   });
   std::vector<int64_t> so, dof;
   std::vector<XTask> tasks[XV];
@@ -127,8 +140,8 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<Op>& ops,
     const int R = xvar_rows(best), O = xvar_ops(best);
     const int32_t base = (int32_t)so.size();
     for (size_t q = i; q < j; ++q) {
-      so.push_back(src_off[ops[ord[q]].src]);
-      dof.push_back(dst_off[ops[ord[q]].dst]);
+      so.push_back(ops[ord[q]].so);
+      dof.push_back(ops[ord[q]].dof);
     }
     for (int64_t c0 = 0; c0 < nops; c0 += O)
       for (int r0 = 0; r0 < rows; r0 += R) {
@@ -149,7 +162,7 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<Op>& ops,
   int64_t total = 0;
   for (int v = 0; v < XV; ++v) total += (int64_t)tasks[v].size();
   const int64_t target = 4 * 148 * 4;  // ≈ 4 waves of 4 resident CTAs per SM
-  if (total < target) {
+  if (atomic && total < target) {
     const int64_t split = (target + total - 1) / total;
     for (int v = 0; v < XV; ++v) {
       std::vector<XTask> out;
@@ -178,7 +191,7 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<Op>& ops,
 
 static void launch_stage(const XStage& st, const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
   for (int v = 0; v < XV; ++v)
-    if (st.ntask[v]) launch_xlate(v, st.ntask[v], st.tasks[v], st.src, st.dst, pool, src, dst, s);
+    if (st.ntask[v]) launch_xlate(v, st.atomic, st.ntask[v], st.tasks[v], st.src, st.dst, pool, src, dst, s);
 }
 
 fda_status engine_create(Context* ctx) {
@@ -279,6 +292,14 @@ fda_status engine_create(Context* ctx) {
   UP(&d->corr_ptr, cptr.data(), cptr.size());
   UP(&d->corr_col, ccol.data(), ccol.size());
   UP(&d->corr_val, reinterpret_cast<const float2*>(p.corr_val.data()), p.corr_val.size());
+  if (ctx->p.opt.rhs_operator) {
+    if (p.corr_col_rhs.size() >= (size_t)INT32_MAX) { ctx->err = "RHS table too large"; return FDA_E_INTERNAL; }
+    std::vector<int32_t> rp(p.corr_ptr_rhs.begin(), p.corr_ptr_rhs.end()),
+        rc(p.corr_col_rhs.begin(), p.corr_col_rhs.end());
+    UP(&d->corr_ptr_rhs, rp.data(), rp.size());
+    UP(&d->corr_col_rhs, rc.data(), rc.size());
+    UP(&d->corr_val_rhs, reinterpret_cast<const float2*>(p.corr_val_rhs.data()), p.corr_val_rhs.size());
+  }
   UP(&d->pool, reinterpret_cast<const float2*>(p.pool.data()), p.pool.size());
   UP(&d->cen, cen.data(), cen.size());
   UP(&d->nrm, nrm.data(), nrm.size());
@@ -293,7 +314,7 @@ fda_status engine_create(Context* ctx) {
   AL(&d->yh, (size_t)n);
 
   // leaf tasks
-  std::vector<LeafTask> s2m, l2t;
+  std::vector<LeafTask> s2m, l2t, s2m_rhs;
   for (int i = 0; i < nleaf; ++i) {
     const Box& B = t.boxes[t.leaves[i]];
     const int T = t.levels[B.level].rank;
@@ -302,6 +323,11 @@ fda_status engine_create(Context* ctx) {
                   (int32_t)(B.end - B.begin), T, 0};
       s2m.push_back(lt);
       d->max_T = std::max(d->max_T, T);
+      if (ctx->p.opt.rhs_operator && p.leaf_S_rhs[i] >= 0) {
+        LeafTask lr = lt;
+        lr.mat_off = p.mats[p.leaf_S_rhs[i]].offset;
+        s2m_rhs.push_back(lr);
+      }
     }
     LeafTask lt{-1, 0, (int32_t)B.begin, (int32_t)(B.end - B.begin), 0, 0};
     if (p.leaf_T[i] >= 0) {
@@ -315,21 +341,46 @@ fda_status engine_create(Context* ctx) {
   d->n_s2m = (int)s2m.size();
   d->n_l2t = (int)l2t.size();
   UP(&d->s2m, s2m.data(), s2m.size());
+  d->n_s2m_rhs = (int)s2m_rhs.size();
+  UP(&d->s2m_rhs, s2m_rhs.data(), s2m_rhs.size());
   UP(&d->l2t, l2t.data(), l2t.size());
 
   const int nlev = (int)t.levels.size();
   d->m2m.resize(nlev); d->l2l.resize(nlev);
-  std::vector<Op> all_m2l;
+  auto xops = [](const std::vector<Op>& ops, const std::vector<int64_t>& so, const std::vector<int64_t>& dof) {
+    std::vector<XOp> v;
+    v.reserve(ops.size());
+    for (const Op& o : ops) v.push_back({so[o.src], dof[o.dst], o.mat});
+    return v;
+  };
+  std::vector<XOp> all_m2l;
   for (int l = 0; l < nlev; ++l) {
     fda_status s;
-    if ((s = build_xstage(ctx, d, p.m2m[l], p.out_offset, p.out_offset, d->m2m[l])) != FDA_OK) return s;
-    if ((s = build_xstage(ctx, d, p.l2l[l], p.in_offset, p.in_offset, d->l2l[l])) != FDA_OK) return s;
-    all_m2l.insert(all_m2l.end(), p.m2l[l].begin(), p.m2l[l].end());
+    if ((s = build_xstage(ctx, d, xops(p.m2m[l], p.out_offset, p.out_offset), true, d->m2m[l])) != FDA_OK) return s;
+    if ((s = build_xstage(ctx, d, xops(p.l2l[l], p.in_offset, p.in_offset), true, d->l2l[l])) != FDA_OK) return s;
+    auto v = xops(p.m2l[l], p.out_offset, p.in_offset);
+    all_m2l.insert(all_m2l.end(), v.begin(), v.end());
   }
   {
     fda_status s;
-    if ((s = build_xstage(ctx, d, all_m2l, p.out_offset, p.in_offset, d->m2l)) != FDA_OK) return s;
+    if ((s = build_xstage(ctx, d, all_m2l, true, d->m2l)) != FDA_OK) return s;
+    std::vector<XOp> a, b;
+    for (const LrOp& o : p.m2l_lr) {
+      a.push_back({p.out_offset[o.src], o.tmp, o.matV});
+      b.push_back({o.tmp, p.in_offset[o.dst], o.matU});
+    }
+    if ((s = build_xstage(ctx, d, a, false, d->m2l_a)) != FDA_OK) return s;
+    if ((s = build_xstage(ctx, d, b, true, d->m2l_b)) != FDA_OK) return s;
+    d->tmp_size = p.tmp_size;
+    AL(&d->tmpb, (size_t)std::max<int64_t>(1, p.tmp_size));
   }
+  // kernels per matvec: gather, near, s2m, every non-empty translation launch, l2t, scatter
+  int64_t nl = 2 + 1 + (d->n_s2m > 0) + 1 + 1;
+  auto cnt = [&](const XStage& st) { for (int v = 0; v < XV; ++v) nl += st.ntask[v] > 0; };
+  for (auto& st : d->m2m) cnt(st);
+  for (auto& st : d->l2l) cnt(st);
+  cnt(d->m2l); cnt(d->m2l_a); cnt(d->m2l_b);
+  ctx->launches_per_matvec = nl - 1;  // "2 + 1" above double-counts gather
   CK(cudaStreamCreateWithFlags(&d->s_near, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&d->s_cap, cudaStreamNonBlocking));
   d->use_graph = ctx->p.opt.use_graph != 0;
@@ -348,7 +399,8 @@ void engine_destroy(Context* ctx) {
   cudaSetDevice(d->device);
   cudaDeviceSynchronize();
   for (void* a : d->allocs) cudaFree(a);
-  if (d->graph_exec) cudaGraphExecDestroy(d->graph_exec);
+  for (auto& ge : d->graph_exec)
+    if (ge) cudaGraphExecDestroy(ge);
   if (d->s_near) cudaStreamDestroy(d->s_near);
   if (d->s_cap) cudaStreamDestroy(d->s_cap);
   if (d->ev_fork) cudaEventDestroy(d->ev_fork);
@@ -361,7 +413,7 @@ void engine_destroy(Context* ctx) {
 }
 
 // the device part of one matvec: x_tree → y_near, y_far (tree order)
-static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s) {
+static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   // profiling mode serialises the near field on the main stream so that every
   // stage time is the isolated duration of its kernels
   const bool prof = ctx->profiling;
@@ -370,15 +422,17 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s) {
   CK(cudaStreamWaitEvent(sn, d->ev_fork, 0));
   if (prof) CK(cudaEventRecord(d->ev_n0, sn));
   launch_near(d->nleaf, d->near_order, d->leaf_begin, d->leaf_end, d->near_ptr, d->near_idx, d->near_off,
-              d->tgt_pos, d->tgt_nrm, d->src, d->src_w, d->corr_ptr, d->corr_col, d->corr_val, d->x_tree, d->y_near,
-              d->kp, d->alpha_pure_imag, sn);
+              d->tgt_pos, d->tgt_nrm, d->src, d->src_w, kind ? d->corr_ptr_rhs : d->corr_ptr,
+              kind ? d->corr_col_rhs : d->corr_col, kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near,
+              d->kp, d->alpha_pure_imag, kind, sn);
   if (prof) CK(cudaEventRecord(d->ev_n1, sn));
   CK(cudaEventRecord(d->ev_join, sn));
 
   if (prof) CK(cudaEventRecord(d->ev[1], s));
   if (d->out_size) CK(cudaMemsetAsync(d->outb, 0, sizeof(float2) * d->out_size, s));
   if (d->in_size) CK(cudaMemsetAsync(d->inb, 0, sizeof(float2) * d->in_size, s));
-  launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s);
+  if (kind) launch_s2m(d->n_s2m_rhs, d->s2m_rhs, d->pool, d->x_tree, d->outb, d->max_T, s);
+  else launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s);
   if (prof) CK(cudaEventRecord(d->ev[2], s));
   const int nlev = (int)d->m2m.size();
   for (int l = nlev - 1; l >= 0; --l) {
@@ -386,7 +440,9 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s) {
     launch_stage(st, d->pool, d->outb, d->outb, s);
   }
   if (prof) CK(cudaEventRecord(d->ev[3], s));
+  launch_stage(d->m2l_a, d->pool, d->outb, d->tmpb, s);
   launch_stage(d->m2l, d->pool, d->outb, d->inb, s);
+  launch_stage(d->m2l_b, d->pool, d->tmpb, d->inb, s);
   if (prof) CK(cudaEventRecord(d->ev[4], s));
   for (int l = 0; l < nlev; ++l) {
     const XStage& st = d->l2l[l];
@@ -402,37 +458,38 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s) {
 
 // run_core through a CUDA graph (captured once: all its buffers are internal,
 // so the same graph serves every call); profiled calls run it eagerly.
-static fda_status core(Context* ctx, Dev* d, cudaStream_t s) {
-  if (ctx->profiling || !d->use_graph) return run_core(ctx, d, s);
-  if (!d->graph_exec) {
+static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
+  if (ctx->profiling || !d->use_graph) return run_core(ctx, d, s, kind);
+  cudaGraphExec_t& ge = d->graph_exec[kind];
+  if (!ge) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(d->s_cap, cudaStreamCaptureModeThreadLocal));
-    fda_status st = run_core(ctx, d, d->s_cap);
+    fda_status st = run_core(ctx, d, d->s_cap, kind);
     cudaError_t e = cudaStreamEndCapture(d->s_cap, &g);
     if (st != FDA_OK) return st;
     if (e != cudaSuccess) {
       ctx->err = std::string("graph capture failed: ") + cudaGetErrorString(e);
       return FDA_E_CUDA;
     }
-    e = cudaGraphInstantiate(&d->graph_exec, g, 0);
+    e = cudaGraphInstantiate(&ge, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
-      d->graph_exec = nullptr;
+      ge = nullptr;
       ctx->err = std::string("graph instantiate failed: ") + cudaGetErrorString(e);
       return FDA_E_CUDA;
     }
   }
-  CK(cudaGraphLaunch(d->graph_exec, s));
+  CK(cudaGraphLaunch(ge, s));
   return FDA_OK;
 }
 
 // device-pointer matvec in caller order (float2 in, float2 out)
-static fda_status matvec_dev(Context* ctx, Dev* d, const float2* x, float2* y, cudaStream_t s) {
+static fda_status matvec_dev(Context* ctx, Dev* d, const float2* x, float2* y, cudaStream_t s, int kind = 0) {
   const bool prof = ctx->profiling;
   if (prof) CK(cudaEventRecord(d->ev[0], s));
   launch_gather_f32(x, d->perm, d->x_tree, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[1], s));
-  fda_status st = core(ctx, d, s);
+  fda_status st = core(ctx, d, s, kind);
   if (st != FDA_OK) return st;
   launch_scatter_f32(d->y_near, d->y_far, d->perm, y, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[7], s));
@@ -441,18 +498,19 @@ static fda_status matvec_dev(Context* ctx, Dev* d, const float2* x, float2* y, c
   return FDA_OK;
 }
 
-fda_status engine_matvec(Context* ctx, const void* x, void* y, int32_t flags, void* stream) {
+fda_status engine_apply(Context* ctx, const void* x, void* y, int32_t flags, void* stream, int kind) {
   Dev* d = static_cast<Dev*>(ctx->dev);
   CK(cudaSetDevice(d->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (flags & FDA_DEVICE) return matvec_dev(ctx, d, static_cast<const float2*>(x), static_cast<float2*>(y), s);
+  if (flags & FDA_DEVICE)
+    return matvec_dev(ctx, d, static_cast<const float2*>(x), static_cast<float2*>(y), s, kind);
   // host complex128 in/out
   const bool prof = ctx->profiling;
   CK(cudaMemcpyAsync(d->xh, x, sizeof(double2) * d->n, cudaMemcpyHostToDevice, s));
   if (prof) CK(cudaEventRecord(d->ev[0], s));
   launch_gather_f64(d->xh, d->perm, d->x_tree, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[1], s));
-  fda_status st = core(ctx, d, s);
+  fda_status st = core(ctx, d, s, kind);
   if (st != FDA_OK) return st;
   launch_scatter_f64(d->y_near, d->y_far, d->perm, d->yh, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[7], s));

@@ -2,6 +2,7 @@
 // orchestration (PAPER.md Algorithm Step 1, and §4 tables) and
 // host-table export for host-logic tests.
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -38,6 +39,8 @@ fda_status fda_options_default(fda_options* opt) {
   opt->build_threads = 0;
   opt->use_graph = 1;
   opt->verbose = 0;
+  opt->m2l_lowrank = 1;
+  opt->rhs_operator = 0;
   return FDA_OK;
 }
 
@@ -93,16 +96,26 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
   if (o.build_threads > 0) omp_set_num_threads(o.build_threads);
   fda_status st = FDA_OK;
   try {
+    auto tp = std::chrono::steady_clock::now();
+    auto phase = [&](const char* name) {
+      auto now = std::chrono::steady_clock::now();
+      if (o.verbose) fprintf(stderr, "[fda_build] %-12s %8.3f s\n", name, std::chrono::duration<double>(now - tp).count());
+      tp = now;
+    };
     st = build_geometry(vertices, nv, triangles, nt, ctx->g, ctx->err);
     if (st == FDA_OK) {
+      phase("geometry");
       build_tree(ctx->g, ctx->p, ctx->t);
+      phase("tree");
       build_lists(ctx->g, ctx->p, ctx->t, ctx->plan);
+      phase("lists");
       Plan& pl = ctx->plan;
       const int nlev = (int)ctx->t.levels.size();
       std::vector<bool> need(nlev, false);
       for (int l = 0; l < nlev; ++l)
         need[l] = pl.out_level_begin[l + 1] > pl.out_level_begin[l] || pl.in_level_begin[l + 1] > pl.in_level_begin[l];
       build_clouds_and_svd(ctx->p, ctx->t, need);
+      phase("svd");
       // state offsets (complex entries)
       pl.out_offset.resize(pl.out_states.size());
       pl.in_offset.resize(pl.in_states.size());
@@ -119,7 +132,28 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
       }
       pl.in_size = off;
       build_operators(ctx->g, ctx->p, ctx->t, pl);
-      build_corrections(ctx->g, ctx->p, pl);
+      phase("operators");
+      // §4.2: route the M2L ops whose K̃ was factored (r < T/2) to the two-stage path
+      pl.n_m2l_total = 0;
+      pl.m2l_lr.clear();
+      pl.tmp_size = 0;
+      for (size_t l = 0; l < pl.m2l.size(); ++l) {
+        std::vector<Op> dense;
+        for (const Op& op : pl.m2l[l]) {
+          ++pl.n_m2l_total;
+          if (!pl.lr_V.empty() && pl.lr_V[op.mat] >= 0) {
+            LrOp lo{op.src, op.dst, pl.lr_V[op.mat], pl.lr_U[op.mat], pl.tmp_size, (int)l};
+            pl.tmp_size += pl.mats[pl.lr_V[op.mat]].rows;
+            pl.m2l_lr.push_back(lo);
+          } else {
+            dense.push_back(op);
+          }
+        }
+        pl.m2l[l].swap(dense);
+      }
+      build_corrections(ctx->g, ctx->p, pl, 0);
+      if (o.rhs_operator) build_corrections(ctx->g, ctx->p, pl, 1);
+      phase("corrections");
     }
   } catch (const std::bad_alloc&) {
     ctx->err = "host allocation failed during build";
@@ -153,7 +187,7 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
   I.n_leaves = (int64_t)t.leaves.size();
   I.n_out_states = (int64_t)pl.out_states.size();
   I.n_in_states = (int64_t)pl.in_states.size();
-  for (auto& v : pl.m2l) I.n_m2l_pairs += (int64_t)v.size();
+  I.n_m2l_pairs = pl.n_m2l_total;
   for (auto& v : pl.m2m) I.n_m2m_ops += (int64_t)v.size();
   for (auto& v : pl.l2l) I.n_l2l_ops += (int64_t)v.size();
   I.n_direct_leaf_pairs = (int64_t)pl.near_idx.size();
@@ -166,7 +200,7 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
   }
   I.n_corrections = (int64_t)pl.corr_col.size();
   I.n_matrices = (int64_t)pl.mats.size();
-  I.table_bytes = (int64_t)pl.pool.size() * 8 + (int64_t)pl.corr_val.size() * 12;
+  I.table_bytes = (int64_t)pl.pool.size() * 8 + (int64_t)(pl.corr_val.size() + pl.corr_val_rhs.size()) * 12;
   I.t_build_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = ctx;
   return FDA_OK;
@@ -176,7 +210,7 @@ fda_status fda_matvec(fda_ctx* ctx, const void* x, void* y, int32_t flags, void*
   if (!ctx) return FDA_E_INVALID_ARG;
   if (!x || !y || x == y) { ctx->err = "x and y must be non-null and must not alias"; return FDA_E_INVALID_ARG; }
   if (!ctx->dev) { ctx->err = "context was built host-only (opt.device = -1): no device matvec"; return FDA_E_STATE; }
-  return engine_matvec(ctx, x, y, flags, stream);
+  return engine_apply(ctx, x, y, flags, stream, 0);
 }
 
 fda_status fda_rhs_plane_wave(fda_ctx* ctx, const double dir[3], void* b, int32_t flags) {
@@ -185,6 +219,14 @@ fda_status fda_rhs_plane_wave(fda_ctx* ctx, const double dir[3], void* b, int32_
   if (!(nrm > 0)) { ctx->err = "plane-wave direction must be non-zero"; return FDA_E_INVALID_ARG; }
   if (!ctx->dev) { ctx->err = "context was built host-only"; return FDA_E_STATE; }
   return engine_rhs_plane_wave(ctx, dir, b, flags);
+}
+
+fda_status fda_rhs_apply(fda_ctx* ctx, const void* v, void* b, int32_t flags, void* stream) {
+  if (!ctx) return FDA_E_INVALID_ARG;
+  if (!v || !b || v == b) { ctx->err = "v and b must be non-null and must not alias"; return FDA_E_INVALID_ARG; }
+  if (!ctx->dev) { ctx->err = "context was built host-only (opt.device = -1)"; return FDA_E_STATE; }
+  if (!ctx->p.opt.rhs_operator) { ctx->err = "context was built without opt.rhs_operator"; return FDA_E_STATE; }
+  return engine_apply(ctx, v, b, flags, stream, 1);
 }
 
 fda_status bm_solve(fda_ctx* ctx, const void* rhs, void* u, double tol, int32_t max_iter, int32_t restart,
@@ -248,6 +290,12 @@ fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int6
   if (nm == "m2m") return put(ops(p.m2m), dst, count, eb);
   if (nm == "m2l") return put(ops(p.m2l), dst, count, eb);
   if (nm == "l2l") return put(ops(p.l2l), dst, count, eb);
+  if (nm == "m2l_lr") {  // level, src, dst, matV, matU, tmp
+    std::vector<int64_t> v;
+    for (auto& o : p.m2l_lr)
+      for (int64_t x : {(int64_t)o.level, o.src, o.dst, o.matV, o.matU, o.tmp}) v.push_back(x);
+    return put(v, dst, count, eb);
+  }
   if (nm == "mats") {
     std::vector<int64_t> v;
     for (auto& m : p.mats) { v.push_back(m.offset); v.push_back(m.rows); v.push_back(m.cols); }
@@ -266,6 +314,10 @@ fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int6
   if (nm == "corr_ptr") return put(p.corr_ptr, dst, count, eb);
   if (nm == "corr_col") return put(p.corr_col, dst, count, eb);
   if (nm == "corr_val") return put(p.corr_val, dst, count, eb);
+  if (nm == "corr_ptr_rhs") return put(p.corr_ptr_rhs, dst, count, eb);
+  if (nm == "corr_col_rhs") return put(p.corr_col_rhs, dst, count, eb);
+  if (nm == "corr_val_rhs") return put(p.corr_val_rhs, dst, count, eb);
+  if (nm == "leaf_S_rhs") return put(p.leaf_S_rhs, dst, count, eb);
   if (nm == "out_states" || nm == "in_states") {
     const auto& S = nm == "out_states" ? p.out_states : p.in_states;
     std::vector<int64_t> v;
@@ -288,6 +340,7 @@ fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int6
     for (auto& L : t.levels) { v.push_back(L.width); v.push_back(L.hf); v.push_back(L.nf); v.push_back(L.rank); }
     return put(v, dst, count, eb);
   }
+  if (nm == "launches") return put(std::vector<int64_t>{ctx->launches_per_matvec}, dst, count, eb);
   if (nm == "root") {
     return put(std::vector<double>{t.root_center.x, t.root_center.y, t.root_center.z, t.root_width, t.lambda},
                dst, count, eb);

@@ -91,12 +91,20 @@ struct Op {
   int64_t mat;       // matrix id
 };
 
+// factored M2L op (§4.2): tmp = V̂ src ; dst += Û tmp
+struct LrOp {
+  int64_t src, dst;  // global out / in state indices
+  int64_t matV, matU;
+  int64_t tmp;       // complex offset of this op's r-vector in the tmp buffer
+  int level;
+};
+
 struct MatInfo {
   int64_t offset;    // complex64 elements into the matrix pool
   int32_t rows, cols;
 };
 
-enum MatKind { MK_S2M = 0, MK_L2T = 1, MK_M2M = 2, MK_L2L = 3, MK_M2L = 4 };
+enum MatKind { MK_S2M = 0, MK_L2T = 1, MK_M2M = 2, MK_L2L = 3, MK_M2L = 4, MK_S2M_RHS = 5 };
 
 // what a matrix is (geometry it is built from); see operators.cpp
 struct MatSpec {
@@ -130,11 +138,19 @@ struct Plan {
   std::vector<int64_t> leaf_out, leaf_in;                  // state ids (-1 = none)
   // ops per level (index = level of the destination for m2m/m2l, of source for l2l)
   std::vector<std::vector<Op>> m2m, m2l, l2l;
+  // §4.2 factored M2L ops (plan.m2l keeps the dense ones)
+  std::vector<LrOp> m2l_lr;
+  int64_t tmp_size = 0;
+  std::vector<int64_t> lr_V, lr_U;   // per matrix id: factor ids (-1 = dense)
+  int64_t n_m2l_total = 0;
   // direct (near) lists: CSR over leaves -> source leaves
   std::vector<int64_t> near_ptr, near_idx;
-  // corrections: CSR over elements (tree order)
+  // corrections: CSR over elements (tree order); index 1 = RHS operator
   std::vector<int64_t> corr_ptr, corr_col;
   std::vector<cf> corr_val;
+  std::vector<int64_t> corr_ptr_rhs, corr_col_rhs;
+  std::vector<cf> corr_val_rhs;
+  std::vector<int64_t> leaf_S_rhs;   // per leaf: S̃ with G sources (RHS pass), -1 = none
   // matrices
   std::vector<MatInfo> mats;
   std::vector<MatSpec> specs;    // parallel to mats
@@ -164,12 +180,15 @@ Mat3 rotation_to_z(const Vec3& u);
 void build_clouds_and_svd(const Params& p, Tree& t, const std::vector<bool>& need);
 void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan);
 // corrections.cpp
-void build_corrections(const Geometry& g, const Params& p, Plan& plan);
+void build_corrections(const Geometry& g, const Params& p, Plan& plan, int kind = 0);
 // quad.cpp (fp64 kernels and rules)
 cd lhs_kernel(const Vec3& x, const Vec3& nx, const Vec3& y, const Vec3& ny, double k, cd alpha);
+cd rhs_kernel(const Vec3& x, const Vec3& nx, const Vec3& y, double k, cd alpha);
+// kind 0: LHS integrand (Eq. 5); kind 1: RHS integrand G + α ∂G/∂n_x (Eq. 4 right side)
 cd entry_rule(int tier, const Vec3& x, const Vec3& nx, const Vec3& a, const Vec3& b, const Vec3& c,
-              const Vec3& ny, double area, double k, cd alpha);
+              const Vec3& ny, double area, double k, cd alpha, int kind = 0);
 cd self_lhs(const Vec3& a, const Vec3& b, const Vec3& c, double k, cd alpha);
+cd self_rhs(const Vec3& a, const Vec3& b, const Vec3& c, double k, cd alpha);
 cd G(const Vec3& x, const Vec3& y, double k);
 cd dGdnx(const Vec3& x, const Vec3& nx, const Vec3& y, double k);
 cd dGdny(const Vec3& x, const Vec3& y, const Vec3& ny, double k);
@@ -179,11 +198,13 @@ void svd_jacobi(int m, int n, std::vector<cd>& A /*col-major m×n, overwritten*/
                 std::vector<cd>& V /*n×n col-major*/);
 void zgemm_cm(int m, int n, int kk, const cd* A, int lda, const cd* B, int ldb, cd* C, int ldc,
               bool conjA_T = false);
+int lowrank_factor(int m, int n, const cd* A, double eps, std::vector<cd>& Uh, std::vector<cd>& Vh);
 
 // engine.cu (device side)
 struct Context;
 fda_status engine_create(Context* ctx);
-fda_status engine_matvec(Context* ctx, const void* x, void* y, int32_t flags, void* stream);
+// kind 0: the LHS operator A (fda_matvec); kind 1: the RHS operator B (fda_rhs_apply)
+fda_status engine_apply(Context* ctx, const void* x, void* y, int32_t flags, void* stream, int kind);
 fda_status engine_rhs_plane_wave(Context* ctx, const double dir[3], void* b, int32_t flags);
 fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int32_t max_iter, int32_t restart,
                         fda_solve_info* info, int32_t flags);
@@ -198,6 +219,7 @@ struct Context {
   std::string err;
   fda_build_info info{};
   void* dev = nullptr;   // engine-owned device state
+  int64_t launches_per_matvec = 0;
   bool profiling = false;
 };
 

@@ -85,14 +85,36 @@ __device__ __forceinline__ void lhs_eval(float3 x, float3 nx, float3 y, float3 n
   const float u1 = fmaf(fmaf(-q, q, 3.0f), ab, cn);  // (3 - q²) ab + c
   float P, Q;
   if (PURE_IMAG) {
-    const float s = kp.alpha_im * ir;
-    P = fmaf(s * q, g, -b);          // -b - α_i ir u2,  u2 = -q g
-    Q = fmaf(s, u1, q * b);          //  q b + α_i ir u1
+    // -b - α_i ir u2 with u2 = -q g and ir·q = k  →  -b + (α_i k) g
+    P = fmaf(kp.alpha_im * kp.k, g, -b);
+    Q = fmaf(kp.alpha_im * ir, u1, q * b);   //  q b + α_i ir u1
   } else {
     const float u2 = -q * g;
     P = fmaf(ir, kp.alpha_re * u1 - kp.alpha_im * u2, -b);
     Q = fmaf(ir, kp.alpha_re * u2 + kp.alpha_im * u1, q * b);
   }
+  const float ir2 = ir * ir;
+  const float Er = ir2 * cs, Ei = ir2 * sn;
+  const float Kr = Er * P - Ei * Q;
+  const float Ki = Er * Q + Ei * P;
+  acc.x = fmaf(Kr, w.x, fmaf(-Ki, w.y, acc.x));
+  acc.y = fmaf(Kr, w.y, fmaf(Ki, w.x, acc.y));
+}
+
+// One Q3 point of the RHS kernel (Eq. 4 right side):
+//   acc += [G + α ∂G/∂n_x](x, y) · w,   4π r² e^{-iq} (G + α ∂G/∂n_x) = r + α (iq - 1) a
+__device__ __forceinline__ void rhs_eval(float3 x, float3 nx, float3 y, float2 w, const KernelParams& kp,
+                                         float2& acc) {
+  const float dx = x.x - y.x, dy = x.y - y.y, dz = x.z - y.z;
+  const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  const float ir = rsqrtf(r2);
+  const float r = r2 * ir;
+  const float q = kp.k * r;
+  const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * ir;
+  float sn, cs;
+  __sincosf(q, &sn, &cs);
+  const float P = fmaf(-a, fmaf(kp.alpha_im, q, kp.alpha_re), r);   // r - a (α_r + α_i q)
+  const float Q = a * fmaf(kp.alpha_re, q, -kp.alpha_im);           // a (α_r q - α_i)
   const float ir2 = ir * ir;
   const float Er = ir2 * cs, Ei = ir2 * sn;
   const float Kr = Er * P - Ei * Q;
@@ -107,7 +129,8 @@ __device__ __forceinline__ void lhs_eval(float3 x, float3 nx, float3 y, float3 n
 // source elements of all direct leaves are staged through shared memory in
 // chunks; P = ⌊NT/n_B⌋ threads share one target and split the sources;
 // partial sums are reduced in shared memory.
-template <bool PURE_IMAG>
+// KIND 0: LHS operator A (Eq. 5); KIND 1: RHS operator B (G sources).
+template <int KIND, bool PURE_IMAG>
 __global__ void __launch_bounds__(NEAR_NT) k_near(
     const int32_t* __restrict__ order, const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end,
     const int32_t* __restrict__ near_ptr, const int32_t* __restrict__ near_idx,
@@ -186,11 +209,17 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
         for (int s = part; s < ns; s += P) {
           const float4 A = sa[s], B = sb[s], C = sc[s];
           const float2 w = sx[s];
-          const float3 ny = make_float3(A.w, B.w, C.w);
-          const float cn = fmaf(nx.x, ny.x, fmaf(nx.y, ny.y, nx.z * ny.z));
-          lhs_eval<PURE_IMAG>(xt, nx, make_float3(A.x, A.y, A.z), ny, cn, w, kp, acc);
-          lhs_eval<PURE_IMAG>(xt, nx, make_float3(B.x, B.y, B.z), ny, cn, w, kp, acc);
-          lhs_eval<PURE_IMAG>(xt, nx, make_float3(C.x, C.y, C.z), ny, cn, w, kp, acc);
+          if (KIND == 0) {
+            const float3 ny = make_float3(A.w, B.w, C.w);
+            const float cn = fmaf(nx.x, ny.x, fmaf(nx.y, ny.y, nx.z * ny.z));
+            lhs_eval<PURE_IMAG>(xt, nx, make_float3(A.x, A.y, A.z), ny, cn, w, kp, acc);
+            lhs_eval<PURE_IMAG>(xt, nx, make_float3(B.x, B.y, B.z), ny, cn, w, kp, acc);
+            lhs_eval<PURE_IMAG>(xt, nx, make_float3(C.x, C.y, C.z), ny, cn, w, kp, acc);
+          } else {
+            rhs_eval(xt, nx, make_float3(A.x, A.y, A.z), w, kp, acc);
+            rhs_eval(xt, nx, make_float3(B.x, B.y, B.z), w, kp, acc);
+            rhs_eval(xt, nx, make_float3(C.x, C.y, C.z), w, kp, acc);
+          }
         }
       }
       __syncthreads();
@@ -223,14 +252,15 @@ void launch_near(int nleaf, const int32_t* order, const int32_t* leaf_begin, con
                  const int32_t* near_ptr, const int32_t* near_idx, const float4* near_off, const float4* tgt_pos,
                  const float4* tgt_nrm, const SrcElem* src, const float* src_w, const int32_t* corr_ptr,
                  const int32_t* corr_col, const float2* corr_val, const float2* x, float2* y, KernelParams kp,
-                 bool alpha_pure_imag, cudaStream_t s) {
+                 bool alpha_pure_imag, int kind, cudaStream_t s) {
   if (nleaf <= 0) return;
-  if (alpha_pure_imag)
-    k_near<true><<<nleaf, NEAR_NT, 0, s>>>(order, leaf_begin, leaf_end, near_ptr, near_idx, near_off, tgt_pos,
-                                           tgt_nrm, src, src_w, corr_ptr, corr_col, corr_val, x, y, kp);
-  else
-    k_near<false><<<nleaf, NEAR_NT, 0, s>>>(order, leaf_begin, leaf_end, near_ptr, near_idx, near_off, tgt_pos,
-                                            tgt_nrm, src, src_w, corr_ptr, corr_col, corr_val, x, y, kp);
+#define NEAR(K, PI)                                                                                          \
+  k_near<K, PI><<<nleaf, NEAR_NT, 0, s>>>(order, leaf_begin, leaf_end, near_ptr, near_idx, near_off, tgt_pos, \
+                                          tgt_nrm, src, src_w, corr_ptr, corr_col, corr_val, x, y, kp)
+  if (kind == 1) NEAR(1, false);
+  else if (alpha_pure_imag) NEAR(0, true);
+  else NEAR(0, false);
+#undef NEAR
 }
 
 // ------------------------------------------------------------------ S2M (a2) / L2T (a6)
@@ -307,7 +337,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-template <int MR, int MO>
+template <int MR, int MO, bool ATOMIC>
 __global__ void __launch_bounds__(128) k_xlate(const XTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
                                                const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
                                                const float2* __restrict__ src, float2* __restrict__ dst) {
@@ -382,19 +412,27 @@ __global__ void __launch_bounds__(128) k_xlate(const XTask* __restrict__ tasks, 
 #pragma unroll
     for (int i = 0; i < MR; ++i) {
       const int row = t.row0 + tr + 16 * i;
-      if (row < t.rows) atomicAdd(d + row, acc[i][j]);
+      if (row < t.rows) {
+        if (ATOMIC) atomicAdd(d + row, acc[i][j]);
+        else d[row] = acc[i][j];
+      }
     }
   }
 }
 
-void launch_xlate(int variant, int ntask, const XTask* tasks, const int64_t* src_off, const int64_t* dst_off,
-                  const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
+void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const int64_t* src_off,
+                  const int64_t* dst_off, const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
   if (ntask <= 0) return;
+#define XL(MR, MO)                                                                                        \
+  (atomic ? k_xlate<MR, MO, true><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst)          \
+          : k_xlate<MR, MO, false><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst))
   switch (variant) {
-    case 0: k_xlate<2, 8><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
-    case 1: k_xlate<4, 4><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
-    default: k_xlate<8, 2><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+    case 0: XL(2, 8); break;
+    case 1: XL(4, 4); break;
+    case 2: XL(8, 2); break;
+    default: XL(1, 16); break;
   }
+#undef XL
 }
 
 // ------------------------------------------------------------------ GMRES helpers (a9)

@@ -21,10 +21,11 @@ struct KernelParams {
 // one CTA of the grouped translation kernel: a tile of XR rows × ≤ XO ops of
 // dst[op] += M · src[op], all ops sharing M (rows × cols, column-major).
 // 128 threads as 16 (rows) × 8 (ops); each thread owns MR × MO outputs.
-// Variants (MR, MO) = (2, 8) → 32 × 64, (4, 4) → 64 × 32, (8, 2) → 128 × 16;
+// Variants (MR, MO) = (2, 8) → 32 × 64, (4, 4) → 64 × 32, (8, 2) → 128 × 16,
+// (1, 16) → 16 × 128 (the r-row V̂ stage of the factored M2L);
 // the host picks per matrix the variant with the least padding.
 constexpr int XK = 16;   // k (column) chunk
-constexpr int XV = 3;    // number of variants
+constexpr int XV = 4;    // number of variants
 struct XTask {
   int64_t mat_off;
   int32_t rows, cols;
@@ -33,8 +34,8 @@ struct XTask {
   int32_t k_begin, k_end;   // column range (split-K: partial products are accumulated atomically)
   int32_t pad;
 };
-inline int xvar_rows(int v) { return v == 0 ? 32 : (v == 1 ? 64 : 128); }
-inline int xvar_ops(int v) { return v == 0 ? 64 : (v == 1 ? 32 : 16); }
+inline int xvar_rows(int v) { return v == 0 ? 32 : (v == 1 ? 64 : (v == 2 ? 128 : 16)); }
+inline int xvar_ops(int v) { return v == 0 ? 64 : (v == 1 ? 32 : (v == 2 ? 16 : 128)); }
 
 // leaf-level ops (S2M / L2T)
 struct LeafTask {
@@ -55,12 +56,12 @@ void launch_near(int nleaf, const int32_t* order, const int32_t* leaf_begin, con
                  const int32_t* near_idx, const float4* near_off, const float4* tgt_pos, const float4* tgt_nrm,
                  const SrcElem* src, const float* src_w, const int32_t* corr_ptr, const int32_t* corr_col,
                  const float2* corr_val, const float2* x, float2* y, KernelParams kp, bool alpha_pure_imag,
-                 cudaStream_t s);
+                 int kind, cudaStream_t s);
 void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const float2* x, float2* out, int max_rows,
                 cudaStream_t s);
 void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s);
-void launch_xlate(int variant, int ntask, const XTask* tasks, const int64_t* src_off, const int64_t* dst_off,
-                  const float2* pool, const float2* src, float2* dst, cudaStream_t s);
+void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const int64_t* src_off,
+                  const int64_t* dst_off, const float2* pool, const float2* src, float2* dst, cudaStream_t s);
 // GMRES / BLAS-1 helpers (fp64 accumulation)
 void launch_dots(const float2* V, int64_t ldv, int nv, const float2* w, int64_t n, double2* partial, int nchunks,
                  cudaStream_t s);

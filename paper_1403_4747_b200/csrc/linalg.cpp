@@ -116,3 +116,97 @@ void svd_jacobi(int m, int n, std::vector<cd>& A, std::vector<double>& S, std::v
 }
 
 }  // namespace fda
+
+namespace fda {
+
+// Second-stage low-rank factorisation of a reduced M2L matrix (§4.2,
+// Eq. (eq_epsk)): K̃ (m×n, column-major) ≈ Û V̂ with Û = U_r S_r
+// (m×r) and V̂ = Q_r^H (r×n), truncating σ_i < ε σ_0 of K̃ itself.
+// The SVD is computed through a rank-revealing range finder: pivoted
+// Gram-Schmidt (reorthogonalised) on the columns until the largest residual
+// column norm times √(remaining columns) drops below 0.1 ε ‖K̃ col‖_max ≤
+// 0.1 ε σ_0, then R = Q^H K̃ (k×n, k ≪ n) and the SVD of R by one-sided
+// Jacobi on R^H.  Returns r (0 if K̃ = 0).
+int lowrank_factor(int m, int n, const cd* A, double eps, std::vector<cd>& Uh, std::vector<cd>& Vh) {
+  std::vector<cd> W(A, A + (size_t)m * n);  // residual columns
+  std::vector<double> nrm(n);
+  double cmax = 0;
+  for (int j = 0; j < n; ++j) {
+    double s = 0;
+    for (int i = 0; i < m; ++i) s += std::norm(W[(size_t)j * m + i]);
+    nrm[j] = s;
+    cmax = std::max(cmax, s);
+  }
+  if (cmax == 0) { Uh.clear(); Vh.clear(); return 0; }
+  const double c0 = std::sqrt(cmax);
+  std::vector<cd> Q;  // m × k
+  std::vector<char> used(n, 0);
+  int k = 0;
+  const int kmax = std::min(m, n);
+  while (k < kmax) {
+    int jp = -1;
+    double best = -1;
+    for (int j = 0; j < n; ++j)
+      if (!used[j] && nrm[j] > best) { best = nrm[j]; jp = j; }
+    if (jp < 0 || std::sqrt(std::max(best, 0.0)) * std::sqrt((double)(n - k)) < 0.1 * eps * c0) break;
+    used[jp] = 1;
+    std::vector<cd> q(W.begin() + (size_t)jp * m, W.begin() + (size_t)(jp + 1) * m);
+    for (int pass = 0; pass < 2; ++pass)  // reorthogonalise against Q
+      for (int c = 0; c < k; ++c) {
+        const cd* qc = Q.data() + (size_t)c * m;
+        cd h = 0;
+        for (int i = 0; i < m; ++i) h += std::conj(qc[i]) * q[i];
+        for (int i = 0; i < m; ++i) q[i] -= h * qc[i];
+      }
+    double qn = 0;
+    for (int i = 0; i < m; ++i) qn += std::norm(q[i]);
+    qn = std::sqrt(qn);
+    if (qn == 0) continue;
+    for (int i = 0; i < m; ++i) q[i] /= qn;
+    Q.insert(Q.end(), q.begin(), q.end());
+    ++k;
+    // remove q from the remaining residual columns
+    for (int j = 0; j < n; ++j) {
+      if (used[j]) { nrm[j] = 0; continue; }
+      cd* w = W.data() + (size_t)j * m;
+      cd h = 0;
+      for (int i = 0; i < m; ++i) h += std::conj(q[i]) * w[i];
+      double s = 0;
+      for (int i = 0; i < m; ++i) {
+        w[i] -= h * q[i];
+        s += std::norm(w[i]);
+      }
+      nrm[j] = s;
+    }
+  }
+  // R = Q^H A  (k × n), then SVD via one-sided Jacobi on R^H (n × k)
+  std::vector<cd> RH((size_t)n * k);  // column c of R^H = conj(row c of R)
+  for (int c = 0; c < k; ++c)
+    for (int j = 0; j < n; ++j) {
+      const cd* qc = Q.data() + (size_t)c * m;
+      const cd* a = A + (size_t)j * m;
+      cd h = 0;
+      for (int i = 0; i < m; ++i) h += std::conj(qc[i]) * a[i];
+      RH[(size_t)c * n + j] = std::conj(h);
+    }
+  std::vector<double> S;
+  std::vector<cd> Z;  // k × k
+  svd_jacobi(n, k, RH, S, Z);  // R^H = Wl S Z^H  → R = Z S Wl^H ; RH now holds Wl (n × k)
+  int r = 0;
+  while (r < k && S[r] >= eps * S[0]) ++r;
+  // Û = Q Z_r S_r (m × r), V̂ = Wl_r^H (r × n)
+  Uh.assign((size_t)m * r, 0.0);
+  for (int c = 0; c < r; ++c)
+    for (int a = 0; a < k; ++a) {
+      const cd z = Z[(size_t)c * k + a] * S[c];
+      const cd* qa = Q.data() + (size_t)a * m;
+      cd* u = Uh.data() + (size_t)c * m;
+      for (int i = 0; i < m; ++i) u[i] += qa[i] * z;
+    }
+  Vh.assign((size_t)r * n, 0.0);
+  for (int j = 0; j < n; ++j)
+    for (int c = 0; c < r; ++c) Vh[(size_t)j * r + c] = std::conj(RH[(size_t)c * n + j]);
+  return r;
+}
+
+}  // namespace fda

@@ -230,7 +230,7 @@ void build_lists(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
     }
   }
   // ---- leaves: S2M / L2T
-  plan.leaf_S.assign(nleaf, -1); plan.leaf_T.assign(nleaf, -1);
+  plan.leaf_S.assign(nleaf, -1); plan.leaf_T.assign(nleaf, -1); plan.leaf_S_rhs.assign(nleaf, -1);
   plan.leaf_out.assign(nleaf, -1); plan.leaf_in.assign(nleaf, -1);
   for (int64_t i = 0; i < nleaf; ++i) {
     const int64_t b = t.leaves[i];
@@ -239,6 +239,8 @@ void build_lists(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
     if (io != out_id.end()) {
       plan.leaf_out[i] = io->second;
       plan.leaf_S[i] = reg.get({MK_S2M, b}, MatSpec{MK_S2M, l, 0, -1, b, 0, 0, 0});
+      if (p.opt.rhs_operator)
+        plan.leaf_S_rhs[i] = reg.get({MK_S2M_RHS, b}, MatSpec{MK_S2M_RHS, l, 0, -1, b, 0, 0, 0});
     }
     auto ii = in_id.find(skey(b, -1));
     if (ii != in_id.end()) {

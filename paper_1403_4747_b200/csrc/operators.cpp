@@ -106,7 +106,8 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
     const MatSpec& s = plan.specs[id];
     int rows = 0, cols = 0;
     switch (s.kind) {
-      case MK_S2M: {
+      case MK_S2M:
+      case MK_S2M_RHS: {
         const Box& B = t.boxes[s.leaf];
         rows = t.levels[s.level].rank; cols = (int)(B.end - B.begin);
       } break;
@@ -122,6 +123,8 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
     off += (int64_t)rows * cols;
   }
   plan.pool.assign(off, cf(0, 0));
+  std::vector<std::vector<cd>> lrU(nm), lrV(nm);
+  std::vector<int> lrR(nm, -1);
 
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t id = 0; id < nm; ++id) {
@@ -130,8 +133,10 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
     const int m = (int)L.chk.size(), n = (int)L.eq.size(), T = L.rank;
     std::vector<cd> E, X, M;
     switch (s.kind) {
-      case MK_S2M: {
-        // E_up[c, j] = Σ_q (A_j/3) ∂G/∂n_y(chk_c, y_jq)   (Eq. 10)
+      case MK_S2M:
+      case MK_S2M_RHS: {
+        // E_up[c, j] = Σ_q (A_j/3) ∂G/∂n_y(chk_c, y_jq)   (Eq. 10);
+        // the RHS pass uses G sources
         const Box& B = t.boxes[s.leaf];
         const int nb = (int)(B.end - B.begin);
         E.resize((size_t)m * nb);
@@ -142,7 +147,7 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
             cd acc = 0.0;
             for (int q = 0; q < 3; ++q) {
               Vec3 y = g.v0[e] * Q3_BARY[q][0] + g.v1[e] * Q3_BARY[q][1] + g.v2[e] * Q3_BARY[q][2];
-              acc += dGdny(xc, y, g.normal[e], p.k);
+              acc += s.kind == MK_S2M ? dGdny(xc, y, g.normal[e], p.k) : G(xc, y, p.k);
             }
             E[(size_t)j * m + c] = acc * (g.area[e] / 3.0);
           }
@@ -236,7 +241,33 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
         M.resize((size_t)T * T);
         zgemm_cm(T, T, n, Vc.data(), n, X.data(), n, M.data(), T, true);  // V^T (K V)
         store(plan, id, T, T, M);
+        if (p.opt.m2l_lowrank) {
+          // §4.2: K̃ ≈ Û V̂, used when r < T/2
+          std::vector<cd> Uh, Vh;
+          const int r = lowrank_factor(T, T, M.data(), p.eps, Uh, Vh);
+          if (r > 0 && 2 * r < T) {
+            lrR[id] = r;
+            lrU[id].swap(Uh);
+            lrV[id].swap(Vh);
+          }
+        }
       } break;
+    }
+  }
+  // append the §4.2 factors as new matrices: V̂ (r × T) then Û (T × r)
+  plan.lr_V.assign(nm, -1);
+  plan.lr_U.assign(nm, -1);
+  for (int64_t id = 0; id < nm; ++id) {
+    if (lrR[id] < 0) continue;
+    const int r = lrR[id], T = plan.mats[id].rows;
+    for (int w = 0; w < 2; ++w) {
+      const int64_t nid = (int64_t)plan.mats.size();
+      MatInfo mi{(int64_t)plan.pool.size(), w == 0 ? r : T, w == 0 ? T : r};
+      plan.mats.push_back(mi);
+      plan.specs.push_back(plan.specs[id]);
+      const std::vector<cd>& src = w == 0 ? lrV[id] : lrU[id];
+      for (const cd& v : src) plan.pool.push_back(cf((float)v.real(), (float)v.imag()));
+      (w == 0 ? plan.lr_V : plan.lr_U)[id] = nid;
     }
   }
 }

@@ -131,8 +131,17 @@ cd lhs_kernel(const Vec3& x, const Vec3& nx, const Vec3& y, const Vec3& ny, doub
   return D + alpha * H;
 }
 
+// RHS integrand of Eq. (4): G + α ∂G/∂n_x = E [ r + α (iq - 1) a ]
+cd rhs_kernel(const Vec3& x, const Vec3& nx, const Vec3& y, double k, cd alpha) {
+  Vec3 d = x - y;
+  double r = d.norm(), q = k * r, ir = 1.0 / r;
+  double a = d.dot(nx) * ir;
+  cd E = std::polar(ir * ir / (4.0 * kPi), q);
+  return E * (r + alpha * cd(-a, q * a));
+}
+
 cd entry_rule(int tier, const Vec3& x, const Vec3& nx, const Vec3& A, const Vec3& B, const Vec3& C,
-              const Vec3& ny, double area, double k, cd alpha) {
+              const Vec3& ny, double area, double k, cd alpha, int kind) {
   const Rules& R = rules();
   const double(*P)[3];
   const double* W;
@@ -144,7 +153,7 @@ cd entry_rule(int tier, const Vec3& x, const Vec3& nx, const Vec3& A, const Vec3
   cd s = 0.0;
   for (int q = 0; q < nq; ++q) {
     Vec3 y = A * P[q][0] + B * P[q][1] + C * P[q][2];
-    s += W[q] * lhs_kernel(x, nx, y, ny, k, alpha);
+    s += W[q] * (kind == 0 ? lhs_kernel(x, nx, y, ny, k, alpha) : rhs_kernel(x, nx, y, k, alpha));
   }
   return area * s;
 }
@@ -192,6 +201,24 @@ cd self_lhs(const Vec3& A, const Vec3& B, const Vec3& C, double k, cd alpha) {
   });
   cd H = fp / (4.0 * kPi) + rem;
   return 0.5 + alpha * H;   // c = ½, D_ii = 0 on a flat panel (C3-C5)
+}
+
+// RHS diagonal: B_ii = -α/2 + S_ii, S_ii = (1/4π)∫r⁻¹ + ∫(e^{ikr}-1)/(4πr), K'_ii = 0
+// (C4-C5; ∫_Δ r⁻¹ = Σ_e δ_e ln[(t_b+ρ_b)/(t_a+ρ_a)], App. B)
+cd self_rhs(const Vec3& A, const Vec3& B, const Vec3& C, double k, cd alpha) {
+  const Vec3 v[3] = {A, B, C};
+  const Vec3 x = (A + B + C) * (1.0 / 3.0);
+  double r1 = 0.0;
+  for (int e = 0; e < 3; ++e) {
+    Vec3 va = v[e], vb = v[(e + 1) % 3];
+    Vec3 u = (vb - va) * (1.0 / (vb - va).norm());
+    double ta = (va - x).dot(u), tb = (vb - x).dot(u);
+    double dlt = ((va - x) - u * ta).norm();
+    r1 += dlt * std::log((tb + (vb - x).norm()) / (ta + (va - x).norm()));
+  }
+  cd rem = polar_remainder(v, x, [k](double r) { return (std::polar(1.0, k * r) - 1.0) / (4.0 * kPi); });
+  cd S = r1 / (4.0 * kPi) + rem;
+  return -0.5 * alpha + S;
 }
 
 }  // namespace fda

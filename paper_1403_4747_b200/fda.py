@@ -26,7 +26,8 @@ STATUS = {0: "FDA_OK", 1: "FDA_E_INVALID_ARG", 2: "FDA_E_MESH", 3: "FDA_E_NOMEM"
           5: "FDA_E_NCCL", 6: "FDA_E_NOT_CONVERGED", 7: "FDA_E_STATE", 8: "FDA_E_INTERNAL"}
 
 # every symbol include/fda.h declares
-EXPORTS = ["fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "bm_solve", "fda_stats",
+EXPORTS = ["fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_apply", "bm_solve",
+           "fda_stats",
            "fda_set_profiling", "fda_stage_times", "fda_debug_table", "fda_last_error", "fda_status_string",
            "fda_free"]
 
@@ -48,7 +49,8 @@ class fda_options(ctypes.Structure):
                 ("p_chk_hf", ctypes.c_int32), ("eq_scale", ctypes.c_double), ("chk_scale_lf", ctypes.c_double),
                 ("tier1_rho", ctypes.c_double), ("tier2_rho", ctypes.c_double), ("direct_all", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("build_threads", ctypes.c_int32), ("use_graph", ctypes.c_int32),
-                ("verbose", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+                ("verbose", ctypes.c_int32), ("m2l_lowrank", ctypes.c_int32),
+                ("rhs_operator", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 class fda_solve_info(ctypes.Structure):
@@ -82,6 +84,7 @@ def load_library(path: str = LIB_PATH):
     lib.fda_build.argtypes = [vp, i64, vp, i64, dp, fda_cplx, dp, ctypes.POINTER(fda_options), ctypes.POINTER(vp)]
     lib.fda_matvec.argtypes = [vp, vp, vp, i32, vp]
     lib.fda_rhs_plane_wave.argtypes = [vp, ctypes.POINTER(ctypes.c_double * 3), vp, i32]
+    lib.fda_rhs_apply.argtypes = [vp, vp, vp, i32, vp]
     lib.bm_solve.argtypes = [vp, vp, vp, dp, i32, i32, ctypes.POINTER(fda_solve_info), i32]
     lib.fda_stats.argtypes = [vp, ctypes.POINTER(fda_build_info)]
     lib.fda_set_profiling.argtypes = [vp, i32]
@@ -93,7 +96,8 @@ def load_library(path: str = LIB_PATH):
     lib.fda_status_string.restype = ctypes.c_char_p
     lib.fda_free.argtypes = [vp]
     lib.fda_free.restype = None
-    for name in ("fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "bm_solve", "fda_stats",
+    for name in ("fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_apply", "bm_solve",
+                 "fda_stats",
                  "fda_set_profiling", "fda_stage_times", "fda_debug_table"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -161,6 +165,13 @@ class FDA:
     def matvec(self, x, y=None, stream=None):
         """y = A x.  numpy complex128 → numpy complex128 (host path), or torch
         complex64 CUDA tensors (device path, asynchronous on ``stream``)."""
+        return self._apply(self.lib.fda_matvec, x, y, stream)
+
+    def rhs_apply(self, v, b=None, stream=None):
+        """b = B v, the right-hand-side operator of Eq. (4) (needs rhs_operator=1)."""
+        return self._apply(self.lib.fda_rhs_apply, v, b, stream)
+
+    def _apply(self, fn, x, y=None, stream=None):
         if _is_torch(x) and not x.is_cuda:
             # host tensors (e.g. pinned complex128): host path with raw pointers
             import torch
@@ -168,7 +179,7 @@ class FDA:
                 raise ValueError("host x must be a contiguous complex128 tensor of length n")
             if y is None:
                 y = torch.empty_like(x)
-            self._check(self.lib.fda_matvec(self.ctx, x.data_ptr(), y.data_ptr(), FDA_HOST, None))
+            self._check(fn(self.ctx, x.data_ptr(), y.data_ptr(), FDA_HOST, None))
             return y
         if _is_torch(x):
             import torch
@@ -177,13 +188,13 @@ class FDA:
             if y is None:
                 y = torch.empty_like(x)
             s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
-            self._check(self.lib.fda_matvec(self.ctx, x.data_ptr(), y.data_ptr(), FDA_DEVICE, s))
+            self._check(fn(self.ctx, x.data_ptr(), y.data_ptr(), FDA_DEVICE, s))
             return y
         xh = np.ascontiguousarray(x, dtype=np.complex128)
         if xh.shape != (self.n,):
             raise ValueError("x must have length n")
         yh = np.empty(self.n, dtype=np.complex128) if y is None else y
-        self._check(self.lib.fda_matvec(self.ctx, _ptr_np(xh), _ptr_np(yh), FDA_HOST, None))
+        self._check(fn(self.ctx, _ptr_np(xh), _ptr_np(yh), FDA_HOST, None))
         return yh
 
     def rhs_plane_wave(self, direction, device: bool = False):
@@ -236,12 +247,13 @@ class FDA:
         return {STAGES[i]: ms[i] for i in range(n.value)}
 
     _DTYPES = {"perm": np.int64, "verts": np.float64, "leaf_range": np.int64, "leaf_S": np.int64,
-               "leaf_T": np.int64, "leaf_out": np.int64, "leaf_in": np.int64, "out_offset": np.int64,
-               "in_offset": np.int64, "sizes": np.int64, "m2m": np.int64, "m2l": np.int64, "l2l": np.int64,
+               "leaf_T": np.int64, "leaf_S_rhs": np.int64, "corr_ptr_rhs": np.int64, "corr_col_rhs": np.int64,
+               "corr_val_rhs": np.complex64, "leaf_out": np.int64, "leaf_in": np.int64, "out_offset": np.int64,
+               "in_offset": np.int64, "sizes": np.int64, "m2m": np.int64, "m2l": np.int64, "l2l": np.int64, "m2l_lr": np.int64,
                "mats": np.int64, "specs": np.int64, "pool": np.complex64, "near_ptr": np.int64,
                "near_idx": np.int64, "corr_ptr": np.int64, "corr_col": np.int64, "corr_val": np.complex64,
                "out_states": np.int64, "in_states": np.int64, "boxes": np.int64, "box_center": np.float64,
-               "levels": np.float64, "root": np.float64}
+               "levels": np.float64, "root": np.float64, "launches": np.int64}
 
     def table(self, name: str) -> np.ndarray:
         """A host-side build table (host-logic tests only)."""

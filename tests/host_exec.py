@@ -17,7 +17,10 @@ def _mat(pool, mats, m):
     return pool[off:off + rows * cols].astype(np.complex128).reshape(cols, rows).T
 
 
-def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bool = True) -> np.ndarray:
+def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bool = True,
+                 kind: str = "lhs") -> np.ndarray:
+    """y = A x (kind 'lhs') or y = B x (kind 'rhs', needs rhs_operator=1)."""
+    sfx = "_rhs" if kind == "rhs" else ""
     n = f.n
     perm = f.table("perm")
     V = f.table("verts").reshape(n, 3, 3)
@@ -43,11 +46,13 @@ def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bo
             NX = nrm[tb:te][:, None, None, :]
             Y = Yq[src][None]
             NY = nrm[src][None, :, None, :]
-            K = O.lhs_kernel(X, NX, Y, NY, k, alpha)      # (nt, ns, 3)
+            K = (O.lhs_kernel(X, NX, Y, NY, k, alpha) if kind == "lhs"
+                 else O.rhs_kernel(X, NX, Y, k, alpha))       # (nt, ns, 3)
             A = (K @ W3) * area[src][None, :]
             y[tb:te] += A @ xt[src]
     if corr:
-        cp, cc, cv = f.table("corr_ptr"), f.table("corr_col"), f.table("corr_val").astype(np.complex128)
+        cp, cc = f.table("corr_ptr" + sfx), f.table("corr_col" + sfx)
+        cv = f.table("corr_val" + sfx).astype(np.complex128)
         rows = np.repeat(np.arange(n), np.diff(cp))
         np.add.at(y, rows, cv * xt[cc])
     if far:
@@ -68,7 +73,7 @@ def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bo
 
         def T_in(s):
             return rank[boxes[ins[s, 0], 0]]
-        lS, lT, lo, li = f.table("leaf_S"), f.table("leaf_T"), f.table("leaf_out"), f.table("leaf_in")
+        lS, lT, lo, li = f.table("leaf_S" + sfx), f.table("leaf_T"), f.table("leaf_out"), f.table("leaf_in")
         for i in range(nl):
             if lS[i] >= 0:
                 s = lo[i]
@@ -79,6 +84,8 @@ def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bo
                 ob[oo[d]:oo[d] + T_out(d)] += _mat(pool, mats, m) @ ob[oo[s]:oo[s] + T_out(s)]
         for (_, s, d, m) in f.table("m2l").reshape(-1, 4):
             ib[io[d]:io[d] + T_in(d)] += _mat(pool, mats, m) @ ob[oo[s]:oo[s] + T_out(s)]
+        for (_, s, d, mv, mu, _t) in f.table("m2l_lr").reshape(-1, 6):   # §4.2: Û (V̂ src)
+            ib[io[d]:io[d] + T_in(d)] += _mat(pool, mats, mu) @ (_mat(pool, mats, mv) @ ob[oo[s]:oo[s] + T_out(s)])
         l2l = f.table("l2l").reshape(-1, 4)
         for l in sorted(set(l2l[:, 0])):
             for (_, s, d, m) in l2l[l2l[:, 0] == l]:

@@ -169,3 +169,65 @@ def test_stage_times(cfg1):
     f.set_profiling(False)
     assert set(t) == {"gather", "near", "s2m", "m2m", "m2l", "l2l", "l2t", "scatter"}
     assert all(v >= 0 for v in t.values()) and t["near"] > 0
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_large_config_sampled_rows(lib, cfg):
+    """Configs 3 (N = 327,680, kD = 100, two HF interaction levels) and 4
+    (graded prolate spheroid, N ≈ 1.3 M, kD = 300, adaptive tree with leaves on
+    several levels): FDA matvec vs the oracle on 2,000 seeded rows."""
+    V, F = config_mesh(cfg)
+    c = CONFIGS[cfg]
+    f = lib(V, F, c.k, c.alpha, c.eps)
+    x = random_density(len(F), c.x_seed)
+    y = f.matvec(x)
+    rows = sampled_rows(len(F), 2000, c.rows_seed)
+    el = O.element_geometry(V, F)
+    yo = fast.matvec_rows(el, rows, x, c.k, c.alpha)
+    err = _rel(y[rows], yo)
+    st = f.stats()
+    print(f"config{cfg} sampled-row rel-L2 = {err:.3e}; N={len(F)} levels={st['n_levels']} "
+          f"hf={st['n_hf_levels']} m2l={st['n_m2l_pairs']} build={st['t_build_s']:.1f}s")
+    assert err <= MATVEC_TOL
+
+
+def test_rhs_apply_parity(lib):
+    """fda_rhs_apply (b = B v) vs the oracle on the octahedral N = 2,048 sphere."""
+    V, F = octasphere(4, 1.0)
+    k = 2 * np.pi
+    f = lib(V, F, k, 1j / k, 1e-4, rhs_operator=1)
+    el = O.element_geometry(V, F)
+    v = random_density(len(F), 21)
+    bo = fast.matvec_rows(el, np.arange(len(F)), v, k, 1j / k, kind="rhs")
+    err = _rel(f.rhs_apply(v), bo)
+    print(f"rhs_apply rel-L2 = {err:.3e}")
+    assert err <= MATVEC_TOL
+    with pytest.raises(Exception):
+        lib(V, F, k, 1j / k, 1e-4).rhs_apply(v)      # built without the RHS pass → FDA_E_STATE
+
+
+@pytest.mark.parametrize("row", [0, 1])
+def test_pulsating_table2_on_gpu(lib, row):
+    """PAPER.md Table 2 solved entirely on the GPU: b = B·1 by the
+    RHS pass, A u = b by bm_solve; the L2 error vs the analytic solution
+    (reading C2) is the paper's within 5%, and u matches the oracle's dense
+    solution within the solve gate."""
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table2_pulsating.json")))
+    r = g["rows"][row]
+    k = np.pi * r["k_over_pi"]
+    V, F = octasphere(r["n"], 1.0)
+    f = lib(V, F, k, 1j / k, 1e-4, rhs_operator=1)
+    b = f.rhs_apply(np.ones(len(F), dtype=complex))
+    u, info = f.solve(b, tol=1e-4, max_iter=100)
+    ue = O.pulsating_sphere_u(k, 1.0)
+    err = np.linalg.norm(u - ue) / (abs(ue) * np.sqrt(len(F)))
+    el = O.element_geometry(V, F)
+    A = fast.dense(el, k, 1j / k, "lhs")
+    B = fast.dense(el, k, 1j / k, "rhs")
+    u_ref = O.lu_solve(A, B @ np.ones(len(F)))
+    print(f"pulsating N={len(F)}: L2 err {err:.4e} (paper {r['l2_error_eps1e-3']}), its {info['iterations']}, "
+          f"vs dense {_rel(u, u_ref):.2e}")
+    assert info["converged"]
+    assert abs(err / r["l2_error_eps1e-3"] - 1) < g["tolerance_rel"]
+    assert _rel(u, u_ref) <= SOLVE_TOL

@@ -97,7 +97,9 @@ def _coverage(f):
             cov[lr[i, 0]:lr[i, 1], lr[j, 0]:lr[j, 1]] += 1
     outs = f.table("out_states").reshape(-1, 2)
     ins = f.table("in_states").reshape(-1, 2)
-    for (_, s, d, _) in f.table("m2l").reshape(-1, 4):
+    pairs = [(s, d) for (_, s, d, _) in f.table("m2l").reshape(-1, 4)]
+    pairs += [(s, d) for (_, s, d, _, _, _) in f.table("m2l_lr").reshape(-1, 6)]   # §4.2 factored ops
+    for s, d in pairs:
         C, B = boxes[outs[s, 0]], boxes[ins[d, 0]]
         cov[B[5]:B[6], C[5]:C[6]] += 1
     return cov
@@ -165,3 +167,18 @@ def test_eps_convergence():
         y = apply_tables(f, x)
         errs.append(np.linalg.norm(y - yo) / np.linalg.norm(yo))
     assert errs[0] > errs[1] > errs[2] and errs[2] < 1e-3, errs
+
+
+def test_rhs_pass_tables_match_oracle():
+    """The second fast directional pass (G sources, same target kernel and
+    translations) applied from the tables vs the oracle's dense
+    B = -(α/2)I + S + αK'."""
+    V, F = octasphere(4, 1.0)
+    k = 2 * np.pi
+    f = FDA(V, F, k, 1j / k, 1e-4, device=-1, rhs_operator=1, max_leaf=32)
+    el = O.element_geometry(V, F)
+    x = random_density(len(F), 3)
+    for kind in ("lhs", "rhs"):
+        y = apply_tables(f, x, kind=kind)
+        yo = fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k, kind=kind)
+        assert np.linalg.norm(y - yo) / np.linalg.norm(yo) < 1e-4, kind

@@ -1,0 +1,82 @@
+"""Reproduce PAPER.md Table 2 (pulsating unit sphere) on one B200.
+
+    python tools/table2.py [--nmax 8] [--eps 1e-4]
+
+Octahedral unit spheres N = 8·4ⁿ with k = π·2^(n-3); ∂u/∂n = 1
+(n into the body); b = B·1 by the RHS fast directional pass, A u = b by GMRES
+(tol = ε); L2 error against u = a/(1-ika) (reading C2).  Prints one
+JSON line per row with the paper's T_it / N_it / error beside ours.  T_it here
+is the device time of one GMRES iteration (matvec + orthogonalisation).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+PAPER = {  # (N): (k/π, eps=1e-3: T_it, N_it, err ; eps=1e-4: T_it, N_it, err)
+    512: (1, (0.02, 3, 3.65e-2), (0.02, 6, 3.65e-2)),
+    2048: (2, (0.07, 3, 1.86e-2), (0.16, 5, 1.85e-2)),
+    8192: (4, (0.46, 3, 9.26e-3), (0.74, 4, 9.27e-3)),
+    32768: (8, (2.63, 3, 4.84e-3), (5.66, 4, 4.63e-3)),
+    131072: (16, (13.79, 3, 3.11e-3), (29.58, 5, 2.35e-3)),
+    524288: (32, (69.15, 3, 2.92e-3), (143.36, 6, 1.32e-3)),
+    2097152: (64, (260.45, 4, 3.90e-3), None),
+}
+
+
+def main():
+    import torch
+    from fda_inputs import octasphere
+    from paper_1403_4747_b200 import FDA
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--nmin", type=int, default=3)
+    ap.add_argument("--nmax", type=int, default=8)
+    ap.add_argument("--eps", type=float, default=1e-4)
+    a = ap.parse_args()
+    for n in range(a.nmin, a.nmax + 1):
+        V, F = octasphere(n, 1.0)
+        N = len(F)
+        k = np.pi * 2.0 ** (n - 3)
+        t0 = time.perf_counter()
+        f = FDA(V, F, k, 1j / k, a.eps, rhs_operator=1)
+        t_build = time.perf_counter() - t0
+        ones = torch.ones(N, dtype=torch.complex64, device="cuda")
+        b = f.rhs_apply(ones)
+        torch.cuda.synchronize()
+        u, info = f.solve(b, tol=a.eps, max_iter=200)
+        torch.cuda.synchronize()
+        ue = 1.0 / (1.0 - 1j * k)
+        err = float(torch.linalg.norm(u.to(torch.complex128) - ue).item() / (abs(ue) * np.sqrt(N)))
+        # matvec device time
+        y = torch.empty_like(ones)
+        for _ in range(3):
+            f.matvec(ones, y)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(20):
+            f.matvec(ones, y)
+        e.record()
+        torch.cuda.synchronize()
+        mv_ms = s.elapsed_time(e) / 20
+        p = PAPER.get(N)
+        ref = None
+        if p is not None:
+            row = p[1] if a.eps >= 1e-3 else p[2]
+            if row is not None:
+                ref = {"T_it_s": row[0], "N_it": row[1], "l2_error": row[2], "hardware": "1 core Xeon 5450",
+                       "eps": 1e-3 if a.eps >= 1e-3 else 1e-4}
+        print(json.dumps({"N": N, "k": k, "kD": 2 * k, "eps": a.eps, "build_s": round(t_build, 2),
+                          "matvec_ms": round(mv_ms, 4), "N_it": info["iterations"],
+                          "T_it_ms": round(info["t_solve_s"] / max(1, info["iterations"]) * 1e3, 3),
+                          "solve_s": round(info["t_solve_s"], 4), "l2_error": err,
+                          "true_residual": info["true_residual"], "paper": ref}), flush=True)
+        f.close()
+
+
+if __name__ == "__main__":
+    main()
