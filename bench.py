@@ -8,9 +8,10 @@ A step = one fda_matvec (gather â†’ near field âˆ¥ S2M â†’ M2M â†’ M2L â†’ L2L â
 scatter, SURVEY Â§8(a) rows a1-a8) over device-resident inputs of the config-2
 workload (BASELINE configs[1]: icosphere s=6, N = 81,920, kD = 50, Îµ = 1e-4,
 leaf 64).  GMRES (row a9) and the build (row a0) are timed once and reported
-under "solve" and "build_s".  Under torchrun (N > 1) every rank runs an
-independent replica ("replicas only" in round 1, DESIGN.md Â§7); the time is
-the max over ranks.
+under "solve" and "build_s".  Under torchrun (N > 1) the operator is sharded
+over the ranks (leaves split by work, upward pass replicated, one NCCL
+all-reduce of y per matvec â€” DESIGN.md Â§7): strong scaling of one matvec, the
+time is the max over ranks.
 """
 from __future__ import annotations
 
@@ -135,7 +136,14 @@ def run_fda(args):
     V, F = config_mesh(args.config)
     N = len(F)
     t0 = time.perf_counter()
-    f = FDA(V, F, c.k, c.alpha, c.eps, device=local, max_leaf=c.max_leaf)
+    if ws > 1:
+        # sharded operator (DESIGN.md Â§7): one NCCL all-reduce of y per matvec
+        threads = max(1, (os.cpu_count() or ws) // ws)
+        f = FDA(V, F, c.k, c.alpha, c.eps, device=local, max_leaf=c.max_leaf, rank=rank, nranks=ws,
+                build_threads=threads)
+        f.comm_init()
+    else:
+        f = FDA(V, F, c.k, c.alpha, c.eps, device=local, max_leaf=c.max_leaf)
     build_s = time.perf_counter() - t0
     st = f.stats()
     x = torch.from_numpy(random_density(N, c.x_seed).astype(np.complex64)).to(dev)
@@ -224,13 +232,13 @@ def run_fda(args):
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "c64", "data": "synthetic",
             "config": {"workload": f"config {c.cfg}: {c.name}, eps={c.eps}, leaf {c.max_leaf}, plane wave "
                                    f"{list(np.round(c.direction, 4))}",
                        "N": N, "k": c.k, "alpha": "i/k", "eps": c.eps, "l2_flush": "256 MB write between steps",
-                       "parallelism": f"replicas x{ws}"},
-            "matvecs_per_s": round(ws * 1e3 / ms, 2),
+                       "parallelism": f"octree-sharded x{ws} (NCCL all-reduce of y)" if ws > 1 else "single GPU"},
+            "matvecs_per_s": round(1e3 / ms, 2),
             "roofline": roof,
             "stages": stages,
             "build_s": round(build_s, 3),
@@ -300,7 +308,7 @@ def run_reference(args):
     v = float(np.mean(ts))
     return {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": "ms", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 2), "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"config {c.cfg}: {c.name}", "N": N, "k": c.k, "eps": c.eps},
             "cpu_baseline": {"value": round(v, 2), "unit": "ms", "cores": fast.num_threads(), "kind": "oracle",
                              "sample": f"{args.ref_rows} seeded rows per step of the N={N} dense fp64 matvec, "

@@ -55,6 +55,7 @@ typedef struct { double re, im; } fda_cplx;
 /* flags for fda_matvec / fda_rhs_plane_wave / bm_solve */
 #define FDA_HOST   0   /* x, y, b, u are host complex128 arrays (copied in/out) */
 #define FDA_DEVICE 1   /* x, y, b, u are device complex64 arrays on opt.device  */
+#define FDA_LOCAL  2   /* (nranks > 1) return this rank's rows only, others zero; no collective */
 
 typedef struct {
   int32_t max_leaf;      /* split an octree cube while it owns more elements (64)        */
@@ -72,7 +73,9 @@ typedef struct {
   int32_t verbose;       /* print build statistics to stderr                             */
   int32_t m2l_lowrank;   /* 1: second-stage SVD K̃ ≈ ÛV̂ where r < T/2 (PAPER §4.2) */
   int32_t rhs_operator;  /* 1: also build the RHS pass B (fda_rhs_apply)        */
-  int32_t reserved[5];
+  int32_t rank;          /* this rank (0-based) when the operator is sharded over nranks GPUs */
+  int32_t nranks;        /* ranks sharing the operator (1 = unsharded)                      */
+  int32_t reserved[3];
 } fda_options;
 
 typedef struct {
@@ -147,6 +150,20 @@ fda_status bm_solve(fda_ctx* ctx, const void* rhs, void* u, double tol, int32_t 
                     int32_t restart, fda_solve_info* info, int32_t flags);
 
 fda_status fda_stats(const fda_ctx* ctx, fda_build_info* info);
+
+/* Multi-GPU.  With opt.nranks > 1 every rank builds the same
+ * mesh with its own opt.rank; the leaves are split into contiguous Morton
+ * ranges balanced by estimated work.  Each rank replicates the upward pass
+ * (S2M, M2M), runs M2L/L2L only for the incoming states of boxes that contain
+ * one of its leaves, and L2T + near field for its own leaves; fda_matvec and
+ * fda_rhs_apply then sum the ranks' rows with one NCCL all-reduce of y (the
+ * only exchange), so every rank returns the full y and bm_solve runs
+ * unchanged on every rank.  Vectors x are full-length on every rank.
+ * fda_nccl_unique_id: 128-byte NCCL id generated on one rank (libnccl is
+ * loaded on first use); the caller broadcasts it (e.g. torch.distributed);
+ * fda_comm_init: collective over the nranks ranks, before the first matvec. */
+fda_status fda_nccl_unique_id(void* id128);
+fda_status fda_comm_init(fda_ctx* ctx, const void* id128);
 
 /* Per-stage device times (ms, CUDA events) of the last fda_matvec timed with
  * fda_set_profiling(ctx, 1): [gather, near, s2m, m2m, m2l, l2l, l2t, scatter].

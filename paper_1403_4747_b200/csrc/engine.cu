@@ -7,6 +7,8 @@
 //                 → M2L (every level) → L2L (top … leaf level) → L2T ─┐
 //   near stream :          near field (Q3 direct pairs + corrections) ─┴→ scatter
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -33,6 +35,53 @@ struct XOp {
   int64_t so, dof, mat;
 };
 
+// ------------------------------------------------------------------ NCCL (loaded on first use)
+namespace {
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl(std::string& err) {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return api;
+    }
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+    api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.errStr = (decltype(api.errStr))dlsym(h, "ncclGetErrorString");
+    api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.errStr;
+    if (!api.ok) err = "libnccl.so.2 lacks a required symbol";
+  }
+  return api;
+}
+}  // namespace
+
+fda_status nccl_unique_id(void* id128, std::string& err) {
+  NcclApi& a = nccl(err);
+  if (!a.ok) return FDA_E_NCCL;
+  ncclUniqueId id;
+  ncclResult_t r = a.getUniqueId(&id);
+  if (r != ncclSuccess) {
+    err = std::string("ncclGetUniqueId: ") + a.errStr(r);
+    return FDA_E_NCCL;
+  }
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  std::memcpy(id128, &id, 128);
+  return FDA_OK;
+}
+
 struct XStage {
   bool atomic = true;
   XTask* tasks[XV] = {};
@@ -55,6 +104,10 @@ struct Dev {
   int32_t *leaf_begin = nullptr, *leaf_end = nullptr, *near_ptr = nullptr, *near_idx = nullptr;
   int32_t* near_order = nullptr;   // leaves by descending near-field work (LPT block order)
   bool alpha_pure_imag = false;
+  int n_near = 0;                  // near-field CTAs (owned leaves)
+  int e0 = 0, e1 = 0;              // owned element range (tree order)
+  int nranks = 1;
+  ncclComm_t comm = nullptr;
   float4* near_off = nullptr;
   int32_t *corr_ptr = nullptr, *corr_col = nullptr;
   float2* corr_val = nullptr;
@@ -276,6 +329,14 @@ fda_status engine_create(Context* ctx) {
   std::vector<int32_t> order(nleaf);
   for (int i = 0; i < nleaf; ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
+  // sharded: this rank evaluates the near field of its own leaves only
+  order.erase(std::remove_if(order.begin(), order.end(),
+                             [&](int32_t i) { return i < p.own_leaf0 || i >= p.own_leaf1; }),
+              order.end());
+  d->n_near = (int)order.size();
+  d->e0 = (int)p.own_e0;
+  d->e1 = (int)p.own_e1;
+  d->nranks = ctx->p.opt.nranks;
   d->alpha_pure_imag = ctx->p.alpha.real() == 0.0;
 
   UP(&d->perm, perm.data(), perm.size());
@@ -375,12 +436,12 @@ fda_status engine_create(Context* ctx) {
     AL(&d->tmpb, (size_t)std::max<int64_t>(1, p.tmp_size));
   }
   // kernels per matvec: gather, near, s2m, every non-empty translation launch, l2t, scatter
-  int64_t nl = 2 + 1 + (d->n_s2m > 0) + 1 + 1;
+  int64_t nl = 4 + (d->n_s2m > 0);  // gather, near, l2t, scatter (+ s2m)
   auto cnt = [&](const XStage& st) { for (int v = 0; v < XV; ++v) nl += st.ntask[v] > 0; };
   for (auto& st : d->m2m) cnt(st);
   for (auto& st : d->l2l) cnt(st);
   cnt(d->m2l); cnt(d->m2l_a); cnt(d->m2l_b);
-  ctx->launches_per_matvec = nl - 1;  // "2 + 1" above double-counts gather
+  ctx->launches_per_matvec = nl;
   CK(cudaStreamCreateWithFlags(&d->s_near, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&d->s_cap, cudaStreamNonBlocking));
   d->use_graph = ctx->p.opt.use_graph != 0;
@@ -393,11 +454,46 @@ fda_status engine_create(Context* ctx) {
   return FDA_OK;
 }
 
+fda_status engine_comm_init(Context* ctx, const void* id128) {
+  Dev* d = static_cast<Dev*>(ctx->dev);
+  CK(cudaSetDevice(d->device));
+  NcclApi& a = nccl(ctx->err);
+  if (!a.ok) return FDA_E_NCCL;
+  if (d->comm) { a.commDestroy(d->comm); d->comm = nullptr; }
+  ncclUniqueId id;
+  std::memcpy(&id, id128, 128);
+  ncclResult_t r = a.commInitRank(&d->comm, ctx->p.opt.nranks, id, ctx->p.opt.rank);
+  if (r != ncclSuccess) {
+    ctx->err = std::string("ncclCommInitRank: ") + a.errStr(r);
+    d->comm = nullptr;
+    return FDA_E_NCCL;
+  }
+  return FDA_OK;
+}
+
+// sum the ranks' rows (each rank holds its own rows, zeros elsewhere)
+static fda_status reduce_y(Context* ctx, Dev* d, void* y, bool f64, cudaStream_t s) {
+  if (d->nranks <= 1) return FDA_OK;
+  if (!d->comm) { ctx->err = "sharded context: call fda_comm_init before fda_matvec (or pass FDA_LOCAL)"; return FDA_E_STATE; }
+  NcclApi& a = nccl(ctx->err);
+  ncclResult_t r = a.allReduce(y, y, (size_t)2 * d->n, f64 ? ncclDouble : ncclFloat, ncclSum, d->comm, s);
+  if (r != ncclSuccess) {
+    ctx->err = std::string("ncclAllReduce: ") + a.errStr(r);
+    return FDA_E_NCCL;
+  }
+  return FDA_OK;
+}
+
 void engine_destroy(Context* ctx) {
   Dev* d = static_cast<Dev*>(ctx->dev);
   if (!d) return;
   cudaSetDevice(d->device);
   cudaDeviceSynchronize();
+  if (d->comm) {
+    std::string e;
+    NcclApi& a = nccl(e);
+    if (a.ok) a.commDestroy(d->comm);
+  }
   for (void* a : d->allocs) cudaFree(a);
   for (auto& ge : d->graph_exec)
     if (ge) cudaGraphExecDestroy(ge);
@@ -421,7 +517,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   CK(cudaEventRecord(d->ev_fork, s));
   CK(cudaStreamWaitEvent(sn, d->ev_fork, 0));
   if (prof) CK(cudaEventRecord(d->ev_n0, sn));
-  launch_near(d->nleaf, d->near_order, d->leaf_begin, d->leaf_end, d->near_ptr, d->near_idx, d->near_off,
+  launch_near(d->n_near, d->near_order, d->leaf_begin, d->leaf_end, d->near_ptr, d->near_idx, d->near_off,
               d->tgt_pos, d->tgt_nrm, d->src, d->src_w, kind ? d->corr_ptr_rhs : d->corr_ptr,
               kind ? d->corr_col_rhs : d->corr_col, kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near,
               d->kp, d->alpha_pure_imag, kind, sn);
@@ -484,17 +580,22 @@ static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
 }
 
 // device-pointer matvec in caller order (float2 in, float2 out)
-static fda_status matvec_dev(Context* ctx, Dev* d, const float2* x, float2* y, cudaStream_t s, int kind = 0) {
+static fda_status matvec_dev(Context* ctx, Dev* d, const float2* x, float2* y, cudaStream_t s, int kind = 0,
+                             bool local = false) {
   const bool prof = ctx->profiling;
   if (prof) CK(cudaEventRecord(d->ev[0], s));
   launch_gather_f32(x, d->perm, d->x_tree, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[1], s));
   fda_status st = core(ctx, d, s, kind);
   if (st != FDA_OK) return st;
-  launch_scatter_f32(d->y_near, d->y_far, d->perm, y, d->n, s);
+  launch_scatter_f32(d->y_near, d->y_far, d->perm, y, d->n, d->e0, d->e1, s);
   if (prof) CK(cudaEventRecord(d->ev[7], s));
   d->timed = prof;
   CK(cudaGetLastError());
+  if (!local) {
+    fda_status r = reduce_y(ctx, d, y, false, s);
+    if (r != FDA_OK) return r;
+  }
   return FDA_OK;
 }
 
@@ -502,8 +603,9 @@ fda_status engine_apply(Context* ctx, const void* x, void* y, int32_t flags, voi
   Dev* d = static_cast<Dev*>(ctx->dev);
   CK(cudaSetDevice(d->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool local = (flags & FDA_LOCAL) != 0;
   if (flags & FDA_DEVICE)
-    return matvec_dev(ctx, d, static_cast<const float2*>(x), static_cast<float2*>(y), s, kind);
+    return matvec_dev(ctx, d, static_cast<const float2*>(x), static_cast<float2*>(y), s, kind, local);
   // host complex128 in/out
   const bool prof = ctx->profiling;
   CK(cudaMemcpyAsync(d->xh, x, sizeof(double2) * d->n, cudaMemcpyHostToDevice, s));
@@ -512,9 +614,13 @@ fda_status engine_apply(Context* ctx, const void* x, void* y, int32_t flags, voi
   if (prof) CK(cudaEventRecord(d->ev[1], s));
   fda_status st = core(ctx, d, s, kind);
   if (st != FDA_OK) return st;
-  launch_scatter_f64(d->y_near, d->y_far, d->perm, d->yh, d->n, s);
+  launch_scatter_f64(d->y_near, d->y_far, d->perm, d->yh, d->n, d->e0, d->e1, s);
   if (prof) CK(cudaEventRecord(d->ev[7], s));
   d->timed = prof;
+  if (!local) {
+    fda_status r = reduce_y(ctx, d, d->yh, true, s);
+    if (r != FDA_OK) return r;
+  }
   CK(cudaMemcpyAsync(y, d->yh, sizeof(double2) * d->n, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return FDA_OK;

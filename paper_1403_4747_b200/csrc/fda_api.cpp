@@ -41,6 +41,8 @@ fda_status fda_options_default(fda_options* opt) {
   opt->verbose = 0;
   opt->m2l_lowrank = 1;
   opt->rhs_operator = 0;
+  opt->rank = 0;
+  opt->nranks = 1;
   return FDA_OK;
 }
 
@@ -86,7 +88,13 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
   ctx->p.eps = eps;
   if (opt) ctx->p.opt = *opt; else fda_options_default(&ctx->p.opt);
   fda_options& o = ctx->p.opt;
-  if (o.max_leaf < 1 || o.p_eq < 2 || o.p_chk_lf < 2 || o.p_chk_hf < 2 || !(o.eq_scale > 0) ||
+  if (o.nranks < 1) o.nranks = 1;
+  if (o.rank < 0 || o.rank >= o.nranks) {
+    g_build_error = "opt.rank must lie in [0, opt.nranks)";
+    delete ctx;
+    return FDA_E_INVALID_ARG;
+  }
+  if (o.max_leaf < 1 || o.max_leaf > 128 || o.p_eq < 2 || o.p_chk_lf < 2 || o.p_chk_hf < 2 || !(o.eq_scale > 0) ||
       !(o.chk_scale_lf > o.eq_scale) || !(o.tier1_rho >= 0) || !(o.tier2_rho >= o.tier1_rho)) {
     g_build_error = "invalid fda_options";
     delete ctx;
@@ -154,6 +162,7 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
       build_corrections(ctx->g, ctx->p, pl, 0);
       if (o.rhs_operator) build_corrections(ctx->g, ctx->p, pl, 1);
       phase("corrections");
+      apply_partition(ctx->p, ctx->t, pl);
     }
   } catch (const std::bad_alloc&) {
     ctx->err = "host allocation failed during build";
@@ -236,6 +245,18 @@ fda_status bm_solve(fda_ctx* ctx, const void* rhs, void* u, double tol, int32_t 
   if (!(tol > 0) || max_iter < 1 || restart < 0) { ctx->err = "tol > 0, max_iter >= 1, restart >= 0"; return FDA_E_INVALID_ARG; }
   if (!ctx->dev) { ctx->err = "context was built host-only"; return FDA_E_STATE; }
   return engine_solve(ctx, rhs, u, tol, max_iter, restart, info, flags);
+}
+
+fda_status fda_nccl_unique_id(void* id128) {
+  if (!id128) return FDA_E_INVALID_ARG;
+  return nccl_unique_id(id128, g_build_error);
+}
+
+fda_status fda_comm_init(fda_ctx* ctx, const void* id128) {
+  if (!ctx || !id128) return FDA_E_INVALID_ARG;
+  if (ctx->p.opt.nranks <= 1) { ctx->err = "fda_comm_init needs a context built with opt.nranks > 1"; return FDA_E_STATE; }
+  if (!ctx->dev) { ctx->err = "context was built host-only"; return FDA_E_STATE; }
+  return engine_comm_init(ctx, id128);
 }
 
 fda_status fda_stats(const fda_ctx* ctx, fda_build_info* info) {
@@ -340,6 +361,8 @@ fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int6
     for (auto& L : t.levels) { v.push_back(L.width); v.push_back(L.hf); v.push_back(L.nf); v.push_back(L.rank); }
     return put(v, dst, count, eb);
   }
+  if (nm == "owned")
+    return put(std::vector<int64_t>{p.own_leaf0, p.own_leaf1, p.own_e0, p.own_e1}, dst, count, eb);
   if (nm == "launches") return put(std::vector<int64_t>{ctx->launches_per_matvec}, dst, count, eb);
   if (nm == "root") {
     return put(std::vector<double>{t.root_center.x, t.root_center.y, t.root_center.z, t.root_width, t.lambda},

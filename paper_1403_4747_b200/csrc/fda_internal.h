@@ -143,6 +143,8 @@ struct Plan {
   int64_t tmp_size = 0;
   std::vector<int64_t> lr_V, lr_U;   // per matrix id: factor ids (-1 = dense)
   int64_t n_m2l_total = 0;
+  // sharding (nranks > 1): owned leaves [own_leaf0, own_leaf1), elements [own_e0, own_e1)
+  int64_t own_leaf0 = 0, own_leaf1 = 0, own_e0 = 0, own_e1 = 0;
   // direct (near) lists: CSR over leaves -> source leaves
   std::vector<int64_t> near_ptr, near_idx;
   // corrections: CSR over elements (tree order); index 1 = RHS operator
@@ -181,6 +183,8 @@ void build_clouds_and_svd(const Params& p, Tree& t, const std::vector<bool>& nee
 void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan);
 // corrections.cpp
 void build_corrections(const Geometry& g, const Params& p, Plan& plan, int kind = 0);
+// partition.cpp
+void apply_partition(const Params& p, const Tree& t, Plan& plan);
 // quad.cpp (fp64 kernels and rules)
 cd lhs_kernel(const Vec3& x, const Vec3& nx, const Vec3& y, const Vec3& ny, double k, cd alpha);
 cd rhs_kernel(const Vec3& x, const Vec3& nx, const Vec3& y, double k, cd alpha);
@@ -209,6 +213,8 @@ fda_status engine_rhs_plane_wave(Context* ctx, const double dir[3], void* b, int
 fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int32_t max_iter, int32_t restart,
                         fda_solve_info* info, int32_t flags);
 fda_status engine_stage_times(Context* ctx, double* ms, int32_t* n);
+fda_status engine_comm_init(Context* ctx, const void* id128);
+fda_status nccl_unique_id(void* id128, std::string& err);
 void engine_destroy(Context* ctx);
 
 struct Context {

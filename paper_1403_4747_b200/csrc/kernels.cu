@@ -22,21 +22,29 @@ __global__ void k_gather_f64(const double2* __restrict__ xc, const int32_t* __re
     xt[i] = make_float2((float)v.x, (float)v.y);
   }
 }
-// a8 scatter: y_caller[perm[i]] = y_near[i] + y_far[i]
+// a8 scatter: y_caller[perm[i]] = y_near[i] + y_far[i] for owned rows i ∈ [e0, e1), 0 otherwise
 __global__ void k_scatter_f32(const float2* __restrict__ yn, const float2* __restrict__ yf,
-                              const int32_t* __restrict__ perm, float2* __restrict__ yc, int n) {
+                              const int32_t* __restrict__ perm, float2* __restrict__ yc, int n, int e0, int e1) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
-    float2 a = yn[i], b = yf[i];
-    yc[perm[i]] = make_float2(a.x + b.x, a.y + b.y);
+    float2 v = make_float2(0.f, 0.f);
+    if (i >= e0 && i < e1) {
+      float2 a = yn[i], b = yf[i];
+      v = make_float2(a.x + b.x, a.y + b.y);
+    }
+    yc[perm[i]] = v;
   }
 }
 __global__ void k_scatter_f64(const float2* __restrict__ yn, const float2* __restrict__ yf,
-                              const int32_t* __restrict__ perm, double2* __restrict__ yc, int n) {
+                              const int32_t* __restrict__ perm, double2* __restrict__ yc, int n, int e0, int e1) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
-    float2 a = yn[i], b = yf[i];
-    yc[perm[i]] = make_double2((double)a.x + (double)b.x, (double)a.y + (double)b.y);
+    double2 v = make_double2(0.0, 0.0);
+    if (i >= e0 && i < e1) {
+      float2 a = yn[i], b = yf[i];
+      v = make_double2((double)a.x + (double)b.x, (double)a.y + (double)b.y);
+    }
+    yc[perm[i]] = v;
   }
 }
 
@@ -46,11 +54,13 @@ void launch_gather_f32(const float2* x, const int32_t* perm, float2* xt, int n, 
 void launch_gather_f64(const double2* x, const int32_t* perm, float2* xt, int n, cudaStream_t s) {
   k_gather_f64<<<(n + 255) / 256, 256, 0, s>>>(x, perm, xt, n);
 }
-void launch_scatter_f32(const float2* yn, const float2* yf, const int32_t* perm, float2* yc, int n, cudaStream_t s) {
-  k_scatter_f32<<<(n + 255) / 256, 256, 0, s>>>(yn, yf, perm, yc, n);
+void launch_scatter_f32(const float2* yn, const float2* yf, const int32_t* perm, float2* yc, int n, int e0, int e1,
+                        cudaStream_t s) {
+  k_scatter_f32<<<(n + 255) / 256, 256, 0, s>>>(yn, yf, perm, yc, n, e0, e1);
 }
-void launch_scatter_f64(const float2* yn, const float2* yf, const int32_t* perm, double2* yc, int n, cudaStream_t s) {
-  k_scatter_f64<<<(n + 255) / 256, 256, 0, s>>>(yn, yf, perm, yc, n);
+void launch_scatter_f64(const float2* yn, const float2* yf, const int32_t* perm, double2* yc, int n, int e0, int e1,
+                        cudaStream_t s) {
+  k_scatter_f64<<<(n + 255) / 256, 256, 0, s>>>(yn, yf, perm, yc, n, e0, e1);
 }
 
 // ------------------------------------------------------------------ near field (a7)

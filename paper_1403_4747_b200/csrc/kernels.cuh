@@ -49,9 +49,9 @@ struct LeafTask {
 void launch_gather_f32(const float2* x_caller, const int32_t* perm, float2* x_tree, int n, cudaStream_t s);
 void launch_gather_f64(const double2* x_caller, const int32_t* perm, float2* x_tree, int n, cudaStream_t s);
 void launch_scatter_f32(const float2* y_near, const float2* y_far, const int32_t* perm, float2* y_caller, int n,
-                        cudaStream_t s);
+                        int e0, int e1, cudaStream_t s);
 void launch_scatter_f64(const float2* y_near, const float2* y_far, const int32_t* perm, double2* y_caller, int n,
-                        cudaStream_t s);
+                        int e0, int e1, cudaStream_t s);
 void launch_near(int nleaf, const int32_t* order, const int32_t* leaf_begin, const int32_t* leaf_end, const int32_t* near_ptr,
                  const int32_t* near_idx, const float4* near_off, const float4* tgt_pos, const float4* tgt_nrm,
                  const SrcElem* src, const float* src_w, const int32_t* corr_ptr, const int32_t* corr_col,

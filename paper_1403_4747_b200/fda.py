@@ -21,13 +21,14 @@ LIB_PATH = os.path.join(_HERE, "libfda.so")
 
 FDA_HOST = 0
 FDA_DEVICE = 1
+FDA_LOCAL = 2
 
 STATUS = {0: "FDA_OK", 1: "FDA_E_INVALID_ARG", 2: "FDA_E_MESH", 3: "FDA_E_NOMEM", 4: "FDA_E_CUDA",
           5: "FDA_E_NCCL", 6: "FDA_E_NOT_CONVERGED", 7: "FDA_E_STATE", 8: "FDA_E_INTERNAL"}
 
 # every symbol include/fda.h declares
 EXPORTS = ["fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_apply", "bm_solve",
-           "fda_stats",
+           "fda_stats", "fda_nccl_unique_id", "fda_comm_init",
            "fda_set_profiling", "fda_stage_times", "fda_debug_table", "fda_last_error", "fda_status_string",
            "fda_free"]
 
@@ -50,7 +51,8 @@ class fda_options(ctypes.Structure):
                 ("tier1_rho", ctypes.c_double), ("tier2_rho", ctypes.c_double), ("direct_all", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("build_threads", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("verbose", ctypes.c_int32), ("m2l_lowrank", ctypes.c_int32),
-                ("rhs_operator", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("rhs_operator", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
 
 
 class fda_solve_info(ctypes.Structure):
@@ -87,6 +89,8 @@ def load_library(path: str = LIB_PATH):
     lib.fda_rhs_apply.argtypes = [vp, vp, vp, i32, vp]
     lib.bm_solve.argtypes = [vp, vp, vp, dp, i32, i32, ctypes.POINTER(fda_solve_info), i32]
     lib.fda_stats.argtypes = [vp, ctypes.POINTER(fda_build_info)]
+    lib.fda_nccl_unique_id.argtypes = [vp]
+    lib.fda_comm_init.argtypes = [vp, vp]
     lib.fda_set_profiling.argtypes = [vp, i32]
     lib.fda_stage_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)]
     lib.fda_debug_table.argtypes = [vp, ctypes.c_char_p, vp, ctypes.POINTER(i64), ctypes.POINTER(i32)]
@@ -97,7 +101,7 @@ def load_library(path: str = LIB_PATH):
     lib.fda_free.argtypes = [vp]
     lib.fda_free.restype = None
     for name in ("fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_apply", "bm_solve",
-                 "fda_stats",
+                 "fda_stats", "fda_nccl_unique_id", "fda_comm_init",
                  "fda_set_profiling", "fda_stage_times", "fda_debug_table"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -162,16 +166,39 @@ class FDA:
             raise FdaError(st, self.lib.fda_last_error(self.ctx).decode())
 
     # -- calls
-    def matvec(self, x, y=None, stream=None):
+    def comm_init(self, group=None):
+        """Sharded contexts (nranks > 1): create the library's NCCL communicator.
+        The 128-byte NCCL id is made on rank 0 by the library and broadcast
+        with torch.distributed (plumbing only)."""
+        import torch
+        import torch.distributed as dist
+        buf = torch.zeros(128, dtype=torch.uint8)
+        if self.opt.rank == 0:
+            idb = (ctypes.c_uint8 * 128)()
+            st = self.lib.fda_nccl_unique_id(ctypes.byref(idb))
+            if st != 0:
+                raise FdaError(st, self.lib.fda_last_error(None).decode())
+            buf = torch.tensor(list(idb), dtype=torch.uint8)
+        if dist.get_backend(group) == "nccl":
+            b = buf.cuda()
+            dist.broadcast(b, src=0, group=group)
+            buf = b.cpu()
+        else:
+            dist.broadcast(buf, src=0, group=group)
+        idb = (ctypes.c_uint8 * 128)(*buf.tolist())
+        self._check(self.lib.fda_comm_init(self.ctx, ctypes.byref(idb)))
+
+    def matvec(self, x, y=None, stream=None, local: bool = False):
         """y = A x.  numpy complex128 → numpy complex128 (host path), or torch
-        complex64 CUDA tensors (device path, asynchronous on ``stream``)."""
-        return self._apply(self.lib.fda_matvec, x, y, stream)
+        complex64 CUDA tensors (device path, asynchronous on ``stream``).
+        local=True (sharded contexts): this rank's rows only, no collective."""
+        return self._apply(self.lib.fda_matvec, x, y, stream, FDA_LOCAL if local else 0)
 
-    def rhs_apply(self, v, b=None, stream=None):
+    def rhs_apply(self, v, b=None, stream=None, local: bool = False):
         """b = B v, the right-hand-side operator of Eq. (4) (needs rhs_operator=1)."""
-        return self._apply(self.lib.fda_rhs_apply, v, b, stream)
+        return self._apply(self.lib.fda_rhs_apply, v, b, stream, FDA_LOCAL if local else 0)
 
-    def _apply(self, fn, x, y=None, stream=None):
+    def _apply(self, fn, x, y=None, stream=None, extra: int = 0):
         if _is_torch(x) and not x.is_cuda:
             # host tensors (e.g. pinned complex128): host path with raw pointers
             import torch
@@ -179,7 +206,7 @@ class FDA:
                 raise ValueError("host x must be a contiguous complex128 tensor of length n")
             if y is None:
                 y = torch.empty_like(x)
-            self._check(fn(self.ctx, x.data_ptr(), y.data_ptr(), FDA_HOST, None))
+            self._check(fn(self.ctx, x.data_ptr(), y.data_ptr(), FDA_HOST | extra, None))
             return y
         if _is_torch(x):
             import torch
@@ -188,13 +215,13 @@ class FDA:
             if y is None:
                 y = torch.empty_like(x)
             s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
-            self._check(fn(self.ctx, x.data_ptr(), y.data_ptr(), FDA_DEVICE, s))
+            self._check(fn(self.ctx, x.data_ptr(), y.data_ptr(), FDA_DEVICE | extra, s))
             return y
         xh = np.ascontiguousarray(x, dtype=np.complex128)
         if xh.shape != (self.n,):
             raise ValueError("x must have length n")
         yh = np.empty(self.n, dtype=np.complex128) if y is None else y
-        self._check(fn(self.ctx, _ptr_np(xh), _ptr_np(yh), FDA_HOST, None))
+        self._check(fn(self.ctx, _ptr_np(xh), _ptr_np(yh), FDA_HOST | extra, None))
         return yh
 
     def rhs_plane_wave(self, direction, device: bool = False):
@@ -253,7 +280,7 @@ class FDA:
                "mats": np.int64, "specs": np.int64, "pool": np.complex64, "near_ptr": np.int64,
                "near_idx": np.int64, "corr_ptr": np.int64, "corr_col": np.int64, "corr_val": np.complex64,
                "out_states": np.int64, "in_states": np.int64, "boxes": np.int64, "box_center": np.float64,
-               "levels": np.float64, "root": np.float64, "launches": np.int64}
+               "levels": np.float64, "root": np.float64, "launches": np.int64, "owned": np.int64}
 
     def table(self, name: str) -> np.ndarray:
         """A host-side build table (host-logic tests only)."""

@@ -37,9 +37,11 @@ def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bo
     P3, W3 = O.RULE_Q3
     Yq = np.einsum("qa,jad->jqd", P3, V)             # (n,3,3) quadrature points
     k, alpha = f.k, f.alpha
+    own = f.table("owned")          # sharded builds: this rank's leaves [l0, l1) / elements [e0, e1)
+    l0, l1, e0, e1 = (int(v) for v in own)
     if near:
         nptr, nidx = f.table("near_ptr"), f.table("near_idx")
-        for i in range(nl):
+        for i in range(l0, l1):
             tb, te = lr[i]
             src = np.concatenate([np.arange(*lr[j]) for j in nidx[nptr[i]:nptr[i + 1]]])
             X = cen[tb:te][:, None, None, :]
@@ -54,7 +56,8 @@ def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bo
         cp, cc = f.table("corr_ptr" + sfx), f.table("corr_col" + sfx)
         cv = f.table("corr_val" + sfx).astype(np.complex128)
         rows = np.repeat(np.arange(n), np.diff(cp))
-        np.add.at(y, rows, cv * xt[cc])
+        m = (rows >= e0) & (rows < e1)
+        np.add.at(y, rows[m], (cv * xt[cc])[m])
     if far:
         pool = f.table("pool")
         mats = f.table("mats").reshape(-1, 3)

@@ -231,3 +231,25 @@ def test_pulsating_table2_on_gpu(lib, row):
     assert info["converged"]
     assert abs(err / r["l2_error_eps1e-3"] - 1) < g["tolerance_rel"]
     assert _rel(u, u_ref) <= SOLVE_TOL
+
+
+def test_sharded_partials_sum_to_full_operator(lib):
+    """Sharded build: for R = 3 ranks, each rank's FDA_LOCAL
+    matvec (its own rows, zero elsewhere, no collective) run on this GPU, and
+    the sum equals the unsharded matvec; a sharded context refuses the
+    collective path before fda_comm_init."""
+    V, F = icosphere(4, 0.5)
+    k = 40.0
+    x = random_density(len(F), 9)
+    full = lib(V, F, k, 1j / k, 1e-4, max_leaf=16).matvec(x)
+    acc = np.zeros(len(F), dtype=complex)
+    for r in range(3):
+        f = lib(V, F, k, 1j / k, 1e-4, max_leaf=16, rank=r, nranks=3)
+        part = f.matvec(x, local=True)
+        l0, l1, e0, e1 = f.table("owned")
+        assert np.count_nonzero(part) <= e1 - e0
+        acc += part
+        if r == 0:
+            with pytest.raises(Exception):
+                f.matvec(x)
+    assert _rel(acc, full) < 1e-5
