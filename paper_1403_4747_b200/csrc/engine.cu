@@ -122,7 +122,11 @@ struct Dev {
   int n_s2m = 0, n_l2t = 0, max_T = 0;
   std::vector<XStage> m2m, l2l;
   XStage m2l;                      // all levels at once (M2L levels are independent)
-  XStage m2l_a, m2l_b;             // §4.2 factored M2L: tmp = V̂ src ; in += Û tmp
+  XStage m2l_a, m2l_b;             // §4.2 factored M2L with r > 32: tmp = V̂ src ; in += Û tmp
+  LrTask* lr_tasks = nullptr;      // §4.2 factored M2L with r ≤ 32: fused kernel
+  int64_t* lr_src = nullptr;
+  int64_t* lr_dst = nullptr;
+  int n_lr = 0;
   float2* tmpb = nullptr;
   int64_t tmp_size = 0;
   cudaStream_t s_cap = nullptr;
@@ -426,10 +430,42 @@ fda_status engine_create(Context* ctx) {
     fda_status s;
     if ((s = build_xstage(ctx, d, all_m2l, true, d->m2l)) != FDA_OK) return s;
     std::vector<XOp> a, b;
+    std::vector<LrOp> fused;
     for (const LrOp& o : p.m2l_lr) {
+      if (p.mats[o.matV].rows <= 32) {
+        fused.push_back(o);
+        continue;
+      }
       a.push_back({p.out_offset[o.src], o.tmp, o.matV});
       b.push_back({o.tmp, p.in_offset[o.dst], o.matU});
     }
+    // fused tasks: ops grouped by factor pair, ≤ LR_O ops per CTA
+    std::stable_sort(fused.begin(), fused.end(), [](const LrOp& x, const LrOp& y) {
+      return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
+    });
+    std::vector<LrTask> lt;
+    std::vector<int64_t> ls, ld;
+    for (size_t i = 0; i < fused.size();) {
+      size_t j = i;
+      while (j < fused.size() && fused[j].matV == fused[i].matV && j - i < (size_t)LR_O) ++j;
+      LrTask tk;
+      tk.v_off = p.mats[fused[i].matV].offset;
+      tk.u_off = p.mats[fused[i].matU].offset;
+      tk.T = p.mats[fused[i].matV].cols;
+      tk.r = p.mats[fused[i].matV].rows;
+      tk.op_begin = (int32_t)ls.size();
+      tk.op_count = (int32_t)(j - i);
+      for (size_t q = i; q < j; ++q) {
+        ls.push_back(p.out_offset[fused[q].src]);
+        ld.push_back(p.in_offset[fused[q].dst]);
+      }
+      lt.push_back(tk);
+      i = j;
+    }
+    d->n_lr = (int)lt.size();
+    UP(&d->lr_tasks, lt.data(), lt.size());
+    UP(&d->lr_src, ls.data(), ls.size());
+    UP(&d->lr_dst, ld.data(), ld.size());
     if ((s = build_xstage(ctx, d, a, false, d->m2l_a)) != FDA_OK) return s;
     if ((s = build_xstage(ctx, d, b, true, d->m2l_b)) != FDA_OK) return s;
     d->tmp_size = p.tmp_size;
@@ -441,6 +477,7 @@ fda_status engine_create(Context* ctx) {
   for (auto& st : d->m2m) cnt(st);
   for (auto& st : d->l2l) cnt(st);
   cnt(d->m2l); cnt(d->m2l_a); cnt(d->m2l_b);
+  nl += d->n_lr > 0;
   ctx->launches_per_matvec = nl;
   CK(cudaStreamCreateWithFlags(&d->s_near, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&d->s_cap, cudaStreamNonBlocking));
@@ -536,6 +573,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
     launch_stage(st, d->pool, d->outb, d->outb, s);
   }
   if (prof) CK(cudaEventRecord(d->ev[3], s));
+  launch_m2l_lr(d->n_lr, d->lr_tasks, d->lr_src, d->lr_dst, d->pool, d->outb, d->inb, s);
   launch_stage(d->m2l_a, d->pool, d->outb, d->tmpb, s);
   launch_stage(d->m2l, d->pool, d->outb, d->inb, s);
   launch_stage(d->m2l_b, d->pool, d->tmpb, d->inb, s);

@@ -73,6 +73,13 @@ constexpr int NEAR_NT = 128;
 constexpr int NEAR_MAXS = 256;
 constexpr int NEAR_MAXL = 256;
 
+// MUFU.RSQ without the denormal guard of rsqrtf (r² ≥ 1e-12 here, never denormal)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // One Q3 point of the LHS kernel, accumulated into acc:
 //   acc += [∂G/∂n_y + α ∂²G/∂n_x∂n_y](x, y) · w      (w = x_j A_j/(12π))
 // With q = kr, a = ∂r/∂n_x, b = ∂r/∂n_y, c = n_x·n_y:
@@ -84,7 +91,7 @@ __device__ __forceinline__ void lhs_eval(float3 x, float3 nx, float3 y, float3 n
                                          const KernelParams& kp, float2& acc) {
   const float dx = x.x - y.x, dy = x.y - y.y, dz = x.z - y.z;
   const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-  const float ir = rsqrtf(r2);
+  const float ir = rsqrt_ftz(r2);
   const float q = kp.k * (r2 * ir);
   const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * ir;   // ∂r/∂n_x
   const float b = -fmaf(dx, ny.x, fmaf(dy, ny.y, dz * ny.z)) * ir;  // ∂r/∂n_y
@@ -117,7 +124,7 @@ __device__ __forceinline__ void rhs_eval(float3 x, float3 nx, float3 y, float2 w
                                          float2& acc) {
   const float dx = x.x - y.x, dy = x.y - y.y, dz = x.z - y.z;
   const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-  const float ir = rsqrtf(r2);
+  const float ir = rsqrt_ftz(r2);
   const float r = r2 * ir;
   const float q = kp.k * r;
   const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * ir;
@@ -443,6 +450,133 @@ void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const
     default: XL(1, 16); break;
   }
 #undef XL
+}
+
+// ------------------------------------------------------------------ fused §4.2 M2L (a4)
+// PAPER.md §4.2: K̃ ≈ Û V̂.  One CTA handles ≤ 64 ops of one K̃:
+// phase 1 tmp = V̂ S (r ≤ 32 rows, K = T streamed through a cp.async double
+// buffer, 2×8 complex register tile per thread), tmp kept in shared memory;
+// phase 2 for each 32-row tile of Û: out = Û_tile tmp (K = r from shared
+// memory), accumulated into the destination states with vector atomics.
+__global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
+                                                const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
+                                                const float2* __restrict__ src, float2* __restrict__ dst) {
+  constexpr int R = 32, O = LR_O;
+  // phase 1: sM[2][XK][R] + sS[2][XK][O+1]; phase 2 (aliased): tmp[R][O+1] + sU[R][R+1]
+  constexpr int P1 = 2 * XK * R + 2 * XK * (O + 1);
+  constexpr int P2 = R * (O + 1) + R * (R + 1);
+  __shared__ __align__(16) float2 sh[P1 > P2 ? P1 : P2];
+  __shared__ int64_t soff[O];
+  float2(*sM)[XK][R] = reinterpret_cast<float2(*)[XK][R]>(sh);
+  float2(*sS)[XK][O + 1] = reinterpret_cast<float2(*)[XK][O + 1]>(sh + 2 * XK * R);
+  float2(*tmp)[O + 1] = reinterpret_cast<float2(*)[O + 1]>(sh);
+  float2(*sU)[R + 1] = reinterpret_cast<float2(*)[R + 1]>(sh + R * (O + 1));
+  const LrTask t = tasks[blockIdx.x];
+  const int tid = threadIdx.x, tr = tid & 15, to = tid >> 4;
+  for (int p = tid; p < O; p += 128) soff[p] = p < t.op_count ? src_off[t.op_begin + p] : -1;
+  __syncthreads();
+  const float2* __restrict__ V = pool + t.v_off;
+  const float2* __restrict__ U = pool + t.u_off;
+  auto issue = [&](int buf, int k0) {
+#pragma unroll
+    for (int e = 0; e < XK * R / 128; ++e) {
+      const int idx = tid + 128 * e;
+      const int kk = idx / R, row = idx % R, col = k0 + kk;
+      const bool ok = row < t.r && col < t.T;
+      cp_async8(&sM[buf][kk][row], ok ? (const void*)(V + (int64_t)col * t.r + row) : (const void*)V, ok);
+    }
+#pragma unroll
+    for (int e = 0; e < XK * O / 128; ++e) {
+      const int idx = tid + 128 * e;
+      const int p = idx / XK, kk = idx % XK, col = k0 + kk;
+      const int64_t so = soff[p];
+      const bool ok = so >= 0 && col < t.T;
+      cp_async8(&sS[buf][kk][p], ok ? (const void*)(src + so + col) : (const void*)src, ok);
+    }
+    cp_async_commit();
+  };
+  float2 acc[2][8];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  issue(0, 0);
+  int buf = 0;
+  for (int k0 = 0; k0 < t.T; k0 += XK) {
+    if (k0 + XK < t.T) {
+      issue(buf ^ 1, k0 + XK);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_0();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < XK; ++kk) {
+      float2 m[2], sv[8];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) m[i] = sM[buf][kk][tr + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sv[j] = sS[buf][kk][to + 8 * j];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc[i][j].x = fmaf(m[i].x, sv[j].x, fmaf(-m[i].y, sv[j].y, acc[i][j].x));
+          acc[i][j].y = fmaf(m[i].x, sv[j].y, fmaf(m[i].y, sv[j].x, acc[i][j].y));
+        }
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  // tmp[row][op] (rows ≥ r are zero because V̂ rows ≥ r were zero-filled)
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tmp[tr + 16 * i][to + 8 * j] = acc[i][j];
+  __syncthreads();
+  for (int r0 = 0; r0 < t.T; r0 += R) {
+    for (int idx = tid; idx < R * R; idx += 128) {   // sU[row][c] = Û[r0 + row, c]
+      const int c = idx / R, row = idx % R;
+      sU[row][c] = (r0 + row < t.T && c < t.r) ? __ldg(U + (int64_t)c * t.T + r0 + row) : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    for (int c = 0; c < t.r; ++c) {
+      float2 m[2], sv[8];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) m[i] = sU[tr + 16 * i][c];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sv[j] = tmp[c][to + 8 * j];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc[i][j].x = fmaf(m[i].x, sv[j].x, fmaf(-m[i].y, sv[j].y, acc[i][j].x));
+          acc[i][j].y = fmaf(m[i].x, sv[j].y, fmaf(m[i].y, sv[j].x, acc[i][j].y));
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int op = to + 8 * j;
+      if (op >= t.op_count) continue;
+      float2* d = dst + dst_off[t.op_begin + op] + r0;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int row = tr + 16 * i;
+        if (r0 + row < t.T) atomicAdd(d + row, acc[i][j]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+void launch_m2l_lr(int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                   const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
+  if (ntask <= 0) return;
+  k_m2l_lr<<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst);
 }
 
 // ------------------------------------------------------------------ GMRES helpers (a9)

@@ -37,6 +37,15 @@ struct XTask {
 inline int xvar_rows(int v) { return v == 0 ? 32 : (v == 1 ? 64 : (v == 2 ? 128 : 16)); }
 inline int xvar_ops(int v) { return v == 0 ? 64 : (v == 1 ? 32 : (v == 2 ? 16 : 128)); }
 
+// fused §4.2 M2L task: for ≤ LR_O ops sharing K̃ ≈ Û V̂ (r ≤ 32):
+// tmp = V̂ · src (r × ops, shared memory), dst += Û · tmp
+constexpr int LR_O = 64;
+struct LrTask {
+  int64_t v_off, u_off;     // V̂ (r × T) and Û (T × r), column-major, in the pool
+  int32_t T, r;
+  int32_t op_begin, op_count;
+};
+
 // leaf-level ops (S2M / L2T)
 struct LeafTask {
   int64_t mat_off;   // -1: no matrix (L2T writes zeros)
@@ -62,6 +71,8 @@ void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const floa
 void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s);
 void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const int64_t* src_off,
                   const int64_t* dst_off, const float2* pool, const float2* src, float2* dst, cudaStream_t s);
+void launch_m2l_lr(int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                   const float2* pool, const float2* src, float2* dst, cudaStream_t s);
 // GMRES / BLAS-1 helpers (fp64 accumulation)
 void launch_dots(const float2* V, int64_t ldv, int nv, const float2* w, int64_t n, double2* partial, int nchunks,
                  cudaStream_t s);

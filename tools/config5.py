@@ -1,0 +1,72 @@
+"""Config 5 (BASELINE configs[4]): icosphere s=9, N = 5,242,880, kD = 1000,
+ε = 1e-4 on one B200: build, matvec time, and parity on 2,000 seeded oracle
+rows.  One JSON line.
+
+    python tools/config5.py [--rows 2000] [--cfg 5]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+    from fda_inputs import config_mesh, CONFIGS, random_density, sampled_rows
+    from paper_1403_4747_b200 import FDA
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg", type=int, default=5)
+    ap.add_argument("--rows", type=int, default=2000)
+    a = ap.parse_args()
+    c = CONFIGS[a.cfg]
+    t0 = time.perf_counter()
+    V, F = config_mesh(a.cfg)
+    t_mesh = time.perf_counter() - t0
+    N = len(F)
+    t0 = time.perf_counter()
+    f = FDA(V, F, c.k, c.alpha, c.eps, verbose=1)
+    t_build = time.perf_counter() - t0
+    st = f.stats()
+    x = random_density(N, c.x_seed)
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda()
+    yd = torch.empty_like(xd)
+    for _ in range(3):
+        f.matvec(xd, yd)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(10):
+        f.matvec(xd, yd)
+    e.record()
+    torch.cuda.synchronize()
+    mv_ms = s.elapsed_time(e) / 10
+    f.set_profiling(True)
+    f.matvec(xd, yd)
+    torch.cuda.synchronize()
+    stages = f.stage_times()
+    f.set_profiling(False)
+    y = yd.cpu().numpy().astype(np.complex128)
+    import oracle as O
+    from oracle import fast
+    rows = sampled_rows(N, a.rows, c.rows_seed)
+    el = O.element_geometry(V, F)
+    t0 = time.perf_counter()
+    yo = fast.matvec_rows(el, rows, x, c.k, c.alpha)
+    t_or = time.perf_counter() - t0
+    err = float(np.linalg.norm(y[rows] - yo) / np.linalg.norm(yo))
+    print(json.dumps({"config": a.cfg, "N": N, "k": c.k, "mesh_s": round(t_mesh, 1), "build_s": round(t_build, 1),
+                      "matvec_ms": round(mv_ms, 3), "stages_ms": {k: round(v, 3) for k, v in stages.items()},
+                      "sampled_rows": len(rows), "rel_l2_sampled": err, "oracle_rows_s": round(t_or, 1),
+                      "oracle_cores": fast.num_threads(),
+                      "tree": {k: st[k] for k in ("n_levels", "n_hf_levels", "n_leaves", "n_m2l_pairs",
+                                                  "n_direct_element_pairs", "n_corrections", "table_bytes",
+                                                  "rank", "dirs")}}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
