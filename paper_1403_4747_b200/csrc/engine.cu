@@ -121,12 +121,25 @@ struct Dev {
   LeafTask *s2m = nullptr, *l2t = nullptr;
   int n_s2m = 0, n_l2t = 0, max_T = 0;
   std::vector<XStage> m2m, l2l;
-  XStage m2l;                      // all levels at once (M2L levels are independent)
-  XStage m2l_a, m2l_b;             // §4.2 factored M2L with r > 32: tmp = V̂ src ; in += Û tmp
-  LrTask* lr_tasks = nullptr;      // §4.2 factored M2L with r ≤ 32: fused kernel
-  int64_t* lr_src = nullptr;
-  int64_t* lr_dst = nullptr;
-  int n_lr = 0;
+  // M2L per level (levels are independent of each other; level l needs only
+  // the outgoing states of level l): dense ops, §4.2 factored ops with r ≤ 32
+  // (fused kernel) and with r > 32 (two stages through tmp)
+  struct M2LLevel {
+    XStage dense, a, b;
+    LrTask* lr_tasks = nullptr;
+    int64_t* lr_src = nullptr;
+    int64_t* lr_dst = nullptr;
+    int n_lr = 0;
+    bool any() const {
+      int n = n_lr;
+      for (int v = 0; v < XV; ++v) n += dense.ntask[v] + a.ntask[v] + b.ntask[v];
+      return n > 0;
+    }
+  };
+  std::vector<M2LLevel> m2lv;
+  static const int kM2LStreams = 3;
+  cudaStream_t s_m2l[kM2LStreams] = {};
+  std::vector<cudaEvent_t> ev_up, ev_m2l;
   float2* tmpb = nullptr;
   int64_t tmp_size = 0;
   cudaStream_t s_cap = nullptr;
@@ -418,69 +431,90 @@ fda_status engine_create(Context* ctx) {
     for (const Op& o : ops) v.push_back({so[o.src], dof[o.dst], o.mat});
     return v;
   };
-  std::vector<XOp> all_m2l;
+  d->m2lv.resize(nlev);
   for (int l = 0; l < nlev; ++l) {
     fda_status s;
     if ((s = build_xstage(ctx, d, xops(p.m2m[l], p.out_offset, p.out_offset), true, d->m2m[l])) != FDA_OK) return s;
     if ((s = build_xstage(ctx, d, xops(p.l2l[l], p.in_offset, p.in_offset), true, d->l2l[l])) != FDA_OK) return s;
-    auto v = xops(p.m2l[l], p.out_offset, p.in_offset);
-    all_m2l.insert(all_m2l.end(), v.begin(), v.end());
+    if ((s = build_xstage(ctx, d, xops(p.m2l[l], p.out_offset, p.in_offset), true, d->m2lv[l].dense)) != FDA_OK)
+      return s;
   }
   {
-    fda_status s;
-    if ((s = build_xstage(ctx, d, all_m2l, true, d->m2l)) != FDA_OK) return s;
-    std::vector<XOp> a, b;
-    std::vector<LrOp> fused;
+    // §4.2 factored ops: r ≤ 32 → fused kernel; r > 32 → tmp = V̂ src (atomic into a zeroed tmp
+    // region, so small stages can be split along K) then in += Û tmp
+    std::vector<std::vector<XOp>> a(nlev), b(nlev);
+    std::vector<std::vector<LrOp>> fused(nlev);
+    int64_t tmp_off = 0;
     for (const LrOp& o : p.m2l_lr) {
       if (p.mats[o.matV].rows <= 32) {
-        fused.push_back(o);
+        fused[o.level].push_back(o);
         continue;
       }
-      a.push_back({p.out_offset[o.src], o.tmp, o.matV});
-      b.push_back({o.tmp, p.in_offset[o.dst], o.matU});
+      a[o.level].push_back({p.out_offset[o.src], tmp_off, o.matV});
+      b[o.level].push_back({tmp_off, p.in_offset[o.dst], o.matU});
+      tmp_off += p.mats[o.matV].rows;
     }
-    // fused tasks: ops grouped by factor pair, ≤ LR_O ops per CTA
-    std::stable_sort(fused.begin(), fused.end(), [](const LrOp& x, const LrOp& y) {
-      return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
-    });
-    std::vector<LrTask> lt;
-    std::vector<int64_t> ls, ld;
-    for (size_t i = 0; i < fused.size();) {
-      size_t j = i;
-      while (j < fused.size() && fused[j].matV == fused[i].matV && j - i < (size_t)LR_O) ++j;
-      LrTask tk;
-      tk.v_off = p.mats[fused[i].matV].offset;
-      tk.u_off = p.mats[fused[i].matU].offset;
-      tk.T = p.mats[fused[i].matV].cols;
-      tk.r = p.mats[fused[i].matV].rows;
-      tk.op_begin = (int32_t)ls.size();
-      tk.op_count = (int32_t)(j - i);
-      for (size_t q = i; q < j; ++q) {
-        ls.push_back(p.out_offset[fused[q].src]);
-        ld.push_back(p.in_offset[fused[q].dst]);
+    d->tmp_size = tmp_off;
+    AL(&d->tmpb, (size_t)std::max<int64_t>(1, tmp_off));
+    for (int l = 0; l < nlev; ++l) {
+      fda_status s;
+      auto& F = fused[l];
+      std::stable_sort(F.begin(), F.end(), [](const LrOp& x, const LrOp& y) {
+        return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
+      });
+      std::vector<LrTask> lt;
+      std::vector<int64_t> ls, ld;
+      for (size_t i = 0; i < F.size();) {
+        size_t j = i;
+        while (j < F.size() && F[j].matV == F[i].matV && j - i < (size_t)LR_O) ++j;
+        LrTask tk;
+        tk.v_off = p.mats[F[i].matV].offset;
+        tk.u_off = p.mats[F[i].matU].offset;
+        tk.T = p.mats[F[i].matV].cols;
+        tk.r = p.mats[F[i].matV].rows;
+        tk.op_begin = (int32_t)ls.size();
+        tk.op_count = (int32_t)(j - i);
+        for (size_t q = i; q < j; ++q) {
+          ls.push_back(p.out_offset[F[q].src]);
+          ld.push_back(p.in_offset[F[q].dst]);
+        }
+        lt.push_back(tk);
+        i = j;
       }
-      lt.push_back(tk);
-      i = j;
+      // longest CTAs first (phase-1 rows 16 or 32, phase-2 row tiles of 32)
+      auto cost = [](const LrTask& t) {
+        const int r1 = t.r <= 16 ? 16 : 32;
+        return (int64_t)(r1 * t.T + ((t.T + 31) / 32) * 32 * t.r) * t.op_count;
+      };
+      std::stable_sort(lt.begin(), lt.end(), [&](const LrTask& x, const LrTask& y) { return cost(x) > cost(y); });
+      Dev::M2LLevel& L = d->m2lv[l];
+      L.n_lr = (int)lt.size();
+      if (L.n_lr) {
+        UP(&L.lr_tasks, lt.data(), lt.size());
+        UP(&L.lr_src, ls.data(), ls.size());
+        UP(&L.lr_dst, ld.data(), ld.size());
+      }
+      if ((s = build_xstage(ctx, d, a[l], true, L.a)) != FDA_OK) return s;
+      if ((s = build_xstage(ctx, d, b[l], true, L.b)) != FDA_OK) return s;
     }
-    d->n_lr = (int)lt.size();
-    UP(&d->lr_tasks, lt.data(), lt.size());
-    UP(&d->lr_src, ls.data(), ls.size());
-    UP(&d->lr_dst, ld.data(), ld.size());
-    if ((s = build_xstage(ctx, d, a, false, d->m2l_a)) != FDA_OK) return s;
-    if ((s = build_xstage(ctx, d, b, true, d->m2l_b)) != FDA_OK) return s;
-    d->tmp_size = p.tmp_size;
-    AL(&d->tmpb, (size_t)std::max<int64_t>(1, p.tmp_size));
   }
   // kernels per matvec: gather, near, s2m, every non-empty translation launch, l2t, scatter
   int64_t nl = 4 + (d->n_s2m > 0);  // gather, near, l2t, scatter (+ s2m)
   auto cnt = [&](const XStage& st) { for (int v = 0; v < XV; ++v) nl += st.ntask[v] > 0; };
   for (auto& st : d->m2m) cnt(st);
   for (auto& st : d->l2l) cnt(st);
-  cnt(d->m2l); cnt(d->m2l_a); cnt(d->m2l_b);
-  nl += d->n_lr > 0;
+  for (auto& L : d->m2lv) {
+    cnt(L.dense); cnt(L.a); cnt(L.b);
+    nl += L.n_lr > 0;
+  }
   ctx->launches_per_matvec = nl;
   CK(cudaStreamCreateWithFlags(&d->s_near, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&d->s_cap, cudaStreamNonBlocking));
+  for (auto& sm : d->s_m2l) CK(cudaStreamCreateWithFlags(&sm, cudaStreamNonBlocking));
+  d->ev_up.resize(nlev);
+  d->ev_m2l.resize(nlev);
+  for (auto& e : d->ev_up) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : d->ev_m2l) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   d->use_graph = ctx->p.opt.use_graph != 0;
   CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
@@ -536,6 +570,10 @@ void engine_destroy(Context* ctx) {
     if (ge) cudaGraphExecDestroy(ge);
   if (d->s_near) cudaStreamDestroy(d->s_near);
   if (d->s_cap) cudaStreamDestroy(d->s_cap);
+  for (auto& sm : d->s_m2l)
+    if (sm) cudaStreamDestroy(sm);
+  for (auto& e : d->ev_up) cudaEventDestroy(e);
+  for (auto& e : d->ev_m2l) cudaEventDestroy(e);
   if (d->ev_fork) cudaEventDestroy(d->ev_fork);
   if (d->ev_join) cudaEventDestroy(d->ev_join);
   for (auto& e : d->ev) if (e) cudaEventDestroy(e);
@@ -564,25 +602,45 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   if (prof) CK(cudaEventRecord(d->ev[1], s));
   if (d->out_size) CK(cudaMemsetAsync(d->outb, 0, sizeof(float2) * d->out_size, s));
   if (d->in_size) CK(cudaMemsetAsync(d->inb, 0, sizeof(float2) * d->in_size, s));
+  if (d->tmp_size) CK(cudaMemsetAsync(d->tmpb, 0, sizeof(float2) * d->tmp_size, s));
   if (kind) launch_s2m(d->n_s2m_rhs, d->s2m_rhs, d->pool, d->x_tree, d->outb, d->max_T, s);
   else launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s);
   if (prof) CK(cudaEventRecord(d->ev[2], s));
   const int nlev = (int)d->m2m.size();
-  for (int l = nlev - 1; l >= 0; --l) {
-    const XStage& st = d->m2m[l];
-    launch_stage(st, d->pool, d->outb, d->outb, s);
+  auto m2l_level = [&](int l, cudaStream_t st) {
+    const Dev::M2LLevel& L = d->m2lv[l];
+    launch_m2l_lr(L.n_lr, L.lr_tasks, L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st);
+    launch_stage(L.dense, d->pool, d->outb, d->inb, st);
+    launch_stage(L.a, d->pool, d->outb, d->tmpb, st);
+    launch_stage(L.b, d->pool, d->tmpb, d->inb, st);
+  };
+  if (prof) {
+    // serialised: every stage time is the isolated duration of its kernels
+    for (int l = nlev - 1; l >= 0; --l) launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);
+    CK(cudaEventRecord(d->ev[3], s));
+    for (int l = 0; l < nlev; ++l) m2l_level(l, s);
+    CK(cudaEventRecord(d->ev[4], s));
+    for (int l = 0; l < nlev; ++l) launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
+    CK(cudaEventRecord(d->ev[5], s));
+  } else {
+    // dependency DAG: the M2L of level l (own stream) starts as soon as the
+    // outgoing states of level l exist, overlapping the M2M chain above it;
+    // L2L out of level l waits for the M2L into level l.
+    int k = 0;
+    for (int l = nlev - 1; l >= 0; --l) {
+      launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);   // writes level-l out-states
+      if (!d->m2lv[l].any()) continue;
+      cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];
+      CK(cudaEventRecord(d->ev_up[l], s));
+      CK(cudaStreamWaitEvent(sm, d->ev_up[l], 0));
+      m2l_level(l, sm);
+      CK(cudaEventRecord(d->ev_m2l[l], sm));
+    }
+    for (int l = 0; l < nlev; ++l) {
+      if (d->m2lv[l].any()) CK(cudaStreamWaitEvent(s, d->ev_m2l[l], 0));
+      launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
+    }
   }
-  if (prof) CK(cudaEventRecord(d->ev[3], s));
-  launch_m2l_lr(d->n_lr, d->lr_tasks, d->lr_src, d->lr_dst, d->pool, d->outb, d->inb, s);
-  launch_stage(d->m2l_a, d->pool, d->outb, d->tmpb, s);
-  launch_stage(d->m2l, d->pool, d->outb, d->inb, s);
-  launch_stage(d->m2l_b, d->pool, d->tmpb, d->inb, s);
-  if (prof) CK(cudaEventRecord(d->ev[4], s));
-  for (int l = 0; l < nlev; ++l) {
-    const XStage& st = d->l2l[l];
-    launch_stage(st, d->pool, d->inb, d->inb, s);
-  }
-  if (prof) CK(cudaEventRecord(d->ev[5], s));
   launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
   if (prof) CK(cudaEventRecord(d->ev[6], s));
   CK(cudaStreamWaitEvent(s, d->ev_join, 0));

@@ -458,30 +458,27 @@ void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const
 // buffer, 2×8 complex register tile per thread), tmp kept in shared memory;
 // phase 2 for each 32-row tile of Û: out = Û_tile tmp (K = r from shared
 // memory), accumulated into the destination states with vector atomics.
-__global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
-                                                const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
-                                                const float2* __restrict__ src, float2* __restrict__ dst) {
-  constexpr int R = 32, O = LR_O;
-  // phase 1: sM[2][XK][R] + sS[2][XK][O+1]; phase 2 (aliased): tmp[R][O+1] + sU[R][R+1]
-  constexpr int P1 = 2 * XK * R + 2 * XK * (O + 1);
-  constexpr int P2 = R * (O + 1) + R * (R + 1);
-  __shared__ __align__(16) float2 sh[P1 > P2 ? P1 : P2];
-  __shared__ int64_t soff[O];
+constexpr int LR_SH1 = 2 * XK * 32 + 2 * XK * (LR_O + 1);   // phase 1: sM[2][XK][32] + sS[2][XK][O+1]
+constexpr int LR_SH2 = 32 * (LR_O + 1) + 32 * 33;            // phase 2: tmp[32][O+1] + sU[32][33]
+constexpr int LR_SH = LR_SH1 > LR_SH2 ? LR_SH1 : LR_SH2;
+
+template <int MR1>  // phase-1 rows = 16·MR1 ≥ r
+__device__ __forceinline__ void m2l_lr_body(const LrTask& t, float2* sh, int64_t* soff,
+                                            const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
+                                            const float2* __restrict__ src, float2* __restrict__ dst) {
+  constexpr int R = 32, O = LR_O, R1 = 16 * MR1;
   float2(*sM)[XK][R] = reinterpret_cast<float2(*)[XK][R]>(sh);
   float2(*sS)[XK][O + 1] = reinterpret_cast<float2(*)[XK][O + 1]>(sh + 2 * XK * R);
   float2(*tmp)[O + 1] = reinterpret_cast<float2(*)[O + 1]>(sh);
   float2(*sU)[R + 1] = reinterpret_cast<float2(*)[R + 1]>(sh + R * (O + 1));
-  const LrTask t = tasks[blockIdx.x];
   const int tid = threadIdx.x, tr = tid & 15, to = tid >> 4;
-  for (int p = tid; p < O; p += 128) soff[p] = p < t.op_count ? src_off[t.op_begin + p] : -1;
-  __syncthreads();
   const float2* __restrict__ V = pool + t.v_off;
   const float2* __restrict__ U = pool + t.u_off;
   auto issue = [&](int buf, int k0) {
 #pragma unroll
-    for (int e = 0; e < XK * R / 128; ++e) {
+    for (int e = 0; e < XK * R1 / 128; ++e) {
       const int idx = tid + 128 * e;
-      const int kk = idx / R, row = idx % R, col = k0 + kk;
+      const int kk = idx / R1, row = idx % R1, col = k0 + kk;
       const bool ok = row < t.r && col < t.T;
       cp_async8(&sM[buf][kk][row], ok ? (const void*)(V + (int64_t)col * t.r + row) : (const void*)V, ok);
     }
@@ -501,6 +498,7 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
   issue(0, 0);
+  static_assert(MR1 == 1 || MR1 == 2, "phase-1 rows");
   int buf = 0;
   for (int k0 = 0; k0 < t.T; k0 += XK) {
     if (k0 + XK < t.T) {
@@ -512,13 +510,13 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < XK; ++kk) {
-      float2 m[2], sv[8];
+      float2 m[MR1], sv[8];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) m[i] = sM[buf][kk][tr + 16 * i];
+      for (int i = 0; i < MR1; ++i) m[i] = sM[buf][kk][tr + 16 * i];
 #pragma unroll
       for (int j = 0; j < 8; ++j) sv[j] = sS[buf][kk][to + 8 * j];
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < MR1; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           acc[i][j].x = fmaf(m[i].x, sv[j].x, fmaf(-m[i].y, sv[j].y, acc[i][j].x));
@@ -530,7 +528,7 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
   }
   // tmp[row][op] (rows ≥ r are zero because V̂ rows ≥ r were zero-filled)
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < MR1; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) tmp[tr + 16 * i][to + 8 * j] = acc[i][j];
   __syncthreads();
@@ -544,6 +542,7 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
+#pragma unroll 4
     for (int c = 0; c < t.r; ++c) {
       float2 m[2], sv[8];
 #pragma unroll
@@ -571,6 +570,18 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
     }
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
+                                                const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
+                                                const float2* __restrict__ src, float2* __restrict__ dst) {
+  __shared__ __align__(16) float2 sh[LR_SH];
+  __shared__ int64_t soff[LR_O];
+  const LrTask t = tasks[blockIdx.x];
+  for (int p = threadIdx.x; p < LR_O; p += 128) soff[p] = p < t.op_count ? src_off[t.op_begin + p] : -1;
+  __syncthreads();
+  if (t.r <= 16) m2l_lr_body<1>(t, sh, soff, dst_off, pool, src, dst);
+  else m2l_lr_body<2>(t, sh, soff, dst_off, pool, src, dst);
 }
 
 void launch_m2l_lr(int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,

@@ -72,7 +72,7 @@ void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const floa
 void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const int64_t* src_off,
                   const int64_t* dst_off, const float2* pool, const float2* src, float2* dst, cudaStream_t s);
 void launch_m2l_lr(int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,
-                   const float2* pool, const float2* src, float2* dst, cudaStream_t s);
+                   const float2* pool, const float2* src, float2* dst, cudaStream_t s);    // r ≤ 32
 // GMRES / BLAS-1 helpers (fp64 accumulation)
 void launch_dots(const float2* V, int64_t ldv, int nv, const float2* w, int64_t n, double2* partial, int nchunks,
                  cudaStream_t s);
