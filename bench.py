@@ -140,10 +140,11 @@ def run_fda(args):
         # sharded operator: one NCCL all-reduce of y per matvec
         threads = max(1, (os.cpu_count() or ws) // ws)
         f = FDA(V, F, c.k, c.alpha, c.eps, device=local, max_leaf=c.max_leaf, rank=rank, nranks=ws,
-                build_threads=threads)
+                build_threads=threads, tensor_cores=args.tensor_cores, m2l_lowrank=args.m2l_lowrank)
         f.comm_init()
     else:
-        f = FDA(V, F, c.k, c.alpha, c.eps, device=local, max_leaf=c.max_leaf)
+        f = FDA(V, F, c.k, c.alpha, c.eps, device=local, max_leaf=c.max_leaf, tensor_cores=args.tensor_cores,
+                m2l_lowrank=args.m2l_lowrank)
     build_s = time.perf_counter() - t0
     st = f.stats()
     x = torch.from_numpy(random_density(N, c.x_seed).astype(np.complex64)).to(dev)
@@ -237,6 +238,7 @@ def run_fda(args):
             "config": {"workload": f"config {c.cfg}: {c.name}, eps={c.eps}, leaf {c.max_leaf}, plane wave "
                                    f"{list(np.round(c.direction, 4))}",
                        "N": N, "k": c.k, "alpha": "i/k", "eps": c.eps, "l2_flush": "256 MB write between steps",
+                       "tensor_cores": bool(args.tensor_cores), "m2l_lowrank": bool(args.m2l_lowrank),
                        "parallelism": f"octree-sharded x{ws} (NCCL all-reduce of y)" if ws > 1 else "single GPU"},
             "matvecs_per_s": round(1e3 / ms, 2),
             "roofline": roof,
@@ -326,6 +328,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=1000)
     ap.add_argument("--ref-rows", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tensor-cores", type=int, default=0, help="dense translations on tcgen05 (3xTF32)")
+    ap.add_argument("--m2l-lowrank", type=int, default=1, help="§4.2 second-stage SVD of the M2L matrices")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

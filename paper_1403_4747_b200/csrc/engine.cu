@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <unordered_map>
 #include <vector>
 
 #include "fda_internal.h"
@@ -30,9 +31,12 @@ namespace fda {
     }                                                                              \
   } while (0)
 
-// one translation op in offsets: dst[dof : +rows] (+)= M[mat] · src[so : +cols]
+// one translation op in offsets: dst[dof : +rows] (+)= M[mat] · src[so : +cols];
+// sp / stp: the source's tensor-core plane offset and plane length (-1: not a state)
 struct XOp {
   int64_t so, dof, mat;
+  int64_t sp = -1;
+  int32_t stp = 0;
 };
 
 // ------------------------------------------------------------------ NCCL (loaded on first use)
@@ -84,6 +88,8 @@ fda_status nccl_unique_id(void* id128, std::string& err) {
 
 struct XStage {
   bool atomic = true;
+  TcTask* tc = nullptr;            // tensor-core tasks (opt.tensor_cores)
+  int n_tc = 0;
   XTask* tasks[XV] = {};
   int ntask[XV] = {};
   int64_t* src = nullptr;
@@ -131,7 +137,7 @@ struct Dev {
     int64_t* lr_dst = nullptr;
     int n_lr = 0;
     bool any() const {
-      int n = n_lr;
+      int n = n_lr + dense.n_tc + a.n_tc + b.n_tc;
       for (int v = 0; v < XV; ++v) n += dense.ntask[v] + a.ntask[v] + b.ntask[v];
       return n > 0;
     }
@@ -151,6 +157,17 @@ struct Dev {
   KernelParams kp{};
   bool timed = false;
   std::vector<void*> allocs;
+  // tensor-core operand pool: per matrix, per 64-row block, per 32-column chunk: [hi | lo] A tiles
+  bool use_tc = false;
+  std::vector<float> tc_host;
+  std::unordered_map<int64_t, int64_t> tc_off;   // matrix id → float offset
+  float* tcpool = nullptr;
+  // pre-split state planes for the tensor-core B operand (4 planes × Tp per state)
+  float *outp = nullptr, *inp = nullptr;
+  std::vector<int64_t> pout_off, pin_off;          // per state (host)
+  int64_t *d_out_off = nullptr, *d_in_off = nullptr, *d_pout = nullptr, *d_pin = nullptr;
+  std::vector<int> lvl_T, lvl_Tp;
+  std::vector<int64_t> out_lb, in_lb;              // per level state ranges (size nlev+1)
 };
 
 template <class T>
@@ -178,11 +195,56 @@ static fda_status alloc(Context* ctx, Dev* d, T** dst, size_t count) {
     if (s_ != FDA_OK) return s_;               \
   } while (0)
 
+// ---- tensor-core operand layout (kernels_tc.cu): A = [M_r; M_i] per 64-row block,
+// TF32 hi/lo, canonical K-major core matrices: element (m, k) of a 128 × 32 tile at
+// ((k/4 · 16 + m/8) · 8 + m%8) · 4 + k%4, chunks of TC_KC columns
+static inline float tf32_rna(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;  // round to nearest, ties away
+  float y;
+  std::memcpy(&y, &u, 4);
+  return y;
+}
+
+static int64_t tc_matrix(Context* ctx, Dev* d, int64_t m) {
+  auto it = d->tc_off.find(m);
+  if (it != d->tc_off.end()) return it->second;
+  const Plan& p = ctx->plan;
+  const MatInfo& mi = p.mats[m];
+  const int R = mi.rows, C = mi.cols, nblk = (R + 63) / 64, nkc = (C + TC_KC - 1) / TC_KC;
+  const int TILE = 128 * TC_KC;
+  const int64_t off = (int64_t)d->tc_host.size();
+  d->tc_host.resize(d->tc_host.size() + (size_t)nblk * nkc * 2 * TILE, 0.0f);
+  float* base = d->tc_host.data() + off;
+  const cf* M = p.pool.data() + mi.offset;
+  for (int b = 0; b < nblk; ++b)
+    for (int kc = 0; kc < nkc; ++kc) {
+      float* hi = base + ((size_t)b * nkc + kc) * 2 * TILE;
+      float* lo = hi + TILE;
+      for (int mrow = 0; mrow < 128; ++mrow) {
+        const int i = b * 64 + (mrow & 63), plane = mrow >> 6;
+        for (int k = 0; k < TC_KC; ++k) {
+          const int j = kc * TC_KC + k;
+          float x = 0.0f;
+          if (i < R && j < C) x = plane ? M[(size_t)j * R + i].imag() : M[(size_t)j * R + i].real();
+          const float h = tf32_rna(x), l = tf32_rna(x - h);
+          const int idx = (((k >> 2) * 16 + (mrow >> 3)) * 8 + (mrow & 7)) * 4 + (k & 3);
+          hi[idx] = h;
+          lo[idx] = l;
+        }
+      }
+    }
+  d->tc_off.emplace(m, off);
+  return off;
+}
+
 // Group the ops of one stage (one level, or all M2L levels at once) by matrix
 // and cut each group into tiles of the kernel variant (rows × ops per CTA)
 // that pads the group least.  Stages with fewer CTAs than ~4 waves are split
 // along K (cols) so that small, latency-bound stages still fill the GPU.
-static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops, bool atomic, XStage& st) {
+static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops, bool atomic, XStage& st,
+                               bool tc_ok = true) {
   const Plan& p = ctx->plan;
   st.atomic = atomic;
   if (ops.empty()) return FDA_OK;
@@ -193,6 +255,42 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   });
   std::vector<int64_t> so, dof;
   std::vector<XTask> tasks[XV];
+  if (d->use_tc && atomic && tc_ok) {
+    std::vector<TcTask> tct;
+    for (size_t i = 0; i < ord.size();) {
+      const int64_t m = ops[ord[i]].mat;
+      size_t j = i;
+      while (j < ord.size() && ops[ord[j]].mat == m) ++j;
+      const int R = p.mats[m].rows, C = p.mats[m].cols, nkc = (C + TC_KC - 1) / TC_KC;
+      const int64_t off = tc_matrix(ctx, d, m);
+      const int32_t base = (int32_t)so.size();
+      for (size_t q = i; q < j; ++q) {
+        so.push_back(ops[ord[q]].sp);   // plane offset of the pre-split source state
+        dof.push_back(ops[ord[q]].dof);
+      }
+      const int32_t tp = ops[ord[i]].stp;
+      const int64_t nops = (int64_t)(j - i);
+      for (int64_t c0 = 0; c0 < nops; c0 += 64)
+        for (int b = 0; b < (R + 63) / 64; ++b) {
+          TcTask t;
+          t.a_off = off + (int64_t)b * nkc * 2 * (128 * TC_KC);
+          t.nkc = nkc;
+          t.R = R;
+          t.C = C;
+          t.row0 = b * 64;
+          t.op_begin = base + (int32_t)c0;
+          t.op_count = (int32_t)std::min<int64_t>(64, nops - c0);
+          t.Tp = tp;
+          tct.push_back(t);
+        }
+      i = j;
+    }
+    st.n_tc = (int)tct.size();
+    UP(&st.tc, tct.data(), tct.size());
+    UP(&st.src, so.data(), so.size());
+    UP(&st.dst, dof.data(), dof.size());
+    return FDA_OK;
+  }
   size_t i = 0;
   while (i < ord.size()) {
     const int64_t m = ops[ord[i]].mat;
@@ -259,7 +357,11 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   return FDA_OK;
 }
 
-static void launch_stage(const XStage& st, const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
+static const float* g_tcpool = nullptr;   // set per context before launches (single-threaded use)
+
+static void launch_stage(const XStage& st, const float2* pool, const float2* src, float2* dst, cudaStream_t s,
+                         const float* srcp = nullptr) {
+  if (st.n_tc) launch_xlate_tc(st.n_tc, st.tc, st.src, st.dst, g_tcpool, srcp, dst, s);
   for (int v = 0; v < XV; ++v)
     if (st.ntask[v]) launch_xlate(v, st.atomic, st.ntask[v], st.tasks[v], st.src, st.dst, pool, src, dst, s);
 }
@@ -286,6 +388,8 @@ fda_status engine_create(Context* ctx) {
   d->kp.k = (float)ctx->p.k;
   d->kp.alpha_re = (float)ctx->p.alpha.real();
   d->kp.alpha_im = (float)ctx->p.alpha.imag();
+  d->use_tc = ctx->p.opt.tensor_cores != 0;
+  if (d->use_tc) CK(tc_prepare());
 
   // leaf-local element data (fp32 offsets from the owning leaf centre, computed in fp64)
   std::vector<float4> tpos(n), tnrm(n);
@@ -425,18 +529,56 @@ fda_status engine_create(Context* ctx) {
 
   const int nlev = (int)t.levels.size();
   d->m2m.resize(nlev); d->l2l.resize(nlev);
-  auto xops = [](const std::vector<Op>& ops, const std::vector<int64_t>& so, const std::vector<int64_t>& dof) {
+  // tensor-core source planes: state s of level l → 4 planes of Tp_l floats
+  d->lvl_T.assign(nlev, 0);
+  d->lvl_Tp.assign(nlev, 0);
+  for (int l = 0; l < nlev; ++l) {
+    d->lvl_T[l] = t.levels[l].rank;
+    d->lvl_Tp[l] = ((t.levels[l].rank + TC_KC - 1) / TC_KC) * TC_KC;
+  }
+  d->out_lb = p.out_level_begin;
+  d->in_lb = p.in_level_begin;
+  auto plane_offsets = [&](const std::vector<State>& S, std::vector<int64_t>& po) {
+    po.resize(S.size());
+    int64_t o = 0;
+    for (size_t i = 0; i < S.size(); ++i) {
+      po[i] = o;
+      o += 4 * (int64_t)d->lvl_Tp[t.boxes[S[i].box].level];
+    }
+    return o;
+  };
+  const int64_t pout_size = plane_offsets(p.out_states, d->pout_off);
+  const int64_t pin_size = plane_offsets(p.in_states, d->pin_off);
+  if (d->use_tc) {
+    AL(&d->outp, (size_t)std::max<int64_t>(1, pout_size));
+    AL(&d->inp, (size_t)std::max<int64_t>(1, pin_size));
+    UP(&d->d_out_off, p.out_offset.data(), p.out_offset.size());
+    UP(&d->d_in_off, p.in_offset.data(), p.in_offset.size());
+    UP(&d->d_pout, d->pout_off.data(), d->pout_off.size());
+    UP(&d->d_pin, d->pin_off.data(), d->pin_off.size());
+  }
+  auto xops = [&](const std::vector<Op>& ops, const std::vector<int64_t>& so, const std::vector<int64_t>& dof,
+                  bool src_in) {
     std::vector<XOp> v;
     v.reserve(ops.size());
-    for (const Op& o : ops) v.push_back({so[o.src], dof[o.dst], o.mat});
+    for (const Op& o : ops) {
+      XOp x{so[o.src], dof[o.dst], o.mat};
+      const State& ss = src_in ? p.in_states[o.src] : p.out_states[o.src];
+      x.sp = src_in ? d->pin_off[o.src] : d->pout_off[o.src];
+      x.stp = d->lvl_Tp[t.boxes[ss.box].level];
+      v.push_back(x);
+    }
     return v;
   };
   d->m2lv.resize(nlev);
   for (int l = 0; l < nlev; ++l) {
     fda_status s;
-    if ((s = build_xstage(ctx, d, xops(p.m2m[l], p.out_offset, p.out_offset), true, d->m2m[l])) != FDA_OK) return s;
-    if ((s = build_xstage(ctx, d, xops(p.l2l[l], p.in_offset, p.in_offset), true, d->l2l[l])) != FDA_OK) return s;
-    if ((s = build_xstage(ctx, d, xops(p.m2l[l], p.out_offset, p.in_offset), true, d->m2lv[l].dense)) != FDA_OK)
+    if ((s = build_xstage(ctx, d, xops(p.m2m[l], p.out_offset, p.out_offset, false), true, d->m2m[l])) != FDA_OK)
+      return s;
+    if ((s = build_xstage(ctx, d, xops(p.l2l[l], p.in_offset, p.in_offset, true), true, d->l2l[l])) != FDA_OK)
+      return s;
+    if ((s = build_xstage(ctx, d, xops(p.m2l[l], p.out_offset, p.in_offset, false), true, d->m2lv[l].dense)) !=
+        FDA_OK)
       return s;
   }
   {
@@ -450,7 +592,10 @@ fda_status engine_create(Context* ctx) {
         fused[o.level].push_back(o);
         continue;
       }
-      a[o.level].push_back({p.out_offset[o.src], tmp_off, o.matV});
+      XOp xa{p.out_offset[o.src], tmp_off, o.matV};
+      xa.sp = d->pout_off[o.src];
+      xa.stp = d->lvl_Tp[o.level];
+      a[o.level].push_back(xa);
       b[o.level].push_back({tmp_off, p.in_offset[o.dst], o.matU});
       tmp_off += p.mats[o.matV].rows;
     }
@@ -495,12 +640,21 @@ fda_status engine_create(Context* ctx) {
         UP(&L.lr_dst, ld.data(), ld.size());
       }
       if ((s = build_xstage(ctx, d, a[l], true, L.a)) != FDA_OK) return s;
-      if ((s = build_xstage(ctx, d, b[l], true, L.b)) != FDA_OK) return s;
+      if ((s = build_xstage(ctx, d, b[l], true, L.b, /*tc_ok=*/false)) != FDA_OK) return s;
     }
+  }
+  if (d->use_tc) {
+    UP(&d->tcpool, d->tc_host.data(), d->tc_host.size());
+    std::vector<float>().swap(d->tc_host);
   }
   // kernels per matvec: gather, near, s2m, every non-empty translation launch, l2t, scatter
   int64_t nl = 4 + (d->n_s2m > 0);  // gather, near, l2t, scatter (+ s2m)
-  auto cnt = [&](const XStage& st) { for (int v = 0; v < XV; ++v) nl += st.ntask[v] > 0; };
+  if (d->use_tc)  // per-level state splits
+    for (int l = 0; l < nlev; ++l) nl += (d->out_lb[l + 1] > d->out_lb[l]) + (d->in_lb[l + 1] > d->in_lb[l]);
+  auto cnt = [&](const XStage& st) {
+    nl += st.n_tc > 0;
+    for (int v = 0; v < XV; ++v) nl += st.ntask[v] > 0;
+  };
   for (auto& st : d->m2m) cnt(st);
   for (auto& st : d->l2l) cnt(st);
   for (auto& L : d->m2lv) {
@@ -585,6 +739,7 @@ void engine_destroy(Context* ctx) {
 
 // the device part of one matvec: x_tree → y_near, y_far (tree order)
 static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
+  g_tcpool = d->tcpool;
   // profiling mode serialises the near field on the main stream so that every
   // stage time is the isolated duration of its kernels
   const bool prof = ctx->profiling;
@@ -610,17 +765,34 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   auto m2l_level = [&](int l, cudaStream_t st) {
     const Dev::M2LLevel& L = d->m2lv[l];
     launch_m2l_lr(L.n_lr, L.lr_tasks, L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st);
-    launch_stage(L.dense, d->pool, d->outb, d->inb, st);
-    launch_stage(L.a, d->pool, d->outb, d->tmpb, st);
+    launch_stage(L.dense, d->pool, d->outb, d->inb, st, d->outp);
+    launch_stage(L.a, d->pool, d->outb, d->tmpb, st, d->outp);
     launch_stage(L.b, d->pool, d->tmpb, d->inb, st);
+  };
+  // tensor-core path: pre-split a completed level of out- / in-states into planes
+  auto split_out = [&](int l, cudaStream_t st) {
+    if (d->use_tc)
+      launch_split_states(d->outb, d->d_out_off, d->d_pout, d->lvl_T[l], d->lvl_Tp[l], d->out_lb[l],
+                          d->out_lb[l + 1], d->outp, st);
+  };
+  auto split_in = [&](int l, cudaStream_t st) {
+    if (d->use_tc)
+      launch_split_states(d->inb, d->d_in_off, d->d_pin, d->lvl_T[l], d->lvl_Tp[l], d->in_lb[l], d->in_lb[l + 1],
+                          d->inp, st);
   };
   if (prof) {
     // serialised: every stage time is the isolated duration of its kernels
-    for (int l = nlev - 1; l >= 0; --l) launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);
+    for (int l = nlev - 1; l >= 0; --l) {
+      launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s, d->outp);
+      split_out(l, s);
+    }
     CK(cudaEventRecord(d->ev[3], s));
     for (int l = 0; l < nlev; ++l) m2l_level(l, s);
     CK(cudaEventRecord(d->ev[4], s));
-    for (int l = 0; l < nlev; ++l) launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
+    for (int l = 0; l < nlev; ++l) {
+      split_in(l, s);
+      launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s, d->inp);
+    }
     CK(cudaEventRecord(d->ev[5], s));
   } else {
     // dependency DAG: the M2L of level l (own stream) starts as soon as the
@@ -628,7 +800,8 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
     // L2L out of level l waits for the M2L into level l.
     int k = 0;
     for (int l = nlev - 1; l >= 0; --l) {
-      launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);   // writes level-l out-states
+      launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s, d->outp);   // writes level-l out-states
+      split_out(l, s);
       if (!d->m2lv[l].any()) continue;
       cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];
       CK(cudaEventRecord(d->ev_up[l], s));
@@ -638,7 +811,8 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
     }
     for (int l = 0; l < nlev; ++l) {
       if (d->m2lv[l].any()) CK(cudaStreamWaitEvent(s, d->ev_m2l[l], 0));
-      launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
+      split_in(l, s);
+      launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s, d->inp);
     }
   }
   launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);

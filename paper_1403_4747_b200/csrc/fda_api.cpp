@@ -43,6 +43,7 @@ fda_status fda_options_default(fda_options* opt) {
   opt->rhs_operator = 0;
   opt->rank = 0;
   opt->nranks = 1;
+  opt->tensor_cores = 0;
   return FDA_OK;
 }
 

@@ -46,6 +46,18 @@ struct LrTask {
   int32_t op_begin, op_count;
 };
 
+// tcgen05 translation task (kernels_tc.cu): ≤ 64 complex rows × ≤ 64 ops of one matrix;
+// A operand pre-laid-out per 64-row block and TC_KC-column chunk as [hi | lo] tiles of 128 × TC_KC floats
+constexpr int TC_KC = 16;
+struct TcTask {
+  int64_t a_off;      // float offset of this row block's pre-laid-out [chunk][hi|lo] A tiles
+  int32_t nkc;        // TC_KC-column chunks
+  int32_t R, C;       // matrix shape (complex)
+  int32_t row0;       // first complex row of the block
+  int32_t op_begin, op_count;
+  int32_t Tp;         // plane length of the (pre-split) source states
+};
+
 // leaf-level ops (S2M / L2T)
 struct LeafTask {
   int64_t mat_off;   // -1: no matrix (L2T writes zeros)
@@ -73,6 +85,11 @@ void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const
                   const int64_t* dst_off, const float2* pool, const float2* src, float2* dst, cudaStream_t s);
 void launch_m2l_lr(int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                    const float2* pool, const float2* src, float2* dst, cudaStream_t s);    // r ≤ 32
+void launch_xlate_tc(int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                     const float* tcpool, const float* srcp, float2* dst, cudaStream_t s);
+void launch_split_states(const float2* states, const int64_t* off, const int64_t* poff, int T, int Tp, int64_t s0,
+                         int64_t s1, float* planes, cudaStream_t s);
+cudaError_t tc_prepare();
 // GMRES / BLAS-1 helpers (fp64 accumulation)
 void launch_dots(const float2* V, int64_t ldv, int nv, const float2* w, int64_t n, double2* partial, int nchunks,
                  cudaStream_t s);

@@ -52,7 +52,7 @@ class fda_options(ctypes.Structure):
                 ("device", ctypes.c_int32), ("build_threads", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("verbose", ctypes.c_int32), ("m2l_lowrank", ctypes.c_int32),
                 ("rhs_operator", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("tensor_cores", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
 class fda_solve_info(ctypes.Structure):

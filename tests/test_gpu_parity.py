@@ -253,3 +253,18 @@ def test_sharded_partials_sum_to_full_operator(lib):
             with pytest.raises(Exception):
                 f.matvec(x)
     assert _rel(acc, full) < 1e-5
+
+
+@pytest.mark.parametrize("lowrank", [1, 0])
+def test_tensor_core_translations(lib, lowrank):
+    """tcgen05 3xTF32 translation path (opt.tensor_cores): same operator as the
+    CUDA-core path to fp32 rounding, and within the gate vs the oracle."""
+    V, F = icosphere(4, 0.5)
+    k = 40.0
+    x = random_density(len(F), 5)
+    y0 = lib(V, F, k, 1j / k, 1e-4, max_leaf=16, m2l_lowrank=lowrank).matvec(x)
+    y1 = lib(V, F, k, 1j / k, 1e-4, max_leaf=16, m2l_lowrank=lowrank, tensor_cores=1).matvec(x)
+    assert _rel(y1, y0) < 1e-5
+    el = O.element_geometry(V, F)
+    yo = fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k)
+    assert _rel(y1, yo) <= MATVEC_TOL

@@ -22,6 +22,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", type=int, default=5)
     ap.add_argument("--rows", type=int, default=2000)
+    ap.add_argument("--tc", type=int, default=0)
+    ap.add_argument("--no-oracle", action="store_true")
     a = ap.parse_args()
     c = CONFIGS[a.cfg]
     t0 = time.perf_counter()
@@ -29,7 +31,7 @@ def main():
     t_mesh = time.perf_counter() - t0
     N = len(F)
     t0 = time.perf_counter()
-    f = FDA(V, F, c.k, c.alpha, c.eps, verbose=1)
+    f = FDA(V, F, c.k, c.alpha, c.eps, verbose=1, tensor_cores=a.tc)
     t_build = time.perf_counter() - t0
     st = f.stats()
     x = random_density(N, c.x_seed)
@@ -54,14 +56,16 @@ def main():
     import oracle as O
     from oracle import fast
     rows = sampled_rows(N, a.rows, c.rows_seed)
-    el = O.element_geometry(V, F)
-    t0 = time.perf_counter()
-    yo = fast.matvec_rows(el, rows, x, c.k, c.alpha)
-    t_or = time.perf_counter() - t0
-    err = float(np.linalg.norm(y[rows] - yo) / np.linalg.norm(yo))
+    err, t_or = None, None
+    if not a.no_oracle:
+        el = O.element_geometry(V, F)
+        t0 = time.perf_counter()
+        yo = fast.matvec_rows(el, rows, x, c.k, c.alpha)
+        t_or = time.perf_counter() - t0
+        err = float(np.linalg.norm(y[rows] - yo) / np.linalg.norm(yo))
     print(json.dumps({"config": a.cfg, "N": N, "k": c.k, "mesh_s": round(t_mesh, 1), "build_s": round(t_build, 1),
                       "matvec_ms": round(mv_ms, 3), "stages_ms": {k: round(v, 3) for k, v in stages.items()},
-                      "sampled_rows": len(rows), "rel_l2_sampled": err, "oracle_rows_s": round(t_or, 1),
+                      "sampled_rows": len(rows), "rel_l2_sampled": err, "oracle_rows_s": t_or, "tensor_cores": bool(a.tc),
                       "oracle_cores": fast.num_threads(),
                       "tree": {k: st[k] for k in ("n_levels", "n_hf_levels", "n_leaves", "n_m2l_pairs",
                                                   "n_direct_element_pairs", "n_corrections", "table_bytes",
