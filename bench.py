@@ -31,6 +31,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FDA Burton-Miller matvec ms and GMRES solve s vs N,kD; %FP32/HBM roofline"
 FP32_FLOPS_PER_EVAL = 62        # FP32 flops (FFMA = 2) of one near-field kernel evaluation
+# ncu --set full capture of one whole config-2 matvec (tools/gpu_ncu_full.sh → tools/ncu_summary.py):
+# source of roofline.traffic (dram bytes read + written) for the dominant stage
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r01_ncu_full_matvec_config2.json")
+STAGE_KERNELS = {"near": ("k_near",), "m2l": ("k_m2l_lr",), "s2m": ("k_s2m",), "l2t": ("k_l2t",)}
 SMS, FP32_LANES = 148, 128
 
 
@@ -121,6 +125,20 @@ def _stage_work(f, N):
     return work
 
 
+def _traffic(stage):
+    """DRAM bytes (read + write) of one matvec's launches of `stage` from the
+    committed ncu summary, or None when the stage's kernels are not uniquely named."""
+    names = STAGE_KERNELS.get(stage)
+    try:
+        launches = json.load(open(PROFILE_SUMMARY))["launches"]
+    except Exception:
+        return None
+    if not names:
+        return None
+    tot = [l.get("traffic_B") for l in launches if any(n in l["kernel"] for n in names)]
+    return float(sum(tot)) if tot and None not in tot else None
+
+
 def run_fda(args):
     import torch
     import torch.distributed as dist
@@ -208,7 +226,7 @@ def run_fda(args):
         stages[sname] = e
     dom = max((s for s in stages if "frac" in stages[s]), key=lambda s: stages[s]["ms"])
     roof = {k: stages[dom][k] for k in ("bound", "achieved", "peak", "unit", "frac")}
-    roof.update({"kernel": dom, "traffic": None, "peak_source": src})
+    roof.update({"kernel": dom, "traffic": _traffic(dom) if args.config == 2 else None, "peak_source": src})
     launches = int(f.table("launches")[0])   # exact count of our kernels per matvec (engine.cu)
 
     # e2e: the C-ABI call with pinned HOST buffers (H2D + D2H inside the timed region)

@@ -107,8 +107,8 @@ struct Dev {
   float4 *tgt_pos = nullptr, *tgt_nrm = nullptr;
   SrcElem* src = nullptr;
   float* src_w = nullptr;
-  int32_t *leaf_begin = nullptr, *leaf_end = nullptr, *near_ptr = nullptr, *near_idx = nullptr;
-  int32_t* near_order = nullptr;   // leaves by descending near-field work (LPT block order)
+  NearTask* near_tasks = nullptr;  // one per owned leaf, by descending near-field work (LPT block order)
+  int2* near_slots = nullptr;      // per task: (source element, index into near_off) of every direct source
   bool alpha_pure_imag = false;
   int n_near = 0;                  // near-field CTAs (owned leaves)
   int e0 = 0, e1 = 0;              // owned element range (tree order)
@@ -132,12 +132,12 @@ struct Dev {
   // (fused kernel) and with r > 32 (two stages through tmp)
   struct M2LLevel {
     XStage dense, a, b;
-    LrTask* lr_tasks = nullptr;
+    LrTask* lr_tasks[3] = {};        // fused §4.2 tasks per phase-1 row class (m2l_lr_class)
+    int n_lr[3] = {};
     int64_t* lr_src = nullptr;
     int64_t* lr_dst = nullptr;
-    int n_lr = 0;
     bool any() const {
-      int n = n_lr + dense.n_tc + a.n_tc + b.n_tc;
+      int n = n_lr[0] + n_lr[1] + n_lr[2] + dense.n_tc + a.n_tc + b.n_tc;
       for (int v = 0; v < XV; ++v) n += dense.ntask[v] + a.ntask[v] + b.ntask[v];
       return n > 0;
     }
@@ -388,32 +388,36 @@ fda_status engine_create(Context* ctx) {
   d->kp.k = (float)ctx->p.k;
   d->kp.alpha_re = (float)ctx->p.alpha.real();
   d->kp.alpha_im = (float)ctx->p.alpha.imag();
+  d->kp.ak_re = (float)(ctx->p.k * ctx->p.alpha.real());
+  d->kp.ak_im = (float)(ctx->p.k * ctx->p.alpha.imag());
+  d->kp.inv_k = (float)(1.0 / ctx->p.k);
   d->use_tc = ctx->p.opt.tensor_cores != 0;
   if (d->use_tc) CK(tc_prepare());
+  CK(m2l_lr_prepare());
 
-  // leaf-local element data (fp32 offsets from the owning leaf centre, computed in fp64)
+  // leaf-local element data in wave units (fp32 k·(offset from the owning leaf
+  // centre), computed in fp64); the near kernel's weight carries k² (kernels.cu)
+  const double kw = ctx->p.k;
   std::vector<float4> tpos(n), tnrm(n);
   std::vector<SrcElem> src(n);
   std::vector<float> w(n);
-  std::vector<int32_t> lb(nleaf), le(nleaf), perm(n);
+  std::vector<int32_t> perm(n);
   std::vector<double> cen(3 * (size_t)n), nrm(3 * (size_t)n);
   const double inv12pi = 1.0 / (12.0 * M_PI);  // Q3 weight 1/3 and 1/(4π)
   for (int i = 0; i < nleaf; ++i) {
     const Box& B = t.boxes[t.leaves[i]];
     if (B.end - B.begin > 128) { ctx->err = "leaf with more than 128 elements (depth cap hit)"; return FDA_E_INTERNAL; }
-    lb[i] = (int32_t)B.begin;
-    le[i] = (int32_t)B.end;
     for (int64_t e = B.begin; e < B.end; ++e) {
-      Vec3 x = g.centroid[e] - B.center;
+      Vec3 x = (g.centroid[e] - B.center) * kw;
       tpos[e] = make_float4((float)x.x, (float)x.y, (float)x.z, 0.f);
       tnrm[e] = make_float4((float)g.normal[e].x, (float)g.normal[e].y, (float)g.normal[e].z, 0.f);
       Vec3 q[3];
       for (int k = 0; k < 3; ++k)
-        q[k] = g.v0[e] * Q3_BARY[k][0] + g.v1[e] * Q3_BARY[k][1] + g.v2[e] * Q3_BARY[k][2] - B.center;
+        q[k] = (g.v0[e] * Q3_BARY[k][0] + g.v1[e] * Q3_BARY[k][1] + g.v2[e] * Q3_BARY[k][2] - B.center) * kw;
       src[e].a = make_float4((float)q[0].x, (float)q[0].y, (float)q[0].z, (float)g.normal[e].x);
       src[e].b = make_float4((float)q[1].x, (float)q[1].y, (float)q[1].z, (float)g.normal[e].y);
       src[e].c = make_float4((float)q[2].x, (float)q[2].y, (float)q[2].z, (float)g.normal[e].z);
-      w[e] = (float)(g.area[e] * inv12pi);
+      w[e] = (float)(g.area[e] * inv12pi * kw * kw);
     }
   }
   for (int i = 0; i < n; ++i) {
@@ -421,13 +425,12 @@ fda_status engine_create(Context* ctx) {
     cen[3 * i] = g.centroid[i].x; cen[3 * i + 1] = g.centroid[i].y; cen[3 * i + 2] = g.centroid[i].z;
     nrm[3 * i] = g.normal[i].x; nrm[3 * i + 1] = g.normal[i].y; nrm[3 * i + 2] = g.normal[i].z;
   }
-  std::vector<int32_t> nptr(p.near_ptr.begin(), p.near_ptr.end()), nidx(p.near_idx.begin(), p.near_idx.end());
   std::vector<float4> noff(p.near_idx.size());
   for (int i = 0; i < nleaf; ++i) {
     const Box& B = t.boxes[t.leaves[i]];
     for (int64_t e = p.near_ptr[i]; e < p.near_ptr[i + 1]; ++e) {
       const Box& C = t.boxes[t.leaves[p.near_idx[e]]];
-      Vec3 o = B.center - C.center;
+      Vec3 o = (B.center - C.center) * kw;
       noff[e] = make_float4((float)o.x, (float)o.y, (float)o.z, 0.f);
     }
   }
@@ -437,23 +440,32 @@ fda_status engine_create(Context* ctx) {
   }
   std::vector<int32_t> cptr(p.corr_ptr.begin(), p.corr_ptr.end()), ccol(p.corr_col.begin(), p.corr_col.end());
   // LPT order of the near-field CTAs: estimated work = targets × (3·sources + corrections)
-  std::vector<int64_t> work(nleaf, 0);
+  std::vector<int64_t> work(nleaf, 0), nsrc(nleaf, 0);
   for (int i = 0; i < nleaf; ++i) {
     const Box& B = t.boxes[t.leaves[i]];
-    int64_t srcs = 0;
     for (int64_t e = p.near_ptr[i]; e < p.near_ptr[i + 1]; ++e) {
       const Box& C = t.boxes[t.leaves[p.near_idx[e]]];
-      srcs += C.end - C.begin;
+      nsrc[i] += C.end - C.begin;
     }
-    work[i] = (B.end - B.begin) * 3 * srcs + (p.corr_ptr[B.end] - p.corr_ptr[B.begin]);
+    work[i] = (B.end - B.begin) * 3 * nsrc[i] + (p.corr_ptr[B.end] - p.corr_ptr[B.begin]);
   }
-  std::vector<int32_t> order(nleaf);
-  for (int i = 0; i < nleaf; ++i) order[i] = i;
+  std::vector<int32_t> order;
+  for (int i = 0; i < nleaf; ++i)   // sharded: this rank evaluates the near field of its own leaves only
+    if (i >= p.own_leaf0 && i < p.own_leaf1) order.push_back(i);
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
-  // sharded: this rank evaluates the near field of its own leaves only
-  order.erase(std::remove_if(order.begin(), order.end(),
-                             [&](int32_t i) { return i < p.own_leaf0 || i >= p.own_leaf1; }),
-              order.end());
+  std::vector<NearTask> ntask;
+  std::vector<int2> slots;
+  for (int32_t i : order) {
+    const Box& B = t.boxes[t.leaves[i]];
+    NearTask nt{(int32_t)B.begin, (int32_t)(B.end - B.begin), (int32_t)slots.size(), 0};
+    for (int64_t e = p.near_ptr[i]; e < p.near_ptr[i + 1]; ++e) {
+      const Box& C = t.boxes[t.leaves[p.near_idx[e]]];
+      for (int64_t el = C.begin; el < C.end; ++el) slots.push_back(make_int2((int)el, (int)e));
+    }
+    if (slots.size() >= (size_t)INT32_MAX) { ctx->err = "near-field slot table too large"; return FDA_E_INTERNAL; }
+    nt.s1 = (int32_t)slots.size();
+    ntask.push_back(nt);
+  }
   d->n_near = (int)order.size();
   d->e0 = (int)p.own_e0;
   d->e1 = (int)p.own_e1;
@@ -465,11 +477,8 @@ fda_status engine_create(Context* ctx) {
   UP(&d->tgt_nrm, tnrm.data(), tnrm.size());
   UP(&d->src, src.data(), src.size());
   UP(&d->src_w, w.data(), w.size());
-  UP(&d->leaf_begin, lb.data(), lb.size());
-  UP(&d->leaf_end, le.data(), le.size());
-  UP(&d->near_ptr, nptr.data(), nptr.size());
-  UP(&d->near_idx, nidx.data(), nidx.size());
-  UP(&d->near_order, order.data(), order.size());
+  UP(&d->near_tasks, ntask.data(), ntask.size());
+  UP(&d->near_slots, slots.data(), slots.size());
   UP(&d->near_off, noff.data(), noff.size());
   UP(&d->corr_ptr, cptr.data(), cptr.size());
   UP(&d->corr_col, ccol.data(), ccol.size());
@@ -505,6 +514,7 @@ fda_status engine_create(Context* ctx) {
                   (int32_t)(B.end - B.begin), T, 0};
       s2m.push_back(lt);
       d->max_T = std::max(d->max_T, T);
+      if (T > 320) { ctx->err = "rank above 320"; return FDA_E_INTERNAL; }
       if (ctx->p.opt.rhs_operator && p.leaf_S_rhs[i] >= 0) {
         LeafTask lr = lt;
         lr.mat_off = p.mats[p.leaf_S_rhs[i]].offset;
@@ -582,13 +592,13 @@ fda_status engine_create(Context* ctx) {
       return s;
   }
   {
-    // §4.2 factored ops: r ≤ 32 → fused kernel; r > 32 → tmp = V̂ src (atomic into a zeroed tmp
+    // §4.2 factored ops: r ≤ 64 → fused kernel; r > 64 → tmp = V̂ src (atomic into a zeroed tmp
     // region, so small stages can be split along K) then in += Û tmp
     std::vector<std::vector<XOp>> a(nlev), b(nlev);
     std::vector<std::vector<LrOp>> fused(nlev);
     int64_t tmp_off = 0;
     for (const LrOp& o : p.m2l_lr) {
-      if (p.mats[o.matV].rows <= 32) {
+      if (p.mats[o.matV].rows <= LR_MAX_R) {
         fused[o.level].push_back(o);
         continue;
       }
@@ -607,7 +617,7 @@ fda_status engine_create(Context* ctx) {
       std::stable_sort(F.begin(), F.end(), [](const LrOp& x, const LrOp& y) {
         return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
       });
-      std::vector<LrTask> lt;
+      std::vector<LrTask> lt[3];
       std::vector<int64_t> ls, ld;
       for (size_t i = 0; i < F.size();) {
         size_t j = i;
@@ -623,19 +633,22 @@ fda_status engine_create(Context* ctx) {
           ls.push_back(p.out_offset[F[q].src]);
           ld.push_back(p.in_offset[F[q].dst]);
         }
-        lt.push_back(tk);
+        lt[m2l_lr_class(tk.r)].push_back(tk);
         i = j;
       }
-      // longest CTAs first (phase-1 rows 16 or 32, phase-2 row tiles of 32)
+      // longest CTAs first (phase-1 rows 16 / 32 / 64, phase-2 row tiles of 32)
       auto cost = [](const LrTask& t) {
-        const int r1 = t.r <= 16 ? 16 : 32;
+        const int r1 = 16 << m2l_lr_class(t.r);
         return (int64_t)(r1 * t.T + ((t.T + 31) / 32) * 32 * t.r) * t.op_count;
       };
-      std::stable_sort(lt.begin(), lt.end(), [&](const LrTask& x, const LrTask& y) { return cost(x) > cost(y); });
       Dev::M2LLevel& L = d->m2lv[l];
-      L.n_lr = (int)lt.size();
-      if (L.n_lr) {
-        UP(&L.lr_tasks, lt.data(), lt.size());
+      for (int c = 0; c < 3; ++c) {
+        std::stable_sort(lt[c].begin(), lt[c].end(),
+                         [&](const LrTask& x, const LrTask& y) { return cost(x) > cost(y); });
+        L.n_lr[c] = (int)lt[c].size();
+        if (L.n_lr[c]) UP(&L.lr_tasks[c], lt[c].data(), lt[c].size());
+      }
+      if (!ls.empty()) {
         UP(&L.lr_src, ls.data(), ls.size());
         UP(&L.lr_dst, ld.data(), ld.size());
       }
@@ -659,7 +672,7 @@ fda_status engine_create(Context* ctx) {
   for (auto& st : d->l2l) cnt(st);
   for (auto& L : d->m2lv) {
     cnt(L.dense); cnt(L.a); cnt(L.b);
-    nl += L.n_lr > 0;
+    for (int c = 0; c < 3; ++c) nl += L.n_lr[c] > 0;
   }
   ctx->launches_per_matvec = nl;
   CK(cudaStreamCreateWithFlags(&d->s_near, cudaStreamNonBlocking));
@@ -747,10 +760,9 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   CK(cudaEventRecord(d->ev_fork, s));
   CK(cudaStreamWaitEvent(sn, d->ev_fork, 0));
   if (prof) CK(cudaEventRecord(d->ev_n0, sn));
-  launch_near(d->n_near, d->near_order, d->leaf_begin, d->leaf_end, d->near_ptr, d->near_idx, d->near_off,
-              d->tgt_pos, d->tgt_nrm, d->src, d->src_w, kind ? d->corr_ptr_rhs : d->corr_ptr,
-              kind ? d->corr_col_rhs : d->corr_col, kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near,
-              d->kp, d->alpha_pure_imag, kind, sn);
+  launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
+              kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
+              kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, sn);
   if (prof) CK(cudaEventRecord(d->ev_n1, sn));
   CK(cudaEventRecord(d->ev_join, sn));
 
@@ -764,7 +776,8 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   const int nlev = (int)d->m2m.size();
   auto m2l_level = [&](int l, cudaStream_t st) {
     const Dev::M2LLevel& L = d->m2lv[l];
-    launch_m2l_lr(L.n_lr, L.lr_tasks, L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st);
+    for (int c = 2; c >= 0; --c)
+      launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st);
     launch_stage(L.dense, d->pool, d->outb, d->inb, st, d->outp);
     launch_stage(L.a, d->pool, d->outb, d->tmpb, st, d->outp);
     launch_stage(L.b, d->pool, d->tmpb, d->inb, st);

@@ -66,180 +66,153 @@ void launch_scatter_f64(const float2* yn, const float2* yf, const int32_t* perm,
 // ------------------------------------------------------------------ near field (a7)
 // y_i = Σ_{j ∈ direct(i)} A^{Q3}_ij x_j + Σ_{j: ρ_ij<3} C_ij x_j
 // A^{Q3}_ij = (A_j/3) Σ_q [∂G/∂n_y + α ∂²G/∂n_x∂n_y](x_i, y_jq)   (Eq. 5)
-// One CTA per target leaf; the source elements of all direct leaves are staged
-// through shared memory in chunks; P = ⌊NT/n_B⌋ threads share one target and
-// split the sources; partial sums are reduced in shared memory.
+//
+// Positions are in WAVE UNITS X = k·x (leaf-local, fp32 offsets computed in
+// fp64), so r² in these units is q² = (kr)² and 1/r = k·rsqrt(q²); the k² of
+// 1/r² is folded into the per-source weight w_j = k² A_j/(12π) x_j, and the
+// constant k of α·k into KernelParams.  Per (target, source element) the
+// kernel values of the three Q3 points are summed first and multiplied by
+// w_j once.
 constexpr int NEAR_NT = 128;
 constexpr int NEAR_MAXS = 256;
-constexpr int NEAR_MAXL = 256;
 
-// MUFU.RSQ without the denormal guard of rsqrtf (r² ≥ 1e-12 here, never denormal)
+// MUFU.RSQ without the denormal guard of rsqrtf (q² ≥ 1e-12 here, never denormal)
 __device__ __forceinline__ float rsqrt_ftz(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
-// One Q3 point of the LHS kernel, accumulated into acc:
-//   acc += [∂G/∂n_y + α ∂²G/∂n_x∂n_y](x, y) · w      (w = x_j A_j/(12π))
-// With q = kr, a = ∂r/∂n_x, b = ∂r/∂n_y, c = n_x·n_y:
+// One Q3 point of the LHS kernel, accumulated into ks (without the weight):
+//   ks += (r²/k²)·[∂G/∂n_y + α ∂²G/∂n_x∂n_y](x, y) · 4π ... i.e. ks += e^{iq}(P + iQ)/q²
+// With q = kr, a = ∂r/∂n_x, b = ∂r/∂n_y, c = n_x·n_y, g = 3ab + c, u1 = (3 - q²)ab + c:
 //   4π r² e^{-iq} ∂G/∂n_y          = (iq - 1) b
-//   4π r² e^{-iq} ∂²G/∂n_x∂n_y     = (1/r) [ (3 - q²) ab + c - iq (3ab + c) ]
-// PURE_IMAG specialises α = i·alpha_im (α = i/k).
+//   4π r² e^{-iq} ∂²G/∂n_x∂n_y     = (1/r) [ u1 - iq g ]
+// so for α = i α_i (PURE_IMAG; α = i/k):  P = -b + α_i k g,  Q = q b + α_i k (1/q) u1.
+// d = X - Y (wave units); xny = X·n_y, cy = Y·n_y, so d·n_y = xny - cy.
 template <bool PURE_IMAG>
-__device__ __forceinline__ void lhs_eval(float3 x, float3 nx, float3 y, float3 ny, float cn, float2 w,
-                                         const KernelParams& kp, float2& acc) {
-  const float dx = x.x - y.x, dy = x.y - y.y, dz = x.z - y.z;
-  const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-  const float ir = rsqrt_ftz(r2);
-  const float q = kp.k * (r2 * ir);
-  const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * ir;   // ∂r/∂n_x
-  const float b = -fmaf(dx, ny.x, fmaf(dy, ny.y, dz * ny.z)) * ir;  // ∂r/∂n_y
-  const float ab = a * b;
+__device__ __forceinline__ void lhs_eval(float3 X, float3 nx, float4 Y, float xny, float cn, const KernelParams& kp,
+                                         float2& ks) {
+  const float dx = X.x - Y.x, dy = X.y - Y.y, dz = X.z - Y.z;
+  const float q2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  const float iq = rsqrt_ftz(q2);
+  const float q = q2 * iq;
   float sn, cs;
-  __sincosf(q, &sn, &cs);  // SFU sin/cos; |q| ≤ k·(near range), argument error ≤ ulp(q/2π)
-  const float g = fmaf(3.0f, ab, cn);           // 3ab + c
-  const float u1 = fmaf(fmaf(-q, q, 3.0f), ab, cn);  // (3 - q²) ab + c
+  __sincosf(q, &sn, &cs);  // MUFU sin/cos; argument error ≤ ulp(q/2π)
+  const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * iq;   // ∂r/∂n_x
+  const float b = (Y.w - xny) * iq;                                  // ∂r/∂n_y = -(d·n_y)/|d|
+  const float ab = a * b;
+  const float g = fmaf(3.0f, ab, cn);               // 3ab + c
+  const float u1 = fmaf(3.0f - q2, ab, cn);         // (3 - q²) ab + c
   float P, Q;
   if (PURE_IMAG) {
-    // -b - α_i ir u2 with u2 = -q g and ir·q = k  →  -b + (α_i k) g
-    P = fmaf(kp.alpha_im * kp.k, g, -b);
-    Q = fmaf(kp.alpha_im * ir, u1, q * b);   //  q b + α_i ir u1
+    P = fmaf(kp.ak_im, g, -b);
+    Q = fmaf(q, b, (kp.ak_im * iq) * u1);
   } else {
     const float u2 = -q * g;
-    P = fmaf(ir, kp.alpha_re * u1 - kp.alpha_im * u2, -b);
-    Q = fmaf(ir, kp.alpha_re * u2 + kp.alpha_im * u1, q * b);
+    P = fmaf(iq, kp.ak_re * u1 - kp.ak_im * u2, -b);
+    Q = fmaf(iq, kp.ak_re * u2 + kp.ak_im * u1, q * b);
   }
-  const float ir2 = ir * ir;
-  const float Er = ir2 * cs, Ei = ir2 * sn;
-  const float Kr = Er * P - Ei * Q;
-  const float Ki = Er * Q + Ei * P;
-  acc.x = fmaf(Kr, w.x, fmaf(-Ki, w.y, acc.x));
-  acc.y = fmaf(Kr, w.y, fmaf(Ki, w.x, acc.y));
+  const float iq2 = iq * iq;
+  const float Er = iq2 * cs, Ei = iq2 * sn;
+  ks.x = fmaf(Er, P, fmaf(-Ei, Q, ks.x));
+  ks.y = fmaf(Er, Q, fmaf(Ei, P, ks.y));
 }
 
-// One Q3 point of the RHS kernel (Eq. 4 right side):
-//   acc += [G + α ∂G/∂n_x](x, y) · w,   4π r² e^{-iq} (G + α ∂G/∂n_x) = r + α (iq - 1) a
-__device__ __forceinline__ void rhs_eval(float3 x, float3 nx, float3 y, float2 w, const KernelParams& kp,
-                                         float2& acc) {
-  const float dx = x.x - y.x, dy = x.y - y.y, dz = x.z - y.z;
-  const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-  const float ir = rsqrt_ftz(r2);
-  const float r = r2 * ir;
-  const float q = kp.k * r;
-  const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * ir;
+// One Q3 point of the RHS kernel (Eq. 4 right side), without the weight:
+//   4π r² e^{-iq} (G + α ∂G/∂n_x) = r + α (iq - 1) a,   r = q/k
+__device__ __forceinline__ void rhs_eval(float3 X, float3 nx, float4 Y, const KernelParams& kp, float2& ks) {
+  const float dx = X.x - Y.x, dy = X.y - Y.y, dz = X.z - Y.z;
+  const float q2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  const float iq = rsqrt_ftz(q2);
+  const float q = q2 * iq;
+  const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * iq;
   float sn, cs;
   __sincosf(q, &sn, &cs);
-  const float P = fmaf(-a, fmaf(kp.alpha_im, q, kp.alpha_re), r);   // r - a (α_r + α_i q)
-  const float Q = a * fmaf(kp.alpha_re, q, -kp.alpha_im);           // a (α_r q - α_i)
-  const float ir2 = ir * ir;
-  const float Er = ir2 * cs, Ei = ir2 * sn;
-  const float Kr = Er * P - Ei * Q;
-  const float Ki = Er * Q + Ei * P;
-  acc.x = fmaf(Kr, w.x, fmaf(-Ki, w.y, acc.x));
-  acc.y = fmaf(Kr, w.y, fmaf(Ki, w.x, acc.y));
+  const float P = fmaf(q, kp.inv_k, -a * fmaf(kp.alpha_im, q, kp.alpha_re));   // r - a (α_r + α_i q)
+  const float Q = a * fmaf(kp.alpha_re, q, -kp.alpha_im);                      // a (α_r q - α_i)
+  const float iq2 = iq * iq;
+  const float Er = iq2 * cs, Ei = iq2 * sn;
+  ks.x = fmaf(Er, P, fmaf(-Ei, Q, ks.x));
+  ks.y = fmaf(Er, Q, fmaf(Ei, P, ks.y));
 }
 
 // y_i = Σ_{j ∈ direct(i)} A^{Q3}_ij x_j + Σ_{j: ρ_ij<3} C_ij x_j   (a7)
-// A^{Q3}_ij = (A_j/3) Σ_q [∂G/∂n_y + α ∂²G/∂n_x∂n_y](x_i, y_jq)   (Eq. 5)
-// One CTA per target leaf (leaves launched in descending-work order); the
-// source elements of all direct leaves are staged through shared memory in
-// chunks; P = ⌊NT/n_B⌋ threads share one target and split the sources;
-// partial sums are reduced in shared memory.
+// One CTA per target leaf (NearTask, in descending-work order).  The source
+// elements of all its direct leaves are listed in a build-time slot table
+// (element, index of its source leaf in the near list → k(c_B − c_C)), so the
+// CTA stages them through shared memory in chunks of NEAR_MAXS with one
+// coalesced table load per slot.  P = ⌊NT/n_B⌋ threads share one target and
+// split the sources; partial sums are reduced in shared memory.  Staged per
+// source element: the three Q3 points with Y_q·n_y in .w (wave units, shifted
+// into the target leaf's frame), the normal, and w_j = x_j·k²A_j/(12π).
 // KIND 0: LHS operator A (Eq. 5); KIND 1: RHS operator B (G sources).
 template <int KIND, bool PURE_IMAG>
 __global__ void __launch_bounds__(NEAR_NT) k_near(
-    const int32_t* __restrict__ order, const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end,
-    const int32_t* __restrict__ near_ptr, const int32_t* __restrict__ near_idx,
-    const float4* __restrict__ near_off, const float4* __restrict__ tgt_pos, const float4* __restrict__ tgt_nrm,
-    const SrcElem* __restrict__ src, const float* __restrict__ src_w, const int32_t* __restrict__ corr_ptr,
-    const int32_t* __restrict__ corr_col, const float2* __restrict__ corr_val, const float2* __restrict__ x,
-    float2* __restrict__ y, KernelParams kp) {
-  __shared__ float4 sa[NEAR_MAXS], sb[NEAR_MAXS], sc[NEAR_MAXS];
-  __shared__ float2 sx[NEAR_MAXS];
-  __shared__ int spre[NEAR_MAXL + 1];
+    const NearTask* __restrict__ tasks, const int2* __restrict__ slots, const float4* __restrict__ near_off,
+    const float4* __restrict__ tgt_pos, const float4* __restrict__ tgt_nrm, const SrcElem* __restrict__ src,
+    const float* __restrict__ src_w, const int32_t* __restrict__ corr_ptr, const int32_t* __restrict__ corr_col,
+    const float2* __restrict__ corr_val, const float2* __restrict__ x, float2* __restrict__ y, KernelParams kp) {
+  // staged source element s: st[5s..5s+4] = Y0, Y1, Y2 (with Y_q·n_y in .w), (n_y, -), (w_j, -, -)
+  __shared__ float4 st[NEAR_MAXS * 5];
   __shared__ float2 sred[NEAR_NT];
-  const int leaf = order[blockIdx.x];
-  const int tb = leaf_begin[leaf];
-  const int nt = leaf_end[leaf] - tb;
+  const NearTask t = tasks[blockIdx.x];
+  const int tb = t.tb, nt = t.nt;
   const int P = max(1, NEAR_NT / nt);
   const int tid = threadIdx.x;
   const int ti = tid % nt, part = tid / nt;
   const bool active = part < P && ti < nt;
-  float3 xt = make_float3(0.f, 0.f, 0.f), nx = xt;
+  float3 X = make_float3(0.f, 0.f, 0.f), nx = X;
   if (active) {
     float4 p = tgt_pos[tb + ti], q = tgt_nrm[tb + ti];
-    xt = make_float3(p.x, p.y, p.z);
+    X = make_float3(p.x, p.y, p.z);
     nx = make_float3(q.x, q.y, q.z);
   }
   float2 acc = make_float2(0.f, 0.f);
-  const int lb = near_ptr[leaf], le = near_ptr[leaf + 1];
-  for (int e0 = lb; e0 < le; e0 += NEAR_MAXL) {
-    const int ne = min(NEAR_MAXL, le - e0);
+  for (int base = t.s0; base < t.s1; base += NEAR_MAXS) {
+    const int ns = min(NEAR_MAXS, t.s1 - base);
     __syncthreads();
-    if (tid < 32) {  // warp-parallel exclusive scan of the source-leaf sizes
-      int carry = 0;
-      for (int j0 = 0; j0 < ne; j0 += 32) {
-        const int j = j0 + tid;
-        int v = 0;
-        if (j < ne) {
-          const int c = near_idx[e0 + j];
-          v = leaf_end[c] - leaf_begin[c];
-        }
-        int incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (tid >= o) incl += t;
-        }
-        if (j < ne) spre[j] = carry + incl - v;
-        carry += __shfl_sync(0xffffffffu, incl, 31);
-      }
-      if (tid == 0) spre[ne] = carry;
+    for (int slot = tid; slot < ns; slot += NEAR_NT) {
+      const int2 sl = slots[base + slot];
+      const int el = sl.x;
+      const float4 off = near_off[sl.y];  // k (c_B - c_C)
+      SrcElem se = src[el];
+      const float2 xv = x[el];
+      const float wv = src_w[el];
+      const float4 n4 = make_float4(se.a.w, se.b.w, se.c.w, 0.f);
+      float4 A = make_float4(se.a.x - off.x, se.a.y - off.y, se.a.z - off.z, 0.f);
+      float4 B = make_float4(se.b.x - off.x, se.b.y - off.y, se.b.z - off.z, 0.f);
+      float4 C = make_float4(se.c.x - off.x, se.c.y - off.y, se.c.z - off.z, 0.f);
+      A.w = fmaf(A.x, n4.x, fmaf(A.y, n4.y, A.z * n4.z));
+      B.w = fmaf(B.x, n4.x, fmaf(B.y, n4.y, B.z * n4.z));
+      C.w = fmaf(C.x, n4.x, fmaf(C.y, n4.y, C.z * n4.z));
+      float4* d = st + 5 * slot;
+      d[0] = A; d[1] = B; d[2] = C; d[3] = n4;
+      d[4] = make_float4(xv.x * wv, xv.y * wv, 0.f, 0.f);
     }
     __syncthreads();
-    const int total = spre[ne];
-    for (int base = 0; base < total; base += NEAR_MAXS) {
-      const int ns = min(NEAR_MAXS, total - base);
-      for (int slot = tid; slot < ns; slot += NEAR_NT) {
-        const int g = base + slot;
-        int lo = 0, hi = ne - 1;  // last j with spre[j] <= g
-        while (lo < hi) {
-          int mid = (lo + hi + 1) >> 1;
-          if (spre[mid] <= g) lo = mid; else hi = mid - 1;
-        }
-        const int c = near_idx[e0 + lo];
-        const int el = leaf_begin[c] + (g - spre[lo]);
-        const float4 off = near_off[e0 + lo];  // c_B - c_C
-        SrcElem se = src[el];
-        se.a.x -= off.x; se.a.y -= off.y; se.a.z -= off.z;
-        se.b.x -= off.x; se.b.y -= off.y; se.b.z -= off.z;
-        se.c.x -= off.x; se.c.y -= off.y; se.c.z -= off.z;
-        sa[slot] = se.a; sb[slot] = se.b; sc[slot] = se.c;
-        const float2 xv = x[el];
-        const float wv = src_w[el];
-        sx[slot] = make_float2(xv.x * wv, xv.y * wv);
-      }
-      __syncthreads();
-      if (active) {
+    if (active) {
 #pragma unroll 2
-        for (int s = part; s < ns; s += P) {
-          const float4 A = sa[s], B = sb[s], C = sc[s];
-          const float2 w = sx[s];
-          if (KIND == 0) {
-            const float3 ny = make_float3(A.w, B.w, C.w);
-            const float cn = fmaf(nx.x, ny.x, fmaf(nx.y, ny.y, nx.z * ny.z));
-            lhs_eval<PURE_IMAG>(xt, nx, make_float3(A.x, A.y, A.z), ny, cn, w, kp, acc);
-            lhs_eval<PURE_IMAG>(xt, nx, make_float3(B.x, B.y, B.z), ny, cn, w, kp, acc);
-            lhs_eval<PURE_IMAG>(xt, nx, make_float3(C.x, C.y, C.z), ny, cn, w, kp, acc);
-          } else {
-            rhs_eval(xt, nx, make_float3(A.x, A.y, A.z), w, kp, acc);
-            rhs_eval(xt, nx, make_float3(B.x, B.y, B.z), w, kp, acc);
-            rhs_eval(xt, nx, make_float3(C.x, C.y, C.z), w, kp, acc);
-          }
+      for (int s = part; s < ns; s += P) {
+        const float4* e = st + 5 * s;
+        const float4 A = e[0], B = e[1], C = e[2];
+        const float4 w = e[4];
+        float2 ks = make_float2(0.f, 0.f);
+        if (KIND == 0) {
+          const float4 ny = e[3];
+          const float cn = fmaf(nx.x, ny.x, fmaf(nx.y, ny.y, nx.z * ny.z));
+          const float xny = fmaf(X.x, ny.x, fmaf(X.y, ny.y, X.z * ny.z));
+          lhs_eval<PURE_IMAG>(X, nx, A, xny, cn, kp, ks);
+          lhs_eval<PURE_IMAG>(X, nx, B, xny, cn, kp, ks);
+          lhs_eval<PURE_IMAG>(X, nx, C, xny, cn, kp, ks);
+        } else {
+          rhs_eval(X, nx, A, kp, ks);
+          rhs_eval(X, nx, B, kp, ks);
+          rhs_eval(X, nx, C, kp, ks);
         }
+        acc.x = fmaf(ks.x, w.x, fmaf(-ks.y, w.y, acc.x));
+        acc.y = fmaf(ks.x, w.y, fmaf(ks.y, w.x, acc.y));
       }
-      __syncthreads();
     }
   }
   // correction SpMV, rows split over the P parts
@@ -265,15 +238,14 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
   }
 }
 
-void launch_near(int nleaf, const int32_t* order, const int32_t* leaf_begin, const int32_t* leaf_end,
-                 const int32_t* near_ptr, const int32_t* near_idx, const float4* near_off, const float4* tgt_pos,
+void launch_near(int ntask, const NearTask* tasks, const int2* slots, const float4* near_off, const float4* tgt_pos,
                  const float4* tgt_nrm, const SrcElem* src, const float* src_w, const int32_t* corr_ptr,
                  const int32_t* corr_col, const float2* corr_val, const float2* x, float2* y, KernelParams kp,
                  bool alpha_pure_imag, int kind, cudaStream_t s) {
-  if (nleaf <= 0) return;
-#define NEAR(K, PI)                                                                                          \
-  k_near<K, PI><<<nleaf, NEAR_NT, 0, s>>>(order, leaf_begin, leaf_end, near_ptr, near_idx, near_off, tgt_pos, \
-                                          tgt_nrm, src, src_w, corr_ptr, corr_col, corr_val, x, y, kp)
+  if (ntask <= 0) return;
+#define NEAR(K, PI)                                                                                              \
+  k_near<K, PI><<<ntask, NEAR_NT, 0, s>>>(tasks, slots, near_off, tgt_pos, tgt_nrm, src, src_w, corr_ptr, corr_col, \
+                                          corr_val, x, y, kp)
   if (kind == 1) NEAR(1, false);
   else if (alpha_pure_imag) NEAR(0, true);
   else NEAR(0, false);
@@ -281,47 +253,90 @@ void launch_near(int nleaf, const int32_t* order, const int32_t* leaf_begin, con
 }
 
 // ------------------------------------------------------------------ S2M (a2) / L2T (a6)
-// S2M: m̃_B = S̃_B x_B (T × n_B, column-major); one CTA per leaf, thread = row.
-__global__ void k_s2m(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
-                      const float2* __restrict__ x, float2* __restrict__ out) {
-  __shared__ float2 sx[128];
-  const LeafTask t = tasks[blockIdx.x];
-  for (int j = threadIdx.x; j < t.elem_count; j += blockDim.x) sx[j] = x[t.elem_begin + j];
-  __syncthreads();
-  const float2* M = pool + t.mat_off;
-  for (int r = threadIdx.x; r < t.T; r += blockDim.x) {
-    float2 acc = make_float2(0.f, 0.f);
-    for (int j = 0; j < t.elem_count; ++j) {
-      const float2 m = M[(int64_t)j * t.T + r];
-      const float2 v = sx[j];
-      acc.x = fmaf(m.x, v.x, fmaf(-m.y, v.y, acc.x));
-      acc.y = fmaf(m.x, v.y, fmaf(m.y, v.x, acc.y));
+// HBM-bound per-leaf matrix-vector products.  Thread (row, group): G = ⌊NT/rows⌋
+// groups split the columns (column c handled by group c mod G), so one warp
+// reads consecutive entries of the column-major matrix; each thread keeps
+// LEAF_U independent loads in flight; the G partial sums meet in shared memory.
+constexpr int LEAF_NT = 128;
+constexpr int LEAF_U = 8;
+constexpr int LEAF_MAXR = 320;
+
+__device__ __forceinline__ float2 leaf_colsum(const float2* __restrict__ M, int64_t ld, int row, int c0, int cstep,
+                                              int ncol, const float2* __restrict__ v) {
+  float2 acc = make_float2(0.f, 0.f);
+  for (int c = c0; c < ncol; c += LEAF_U * cstep) {
+    float2 m[LEAF_U];
+#pragma unroll
+    for (int u = 0; u < LEAF_U; ++u) {
+      const int cc = c + u * cstep;
+      m[u] = cc < ncol ? __ldg(M + (int64_t)cc * ld + row) : make_float2(0.f, 0.f);
     }
-    out[t.state_off + r] = acc;
+#pragma unroll
+    for (int u = 0; u < LEAF_U; ++u) {
+      const int cc = min(c + u * cstep, ncol - 1);
+      const float2 x = v[cc];
+      acc.x = fmaf(m[u].x, x.x, fmaf(-m[u].y, x.y, acc.x));
+      acc.y = fmaf(m[u].x, x.y, fmaf(m[u].y, x.x, acc.y));
+    }
+  }
+  return acc;
+}
+
+// S2M: m̃_B = S̃_B x_B (T × n_B, column-major)   (Eq. 10; compressed S̃)
+__global__ void __launch_bounds__(LEAF_MAXR) k_s2m(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
+                                                   const float2* __restrict__ x, float2* __restrict__ out) {
+  __shared__ float2 sx[128];
+  __shared__ float2 red[LEAF_MAXR];
+  const LeafTask t = tasks[blockIdx.x];
+  const int nb = t.elem_count, T = t.T;
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) sx[j] = x[t.elem_begin + j];
+  __syncthreads();
+  const int G = max(1, (int)blockDim.x / T);
+  const int r = threadIdx.x % T, g = threadIdx.x / T;
+  float2 acc = make_float2(0.f, 0.f);
+  if (g < G) acc = leaf_colsum(pool + t.mat_off, T, r, g, G, nb, sx);
+  if (G == 1) {
+    if (threadIdx.x < T) out[t.state_off + r] = acc;
+    return;
+  }
+  if (g < G) red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < T) {
+    float2 s = red[threadIdx.x];
+    for (int q = 1; q < G; ++q) {
+      const float2 v = red[q * T + threadIdx.x];
+      s.x += v.x; s.y += v.y;
+    }
+    out[t.state_off + r] = s;
   }
 }
 
-// L2T: y_B = T̃_B ℓ̃_B (n_B × T column-major); thread = target element.
-__global__ void k_l2t(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
-                      const float2* __restrict__ in, float2* __restrict__ y) {
-  __shared__ float2 sl[320];
+// L2T: y_B = T̃_B ℓ̃_B (n_B × T column-major)   (Eq. 12; compressed T̃)
+__global__ void __launch_bounds__(LEAF_NT) k_l2t(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
+                                                 const float2* __restrict__ in, float2* __restrict__ y) {
+  __shared__ float2 sl[LEAF_MAXR];
+  __shared__ float2 red[LEAF_NT];
   const LeafTask t = tasks[blockIdx.x];
+  const int nb = t.elem_count;
   if (t.mat_off < 0) {
-    for (int i = threadIdx.x; i < t.elem_count; i += blockDim.x) y[t.elem_begin + i] = make_float2(0.f, 0.f);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) y[t.elem_begin + i] = make_float2(0.f, 0.f);
     return;
   }
   for (int c = threadIdx.x; c < t.T; c += blockDim.x) sl[c] = in[t.state_off + c];
   __syncthreads();
-  const float2* M = pool + t.mat_off;
-  for (int i = threadIdx.x; i < t.elem_count; i += blockDim.x) {
-    float2 acc = make_float2(0.f, 0.f);
-    for (int c = 0; c < t.T; ++c) {
-      const float2 m = M[(int64_t)c * t.elem_count + i];
-      const float2 v = sl[c];
-      acc.x = fmaf(m.x, v.x, fmaf(-m.y, v.y, acc.x));
-      acc.y = fmaf(m.x, v.y, fmaf(m.y, v.x, acc.y));
+  const int G = max(1, LEAF_NT / nb);
+  const int i = threadIdx.x % nb, g = threadIdx.x / nb;
+  float2 acc = make_float2(0.f, 0.f);
+  if (g < G) acc = leaf_colsum(pool + t.mat_off, nb, i, g, G, t.T, sl);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    float2 s = red[threadIdx.x];
+    for (int q = 1; q < G; ++q) {
+      const float2 v = red[q * nb + threadIdx.x];
+      s.x += v.x; s.y += v.y;
     }
-    y[t.elem_begin + i] = acc;
+    y[t.elem_begin + threadIdx.x] = s;
   }
 }
 
@@ -329,12 +344,12 @@ void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const floa
                 cudaStream_t s) {
   if (ntask <= 0) return;
   int bd = ((max_rows + 31) / 32) * 32;
-  bd = bd < 32 ? 32 : (bd > 256 ? 256 : bd);
+  bd = bd < LEAF_NT ? LEAF_NT : (bd > LEAF_MAXR ? LEAF_MAXR : bd);
   k_s2m<<<ntask, bd, 0, s>>>(tasks, pool, x, out);
 }
 void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s) {
   if (ntask <= 0) return;
-  k_l2t<<<ntask, 64, 0, s>>>(tasks, pool, in, y);
+  k_l2t<<<ntask, LEAF_NT, 0, s>>>(tasks, pool, in, y);
 }
 
 // ------------------------------------------------------------------ translations (a3 M2M, a4 M2L, a5 L2L)
@@ -354,17 +369,37 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-template <int MR, int MO, bool ATOMIC>
+__device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, fmaf(-a.y, b.y, acc.x));
+  acc.y = fmaf(a.x, b.y, fmaf(a.y, b.x, acc.y));
+}
+
+// Tile R rows × O ops per CTA (128 threads); thread (tr, to) owns rows
+// {2tr, 2tr+1} + 2·NR·i and ops {2to, 2to+1} + 2·NO·j; a warp spans 4 row
+// groups × 8 op groups, so every shared load is a one-wavefront LDS.128.
+template <int R, int O>
+struct XCfg {
+  static constexpr int RT = (R == 128) ? 8 : (R == 16 ? 2 : 4);   // rows per thread
+  static constexpr int NR = R / RT;                                // row groups
+  static constexpr int NO = 128 / NR;                              // op groups
+  static constexpr int OT = O / NO;                                // ops per thread
+  static constexpr int SO = O + 2;                                 // padded sS row
+  static_assert(NR % 4 == 0 && NO % 8 == 0 && OT % 2 == 0 && RT % 2 == 0, "tile");
+};
+
+template <int R, int O, bool ATOMIC>
 __global__ void __launch_bounds__(128) k_xlate(const XTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
                                                const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
                                                const float2* __restrict__ src, float2* __restrict__ dst) {
-  constexpr int R = 16 * MR, O = 8 * MO;
+  using C = XCfg<R, O>;
+  constexpr int RT = C::RT, NR = C::NR, NO = C::NO, OT = C::OT, SO = C::SO;
   constexpr int ML = XK * R / 128, SL = XK * O / 128;  // cp.async per thread per chunk
   __shared__ __align__(16) float2 sM[2][XK][R];
-  __shared__ __align__(16) float2 sS[2][XK][O + 1];
+  __shared__ __align__(16) float2 sS[2][XK][SO];
   __shared__ int64_t soff[O];
   const XTask t = tasks[blockIdx.x];
-  const int tid = threadIdx.x, tr = tid & 15, to = tid >> 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tr = (warp % (NR / 4)) * 4 + (lane >> 3), to = (warp / (NR / 4)) * 8 + (lane & 7);
   for (int p = tid; p < O; p += 128) soff[p] = p < t.op_count ? src_off[t.op_begin + p] : -1;
   __syncthreads();
   const float2* __restrict__ M = pool + t.mat_off;
@@ -388,11 +423,11 @@ __global__ void __launch_bounds__(128) k_xlate(const XTask* __restrict__ tasks, 
     }
     cp_async_commit();
   };
-  float2 acc[MR][MO];
+  float2 acc[RT][OT];
 #pragma unroll
-  for (int i = 0; i < MR; ++i)
+  for (int i = 0; i < RT; ++i)
 #pragma unroll
-    for (int j = 0; j < MO; ++j) acc[i][j] = make_float2(0.f, 0.f);
+    for (int j = 0; j < OT; ++j) acc[i][j] = make_float2(0.f, 0.f);
   issue(0, t.k_begin);
   int buf = 0;
   for (int k0 = t.k_begin; k0 < t.k_end; k0 += XK) {
@@ -405,30 +440,37 @@ __global__ void __launch_bounds__(128) k_xlate(const XTask* __restrict__ tasks, 
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < XK; ++kk) {
-      float2 m[MR], sv[MO];
+      const float4* mv = reinterpret_cast<const float4*>(&sM[buf][kk][2 * tr]);
+      const float4* sv = reinterpret_cast<const float4*>(&sS[buf][kk][2 * to]);
+      float2 m[RT], v[OT];
 #pragma unroll
-      for (int i = 0; i < MR; ++i) m[i] = sM[buf][kk][tr + 16 * i];
+      for (int i = 0; i < RT / 2; ++i) {
+        const float4 q = mv[NR * i];
+        m[2 * i] = make_float2(q.x, q.y);
+        m[2 * i + 1] = make_float2(q.z, q.w);
+      }
 #pragma unroll
-      for (int j = 0; j < MO; ++j) sv[j] = sS[buf][kk][to + 8 * j];
+      for (int j = 0; j < OT / 2; ++j) {
+        const float4 q = sv[NO * j];
+        v[2 * j] = make_float2(q.x, q.y);
+        v[2 * j + 1] = make_float2(q.z, q.w);
+      }
 #pragma unroll
-      for (int i = 0; i < MR; ++i)
+      for (int i = 0; i < RT; ++i)
 #pragma unroll
-        for (int j = 0; j < MO; ++j) {
-          acc[i][j].x = fmaf(m[i].x, sv[j].x, fmaf(-m[i].y, sv[j].y, acc[i][j].x));
-          acc[i][j].y = fmaf(m[i].x, sv[j].y, fmaf(m[i].y, sv[j].x, acc[i][j].y));
-        }
+        for (int j = 0; j < OT; ++j) cmac(acc[i][j], m[i], v[j]);
     }
     __syncthreads();
     buf ^= 1;
   }
 #pragma unroll
-  for (int j = 0; j < MO; ++j) {
-    const int op = to + 8 * j;
+  for (int j = 0; j < OT; ++j) {
+    const int op = 2 * to + (j & 1) + 2 * NO * (j >> 1);
     if (op >= t.op_count) continue;
     float2* d = dst + dst_off[t.op_begin + op];
 #pragma unroll
-    for (int i = 0; i < MR; ++i) {
-      const int row = t.row0 + tr + 16 * i;
+    for (int i = 0; i < RT; ++i) {
+      const int row = t.row0 + 2 * tr + (i & 1) + 2 * NR * (i >> 1);
       if (row < t.rows) {
         if (ATOMIC) atomicAdd(d + row, acc[i][j]);
         else d[row] = acc[i][j];
@@ -440,47 +482,75 @@ __global__ void __launch_bounds__(128) k_xlate(const XTask* __restrict__ tasks, 
 void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const int64_t* src_off,
                   const int64_t* dst_off, const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
   if (ntask <= 0) return;
-#define XL(MR, MO)                                                                                        \
-  (atomic ? k_xlate<MR, MO, true><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst)          \
-          : k_xlate<MR, MO, false><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst))
+#define XL(R, O)                                                                                          \
+  (atomic ? k_xlate<R, O, true><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst)            \
+          : k_xlate<R, O, false><<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst))
   switch (variant) {
-    case 0: XL(2, 8); break;
-    case 1: XL(4, 4); break;
-    case 2: XL(8, 2); break;
-    default: XL(1, 16); break;
+    case 0: XL(32, 64); break;
+    case 1: XL(64, 32); break;
+    case 2: XL(128, 16); break;
+    default: XL(16, 128); break;
   }
 #undef XL
 }
 
 // ------------------------------------------------------------------ fused §4.2 M2L (a4)
-// PAPER.md §4.2: K̃ ≈ Û V̂.  One CTA handles ≤ 64 ops of one K̃:
-// phase 1 tmp = V̂ S (r ≤ 32 rows, K = T streamed through a cp.async double
-// buffer, 2×8 complex register tile per thread), tmp kept in shared memory;
-// phase 2 for each 32-row tile of Û: out = Û_tile tmp (K = r from shared
-// memory), accumulated into the destination states with vector atomics.
-constexpr int LR_SH1 = 2 * XK * 32 + 2 * XK * (LR_O + 1);   // phase 1: sM[2][XK][32] + sS[2][XK][O+1]
-constexpr int LR_SH2 = 32 * (LR_O + 1) + 32 * 33;            // phase 2: tmp[32][O+1] + sU[32][33]
-constexpr int LR_SH = LR_SH1 > LR_SH2 ? LR_SH1 : LR_SH2;
+// PAPER.md §4.2: K̃ ≈ Û V̂ (Û: T × r, V̂: r × T, r ≤ 64).  One CTA
+// handles ≤ LR_O = 64 ops sharing one K̃:
+//   phase 1  tmp = V̂ S        (R1 ≥ r rows × 64 ops, K = T streamed through a
+//                              cp.async double buffer), tmp kept in shared memory;
+//   phase 2  dst += Û tmp      (32-row tiles of Û, double-buffered, K = r),
+//            accumulated into the destination states with vector atomics.
+// Register tiles: phase 1 RT1 rows × OT1 ops per thread, phase 2 4 × 4.  A
+// thread's rows are pairs {2tr, 2tr+1} + 2·NR·i and its ops pairs
+// {2to, 2to+1} + 2·NO·j, and a warp spans 4 row groups × 8 op groups, so every
+// shared load is an LDS.128 (2 complex values) touching ≤ 128 bytes: one
+// wavefront per load, ≤ RT1/2 + OT1/2 wavefronts per 4·RT1·OT1 FFMA.
+template <int R1>
+struct LrCfg {
+  static constexpr int RT1 = R1 == 64 ? 8 : 4;
+  static constexpr int NR1 = R1 / RT1;        // 4, 8, 8
+  static constexpr int NO1 = 128 / NR1;       // 32, 16, 16
+  static constexpr int OT1 = LR_O / NO1;      // 2, 4, 4
+  static constexpr int SO = LR_O + 2;         // padded sS row (conflict-free cp.async writes, 16-B aligned rows)
+  static constexpr int PH1 = 2 * XK * R1 + 2 * XK * SO;     // sV[2][XK][R1] + sS[2][XK][SO] (float2)
+  static constexpr int PH2 = R1 * LR_O + 2 * R1 * 32;        // tmp[R1][64] + sU[2][R1][32]
+  static constexpr int SMEM = (PH1 > PH2 ? PH1 : PH2) * 8;
+};
 
-template <int MR1>  // phase-1 rows = 16·MR1 ≥ r
-__device__ __forceinline__ void m2l_lr_body(const LrTask& t, float2* sh, int64_t* soff,
-                                            const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
-                                            const float2* __restrict__ src, float2* __restrict__ dst) {
-  constexpr int R = 32, O = LR_O, R1 = 16 * MR1;
-  float2(*sM)[XK][R] = reinterpret_cast<float2(*)[XK][R]>(sh);
-  float2(*sS)[XK][O + 1] = reinterpret_cast<float2(*)[XK][O + 1]>(sh + 2 * XK * R);
-  float2(*tmp)[O + 1] = reinterpret_cast<float2(*)[O + 1]>(sh);
-  float2(*sU)[R + 1] = reinterpret_cast<float2(*)[R + 1]>(sh + R * (O + 1));
-  const int tid = threadIdx.x, tr = tid & 15, to = tid >> 4;
+
+template <int R1>
+__global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
+                                                const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
+                                                const float2* __restrict__ src, float2* __restrict__ dst) {
+  using C = LrCfg<R1>;
+  constexpr int RT1 = C::RT1, NO1 = C::NO1, OT1 = C::OT1, O = LR_O;
+  extern __shared__ float4 smem4[];
+  float2* sh = reinterpret_cast<float2*>(smem4);
+  __shared__ int64_t soff[O];
+  __shared__ int64_t doff[O];
+  const LrTask t = tasks[blockIdx.x];
+  const int tid = threadIdx.x;
+  for (int p = tid; p < O; p += 128) {
+    soff[p] = p < t.op_count ? src_off[t.op_begin + p] : -1;
+    doff[p] = p < t.op_count ? dst_off[t.op_begin + p] : -1;
+  }
+  __syncthreads();
   const float2* __restrict__ V = pool + t.v_off;
   const float2* __restrict__ U = pool + t.u_off;
-  auto issue = [&](int buf, int k0) {
+
+  // ---- phase 1: tmp[R1][64] = V̂ · S
+  float2* sV = sh;                      // [2][XK][R1]
+  constexpr int SO = C::SO;
+  float2* sS = sh + 2 * XK * R1;        // [2][XK][SO]
+  auto issue1 = [&](int buf, int k0) {
 #pragma unroll
     for (int e = 0; e < XK * R1 / 128; ++e) {
       const int idx = tid + 128 * e;
       const int kk = idx / R1, row = idx % R1, col = k0 + kk;
       const bool ok = row < t.r && col < t.T;
-      cp_async8(&sM[buf][kk][row], ok ? (const void*)(V + (int64_t)col * t.r + row) : (const void*)V, ok);
+      cp_async8(sV + (buf * XK + kk) * R1 + row, ok ? (const void*)(V + (int64_t)col * t.r + row) : (const void*)V,
+                ok);
     }
 #pragma unroll
     for (int e = 0; e < XK * O / 128; ++e) {
@@ -488,106 +558,143 @@ __device__ __forceinline__ void m2l_lr_body(const LrTask& t, float2* sh, int64_t
       const int p = idx / XK, kk = idx % XK, col = k0 + kk;
       const int64_t so = soff[p];
       const bool ok = so >= 0 && col < t.T;
-      cp_async8(&sS[buf][kk][p], ok ? (const void*)(src + so + col) : (const void*)src, ok);
+      cp_async8(sS + (buf * XK + kk) * SO + p, ok ? (const void*)(src + so + col) : (const void*)src, ok);
     }
     cp_async_commit();
   };
-  float2 acc[2][8];
+  constexpr int NR1 = C::NR1;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int tr1 = (warp % (NR1 / 4)) * 4 + (lane >> 3), to1 = (warp / (NR1 / 4)) * 8 + (lane & 7);
+  float2 acc[RT1][OT1];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < RT1; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
-  issue(0, 0);
-  static_assert(MR1 == 1 || MR1 == 2, "phase-1 rows");
+    for (int j = 0; j < OT1; ++j) acc[i][j] = make_float2(0.f, 0.f);
+  issue1(0, 0);
   int buf = 0;
   for (int k0 = 0; k0 < t.T; k0 += XK) {
     if (k0 + XK < t.T) {
-      issue(buf ^ 1, k0 + XK);
+      issue1(buf ^ 1, k0 + XK);
       cp_async_wait_1();
     } else {
       cp_async_wait_0();
     }
     __syncthreads();
+    const float4* mv = reinterpret_cast<const float4*>(sV + buf * XK * R1 + 2 * tr1);
+    const float4* sv = reinterpret_cast<const float4*>(sS + buf * XK * SO + 2 * to1);
 #pragma unroll
     for (int kk = 0; kk < XK; ++kk) {
-      float2 m[MR1], sv[8];
+      float2 m[RT1], v[OT1];
 #pragma unroll
-      for (int i = 0; i < MR1; ++i) m[i] = sM[buf][kk][tr + 16 * i];
+      for (int i = 0; i < RT1 / 2; ++i) {
+        const float4 q = mv[kk * (R1 / 2) + NR1 * i];
+        m[2 * i] = make_float2(q.x, q.y);
+        m[2 * i + 1] = make_float2(q.z, q.w);
+      }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sv[j] = sS[buf][kk][to + 8 * j];
+      for (int j = 0; j < OT1 / 2; ++j) {
+        const float4 q = sv[kk * (SO / 2) + NO1 * j];
+        v[2 * j] = make_float2(q.x, q.y);
+        v[2 * j + 1] = make_float2(q.z, q.w);
+      }
 #pragma unroll
-      for (int i = 0; i < MR1; ++i)
+      for (int i = 0; i < RT1; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          acc[i][j].x = fmaf(m[i].x, sv[j].x, fmaf(-m[i].y, sv[j].y, acc[i][j].x));
-          acc[i][j].y = fmaf(m[i].x, sv[j].y, fmaf(m[i].y, sv[j].x, acc[i][j].y));
-        }
+        for (int j = 0; j < OT1; ++j) cmac(acc[i][j], m[i], v[j]);
     }
     __syncthreads();
     buf ^= 1;
   }
-  // tmp[row][op] (rows ≥ r are zero because V̂ rows ≥ r were zero-filled)
+  // tmp[row][op] (rows ≥ r are zero: V̂ rows ≥ r were zero-filled)
+  float2* tmp = sh;                    // [R1][64]
+  float2* sU = sh + R1 * O;            // [2][R1][32]
 #pragma unroll
-  for (int i = 0; i < MR1; ++i)
+  for (int i = 0; i < RT1; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) tmp[tr + 16 * i][to + 8 * j] = acc[i][j];
-  __syncthreads();
-  for (int r0 = 0; r0 < t.T; r0 += R) {
-    for (int idx = tid; idx < R * R; idx += 128) {   // sU[row][c] = Û[r0 + row, c]
-      const int c = idx / R, row = idx % R;
-      sU[row][c] = (r0 + row < t.T && c < t.r) ? __ldg(U + (int64_t)c * t.T + r0 + row) : make_float2(0.f, 0.f);
+    for (int j = 0; j < OT1 / 2; ++j) {
+      float4 q = make_float4(acc[i][2 * j].x, acc[i][2 * j].y, acc[i][2 * j + 1].x, acc[i][2 * j + 1].y);
+      const int row = 2 * tr1 + (i & 1) + 2 * NR1 * (i >> 1);
+      *reinterpret_cast<float4*>(tmp + row * O + 2 * to1 + 2 * NO1 * j) = q;
+    }
+
+  // ---- phase 2: dst[:, op] += Û[r0:r0+32, :] · tmp[:, op]
+  auto issue2 = [&](int b, int r0) {
+    for (int idx = tid; idx < R1 * 32; idx += 128) {
+      const int c = idx / 32, row = idx % 32;
+      const bool ok = c < t.r && r0 + row < t.T;
+      cp_async8(sU + (b * R1 + c) * 32 + row, ok ? (const void*)(U + (int64_t)c * t.T + r0 + row) : (const void*)U,
+                ok);
+    }
+    cp_async_commit();
+  };
+  // rows {2·tr2, 2·tr2+1} + 16i, ops {2·to2, 2·to2+1} + 32j; warps 2 × 2 of 4 × 8 lanes
+  const int tr2 = (warp & 1) * 4 + (lane >> 3), to2 = (warp >> 1) * 8 + (lane & 7);
+  int b2 = 0;
+  issue2(0, 0);
+  for (int r0 = 0; r0 < t.T; r0 += 32) {
+    if (r0 + 32 < t.T) {
+      issue2(b2 ^ 1, r0 + 32);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_0();
     }
     __syncthreads();
+    float2 a2[4][4];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
+      for (int j = 0; j < 4; ++j) a2[i][j] = make_float2(0.f, 0.f);
+    const float4* uv = reinterpret_cast<const float4*>(sU + b2 * R1 * 32 + 2 * tr2);
+    const float4* tv = reinterpret_cast<const float4*>(tmp + 2 * to2);
 #pragma unroll 4
     for (int c = 0; c < t.r; ++c) {
-      float2 m[2], sv[8];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) m[i] = sU[tr + 16 * i][c];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) sv[j] = tmp[c][to + 8 * j];
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          acc[i][j].x = fmaf(m[i].x, sv[j].x, fmaf(-m[i].y, sv[j].y, acc[i][j].x));
-          acc[i][j].y = fmaf(m[i].x, sv[j].y, fmaf(m[i].y, sv[j].x, acc[i][j].y));
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int op = to + 8 * j;
-      if (op >= t.op_count) continue;
-      float2* d = dst + dst_off[t.op_begin + op] + r0;
+      float2 m[4], v[4];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int row = tr + 16 * i;
-        if (r0 + row < t.T) atomicAdd(d + row, acc[i][j]);
+        const float4 q = uv[c * 16 + 8 * i];
+        m[2 * i] = make_float2(q.x, q.y);
+        m[2 * i + 1] = make_float2(q.z, q.w);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float4 q = tv[c * (O / 2) + 16 * j];
+        v[2 * j] = make_float2(q.x, q.y);
+        v[2 * j + 1] = make_float2(q.z, q.w);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cmac(a2[i][j], m[i], v[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int op = 2 * to2 + (j & 1) + 32 * (j >> 1);
+      if (op >= t.op_count) continue;
+      float2* d = dst + doff[op] + r0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = 2 * tr2 + (i & 1) + 16 * (i >> 1);
+        if (r0 + row < t.T) atomicAdd(d + row, a2[i][j]);
       }
     }
     __syncthreads();
+    b2 ^= 1;
   }
 }
 
-__global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
-                                                const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
-                                                const float2* __restrict__ src, float2* __restrict__ dst) {
-  __shared__ __align__(16) float2 sh[LR_SH];
-  __shared__ int64_t soff[LR_O];
-  const LrTask t = tasks[blockIdx.x];
-  for (int p = threadIdx.x; p < LR_O; p += 128) soff[p] = p < t.op_count ? src_off[t.op_begin + p] : -1;
-  __syncthreads();
-  if (t.r <= 16) m2l_lr_body<1>(t, sh, soff, dst_off, pool, src, dst);
-  else m2l_lr_body<2>(t, sh, soff, dst_off, pool, src, dst);
-}
-
-void launch_m2l_lr(int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+// one launch per phase-1 row class (r ≤ 16, ≤ 32, ≤ 64); tasks[cls] sorted longest first
+void launch_m2l_lr(int cls, int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                    const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
   if (ntask <= 0) return;
-  k_m2l_lr<<<ntask, 128, 0, s>>>(tasks, src_off, dst_off, pool, src, dst);
+  switch (cls) {
+    case 0: k_m2l_lr<16><<<ntask, 128, LrCfg<16>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+    case 1: k_m2l_lr<32><<<ntask, 128, LrCfg<32>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+    default: k_m2l_lr<64><<<ntask, 128, LrCfg<64>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+  }
+}
+int m2l_lr_class(int r) { return r <= 16 ? 0 : (r <= 32 ? 1 : 2); }
+cudaError_t m2l_lr_prepare() {
+  return cudaFuncSetAttribute(k_m2l_lr<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, LrCfg<64>::SMEM);
 }
 
 // ------------------------------------------------------------------ GMRES helpers (a9)

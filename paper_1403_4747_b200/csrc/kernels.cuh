@@ -6,16 +6,25 @@
 
 namespace fda {
 
-// per source element, positions local to the source leaf centre:
-//   a = (q0.x, q0.y, q0.z, n.x), b = (q1.xyz, n.y), c = (q2.xyz, n.z)
+// per source element, positions local to the source leaf centre in wave
+// units (k·(y_q - c_leaf)): a = (Y0.x, Y0.y, Y0.z, n.x), b = (Y1.xyz, n.y), c = (Y2.xyz, n.z)
 struct __align__(16) SrcElem {
   float4 a, b, c;
+};
+
+// near-field CTA (one target leaf): elements [tb, tb+nt), source slots [s0, s1)
+// of the slot table (int2: source element, index into near_off)
+struct NearTask {
+  int32_t tb, nt, s0, s1;
 };
 
 struct KernelParams {
   float k;          // wavenumber
   float alpha_re;   // Burton–Miller coupling α
   float alpha_im;
+  float ak_re;      // k·Re α (near kernel in wave units)
+  float ak_im;      // k·Im α
+  float inv_k;      // 1/k
 };
 
 // one CTA of the grouped translation kernel: a tile of XR rows × ≤ XO ops of
@@ -37,7 +46,7 @@ struct XTask {
 inline int xvar_rows(int v) { return v == 0 ? 32 : (v == 1 ? 64 : (v == 2 ? 128 : 16)); }
 inline int xvar_ops(int v) { return v == 0 ? 64 : (v == 1 ? 32 : (v == 2 ? 16 : 128)); }
 
-// fused §4.2 M2L task: for ≤ LR_O ops sharing K̃ ≈ Û V̂ (r ≤ 32):
+// fused §4.2 M2L task: for ≤ LR_O ops sharing K̃ ≈ Û V̂ (r ≤ 64):
 // tmp = V̂ · src (r × ops, shared memory), dst += Û · tmp
 constexpr int LR_O = 64;
 struct LrTask {
@@ -73,18 +82,21 @@ void launch_scatter_f32(const float2* y_near, const float2* y_far, const int32_t
                         int e0, int e1, cudaStream_t s);
 void launch_scatter_f64(const float2* y_near, const float2* y_far, const int32_t* perm, double2* y_caller, int n,
                         int e0, int e1, cudaStream_t s);
-void launch_near(int nleaf, const int32_t* order, const int32_t* leaf_begin, const int32_t* leaf_end, const int32_t* near_ptr,
-                 const int32_t* near_idx, const float4* near_off, const float4* tgt_pos, const float4* tgt_nrm,
-                 const SrcElem* src, const float* src_w, const int32_t* corr_ptr, const int32_t* corr_col,
-                 const float2* corr_val, const float2* x, float2* y, KernelParams kp, bool alpha_pure_imag,
-                 int kind, cudaStream_t s);
+void launch_near(int ntask, const NearTask* tasks, const int2* slots, const float4* near_off, const float4* tgt_pos,
+                 const float4* tgt_nrm, const SrcElem* src, const float* src_w, const int32_t* corr_ptr,
+                 const int32_t* corr_col, const float2* corr_val, const float2* x, float2* y, KernelParams kp,
+                 bool alpha_pure_imag, int kind, cudaStream_t s);
 void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const float2* x, float2* out, int max_rows,
                 cudaStream_t s);
 void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s);
 void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const int64_t* src_off,
                   const int64_t* dst_off, const float2* pool, const float2* src, float2* dst, cudaStream_t s);
-void launch_m2l_lr(int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,
-                   const float2* pool, const float2* src, float2* dst, cudaStream_t s);    // r ≤ 32
+// fused §4.2 M2L for r ≤ 64; cls = m2l_lr_class(r) (phase-1 rows 16 / 32 / 64)
+void launch_m2l_lr(int cls, int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                   const float2* pool, const float2* src, float2* dst, cudaStream_t s);
+int m2l_lr_class(int r);
+constexpr int LR_MAX_R = 64;
+cudaError_t m2l_lr_prepare();
 void launch_xlate_tc(int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                      const float* tcpool, const float* srcp, float2* dst, cudaStream_t s);
 void launch_split_states(const float2* states, const int64_t* off, const int64_t* poff, int T, int Tp, int64_t s0,
