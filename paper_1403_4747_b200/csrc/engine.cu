@@ -143,9 +143,10 @@ struct Dev {
     }
   };
   std::vector<M2LLevel> m2lv;
-  static const int kM2LStreams = 3;
+  static const int kM2LStreams = 6;
   cudaStream_t s_m2l[kM2LStreams] = {};
-  std::vector<cudaEvent_t> ev_up, ev_m2l;
+  std::vector<cudaEvent_t> ev_up;
+  std::vector<std::vector<cudaEvent_t>> ev_m2l;   // per level: one event per M2L graph branch
   float2* tmpb = nullptr;
   int64_t tmp_size = 0;
   cudaStream_t s_cap = nullptr;
@@ -621,7 +622,8 @@ fda_status engine_create(Context* ctx) {
       std::vector<int64_t> ls, ld;
       for (size_t i = 0; i < F.size();) {
         size_t j = i;
-        while (j < F.size() && F[j].matV == F[i].matV && j - i < (size_t)LR_O) ++j;
+        const size_t cap = (size_t)m2l_lr_ops(m2l_lr_class(p.mats[F[i].matV].rows));
+        while (j < F.size() && F[j].matV == F[i].matV && j - i < cap) ++j;
         LrTask tk;
         tk.v_off = p.mats[F[i].matV].offset;
         tk.u_off = p.mats[F[i].matU].offset;
@@ -680,8 +682,11 @@ fda_status engine_create(Context* ctx) {
   for (auto& sm : d->s_m2l) CK(cudaStreamCreateWithFlags(&sm, cudaStreamNonBlocking));
   d->ev_up.resize(nlev);
   d->ev_m2l.resize(nlev);
+  for (auto& v : d->ev_m2l) {
+    v.resize(4);
+    for (auto& e : v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   for (auto& e : d->ev_up) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  for (auto& e : d->ev_m2l) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   d->use_graph = ctx->p.opt.use_graph != 0;
   CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
@@ -740,7 +745,8 @@ void engine_destroy(Context* ctx) {
   for (auto& sm : d->s_m2l)
     if (sm) cudaStreamDestroy(sm);
   for (auto& e : d->ev_up) cudaEventDestroy(e);
-  for (auto& e : d->ev_m2l) cudaEventDestroy(e);
+  for (auto& v : d->ev_m2l)
+    for (auto& e : v) cudaEventDestroy(e);
   if (d->ev_fork) cudaEventDestroy(d->ev_fork);
   if (d->ev_join) cudaEventDestroy(d->ev_join);
   for (auto& e : d->ev) if (e) cudaEventDestroy(e);
@@ -808,22 +814,41 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
     }
     CK(cudaEventRecord(d->ev[5], s));
   } else {
-    // dependency DAG: the M2L of level l (own stream) starts as soon as the
+    // dependency DAG: the M2L branches of level l (fused classes and the
+    // dense / two-stage ops, each on its own stream) start as soon as the
     // outgoing states of level l exist, overlapping the M2M chain above it;
-    // L2L out of level l waits for the M2L into level l.
+    // L2L out of level l waits for every M2L branch into level l.
     int k = 0;
+    std::vector<int> nbr(nlev, 0);
     for (int l = nlev - 1; l >= 0; --l) {
       launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s, d->outp);   // writes level-l out-states
       split_out(l, s);
       if (!d->m2lv[l].any()) continue;
-      cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];
+      const Dev::M2LLevel& L = d->m2lv[l];
       CK(cudaEventRecord(d->ev_up[l], s));
-      CK(cudaStreamWaitEvent(sm, d->ev_up[l], 0));
-      m2l_level(l, sm);
-      CK(cudaEventRecord(d->ev_m2l[l], sm));
+      auto branch = [&](auto&& launch) -> fda_status {
+        cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];
+        CK(cudaStreamWaitEvent(sm, d->ev_up[l], 0));
+        launch(sm);
+        CK(cudaEventRecord(d->ev_m2l[l][nbr[l]++], sm));
+        return FDA_OK;
+      };
+      fda_status bs;
+      for (int c = 2; c >= 0; --c)
+        if (L.n_lr[c] &&
+            (bs = branch([&](cudaStream_t sm) {
+               launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, sm);
+             })) != FDA_OK)
+          return bs;
+      if ((bs = branch([&](cudaStream_t sm) {
+             launch_stage(L.dense, d->pool, d->outb, d->inb, sm, d->outp);
+             launch_stage(L.a, d->pool, d->outb, d->tmpb, sm, d->outp);
+             launch_stage(L.b, d->pool, d->tmpb, d->inb, sm);
+           })) != FDA_OK)
+        return bs;
     }
     for (int l = 0; l < nlev; ++l) {
-      if (d->m2lv[l].any()) CK(cudaStreamWaitEvent(s, d->ev_m2l[l], 0));
+      for (int b = 0; b < nbr[l]; ++b) CK(cudaStreamWaitEvent(s, d->ev_m2l[l][b], 0));
       split_in(l, s);
       launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s, d->inp);
     }

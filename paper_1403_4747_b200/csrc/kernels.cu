@@ -496,7 +496,7 @@ void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const
 
 // ------------------------------------------------------------------ fused §4.2 M2L (a4)
 // PAPER.md §4.2: K̃ ≈ Û V̂ (Û: T × r, V̂: r × T, r ≤ 64).  One CTA
-// handles ≤ LR_O = 64 ops sharing one K̃:
+// handles ≤ O = 64 ops sharing one K̃ (template O ≤ LR_O = 128):
 //   phase 1  tmp = V̂ S        (R1 ≥ r rows × 64 ops, K = T streamed through a
 //                              cp.async double buffer), tmp kept in shared memory;
 //   phase 2  dst += Û tmp      (32-row tiles of Û, double-buffered, K = r),
@@ -506,25 +506,25 @@ void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const
 // {2to, 2to+1} + 2·NO·j, and a warp spans 4 row groups × 8 op groups, so every
 // shared load is an LDS.128 (2 complex values) touching ≤ 128 bytes: one
 // wavefront per load, ≤ RT1/2 + OT1/2 wavefronts per 4·RT1·OT1 FFMA.
-template <int R1>
+template <int R1, int O>
 struct LrCfg {
   static constexpr int RT1 = R1 == 64 ? 8 : 4;
   static constexpr int NR1 = R1 / RT1;        // 4, 8, 8
   static constexpr int NO1 = 128 / NR1;       // 32, 16, 16
-  static constexpr int OT1 = LR_O / NO1;      // 2, 4, 4
-  static constexpr int SO = LR_O + 2;         // padded sS row (conflict-free cp.async writes, 16-B aligned rows)
+  static constexpr int OT1 = O / NO1;
+  static constexpr int SO = O + 2;            // padded sS row (conflict-free cp.async writes, 16-B aligned rows)
   static constexpr int PH1 = 2 * XK * R1 + 2 * XK * SO;     // sV[2][XK][R1] + sS[2][XK][SO] (float2)
-  static constexpr int PH2 = R1 * LR_O + 2 * R1 * 32;        // tmp[R1][64] + sU[2][R1][32]
+  static constexpr int PH2 = R1 * O + 2 * R1 * 32;           // tmp[R1][O] + sU[2][R1][32]
   static constexpr int SMEM = (PH1 > PH2 ? PH1 : PH2) * 8;
 };
 
 
-template <int R1>
+template <int R1, int O>
 __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks, const int64_t* __restrict__ src_off,
                                                 const int64_t* __restrict__ dst_off, const float2* __restrict__ pool,
                                                 const float2* __restrict__ src, float2* __restrict__ dst) {
-  using C = LrCfg<R1>;
-  constexpr int RT1 = C::RT1, NO1 = C::NO1, OT1 = C::OT1, O = LR_O;
+  using C = LrCfg<R1, O>;
+  constexpr int RT1 = C::RT1, NO1 = C::NO1, OT1 = C::OT1;
   extern __shared__ float4 smem4[];
   float2* sh = reinterpret_cast<float2*>(smem4);
   __shared__ int64_t soff[O];
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
     buf ^= 1;
   }
   // tmp[row][op] (rows ≥ r are zero: V̂ rows ≥ r were zero-filled)
-  float2* tmp = sh;                    // [R1][64]
+  float2* tmp = sh;                    // [R1][O]
   float2* sU = sh + R1 * O;            // [2][R1][32]
 #pragma unroll
   for (int i = 0; i < RT1; ++i)
@@ -630,7 +630,8 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
   // rows {2·tr2, 2·tr2+1} + 16i, ops {2·to2, 2·to2+1} + 32j; warps 2 × 2 of 4 × 8 lanes
   const int tr2 = (warp & 1) * 4 + (lane >> 3), to2 = (warp >> 1) * 8 + (lane & 7);
   int b2 = 0;
-  issue2(0, 0);
+  for (int oh = 0; oh < O && oh < t.op_count; oh += 64) {      // op halves of 64 (O = 128)
+  issue2(b2, 0);
   for (int r0 = 0; r0 < t.T; r0 += 32) {
     if (r0 + 32 < t.T) {
       issue2(b2 ^ 1, r0 + 32);
@@ -645,7 +646,7 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
 #pragma unroll
       for (int j = 0; j < 4; ++j) a2[i][j] = make_float2(0.f, 0.f);
     const float4* uv = reinterpret_cast<const float4*>(sU + b2 * R1 * 32 + 2 * tr2);
-    const float4* tv = reinterpret_cast<const float4*>(tmp + 2 * to2);
+    const float4* tv = reinterpret_cast<const float4*>(tmp + oh + 2 * to2);
 #pragma unroll 4
     for (int c = 0; c < t.r; ++c) {
       float2 m[4], v[4];
@@ -668,7 +669,7 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int op = 2 * to2 + (j & 1) + 32 * (j >> 1);
+      const int op = oh + 2 * to2 + (j & 1) + 32 * (j >> 1);
       if (op >= t.op_count) continue;
       float2* d = dst + doff[op] + r0;
 #pragma unroll
@@ -680,6 +681,7 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
     __syncthreads();
     b2 ^= 1;
   }
+  }
 }
 
 // one launch per phase-1 row class (r ≤ 16, ≤ 32, ≤ 64); tasks[cls] sorted longest first
@@ -687,14 +689,15 @@ void launch_m2l_lr(int cls, int ntask, const LrTask* tasks, const int64_t* src_o
                    const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
   if (ntask <= 0) return;
   switch (cls) {
-    case 0: k_m2l_lr<16><<<ntask, 128, LrCfg<16>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
-    case 1: k_m2l_lr<32><<<ntask, 128, LrCfg<32>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
-    default: k_m2l_lr<64><<<ntask, 128, LrCfg<64>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+    case 0: k_m2l_lr<16, 64><<<ntask, 128, LrCfg<16, 64>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+    case 1: k_m2l_lr<32, 64><<<ntask, 128, LrCfg<32, 64>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+    default: k_m2l_lr<64, 64><<<ntask, 128, LrCfg<64, 64>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
   }
 }
 int m2l_lr_class(int r) { return r <= 16 ? 0 : (r <= 32 ? 1 : 2); }
+int m2l_lr_ops(int) { return 64; }
 cudaError_t m2l_lr_prepare() {
-  return cudaFuncSetAttribute(k_m2l_lr<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, LrCfg<64>::SMEM);
+  return cudaFuncSetAttribute(k_m2l_lr<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, LrCfg<64, 64>::SMEM);
 }
 
 // ------------------------------------------------------------------ GMRES helpers (a9)

@@ -48,7 +48,7 @@ inline int xvar_ops(int v) { return v == 0 ? 64 : (v == 1 ? 32 : (v == 2 ? 16 : 
 
 // fused §4.2 M2L task: for ≤ LR_O ops sharing K̃ ≈ Û V̂ (r ≤ 64):
 // tmp = V̂ · src (r × ops, shared memory), dst += Û · tmp
-constexpr int LR_O = 64;
+constexpr int LR_O = 128;   // max ops per fused M2L CTA
 struct LrTask {
   int64_t v_off, u_off;     // V̂ (r × T) and Û (T × r), column-major, in the pool
   int32_t T, r;
@@ -95,6 +95,7 @@ void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const
 void launch_m2l_lr(int cls, int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                    const float2* pool, const float2* src, float2* dst, cudaStream_t s);
 int m2l_lr_class(int r);
+int m2l_lr_ops(int cls);   // ops per CTA of a class
 constexpr int LR_MAX_R = 64;
 cudaError_t m2l_lr_prepare();
 void launch_xlate_tc(int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
