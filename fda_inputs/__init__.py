@@ -10,6 +10,6 @@ Workload recipe: SURVEY.md §8(d) (configs 1-5 of BASELINE.json) and the
 pulsating-sphere family of PAPER.md §5.1 (octahedral spheres with
 N = 8·4^n, k = π·2^(n-3)).
 """
-from .meshes import icosphere, octasphere, graded_spheroid  # noqa: F401
+from .meshes import icosphere, octasphere, graded_spheroid, geodesic_sphere  # noqa: F401
 from .vectors import random_density, sampled_rows, plane_wave_direction  # noqa: F401
-from .configs import CONFIGS, config_mesh, WorkloadConfig  # noqa: F401
+from .configs import CONFIGS, config_mesh, WorkloadConfig, POINT_SOURCE, point_source_mesh  # noqa: F401

@@ -4,6 +4,9 @@
   permutations of (0, ±1, ±φ), normalised), subdivided s times 1:4 at edge
   midpoints projected to the sphere.  20·4^s triangles, CCW seen from outside,
   generation order = caller order.
+* ``geodesic_sphere(nu, radius)``: icosahedron with every face split at
+  edge frequency ν into ν² triangles, vertices projected to the sphere;
+  20·ν² triangles (ν = 73: 106,580 ≈ the 106,032 of PAPER.md Table 3).
 * ``octasphere(n, radius)``: regular octahedron subdivided the same way;
   8·4^n triangles, the N sequence of PAPER.md Table 2.
 * ``graded_spheroid(...)``: prolate spheroid x²/a² + (y²+z²)/b² = 1 meshed in
@@ -86,6 +89,42 @@ def icosphere(s: int, radius: float = 0.5):
     faces = _orient_outward(verts, faces)
     verts, faces = _subdivide(verts, faces, s, radius)
     return _finish(verts, faces)
+
+
+def geodesic_sphere(nu: int, radius: float = 1.0):
+    """Frequency-ν geodesic icosphere: 20·ν² triangles, CCW seen from outside;
+    caller order = (face of the icosahedron, row i, column j, up/down)."""
+    if nu < 1 or nu > 1000:
+        raise ValueError("frequency out of range [1, 1000]")
+    V0, F0 = icosphere(0, 1.0)
+    pts, tris = [], []
+    nloc = (nu + 1) * (nu + 2) // 2
+    for f, (a, b, c) in enumerate(F0):
+        A, B, C = V0[a], V0[b], V0[c]
+        ij = [(i, j) for i in range(nu + 1) for j in range(nu + 1 - i)]
+        idx = {p: f * nloc + q for q, p in enumerate(ij)}
+        for (i, j) in ij:
+            pts.append(A + (i / nu) * (B - A) + (j / nu) * (C - A))
+        for i in range(nu):
+            for j in range(nu - i):
+                tris.append((idx[(i, j)], idx[(i + 1, j)], idx[(i, j + 1)]))
+                if i + j < nu - 1:
+                    tris.append((idx[(i + 1, j)], idx[(i + 1, j + 1)], idx[(i, j + 1)]))
+    P = np.array(pts)
+    P /= np.linalg.norm(P, axis=1)[:, None]
+    # merge the copies of shared edge / corner vertices
+    key = np.round(P * 1e9).astype(np.int64)
+    uniq, first, inv = np.unique(key, axis=0, return_index=True, return_inverse=True)
+    order = np.argsort(first)                    # keep first-appearance order
+    rank = np.empty_like(order)
+    rank[order] = np.arange(len(order))
+    V = P[first[order]] * radius
+    F = rank[inv.reshape(-1)][np.array(tris)]
+    # orient CCW seen from outside (vectorised _orient_outward)
+    pa, pb, pc = V[F[:, 0]], V[F[:, 1]], V[F[:, 2]]
+    flip = np.einsum("ij,ij->i", np.cross(pb - pa, pc - pa), pa + pb + pc) < 0
+    F[flip] = F[flip][:, [0, 2, 1]]
+    return _finish(V, F)
 
 
 def octasphere(n: int, radius: float = 1.0):

@@ -56,6 +56,13 @@ typedef struct { double re, im; } fda_cplx;
 #define FDA_HOST   0   /* x, y, b, u are host complex128 arrays (copied in/out) */
 #define FDA_DEVICE 1   /* x, y, b, u are device complex64 arrays on opt.device  */
 #define FDA_LOCAL  2   /* (nranks > 1) return this rank's rows only, others zero; no collective */
+/* (nranks > 1, with FDA_DEVICE | FDA_LOCAL) the two halves of a sharded matvec
+ * around the exchange of partial outgoing states: UP = gather, near field
+ * (launched), S2M + M2M of this rank's elements, pack; DOWN = unpack, M2L,
+ * L2L, L2T, scatter.  Used with fda_exchange_local as a one-GPU test
+ * transport; fda_matvec without these flags does UP, NCCL, DOWN. */
+#define FDA_PHASE_UP   4
+#define FDA_PHASE_DOWN 8
 
 typedef struct {
   int32_t max_leaf;      /* split an octree cube while it owns more elements (64)        */
@@ -135,6 +142,16 @@ fda_status fda_matvec(fda_ctx* ctx, const void* x, void* y, int32_t flags, void*
  * side with ∂u/∂n = 0, reading C22).  dir need not be unit. */
 fda_status fda_rhs_plane_wave(fda_ctx* ctx, const double dir[3], void* b, int32_t flags);
 
+/* b_i = u_inc(x_i) + α ∂u_inc/∂n(x_i) for a unit point source
+ * u_inc(x) = e^{ikR}/(4πR), R = |x - src| (Eq. (3)), outside the
+ * scatterer — the incident field of PAPER.md §5.2 ("The point source is at
+ * (-2, 0, 0)"; Table 3).  n_i is the kernel normal (into the
+ * body, reading C1).  src: 3 doubles (host).  b: caller order, FDA_HOST
+ * (complex128) or FDA_DEVICE (complex64), computed in fp64 on the device.
+ * FDA_E_INVALID_ARG if src is not finite or coincides with a collocation
+ * point. */
+fda_status fda_rhs_point_source(fda_ctx* ctx, const double src[3], void* b, int32_t flags);
+
 /* b = B v with B = -(α/2)I + S + αK' — the right-hand-side operator of Eq. (4)
  * (P:176-181): (B v)_i = -(α/2) v_i + Σ_j ∫_Δj [G + α ∂G/∂n_x](x_i, y) dS_y v_j,
  * applied by the second fast directional pass (G sources, the same target
@@ -154,17 +171,32 @@ fda_status fda_stats(const fda_ctx* ctx, fda_build_info* info);
 
 /* Multi-GPU.  With opt.nranks > 1 every rank builds the same
  * mesh with its own opt.rank; the leaves are split into contiguous Morton
- * ranges balanced by estimated work.  Each rank replicates the upward pass
- * (S2M, M2M), runs M2L/L2L only for the incoming states of boxes that contain
- * one of its leaves, and L2T + near field for its own leaves; fda_matvec and
- * fda_rhs_apply then sum the ranks' rows with one NCCL all-reduce of y (the
- * only exchange), so every rank returns the full y and bm_solve runs
- * unchanged on every rank.  Vectors x are full-length on every rank.
+ * ranges balanced by estimated work.  Per matvec each rank runs the upward
+ * pass (S2M, M2M; Algorithm Step 2) on its own elements only,
+ * producing PARTIAL outgoing states (the full state is the sum over ranks, by
+ * linearity); one grouped ncclSend/ncclRecv then delivers to every rank the
+ * other ranks' partials of exactly the outgoing states its M2L ops read (the
+ * equivalent densities of boxes in its interaction lists, including the top
+ * levels of the tree); the rank adds them and runs M2L/L2L for the incoming
+ * states of boxes containing its leaves, L2T and the near field (which
+ * overlaps the exchange) for its own leaves.  fda_matvec / fda_rhs_apply then
+ * sum the ranks' rows with one NCCL all-reduce of y (skipped with FDA_LOCAL),
+ * so every rank returns the full y and bm_solve runs unchanged on every rank.
+ * Vectors x are full-length on every rank.
  * fda_nccl_unique_id: 128-byte NCCL id generated on one rank (libnccl is
  * loaded on first use); the caller broadcasts it (e.g. torch.distributed);
  * fda_comm_init: collective over the nranks ranks, before the first matvec. */
 fda_status fda_nccl_unique_id(void* id128);
 fda_status fda_comm_init(fda_ctx* ctx, const void* id128);
+
+/* Test transport of the sharded exchange on ONE GPU ("fake-partition mode",
+ * SURVEY §4): ctxs[0..n) are the n rank contexts of one sharded build
+ * (opt.nranks = n, opt.rank = index), all on the same device, each having
+ * completed fda_matvec(..., FDA_DEVICE | FDA_LOCAL | FDA_PHASE_UP); copies
+ * every rank's packed partials into its peers' receive buffers (synchronous),
+ * after which each rank runs FDA_PHASE_DOWN.  FDA_E_INTERNAL if the ranks'
+ * send / receive plans disagree. */
+fda_status fda_exchange_local(fda_ctx** ctxs, int32_t n);
 
 /* Per-stage device times (ms, CUDA events) of the last fda_matvec timed with
  * fda_set_profiling(ctx, 1): [gather, near, s2m, m2m, m2l, l2l, l2t, scatter].

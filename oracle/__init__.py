@@ -33,4 +33,5 @@ from .selfterms import self_lhs, self_rhs, self_integrals  # noqa: F401
 from .dense import (lhs_rows, rhs_rows, lhs_matvec_rows, lhs_dense, rhs_dense,  # noqa: F401
                     tier_of)
 from .solvers import gmres, lu_solve  # noqa: F401
-from .analytic import rigid_sphere_total, pulsating_sphere_u, plane_wave_rhs  # noqa: F401
+from .analytic import (rigid_sphere_total, pulsating_sphere_u, plane_wave_rhs,  # noqa: F401
+                       point_source_rhs, rigid_sphere_point_source_total)

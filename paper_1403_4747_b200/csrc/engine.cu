@@ -49,6 +49,10 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
 };
 NcclApi& nccl(std::string& err) {
   static NcclApi api;
@@ -65,7 +69,12 @@ NcclApi& nccl(std::string& err) {
     api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
     api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
     api.errStr = (decltype(api.errStr))dlsym(h, "ncclGetErrorString");
-    api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.errStr;
+    api.send = (decltype(api.send))dlsym(h, "ncclSend");
+    api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+    api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+    api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
+    api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.errStr && api.send &&
+             api.recv && api.groupStart && api.groupEnd;
     if (!api.ok) err = "libnccl.so.2 lacks a required symbol";
   }
   return api;
@@ -112,8 +121,14 @@ struct Dev {
   bool alpha_pure_imag = false;
   int n_near = 0;                  // near-field CTAs (owned leaves)
   int e0 = 0, e1 = 0;              // owned element range (tree order)
-  int nranks = 1;
+  int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
+  // sharded: exchange of partial outgoing states (partition.cpp); per peer the
+  // entries (complex) sent / received, packed in state-id order
+  float2 *sendb = nullptr, *recvb = nullptr;
+  int64_t *xs_idx = nullptr, *xr_idx = nullptr;       // outb position of every packed entry
+  int64_t n_send = 0, n_recv = 0;
+  std::vector<int64_t> soff, scnt, roff, rcnt;         // per peer, in complex entries
   float4* near_off = nullptr;
   int32_t *corr_ptr = nullptr, *corr_col = nullptr;
   float2* corr_val = nullptr;
@@ -662,6 +677,32 @@ fda_status engine_create(Context* ctx) {
     UP(&d->tcpool, d->tc_host.data(), d->tc_host.size());
     std::vector<float>().swap(d->tc_host);
   }
+  // sharded: packed exchange lists (partition.cpp xsend / xrecv)
+  d->rank = ctx->p.opt.rank;
+  if (d->nranks > 1) {
+    const int R = d->nranks;
+    auto Tof = [&](int64_t st) { return (int64_t)t.levels[t.boxes[p.out_states[st].box].level].rank; };
+    std::vector<int64_t> xs, xr;
+    d->soff.assign(R, 0); d->scnt.assign(R, 0); d->roff.assign(R, 0); d->rcnt.assign(R, 0);
+    for (int q = 0; q < R; ++q) {
+      d->soff[q] = (int64_t)xs.size();
+      for (int64_t st : p.xsend[q])
+        for (int64_t e = 0; e < Tof(st); ++e) xs.push_back(p.out_offset[st] + e);
+      d->scnt[q] = (int64_t)xs.size() - d->soff[q];
+      d->roff[q] = (int64_t)xr.size();
+      for (int64_t st : p.xrecv[q])
+        for (int64_t e = 0; e < Tof(st); ++e) xr.push_back(p.out_offset[st] + e);
+      d->rcnt[q] = (int64_t)xr.size() - d->roff[q];
+    }
+    d->n_send = (int64_t)xs.size();
+    d->n_recv = (int64_t)xr.size();
+    UP(&d->xs_idx, xs.data(), xs.size());
+    UP(&d->xr_idx, xr.data(), xr.size());
+    AL(&d->sendb, (size_t)std::max<int64_t>(1, d->n_send));
+    AL(&d->recvb, (size_t)std::max<int64_t>(1, d->n_recv));
+    CK(cudaMemset(d->recvb, 0, sizeof(float2) * std::max<int64_t>(1, d->n_recv)));
+    d->use_graph = false;   // the NCCL exchange sits between the passes: eager launches
+  }
   // kernels per matvec: gather, near, s2m, every non-empty translation launch, l2t, scatter
   int64_t nl = 4 + (d->n_s2m > 0);  // gather, near, l2t, scatter (+ s2m)
   if (d->use_tc)  // per-level state splits
@@ -687,7 +728,7 @@ fda_status engine_create(Context* ctx) {
     for (auto& e : v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   for (auto& e : d->ev_up) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  d->use_graph = ctx->p.opt.use_graph != 0;
+  d->use_graph = ctx->p.opt.use_graph != 0 && d->nranks <= 1;
   CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
   for (auto& e : d->ev) CK(cudaEventCreate(&e));
@@ -860,9 +901,102 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   return FDA_OK;
 }
 
+// ---- sharded matvec (nranks > 1): partial upward pass →
+// exchange of partial outgoing states → downward pass for the owned targets.
+// Eager launches; the near field runs on its own stream across the exchange.
+static fda_status run_sharded_up(Context* ctx, Dev* d, cudaStream_t s, int kind) {
+  CK(cudaEventRecord(d->ev_fork, s));
+  CK(cudaStreamWaitEvent(d->s_near, d->ev_fork, 0));
+  launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
+              kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
+              kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, d->s_near);
+  CK(cudaEventRecord(d->ev_join, d->s_near));
+  if (d->out_size) CK(cudaMemsetAsync(d->outb, 0, sizeof(float2) * d->out_size, s));
+  if (d->in_size) CK(cudaMemsetAsync(d->inb, 0, sizeof(float2) * d->in_size, s));
+  if (d->tmp_size) CK(cudaMemsetAsync(d->tmpb, 0, sizeof(float2) * d->tmp_size, s));
+  if (kind) launch_s2m(d->n_s2m_rhs, d->s2m_rhs, d->pool, d->x_tree, d->outb, d->max_T, s);
+  else launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s);
+  const int nlev = (int)d->m2m.size();
+  for (int l = nlev - 1; l >= 0; --l) launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s, d->outp);   // partials
+  launch_pack(d->outb, d->xs_idx, d->sendb, d->n_send, s);
+  CK(cudaGetLastError());
+  return FDA_OK;
+}
+
+static fda_status exchange_nccl(Context* ctx, Dev* d, cudaStream_t s) {
+  if (!d->comm) { ctx->err = "sharded context: call fda_comm_init before fda_matvec"; return FDA_E_STATE; }
+  NcclApi& a = nccl(ctx->err);
+  if (!a.ok) return FDA_E_NCCL;
+  ncclResult_t r = a.groupStart();
+  for (int q = 0; q < d->nranks && r == ncclSuccess; ++q) {
+    if (q == d->rank) continue;
+    if (d->scnt[q] > 0) r = a.send(d->sendb + d->soff[q], (size_t)(2 * d->scnt[q]), ncclFloat, q, d->comm, s);
+    if (r == ncclSuccess && d->rcnt[q] > 0)
+      r = a.recv(d->recvb + d->roff[q], (size_t)(2 * d->rcnt[q]), ncclFloat, q, d->comm, s);
+  }
+  ncclResult_t r2 = a.groupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) {
+    ctx->err = std::string("NCCL exchange of outgoing states: ") + a.errStr(r);
+    return FDA_E_NCCL;
+  }
+  return FDA_OK;
+}
+
+static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
+  g_tcpool = d->tcpool;
+  launch_unpack_add(d->recvb, d->xr_idx, d->outb, d->n_recv, s);
+  const int nlev = (int)d->m2m.size();
+  if (d->use_tc)
+    for (int l = 0; l < nlev; ++l)
+      launch_split_states(d->outb, d->d_out_off, d->d_pout, d->lvl_T[l], d->lvl_Tp[l], d->out_lb[l],
+                          d->out_lb[l + 1], d->outp, s);
+  CK(cudaEventRecord(d->ev_up[0], s));
+  int k = 0;
+  std::vector<int> nbr(nlev, 0);
+  for (int l = nlev - 1; l >= 0; --l) {   // M2L branches of every level, concurrent
+    const Dev::M2LLevel& L = d->m2lv[l];
+    if (!L.any()) continue;
+    for (int c = 2; c >= -1; --c) {
+      if (c >= 0 && !L.n_lr[c]) continue;
+      cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];
+      CK(cudaStreamWaitEvent(sm, d->ev_up[0], 0));
+      if (c >= 0) {
+        launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, sm);
+      } else {
+        launch_stage(L.dense, d->pool, d->outb, d->inb, sm, d->outp);
+        launch_stage(L.a, d->pool, d->outb, d->tmpb, sm, d->outp);
+        launch_stage(L.b, d->pool, d->tmpb, d->inb, sm);
+      }
+      CK(cudaEventRecord(d->ev_m2l[l][nbr[l]++], sm));
+    }
+  }
+  for (int l = 0; l < nlev; ++l) {
+    for (int b = 0; b < nbr[l]; ++b) CK(cudaStreamWaitEvent(s, d->ev_m2l[l][b], 0));
+    if (d->use_tc)
+      launch_split_states(d->inb, d->d_in_off, d->d_pin, d->lvl_T[l], d->lvl_Tp[l], d->in_lb[l], d->in_lb[l + 1],
+                          d->inp, s);
+    launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s, d->inp);
+  }
+  launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
+  CK(cudaStreamWaitEvent(s, d->ev_join, 0));
+  CK(cudaGetLastError());
+  return FDA_OK;
+}
+
 // run_core through a CUDA graph (captured once: all its buffers are internal,
 // so the same graph serves every call); profiled calls run it eagerly.
-static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
+// phase (sharded contexts only): 0 = whole matvec with the NCCL exchange,
+// FDA_PHASE_UP / FDA_PHASE_DOWN = the halves around an external exchange
+// (fda_exchange_local, the one-GPU test transport)
+static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind, int phase = 0) {
+  if (d->nranks > 1) {
+    fda_status st = FDA_OK;
+    if (phase != FDA_PHASE_DOWN && (st = run_sharded_up(ctx, d, s, kind)) != FDA_OK) return st;
+    if (phase == 0 && (st = exchange_nccl(ctx, d, s)) != FDA_OK) return st;
+    if (phase != FDA_PHASE_UP) st = run_sharded_down(ctx, d, s);
+    return st;
+  }
   if (ctx->profiling || !d->use_graph) return run_core(ctx, d, s, kind);
   cudaGraphExec_t& ge = d->graph_exec[kind];
   if (!ge) {
@@ -889,13 +1023,14 @@ static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
 
 // device-pointer matvec in caller order (float2 in, float2 out)
 static fda_status matvec_dev(Context* ctx, Dev* d, const float2* x, float2* y, cudaStream_t s, int kind = 0,
-                             bool local = false) {
-  const bool prof = ctx->profiling;
+                             bool local = false, int phase = 0) {
+  const bool prof = ctx->profiling && d->nranks <= 1;
   if (prof) CK(cudaEventRecord(d->ev[0], s));
-  launch_gather_f32(x, d->perm, d->x_tree, d->n, s);
+  if (phase != FDA_PHASE_DOWN) launch_gather_f32(x, d->perm, d->x_tree, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[1], s));
-  fda_status st = core(ctx, d, s, kind);
+  fda_status st = core(ctx, d, s, kind, phase);
   if (st != FDA_OK) return st;
+  if (phase == FDA_PHASE_UP) return FDA_OK;
   launch_scatter_f32(d->y_near, d->y_far, d->perm, y, d->n, d->e0, d->e1, s);
   if (prof) CK(cudaEventRecord(d->ev[7], s));
   d->timed = prof;
@@ -912,10 +1047,17 @@ fda_status engine_apply(Context* ctx, const void* x, void* y, int32_t flags, voi
   CK(cudaSetDevice(d->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool local = (flags & FDA_LOCAL) != 0;
+  const int phase = flags & (FDA_PHASE_UP | FDA_PHASE_DOWN);
+  if (phase) {
+    if (d->nranks <= 1 || !(flags & FDA_DEVICE) || !local || phase == (FDA_PHASE_UP | FDA_PHASE_DOWN)) {
+      ctx->err = "FDA_PHASE_UP / FDA_PHASE_DOWN need a sharded context, FDA_DEVICE and FDA_LOCAL";
+      return FDA_E_INVALID_ARG;
+    }
+  }
   if (flags & FDA_DEVICE)
-    return matvec_dev(ctx, d, static_cast<const float2*>(x), static_cast<float2*>(y), s, kind, local);
+    return matvec_dev(ctx, d, static_cast<const float2*>(x), static_cast<float2*>(y), s, kind, local, phase);
   // host complex128 in/out
-  const bool prof = ctx->profiling;
+  const bool prof = ctx->profiling && d->nranks <= 1;
   CK(cudaMemcpyAsync(d->xh, x, sizeof(double2) * d->n, cudaMemcpyHostToDevice, s));
   if (prof) CK(cudaEventRecord(d->ev[0], s));
   launch_gather_f64(d->xh, d->perm, d->x_tree, d->n, s);
@@ -931,6 +1073,29 @@ fda_status engine_apply(Context* ctx, const void* x, void* y, int32_t flags, voi
   }
   CK(cudaMemcpyAsync(y, d->yh, sizeof(double2) * d->n, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return FDA_OK;
+}
+
+// one-GPU test transport of the sharded exchange: copies every rank's packed
+// partials for every peer into that peer's receive buffer (what the grouped
+// ncclSend / ncclRecv of exchange_nccl does across GPUs)
+fda_status engine_exchange_local(Context** ctxs, int n) {
+  for (int r = 0; r < n; ++r) {
+    Dev* dr = static_cast<Dev*>(ctxs[r]->dev);
+    for (int q = 0; q < n; ++q) {
+      if (q == r) continue;
+      Dev* dq = static_cast<Dev*>(ctxs[q]->dev);
+      if (dr->rcnt[q] != dq->scnt[r]) {
+        ctxs[r]->err = "exchange plan mismatch between ranks";
+        return FDA_E_INTERNAL;
+      }
+      if (dr->rcnt[q] > 0) {
+        Context* ctx = ctxs[r];
+        CK(cudaMemcpy(dr->recvb + dr->roff[q], dq->sendb + dq->soff[r], sizeof(float2) * dr->rcnt[q],
+                      cudaMemcpyDeviceToDevice));
+      }
+    }
+  }
   return FDA_OK;
 }
 
@@ -965,6 +1130,22 @@ fda_status engine_rhs_plane_wave(Context* ctx, const double dir[3], void* b, int
   }
   launch_plane_wave(d->cen, d->nrm, d->perm, d->n, ctx->p.k, ctx->p.alpha.real(), ctx->p.alpha.imag(), dir[0] / nn,
                     dir[1] / nn, dir[2] / nn, nullptr, d->yh, 0);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(b, d->yh, sizeof(double2) * d->n, cudaMemcpyDeviceToHost));
+  return FDA_OK;
+}
+
+fda_status engine_rhs_point_source(Context* ctx, const double src[3], void* b, int32_t flags) {
+  Dev* d = static_cast<Dev*>(ctx->dev);
+  CK(cudaSetDevice(d->device));
+  const double are = ctx->p.alpha.real(), aim = ctx->p.alpha.imag();
+  if (flags & FDA_DEVICE) {
+    launch_point_source(d->cen, d->nrm, d->perm, d->n, ctx->p.k, are, aim, src[0], src[1], src[2],
+                        static_cast<float2*>(b), nullptr, 0);
+    CK(cudaGetLastError());
+    return FDA_OK;
+  }
+  launch_point_source(d->cen, d->nrm, d->perm, d->n, ctx->p.k, are, aim, src[0], src[1], src[2], nullptr, d->yh, 0);
   CK(cudaGetLastError());
   CK(cudaMemcpy(b, d->yh, sizeof(double2) * d->n, cudaMemcpyDeviceToHost));
   return FDA_OK;

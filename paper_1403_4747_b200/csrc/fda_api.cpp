@@ -231,6 +231,32 @@ fda_status fda_rhs_plane_wave(fda_ctx* ctx, const double dir[3], void* b, int32_
   return engine_rhs_plane_wave(ctx, dir, b, flags);
 }
 
+fda_status fda_exchange_local(fda_ctx** ctxs, int32_t n) {
+  if (!ctxs || n < 2) return FDA_E_INVALID_ARG;
+  std::vector<fda::Context*> cs(n);
+  for (int i = 0; i < n; ++i) {
+    if (!ctxs[i] || !ctxs[i]->dev || ctxs[i]->p.opt.nranks != n || ctxs[i]->p.opt.rank != i) {
+      if (ctxs[i]) ctxs[i]->err = "fda_exchange_local: ctxs[i] must be rank i of an n-rank device build";
+      return FDA_E_INVALID_ARG;
+    }
+    cs[i] = ctxs[i];
+  }
+  return fda::engine_exchange_local(cs.data(), n);
+}
+
+fda_status fda_rhs_point_source(fda_ctx* ctx, const double src[3], void* b, int32_t flags) {
+  if (!ctx || !src || !b) return FDA_E_INVALID_ARG;
+  if (!std::isfinite(src[0]) || !std::isfinite(src[1]) || !std::isfinite(src[2])) {
+    ctx->err = "point-source position must be finite";
+    return FDA_E_INVALID_ARG;
+  }
+  const fda::Vec3 xs(src[0], src[1], src[2]);
+  for (const fda::Vec3& c : ctx->g.centroid)
+    if ((c - xs).norm() == 0.0) { ctx->err = "point source coincides with a collocation point"; return FDA_E_INVALID_ARG; }
+  if (!ctx->dev) { ctx->err = "context was built host-only"; return FDA_E_STATE; }
+  return engine_rhs_point_source(ctx, src, b, flags);
+}
+
 fda_status fda_rhs_apply(fda_ctx* ctx, const void* v, void* b, int32_t flags, void* stream) {
   if (!ctx) return FDA_E_INVALID_ARG;
   if (!v || !b || v == b) { ctx->err = "v and b must be non-null and must not alias"; return FDA_E_INVALID_ARG; }
@@ -309,6 +335,15 @@ fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int6
   if (nm == "out_offset") return put(p.out_offset, dst, count, eb);
   if (nm == "in_offset") return put(p.in_offset, dst, count, eb);
   if (nm == "sizes") return put(std::vector<int64_t>{p.out_size, p.in_size}, dst, count, eb);
+  if (nm == "xsend" || nm == "xrecv") {   // per peer: count, sorted out-state ids
+    const auto& L = nm == "xsend" ? p.xsend : p.xrecv;
+    std::vector<int64_t> v;
+    for (const auto& q : L) {
+      v.push_back((int64_t)q.size());
+      v.insert(v.end(), q.begin(), q.end());
+    }
+    return put(v, dst, count, eb);
+  }
   if (nm == "m2m") return put(ops(p.m2m), dst, count, eb);
   if (nm == "m2l") return put(ops(p.m2l), dst, count, eb);
   if (nm == "l2l") return put(ops(p.l2l), dst, count, eb);

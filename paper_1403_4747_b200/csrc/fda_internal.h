@@ -145,6 +145,9 @@ struct Plan {
   int64_t n_m2l_total = 0;
   // sharding (nranks > 1): owned leaves [own_leaf0, own_leaf1), elements [own_e0, own_e1)
   int64_t own_leaf0 = 0, own_leaf1 = 0, own_e0 = 0, own_e1 = 0;
+  // exchange of partial outgoing states between the passes (partition.cpp):
+  // per peer rank, the sorted out-state ids this rank sends / receives
+  std::vector<std::vector<int64_t>> xsend, xrecv;
   // direct (near) lists: CSR over leaves -> source leaves
   std::vector<int64_t> near_ptr, near_idx;
   // corrections: CSR over elements (tree order); index 1 = RHS operator
@@ -210,10 +213,12 @@ fda_status engine_create(Context* ctx);
 // kind 0: the LHS operator A (fda_matvec); kind 1: the RHS operator B (fda_rhs_apply)
 fda_status engine_apply(Context* ctx, const void* x, void* y, int32_t flags, void* stream, int kind);
 fda_status engine_rhs_plane_wave(Context* ctx, const double dir[3], void* b, int32_t flags);
+fda_status engine_rhs_point_source(Context* ctx, const double src[3], void* b, int32_t flags);
 fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int32_t max_iter, int32_t restart,
                         fda_solve_info* info, int32_t flags);
 fda_status engine_stage_times(Context* ctx, double* ms, int32_t* n);
 fda_status engine_comm_init(Context* ctx, const void* id128);
+fda_status engine_exchange_local(Context** ctxs, int n);
 fda_status nccl_unique_id(void* id128, std::string& err);
 void engine_destroy(Context* ctx);
 

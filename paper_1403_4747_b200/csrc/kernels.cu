@@ -48,6 +48,26 @@ __global__ void k_scatter_f64(const float2* __restrict__ yn, const float2* __res
   }
 }
 
+// sharded exchange of partial outgoing states (partition.cpp):
+// pack  send[i] = out[idx[i]];  unpack  out[idx[i]] += recv[i]  (a state may
+// arrive from several peers: vector atomics)
+__global__ void k_pack(const float2* __restrict__ out, const int64_t* __restrict__ idx, float2* __restrict__ send,
+                       int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) send[i] = out[idx[i]];
+}
+__global__ void k_unpack_add(const float2* __restrict__ recv, const int64_t* __restrict__ idx, float2* __restrict__ out,
+                             int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(out + idx[i], recv[i]);
+}
+void launch_pack(const float2* out, const int64_t* idx, float2* send, int64_t n, cudaStream_t s) {
+  if (n > 0) k_pack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(out, idx, send, n);
+}
+void launch_unpack_add(const float2* recv, const int64_t* idx, float2* out, int64_t n, cudaStream_t s) {
+  if (n > 0) k_unpack_add<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(recv, idx, out, n);
+}
+
 void launch_gather_f32(const float2* x, const int32_t* perm, float2* xt, int n, cudaStream_t s) {
   k_gather_f32<<<(n + 255) / 256, 256, 0, s>>>(x, perm, xt, n);
 }
@@ -867,6 +887,34 @@ __global__ void k_plane_wave(const double* __restrict__ cen, const double* __res
 void launch_plane_wave(const double* cen, const double* nrm, const int32_t* perm, int n, double k, double are,
                        double aim, double dx, double dy, double dz, float2* b32, double2* b64, cudaStream_t s) {
   k_plane_wave<<<(n + 255) / 256, 256, 0, s>>>(cen, nrm, perm, n, k, are, aim, dx, dy, dz, b32, b64);
+}
+
+// b_i = u_inc(x_i) + α ∂u_inc/∂n(x_i) for a unit point source u_inc = e^{ikR}/(4πR),
+// R = |x_i - x_s| (§5.2; Eq. 3), n_i = kernel normal:
+//   b_i = G [1 + α (ik - 1/R) (x_i - x_s)·n_i / R]      (fp64, caller order)
+__global__ void k_point_source(const double* __restrict__ cen, const double* __restrict__ nrm,
+                               const int32_t* __restrict__ perm, int n, double k, double are, double aim, double sx,
+                               double sy, double sz, float2* b32, double2* b64) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double dx = cen[3 * i] - sx, dy = cen[3 * i + 1] - sy, dz = cen[3 * i + 2] - sz;
+  const double R = sqrt(dx * dx + dy * dy + dz * dz);
+  const double dRdn = (dx * nrm[3 * i] + dy * nrm[3 * i + 1] + dz * nrm[3 * i + 2]) / R;
+  double s, c;
+  sincos(k * R, &s, &c);
+  const double g = 1.0 / (4.0 * CUDART_PI * R);
+  const double gr = g * c, gi = g * s;
+  // f = 1 + α (ik - 1/R) dRdn,  α (ik - 1/R) = (are + i aim)(-1/R + i k)
+  const double tr = -are / R - aim * k, ti = are * k - aim / R;
+  const double fr = 1.0 + tr * dRdn, fi = ti * dRdn;
+  const double br = gr * fr - gi * fi, bi = gr * fi + gi * fr;
+  const int j = perm[i];
+  if (b32) b32[j] = make_float2((float)br, (float)bi);
+  if (b64) b64[j] = make_double2(br, bi);
+}
+void launch_point_source(const double* cen, const double* nrm, const int32_t* perm, int n, double k, double are,
+                         double aim, double sx, double sy, double sz, float2* b32, double2* b64, cudaStream_t s) {
+  k_point_source<<<(n + 255) / 256, 256, 0, s>>>(cen, nrm, perm, n, k, are, aim, sx, sy, sz, b32, b64);
 }
 
 __global__ void k_f64_to_f32(const double2* a, float2* b, int64_t n) {

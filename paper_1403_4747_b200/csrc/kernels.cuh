@@ -76,6 +76,8 @@ struct LeafTask {
   int32_t pad;
 };
 
+void launch_pack(const float2* out, const int64_t* idx, float2* send, int64_t n, cudaStream_t s);
+void launch_unpack_add(const float2* recv, const int64_t* idx, float2* out, int64_t n, cudaStream_t s);
 void launch_gather_f32(const float2* x_caller, const int32_t* perm, float2* x_tree, int n, cudaStream_t s);
 void launch_gather_f64(const double2* x_caller, const int32_t* perm, float2* x_tree, int n, cudaStream_t s);
 void launch_scatter_f32(const float2* y_near, const float2* y_far, const int32_t* perm, float2* y_caller, int n,
@@ -117,6 +119,8 @@ void launch_scale(float2* dst, const float2* src, double sre, double sim, int64_
 void launch_axpby(float2* y, const float2* x, double a, double b, int64_t n, cudaStream_t s);  // y = a*x + b*y (real)
 void launch_plane_wave(const double* cen, const double* nrm, const int32_t* perm, int n, double k, double are,
                        double aim, double dx, double dy, double dz, float2* b32, double2* b64, cudaStream_t s);
+void launch_point_source(const double* cen, const double* nrm, const int32_t* perm, int n, double k, double are,
+                         double aim, double sx, double sy, double sz, float2* b32, double2* b64, cudaStream_t s);
 void launch_f64_to_f32(const double2* a, float2* b, int64_t n, cudaStream_t s);
 void launch_f32_to_f64(const float2* a, double2* b, int64_t n, cudaStream_t s);
 

@@ -1,16 +1,23 @@
-// Sharding of the FDA over nranks GPUs (SURVEY §8(e), round-1 design).
+// Sharding of the FDA over nranks GPUs.
 //
 // Leaves (Morton / tree order) are split into contiguous ranges balanced by
 // an estimate of their downward + near-field work.  A rank keeps
-//  * every S2M and M2M op (the upward pass is replicated: it is ~15% of the
-//    matvec and needs no exchange of outgoing states),
+//  * the S2M of its own leaves and the M2M ops whose child box intersects its
+//    element range: its upward pass produces PARTIAL outgoing states (the
+//    contribution of its own elements; the full state is the sum over the
+//    ranks by linearity of S2M / M2M, Algorithm Step 2),
 //  * the M2L (dense and §4.2 factored) and L2L ops whose destination is an
 //    incoming state of a box that contains at least one of its leaves
 //    (ancestors shared by several ranks are computed by each of them),
 //  * the near field and L2T of its own leaves.
-// Its y rows are therefore exact for its elements and zero elsewhere; one
-// all-reduce over the ranks forms the full y.  Every (target, source) pair of
-// the operator is computed by exactly the rank that owns the target.
+// Between the passes the ranks exchange partial outgoing states: rank r
+// receives, from every other rank q contributing to an outgoing state that
+// one of r's M2L ops reads, q's partial of that state (xrecv[q] / xsend[r],
+// both sorted by state id, derived from the same global plan on every rank)
+// and adds it to its own partial.  Its y rows are then exact for its elements
+// and zero elsewhere; one all-reduce over the ranks forms the full y.  Every
+// (target, source) pair of the operator is computed by exactly the rank that
+// owns the target.
 #include <algorithm>
 
 #include "fda_internal.h"
@@ -63,24 +70,68 @@ void apply_partition(const Params& p, const Tree& t, Plan& plan) {
   plan.own_leaf1 = start[r + 1];
   plan.own_e0 = plan.own_leaf0 < nleaf ? t.boxes[plan.leaf_box[plan.own_leaf0]].begin : 0;
   plan.own_e1 = plan.own_leaf1 > plan.own_leaf0 ? t.boxes[plan.leaf_box[plan.own_leaf1 - 1]].end : plan.own_e0;
+  // element range of every rank (contiguous, in rank order; empty ranks have e0 = e1)
+  std::vector<int64_t> re0(R), re1(R);
+  for (int k = 0; k < R; ++k) {
+    re0[k] = start[k] < nleaf ? t.boxes[plan.leaf_box[start[k]]].begin : (nleaf ? t.boxes[plan.leaf_box[nleaf - 1]].end : 0);
+    re1[k] = start[k + 1] > start[k] ? t.boxes[plan.leaf_box[start[k + 1] - 1]].end : re0[k];
+  }
+  // ranks whose element range intersects [b, e): a contiguous run [lo, hi]
+  auto ranks_of = [&](int64_t b, int64_t e, int& lo, int& hi) {
+    lo = R; hi = -1;
+    for (int k = 0; k < R; ++k)
+      if (re0[k] < re1[k] && re0[k] < e && re1[k] > b) { lo = std::min(lo, k); hi = std::max(hi, k); }
+  };
   const int64_t e0 = plan.own_e0, e1 = plan.own_e1;
   auto needed = [&](int64_t in_state) {
     const Box& B = t.boxes[plan.in_states[in_state].box];
     return B.begin < e1 && B.end > e0;
   };
-  for (auto& lev : plan.m2l) {
-    std::vector<Op> keep;
-    for (const Op& o : lev) if (needed(o.dst)) keep.push_back(o);
-    lev.swap(keep);
-  }
+  auto mine_out = [&](int64_t out_state) {
+    const Box& B = t.boxes[plan.out_states[out_state].box];
+    return B.begin < e1 && B.end > e0;
+  };
+  // exchange plan: for every M2L op, the ranks needing its destination (box ∩ range)
+  // need the full source state, i.e. the partials of every contributing rank
+  const int64_t nout = (int64_t)plan.out_states.size();
+  std::vector<std::vector<int64_t>> need_by(R);   // out-states each rank reads in M2L
   {
-    std::vector<LrOp> keep;
-    for (const LrOp& o : plan.m2l_lr) if (needed(o.dst)) keep.push_back(o);
-    plan.m2l_lr.swap(keep);
+    std::vector<std::vector<char>> mark(R, std::vector<char>(nout, 0));
+    auto visit = [&](int64_t src, int64_t dst) {
+      const Box& D = t.boxes[plan.in_states[dst].box];
+      int lo, hi;
+      ranks_of(D.begin, D.end, lo, hi);
+      for (int k = lo; k <= hi; ++k) mark[k][src] = 1;
+    };
+    for (auto& lev : plan.m2l)
+      for (const Op& o : lev) visit(o.src, o.dst);
+    for (const LrOp& o : plan.m2l_lr) visit(o.src, o.dst);
+    for (int k = 0; k < R; ++k)
+      for (int64_t sidx = 0; sidx < nout; ++sidx)
+        if (mark[k][sidx]) need_by[k].push_back(sidx);
   }
-  for (auto& lev : plan.l2l) {
+  plan.xsend.assign(R, {});
+  plan.xrecv.assign(R, {});
+  for (int k = 0; k < R; ++k)
+    for (int64_t sidx : need_by[k]) {
+      const Box& B = t.boxes[plan.out_states[sidx].box];
+      int lo, hi;
+      ranks_of(B.begin, B.end, lo, hi);
+      for (int q = lo; q <= hi; ++q) {
+        if (q == k) continue;
+        if (q == r) plan.xsend[k].push_back(sidx);   // I contribute a partial that k needs
+        if (k == r) plan.xrecv[q].push_back(sidx);   // I need q's partial
+      }
+    }
+  // partial upward pass: S2M of own leaves, M2M ops whose child box holds own elements
+  for (int64_t i = 0; i < nleaf; ++i)
+    if (i < plan.own_leaf0 || i >= plan.own_leaf1) {
+      plan.leaf_S[i] = -1;
+      if (!plan.leaf_S_rhs.empty()) plan.leaf_S_rhs[i] = -1;
+    }
+  for (auto& lev : plan.m2m) {
     std::vector<Op> keep;
-    for (const Op& o : lev) if (needed(o.dst)) keep.push_back(o);
+    for (const Op& o : lev) if (mine_out(o.src)) keep.push_back(o);
     lev.swap(keep);
   }
   // L2T only for owned leaves

@@ -22,13 +22,16 @@ LIB_PATH = os.path.join(_HERE, "libfda.so")
 FDA_HOST = 0
 FDA_DEVICE = 1
 FDA_LOCAL = 2
+FDA_PHASE_UP = 4
+FDA_PHASE_DOWN = 8
 
 STATUS = {0: "FDA_OK", 1: "FDA_E_INVALID_ARG", 2: "FDA_E_MESH", 3: "FDA_E_NOMEM", 4: "FDA_E_CUDA",
           5: "FDA_E_NCCL", 6: "FDA_E_NOT_CONVERGED", 7: "FDA_E_STATE", 8: "FDA_E_INTERNAL"}
 
 # every symbol include/fda.h declares
-EXPORTS = ["fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_apply", "bm_solve",
-           "fda_stats", "fda_nccl_unique_id", "fda_comm_init",
+EXPORTS = ["fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_point_source",
+           "fda_rhs_apply", "bm_solve",
+           "fda_stats", "fda_nccl_unique_id", "fda_comm_init", "fda_exchange_local",
            "fda_set_profiling", "fda_stage_times", "fda_debug_table", "fda_last_error", "fda_status_string",
            "fda_free"]
 
@@ -73,6 +76,16 @@ class fda_build_info(ctypes.Structure):
 _lib = None
 
 
+def exchange_local(contexts) -> None:
+    """fda_exchange_local: the one-GPU test transport of the sharded exchange
+    (contexts = the FDA objects of ranks 0..n-1 of one sharded build)."""
+    lib = load_library()
+    arr = (ctypes.c_void_p * len(contexts))(*[c.ctx for c in contexts])
+    st = lib.fda_exchange_local(arr, len(contexts))
+    if st != 0:
+        raise FdaError(st, (lib.fda_last_error(contexts[0].ctx) or b"").decode())
+
+
 def load_library(path: str = LIB_PATH):
     """Load libfda.so (raises if it is missing — there is no fallback)."""
     global _lib
@@ -86,11 +99,13 @@ def load_library(path: str = LIB_PATH):
     lib.fda_build.argtypes = [vp, i64, vp, i64, dp, fda_cplx, dp, ctypes.POINTER(fda_options), ctypes.POINTER(vp)]
     lib.fda_matvec.argtypes = [vp, vp, vp, i32, vp]
     lib.fda_rhs_plane_wave.argtypes = [vp, ctypes.POINTER(ctypes.c_double * 3), vp, i32]
+    lib.fda_rhs_point_source.argtypes = [vp, ctypes.POINTER(ctypes.c_double * 3), vp, i32]
     lib.fda_rhs_apply.argtypes = [vp, vp, vp, i32, vp]
     lib.bm_solve.argtypes = [vp, vp, vp, dp, i32, i32, ctypes.POINTER(fda_solve_info), i32]
     lib.fda_stats.argtypes = [vp, ctypes.POINTER(fda_build_info)]
     lib.fda_nccl_unique_id.argtypes = [vp]
     lib.fda_comm_init.argtypes = [vp, vp]
+    lib.fda_exchange_local.argtypes = [ctypes.POINTER(vp), i32]
     lib.fda_set_profiling.argtypes = [vp, i32]
     lib.fda_stage_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)]
     lib.fda_debug_table.argtypes = [vp, ctypes.c_char_p, vp, ctypes.POINTER(i64), ctypes.POINTER(i32)]
@@ -100,8 +115,9 @@ def load_library(path: str = LIB_PATH):
     lib.fda_status_string.restype = ctypes.c_char_p
     lib.fda_free.argtypes = [vp]
     lib.fda_free.restype = None
-    for name in ("fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_apply", "bm_solve",
-                 "fda_stats", "fda_nccl_unique_id", "fda_comm_init",
+    for name in ("fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_point_source",
+                 "fda_rhs_apply", "bm_solve",
+                 "fda_stats", "fda_nccl_unique_id", "fda_comm_init", "fda_exchange_local", "fda_exchange_local",
                  "fda_set_profiling", "fda_stage_times", "fda_debug_table"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -194,6 +210,13 @@ class FDA:
         local=True (sharded contexts): this rank's rows only, no collective."""
         return self._apply(self.lib.fda_matvec, x, y, stream, FDA_LOCAL if local else 0)
 
+    def matvec_phase(self, x, y, phase: str, kind: str = "lhs"):
+        """One half of a sharded matvec around an external exchange ("up" or
+        "down"; device tensors, this rank's rows only) — see fda_exchange_local."""
+        flag = FDA_PHASE_UP if phase == "up" else FDA_PHASE_DOWN
+        fn = self.lib.fda_matvec if kind == "lhs" else self.lib.fda_rhs_apply
+        return self._apply(fn, x, y, None, FDA_LOCAL | flag)
+
     def rhs_apply(self, v, b=None, stream=None, local: bool = False):
         """b = B v, the right-hand-side operator of Eq. (4) (needs rhs_operator=1)."""
         return self._apply(self.lib.fda_rhs_apply, v, b, stream, FDA_LOCAL if local else 0)
@@ -233,6 +256,18 @@ class FDA:
             return b
         b = np.empty(self.n, dtype=np.complex128)
         self._check(self.lib.fda_rhs_plane_wave(self.ctx, ctypes.byref(d), _ptr_np(b), FDA_HOST))
+        return b
+
+    def rhs_point_source(self, source, device: bool = False):
+        """fda_rhs_point_source: BM right-hand side of a unit point source (§5.2)."""
+        d = (ctypes.c_double * 3)(*[float(v) for v in source])
+        if device:
+            import torch
+            b = torch.empty(self.n, dtype=torch.complex64, device=f"cuda:{self.device}")
+            self._check(self.lib.fda_rhs_point_source(self.ctx, ctypes.byref(d), b.data_ptr(), FDA_DEVICE))
+            return b
+        b = np.empty(self.n, dtype=np.complex128)
+        self._check(self.lib.fda_rhs_point_source(self.ctx, ctypes.byref(d), _ptr_np(b), FDA_HOST))
         return b
 
     def solve(self, rhs, tol: float = 1e-4, max_iter: int = 200, restart: int = 0, check: bool = True):
@@ -280,7 +315,8 @@ class FDA:
                "mats": np.int64, "specs": np.int64, "pool": np.complex64, "near_ptr": np.int64,
                "near_idx": np.int64, "corr_ptr": np.int64, "corr_col": np.int64, "corr_val": np.complex64,
                "out_states": np.int64, "in_states": np.int64, "boxes": np.int64, "box_center": np.float64,
-               "levels": np.float64, "root": np.float64, "launches": np.int64, "owned": np.int64}
+               "levels": np.float64, "root": np.float64, "launches": np.int64, "owned": np.int64,
+               "xsend": np.int64, "xrecv": np.int64}
 
     def table(self, name: str) -> np.ndarray:
         """A host-side build table (host-logic tests only)."""

@@ -18,8 +18,10 @@ def _mat(pool, mats, m):
 
 
 def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bool = True,
-                 kind: str = "lhs") -> np.ndarray:
-    """y = A x (kind 'lhs') or y = B x (kind 'rhs', needs rhs_operator=1)."""
+                 kind: str = "lhs", exchange=None) -> np.ndarray:
+    """y = A x (kind 'lhs') or y = B x (kind 'rhs', needs rhs_operator=1).
+    exchange(ob) (sharded builds): called between the passes with this rank's
+    partial outgoing states; must add the peers' partials (xsend / xrecv)."""
     sfx = "_rhs" if kind == "rhs" else ""
     n = f.n
     perm = f.table("perm")
@@ -85,6 +87,8 @@ def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bo
         for l in sorted(set(m2m[:, 0]), reverse=True):
             for (_, s, d, m) in m2m[m2m[:, 0] == l]:
                 ob[oo[d]:oo[d] + T_out(d)] += _mat(pool, mats, m) @ ob[oo[s]:oo[s] + T_out(s)]
+        if exchange is not None:
+            exchange(ob)
         for (_, s, d, m) in f.table("m2l").reshape(-1, 4):
             ib[io[d]:io[d] + T_in(d)] += _mat(pool, mats, m) @ ob[oo[s]:oo[s] + T_out(s)]
         for (_, s, d, mv, mu, _t) in f.table("m2l_lr").reshape(-1, 6):   # §4.2: Û (V̂ src)

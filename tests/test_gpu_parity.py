@@ -161,6 +161,28 @@ def test_bm_solve_config1(cfg1):
     assert info2["converged"] and _rel(u2, u_ref) <= SOLVE_TOL
 
 
+def test_point_source_rhs_and_solve(cfg1):
+    """PAPER.md §5.2 workload (point source outside the rigid sphere, source at
+    2 radii as in P:1016-1019): the library's right-hand side vs the oracle's
+    definition, and the FDA + GMRES solution vs the dense LU solution and the
+    series (discretisation sanity)."""
+    import torch
+    V, F, c, el, A, f = cfg1
+    xs = np.array([-1.0, 0.0, 0.0])
+    bo = O.point_source_rhs(el.centroid, el.normal, c.k, c.alpha, xs)
+    b = f.rhs_point_source(xs)
+    assert _rel(b, bo) < 1e-12
+    bd = f.rhs_point_source(xs, device=True)
+    torch.cuda.synchronize()
+    assert _rel(bd.cpu().numpy().astype(np.complex128), bo) < 1e-6
+    u_ref = O.lu_solve(A, bo)
+    u, info = f.solve(b, tol=c.gmres_tol, max_iter=100)
+    err = _rel(u, u_ref)
+    ser = _rel(u, O.rigid_sphere_point_source_total(el.centroid, c.k, 0.5, xs))
+    print(f"point source: {info}, vs dense LU {err:.3e}, vs series {ser:.3e}")
+    assert info["converged"] and err <= SOLVE_TOL and ser < 3e-2
+
+
 def test_stage_times(cfg1):
     V, F, c, el, A, f = cfg1
     f.set_profiling(True)
@@ -233,26 +255,51 @@ def test_pulsating_table2_on_gpu(lib, row):
     assert _rel(u, u_ref) <= SOLVE_TOL
 
 
-def test_sharded_partials_sum_to_full_operator(lib):
-    """Sharded build: for R = 3 ranks, each rank's FDA_LOCAL
-    matvec (its own rows, zero elsewhere, no collective) run on this GPU, and
-    the sum equals the unsharded matvec; a sharded context refuses the
-    collective path before fda_comm_init."""
+@pytest.mark.parametrize("R", [2, 3])
+def test_sharded_exchange_one_gpu(lib, R):
+    """Sharded build in fake-partition mode: R rank contexts on
+    this GPU run the partial upward pass (FDA_PHASE_UP), exchange their partial
+    outgoing states through fda_exchange_local (the copies the grouped
+    ncclSend/ncclRecv make across GPUs), run the downward pass for their own
+    targets (FDA_PHASE_DOWN); the sum of the ranks' rows equals the unsharded
+    matvec.  A sharded context refuses the NCCL path before fda_comm_init."""
+    import torch
+    from paper_1403_4747_b200 import exchange_local
     V, F = icosphere(4, 0.5)
     k = 40.0
     x = random_density(len(F), 9)
     full = lib(V, F, k, 1j / k, 1e-4, max_leaf=16).matvec(x)
+    ranks = [lib(V, F, k, 1j / k, 1e-4, max_leaf=16, rank=r, nranks=R) for r in range(R)]
+    xd = torch.from_numpy(x.astype(np.complex64)).cuda()
+    ys = [torch.empty_like(xd) for _ in range(R)]
+    for f, y in zip(ranks, ys):
+        f.matvec_phase(xd, y, "up")
+    torch.cuda.synchronize()
+    exchange_local(ranks)
+    for f, y in zip(ranks, ys):
+        f.matvec_phase(xd, y, "down")
+    torch.cuda.synchronize()
     acc = np.zeros(len(F), dtype=complex)
-    for r in range(3):
-        f = lib(V, F, k, 1j / k, 1e-4, max_leaf=16, rank=r, nranks=3)
-        part = f.matvec(x, local=True)
+    for f, y in zip(ranks, ys):
+        part = y.cpu().numpy().astype(np.complex128)
         l0, l1, e0, e1 = f.table("owned")
         assert np.count_nonzero(part) <= e1 - e0
         acc += part
-        if r == 0:
-            with pytest.raises(Exception):
-                f.matvec(x)
-    assert _rel(acc, full) < 1e-5
+    err = _rel(acc, full)
+    print(f"sharded R={R}: rel-L2 vs unsharded {err:.3e}")
+    assert err < 1e-5
+    with pytest.raises(Exception):
+        ranks[0].matvec(x)
+    # without the exchange the result is wrong (the partial states alone are not enough)
+    fresh = [lib(V, F, k, 1j / k, 1e-4, max_leaf=16, rank=r, nranks=R) for r in range(R)]
+    y0 = [torch.empty_like(xd) for _ in range(R)]
+    for f, y in zip(fresh, y0):
+        f.matvec_phase(xd, y, "up")
+    for f, y in zip(fresh, y0):
+        f.matvec_phase(xd, y, "down")
+    torch.cuda.synchronize()
+    bad = sum(y.cpu().numpy().astype(np.complex128) for y in y0)
+    assert _rel(bad, full) > 1e-3
 
 
 @pytest.mark.parametrize("lowrank", [1, 0])

@@ -1,9 +1,12 @@
-"""Multi-rank (sharded) FDA host logic with a real collective:
-two gloo ranks on CPU, each builds its shard of the operator (host-only
-tables), applies it in complex128 (tests/host_exec.py) and the partial y are
-summed with torch.distributed.all_reduce — the same exchange the GPU path does
-with NCCL.  The sum must equal the oracle operator to the FDA tolerance and
-the owned leaf ranges must partition the tree."""
+"""Multi-rank (sharded) FDA host logic with real collectives:
+gloo ranks on CPU, each builds its shard of the operator (host-only tables)
+and applies it in complex128 (tests/host_exec.py): partial upward pass on its
+own elements, exchange of partial outgoing states with point-to-point
+send/recv following the plan's xsend / xrecv lists (what the GPU path does
+with grouped ncclSend/ncclRecv), downward pass for its own targets; the
+partial y are summed with all_reduce.  The sum must equal the oracle operator
+to the FDA tolerance, the owned leaf ranges must partition the tree, and
+every rank's send list to a peer must be that peer's receive list."""
 import os
 import socket
 
@@ -40,31 +43,83 @@ def _worker(rank, world, port, out):
     k = 40.0
     f = FDA(V, F, k, 1j / k, 1e-4, device=-1, max_leaf=16, rank=rank, nranks=world, build_threads=threads)
     x = random_density(len(F), 11)
-    y = apply_tables(f, x)
+    xs_t, xr_t = f.table("xsend"), f.table("xrecv")
+
+    def lists(tab):
+        out, i = [], 0
+        for _ in range(world):
+            c = int(tab[i])
+            out.append([int(v) for v in tab[i + 1:i + 1 + c]])
+            i += 1 + c
+        return out
+    xsend, xrecv = lists(xs_t), lists(xr_t)
+    oo = f.table("out_offset")
+    lev = f.table("levels").reshape(-1, 4)
+    boxes = f.table("boxes").reshape(-1, 8)
+    outs = f.table("out_states").reshape(-1, 2)
+    T = lambda s: int(lev[boxes[outs[s, 0], 0], 3])   # noqa: E731
+
+    def exchange(ob):
+        reqs, bufs = [], {}
+        for q in range(world):
+            if q == rank:
+                continue
+            if xsend[q]:
+                pk = np.concatenate([ob[oo[s]:oo[s] + T(s)] for s in xsend[q]])
+                reqs.append(dist.isend(torch.from_numpy(np.stack([pk.real, pk.imag])), dst=q))
+            if xrecv[q]:
+                n = sum(T(s) for s in xrecv[q])
+                bufs[q] = torch.zeros(2, n, dtype=torch.float64)
+                reqs.append(dist.irecv(bufs[q], src=q))
+        for r in reqs:
+            r.wait()
+        for q, b in bufs.items():
+            v = (b[0] + 1j * b[1]).numpy()
+            o = 0
+            for s in xrecv[q]:
+                ob[oo[s]:oo[s] + T(s)] += v[o:o + T(s)]
+                o += T(s)
+    y = apply_tables(f, x, exchange=exchange)
+    y_noex = apply_tables(f, x, near=False, corr=False) - apply_tables(f, x, near=False, corr=False, exchange=exchange)
     t = torch.from_numpy(np.stack([y.real, y.imag]))
     dist.all_reduce(t)
+    t0 = torch.from_numpy(np.stack([y_noex.real, y_noex.imag]))
+    dist.all_reduce(t0)
+    plans = [None] * world
+    dist.all_gather_object(plans, (xsend, xrecv))
     owned = torch.from_numpy(f.table("owned").astype(np.int64))
     allowned = [torch.zeros_like(owned) for _ in range(world)]
     dist.all_gather(allowned, owned)
     if rank == 0:
         np.save(out + ".y.npy", (t[0] + 1j * t[1]).numpy())
+        np.save(out + ".y_noex.npy", (t0[0] + 1j * t0[1]).numpy())
         np.save(out + ".own.npy", torch.stack(allowned).numpy())
+        ok = all(plans[a][0][b] == plans[b][1][a] for a in range(world) for b in range(world) if a != b)
+        np.save(out + ".plan_ok.npy", np.array([ok, sum(len(v) for p in plans for v in p[0])]))
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_sharded_matvec(tmp_path):
+@pytest.mark.parametrize("world", [3])
+def test_gloo_sharded_matvec(tmp_path, world):
     import oracle as O
     from oracle import fast
     from fda_inputs import icosphere, random_density
     out = str(tmp_path / "r")
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     y = np.load(out + ".y.npy")
+    y_noex = np.load(out + ".y_noex.npy")
     own = np.load(out + ".own.npy")
+    ok, nsent = np.load(out + ".plan_ok.npy")
+    assert ok and nsent > 0
     # contiguous, disjoint, covering ownership
-    assert own[0, 0] == 0 and own[0, 1] == own[1, 0] and own[0, 3] == own[1, 2] and own[1, 3] == 5120
+    assert own[0, 0] == 0 and own[0, 2] == 0 and own[-1, 3] == 5120
+    for r in range(world - 1):
+        assert own[r, 1] == own[r + 1, 0] and own[r, 3] == own[r + 1, 2]
     V, F = icosphere(4, 0.5)
     k = 40.0
     el = O.element_geometry(V, F)
     x = random_density(len(F), 11)
     yo = fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k)
     assert np.linalg.norm(y - yo) / np.linalg.norm(yo) < 1e-3
+    # the exchange is needed: without it the far field changes by O(1)
+    assert np.linalg.norm(y_noex) / np.linalg.norm(yo) > 1e-2
