@@ -15,6 +15,28 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
+def _level_stats(f):
+    """Per level and translation stage: ops, distinct matrices, shape, GFLOP."""
+    mats = f.table("mats").reshape(-1, 3)
+    out = {}
+    for stage in ("m2m", "m2l", "l2l"):
+        ops = f.table(stage).reshape(-1, 4)
+        for l in sorted(set(ops[:, 0].tolist())):
+            o = ops[ops[:, 0] == l]
+            rc = mats[o[:, 3], 1] * mats[o[:, 3], 2]
+            out[f"{stage}_L{l}"] = {"ops": int(len(o)), "mats": int(len(set(o[:, 3].tolist()))),
+                                    "rows": int(mats[o[0, 3], 1]), "cols": int(mats[o[0, 3], 2]),
+                                    "gflop": round(8 * float(rc.sum()) / 1e9, 3)}
+    lr = f.table("m2l_lr").reshape(-1, 6)
+    for l in sorted(set(lr[:, 0].tolist())):
+        o = lr[lr[:, 0] == l]
+        r, T = mats[o[:, 3], 1], mats[o[:, 3], 2]
+        out[f"m2l_lr_L{l}"] = {"ops": int(len(o)), "mats": int(len(set(o[:, 3].tolist()))), "T": int(T[0]),
+                               "r_mean": round(float(r.mean()), 1), "r_max": int(r.max()),
+                               "gflop": round(16 * float((r * T).sum()) / 1e9, 3)}
+    return out
+
+
 def main():
     import torch
     from fda_inputs import config_mesh, CONFIGS, random_density, sampled_rows
@@ -34,6 +56,7 @@ def main():
     f = FDA(V, F, c.k, c.alpha, c.eps, verbose=1, tensor_cores=a.tc)
     t_build = time.perf_counter() - t0
     st = f.stats()
+    levels = _level_stats(f)
     x = random_density(N, c.x_seed)
     xd = torch.from_numpy(x.astype(np.complex64)).cuda()
     yd = torch.empty_like(xd)
@@ -66,7 +89,7 @@ def main():
     print(json.dumps({"config": a.cfg, "N": N, "k": c.k, "mesh_s": round(t_mesh, 1), "build_s": round(t_build, 1),
                       "matvec_ms": round(mv_ms, 3), "stages_ms": {k: round(v, 3) for k, v in stages.items()},
                       "sampled_rows": len(rows), "rel_l2_sampled": err, "oracle_rows_s": t_or, "tensor_cores": bool(a.tc),
-                      "oracle_cores": fast.num_threads(),
+                      "oracle_cores": fast.num_threads(), "levels": levels,
                       "tree": {k: st[k] for k in ("n_levels", "n_hf_levels", "n_leaves", "n_m2l_pairs",
                                                   "n_direct_element_pairs", "n_corrections", "table_bytes",
                                                   "rank", "dirs")}}), flush=True)
