@@ -31,12 +31,9 @@ namespace fda {
     }                                                                              \
   } while (0)
 
-// one translation op in offsets: dst[dof : +rows] (+)= M[mat] · src[so : +cols];
-// sp / stp: the source's tensor-core plane offset and plane length (-1: not a state)
+// one translation op in offsets: dst[dof : +rows] (+)= M[mat] · src[so : +cols]
 struct XOp {
   int64_t so, dof, mat;
-  int64_t sp = -1;
-  int32_t stp = 0;
 };
 
 // ------------------------------------------------------------------ NCCL (loaded on first use)
@@ -97,8 +94,8 @@ fda_status nccl_unique_id(void* id128, std::string& err) {
 
 struct XStage {
   bool atomic = true;
-  TcTask* tc = nullptr;            // tensor-core tasks (opt.tensor_cores)
-  int n_tc = 0;
+  TcTask* tc[TC_NV] = {};          // tensor-core tasks per kernel variant (opt.tensor_cores)
+  int n_tc[TC_NV] = {};
   XTask* tasks[XV] = {};
   int ntask[XV] = {};
   int64_t* src = nullptr;
@@ -152,7 +149,8 @@ struct Dev {
     int64_t* lr_src = nullptr;
     int64_t* lr_dst = nullptr;
     bool any() const {
-      int n = n_lr[0] + n_lr[1] + n_lr[2] + dense.n_tc + a.n_tc + b.n_tc;
+      int n = n_lr[0] + n_lr[1] + n_lr[2];
+      for (int v = 0; v < TC_NV; ++v) n += dense.n_tc[v] + a.n_tc[v] + b.n_tc[v];
       for (int v = 0; v < XV; ++v) n += dense.ntask[v] + a.ntask[v] + b.ntask[v];
       return n > 0;
     }
@@ -173,17 +171,11 @@ struct Dev {
   KernelParams kp{};
   bool timed = false;
   std::vector<void*> allocs;
-  // tensor-core operand pool: per matrix, per 64-row block, per 32-column chunk: [hi | lo] A tiles
+  // tensor-core operand pool: per matrix, per 128-row tile, per TC_KC-float K chunk: [hi | lo] A tiles
   bool use_tc = false;
   std::vector<float> tc_host;
   std::unordered_map<int64_t, int64_t> tc_off;   // matrix id → float offset
   float* tcpool = nullptr;
-  // pre-split state planes for the tensor-core B operand (4 planes × Tp per state)
-  float *outp = nullptr, *inp = nullptr;
-  std::vector<int64_t> pout_off, pin_off;          // per state (host)
-  int64_t *d_out_off = nullptr, *d_in_off = nullptr, *d_pout = nullptr, *d_pin = nullptr;
-  std::vector<int> lvl_T, lvl_Tp;
-  std::vector<int64_t> out_lb, in_lb;              // per level state ranges (size nlev+1)
 };
 
 template <class T>
@@ -211,9 +203,10 @@ static fda_status alloc(Context* ctx, Dev* d, T** dst, size_t count) {
     if (s_ != FDA_OK) return s_;               \
   } while (0)
 
-// ---- tensor-core operand layout (kernels_tc.cu): A = [M_r; M_i] per 64-row block,
-// TF32 hi/lo, canonical K-major core matrices: element (m, k) of a 128 × 32 tile at
-// ((k/4 · 16 + m/8) · 8 + m%8) · 4 + k%4, chunks of TC_KC columns
+// ---- tensor-core operand layout (kernels_tc.cu): the real 2R × 2C matrix with
+// interleaved rows / columns (A[2i][2j] = Re M, A[2i][2j+1] = −Im M, A[2i+1][2j] = Im M,
+// A[2i+1][2j+1] = Re M), TF32 hi/lo, per 128-row tile and TC_KC-float K chunk, canonical
+// K-major core matrices: element (r, k) of a 128 × TC_KC tile at ((k/4 · 16 + r/8) · 8 + r%8) · 4 + k%4
 static inline float tf32_rna(float x) {
   uint32_t u;
   std::memcpy(&u, &x, 4);
@@ -223,29 +216,34 @@ static inline float tf32_rna(float x) {
   return y;
 }
 
+static int tc_tiles(int rows) { return (2 * rows + 127) / 128; }
+
 static int64_t tc_matrix(Context* ctx, Dev* d, int64_t m) {
   auto it = d->tc_off.find(m);
   if (it != d->tc_off.end()) return it->second;
   const Plan& p = ctx->plan;
   const MatInfo& mi = p.mats[m];
-  const int R = mi.rows, C = mi.cols, nblk = (R + 63) / 64, nkc = (C + TC_KC - 1) / TC_KC;
+  const int R = mi.rows, C = mi.cols, ntile = tc_tiles(R), nkc = (2 * C + TC_KC - 1) / TC_KC;
   const int TILE = 128 * TC_KC;
   const int64_t off = (int64_t)d->tc_host.size();
-  d->tc_host.resize(d->tc_host.size() + (size_t)nblk * nkc * 2 * TILE, 0.0f);
+  d->tc_host.resize(d->tc_host.size() + (size_t)ntile * nkc * 2 * TILE, 0.0f);
   float* base = d->tc_host.data() + off;
   const cf* M = p.pool.data() + mi.offset;
-  for (int b = 0; b < nblk; ++b)
+  for (int ti = 0; ti < ntile; ++ti)
     for (int kc = 0; kc < nkc; ++kc) {
-      float* hi = base + ((size_t)b * nkc + kc) * 2 * TILE;
+      float* hi = base + ((size_t)ti * nkc + kc) * 2 * TILE;
       float* lo = hi + TILE;
-      for (int mrow = 0; mrow < 128; ++mrow) {
-        const int i = b * 64 + (mrow & 63), plane = mrow >> 6;
+      for (int r = 0; r < 128; ++r) {
+        const int gr = 128 * ti + r, i = gr >> 1;
         for (int k = 0; k < TC_KC; ++k) {
-          const int j = kc * TC_KC + k;
+          const int gk = kc * TC_KC + k, j = gk >> 1;
           float x = 0.0f;
-          if (i < R && j < C) x = plane ? M[(size_t)j * R + i].imag() : M[(size_t)j * R + i].real();
+          if (i < R && j < C) {
+            const cf v = M[(size_t)j * R + i];
+            x = (gr & 1) == 0 ? ((gk & 1) == 0 ? v.real() : -v.imag()) : ((gk & 1) == 0 ? v.imag() : v.real());
+          }
           const float h = tf32_rna(x), l = tf32_rna(x - h);
-          const int idx = (((k >> 2) * 16 + (mrow >> 3)) * 8 + (mrow & 7)) * 4 + (k & 3);
+          const int idx = (((k >> 2) * 16 + (r >> 3)) * 8 + (r & 7)) * 4 + (k & 3);
           hi[idx] = h;
           lo[idx] = l;
         }
@@ -272,37 +270,38 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   std::vector<int64_t> so, dof;
   std::vector<XTask> tasks[XV];
   if (d->use_tc && atomic && tc_ok) {
-    std::vector<TcTask> tct;
+    std::vector<TcTask> tct[TC_NV];
     for (size_t i = 0; i < ord.size();) {
       const int64_t m = ops[ord[i]].mat;
       size_t j = i;
       while (j < ord.size() && ops[ord[j]].mat == m) ++j;
-      const int R = p.mats[m].rows, C = p.mats[m].cols, nkc = (C + TC_KC - 1) / TC_KC;
+      const int R = p.mats[m].rows, C = p.mats[m].cols, ntile = tc_tiles(R);
+      if (ntile > 3) { ctx->err = "matrix too tall for the tensor-core path (rows > 192)"; return FDA_E_INTERNAL; }
+      const int64_t nops = (int64_t)(j - i);
+      const int v = tc_variant(nops >= 160 && ntile <= 2 ? 256 : 128, ntile), nmax = tc_variant_ops(v);
       const int64_t off = tc_matrix(ctx, d, m);
       const int32_t base = (int32_t)so.size();
       for (size_t q = i; q < j; ++q) {
-        so.push_back(ops[ord[q]].sp);   // plane offset of the pre-split source state
+        so.push_back(ops[ord[q]].so);
         dof.push_back(ops[ord[q]].dof);
       }
-      const int32_t tp = ops[ord[i]].stp;
-      const int64_t nops = (int64_t)(j - i);
-      for (int64_t c0 = 0; c0 < nops; c0 += 64)
-        for (int b = 0; b < (R + 63) / 64; ++b) {
-          TcTask t;
-          t.a_off = off + (int64_t)b * nkc * 2 * (128 * TC_KC);
-          t.nkc = nkc;
-          t.R = R;
-          t.C = C;
-          t.row0 = b * 64;
-          t.op_begin = base + (int32_t)c0;
-          t.op_count = (int32_t)std::min<int64_t>(64, nops - c0);
-          t.Tp = tp;
-          tct.push_back(t);
-        }
+      for (int64_t c0 = 0; c0 < nops; c0 += nmax) {
+        TcTask t;
+        t.a_off = off;
+        t.R = R;
+        t.C = C;
+        t.nkc = (2 * C + TC_KC - 1) / TC_KC;
+        t.ntile = ntile;
+        t.op_begin = base + (int32_t)c0;
+        t.op_count = (int32_t)std::min<int64_t>(nmax, nops - c0);
+        tct[v].push_back(t);
+      }
       i = j;
     }
-    st.n_tc = (int)tct.size();
-    UP(&st.tc, tct.data(), tct.size());
+    for (int v = 0; v < TC_NV; ++v) {
+      st.n_tc[v] = (int)tct[v].size();
+      if (st.n_tc[v]) UP(&st.tc[v], tct[v].data(), tct[v].size());
+    }
     UP(&st.src, so.data(), so.size());
     UP(&st.dst, dof.data(), dof.size());
     return FDA_OK;
@@ -375,9 +374,9 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
 
 static const float* g_tcpool = nullptr;   // set per context before launches (single-threaded use)
 
-static void launch_stage(const XStage& st, const float2* pool, const float2* src, float2* dst, cudaStream_t s,
-                         const float* srcp = nullptr) {
-  if (st.n_tc) launch_xlate_tc(st.n_tc, st.tc, st.src, st.dst, g_tcpool, srcp, dst, s);
+static void launch_stage(const XStage& st, const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
+  for (int v = 0; v < TC_NV; ++v)
+    if (st.n_tc[v]) launch_xlate_tc(v, st.n_tc[v], st.tc[v], st.src, st.dst, g_tcpool, src, dst, s);
   for (int v = 0; v < XV; ++v)
     if (st.ntask[v]) launch_xlate(v, st.atomic, st.ntask[v], st.tasks[v], st.src, st.dst, pool, src, dst, s);
 }
@@ -555,44 +554,13 @@ fda_status engine_create(Context* ctx) {
 
   const int nlev = (int)t.levels.size();
   d->m2m.resize(nlev); d->l2l.resize(nlev);
-  // tensor-core source planes: state s of level l → 4 planes of Tp_l floats
-  d->lvl_T.assign(nlev, 0);
-  d->lvl_Tp.assign(nlev, 0);
-  for (int l = 0; l < nlev; ++l) {
-    d->lvl_T[l] = t.levels[l].rank;
-    d->lvl_Tp[l] = ((t.levels[l].rank + TC_KC - 1) / TC_KC) * TC_KC;
-  }
-  d->out_lb = p.out_level_begin;
-  d->in_lb = p.in_level_begin;
-  auto plane_offsets = [&](const std::vector<State>& S, std::vector<int64_t>& po) {
-    po.resize(S.size());
-    int64_t o = 0;
-    for (size_t i = 0; i < S.size(); ++i) {
-      po[i] = o;
-      o += 4 * (int64_t)d->lvl_Tp[t.boxes[S[i].box].level];
-    }
-    return o;
-  };
-  const int64_t pout_size = plane_offsets(p.out_states, d->pout_off);
-  const int64_t pin_size = plane_offsets(p.in_states, d->pin_off);
-  if (d->use_tc) {
-    AL(&d->outp, (size_t)std::max<int64_t>(1, pout_size));
-    AL(&d->inp, (size_t)std::max<int64_t>(1, pin_size));
-    UP(&d->d_out_off, p.out_offset.data(), p.out_offset.size());
-    UP(&d->d_in_off, p.in_offset.data(), p.in_offset.size());
-    UP(&d->d_pout, d->pout_off.data(), d->pout_off.size());
-    UP(&d->d_pin, d->pin_off.data(), d->pin_off.size());
-  }
   auto xops = [&](const std::vector<Op>& ops, const std::vector<int64_t>& so, const std::vector<int64_t>& dof,
                   bool src_in) {
     std::vector<XOp> v;
     v.reserve(ops.size());
     for (const Op& o : ops) {
-      XOp x{so[o.src], dof[o.dst], o.mat};
-      const State& ss = src_in ? p.in_states[o.src] : p.out_states[o.src];
-      x.sp = src_in ? d->pin_off[o.src] : d->pout_off[o.src];
-      x.stp = d->lvl_Tp[t.boxes[ss.box].level];
-      v.push_back(x);
+      (void)src_in;
+      v.push_back(XOp{so[o.src], dof[o.dst], o.mat});
     }
     return v;
   };
@@ -618,12 +586,9 @@ fda_status engine_create(Context* ctx) {
         fused[o.level].push_back(o);
         continue;
       }
-      XOp xa{p.out_offset[o.src], tmp_off, o.matV};
-      xa.sp = d->pout_off[o.src];
-      xa.stp = d->lvl_Tp[o.level];
-      a[o.level].push_back(xa);
+      a[o.level].push_back(XOp{p.out_offset[o.src], tmp_off, o.matV});
       b[o.level].push_back({tmp_off, p.in_offset[o.dst], o.matU});
-      tmp_off += p.mats[o.matV].rows;
+      tmp_off += (p.mats[o.matV].rows + 1) & ~1;   // even offsets (16-B aligned tensor-core operands)
     }
     d->tmp_size = tmp_off;
     AL(&d->tmpb, (size_t)std::max<int64_t>(1, tmp_off));
@@ -705,10 +670,8 @@ fda_status engine_create(Context* ctx) {
   }
   // kernels per matvec: gather, near, s2m, every non-empty translation launch, l2t, scatter
   int64_t nl = 4 + (d->n_s2m > 0);  // gather, near, l2t, scatter (+ s2m)
-  if (d->use_tc)  // per-level state splits
-    for (int l = 0; l < nlev; ++l) nl += (d->out_lb[l + 1] > d->out_lb[l]) + (d->in_lb[l + 1] > d->in_lb[l]);
   auto cnt = [&](const XStage& st) {
-    nl += st.n_tc > 0;
+    for (int v = 0; v < TC_NV; ++v) nl += st.n_tc[v] > 0;
     for (int v = 0; v < XV; ++v) nl += st.ntask[v] > 0;
   };
   for (auto& st : d->m2m) cnt(st);
@@ -825,33 +788,20 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
     const Dev::M2LLevel& L = d->m2lv[l];
     for (int c = 2; c >= 0; --c)
       launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st);
-    launch_stage(L.dense, d->pool, d->outb, d->inb, st, d->outp);
-    launch_stage(L.a, d->pool, d->outb, d->tmpb, st, d->outp);
+    launch_stage(L.dense, d->pool, d->outb, d->inb, st);
+    launch_stage(L.a, d->pool, d->outb, d->tmpb, st);
     launch_stage(L.b, d->pool, d->tmpb, d->inb, st);
-  };
-  // tensor-core path: pre-split a completed level of out- / in-states into planes
-  auto split_out = [&](int l, cudaStream_t st) {
-    if (d->use_tc)
-      launch_split_states(d->outb, d->d_out_off, d->d_pout, d->lvl_T[l], d->lvl_Tp[l], d->out_lb[l],
-                          d->out_lb[l + 1], d->outp, st);
-  };
-  auto split_in = [&](int l, cudaStream_t st) {
-    if (d->use_tc)
-      launch_split_states(d->inb, d->d_in_off, d->d_pin, d->lvl_T[l], d->lvl_Tp[l], d->in_lb[l], d->in_lb[l + 1],
-                          d->inp, st);
   };
   if (prof) {
     // serialised: every stage time is the isolated duration of its kernels
     for (int l = nlev - 1; l >= 0; --l) {
-      launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s, d->outp);
-      split_out(l, s);
+      launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);
     }
     CK(cudaEventRecord(d->ev[3], s));
     for (int l = 0; l < nlev; ++l) m2l_level(l, s);
     CK(cudaEventRecord(d->ev[4], s));
     for (int l = 0; l < nlev; ++l) {
-      split_in(l, s);
-      launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s, d->inp);
+      launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
     }
     CK(cudaEventRecord(d->ev[5], s));
   } else {
@@ -862,8 +812,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
     int k = 0;
     std::vector<int> nbr(nlev, 0);
     for (int l = nlev - 1; l >= 0; --l) {
-      launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s, d->outp);   // writes level-l out-states
-      split_out(l, s);
+      launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);   // writes level-l out-states
       if (!d->m2lv[l].any()) continue;
       const Dev::M2LLevel& L = d->m2lv[l];
       CK(cudaEventRecord(d->ev_up[l], s));
@@ -882,16 +831,15 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
              })) != FDA_OK)
           return bs;
       if ((bs = branch([&](cudaStream_t sm) {
-             launch_stage(L.dense, d->pool, d->outb, d->inb, sm, d->outp);
-             launch_stage(L.a, d->pool, d->outb, d->tmpb, sm, d->outp);
+             launch_stage(L.dense, d->pool, d->outb, d->inb, sm);
+             launch_stage(L.a, d->pool, d->outb, d->tmpb, sm);
              launch_stage(L.b, d->pool, d->tmpb, d->inb, sm);
            })) != FDA_OK)
         return bs;
     }
     for (int l = 0; l < nlev; ++l) {
       for (int b = 0; b < nbr[l]; ++b) CK(cudaStreamWaitEvent(s, d->ev_m2l[l][b], 0));
-      split_in(l, s);
-      launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s, d->inp);
+      launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
     }
   }
   launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
@@ -917,7 +865,7 @@ static fda_status run_sharded_up(Context* ctx, Dev* d, cudaStream_t s, int kind)
   if (kind) launch_s2m(d->n_s2m_rhs, d->s2m_rhs, d->pool, d->x_tree, d->outb, d->max_T, s);
   else launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s);
   const int nlev = (int)d->m2m.size();
-  for (int l = nlev - 1; l >= 0; --l) launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s, d->outp);   // partials
+  for (int l = nlev - 1; l >= 0; --l) launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);   // partials
   launch_pack(d->outb, d->xs_idx, d->sendb, d->n_send, s);
   CK(cudaGetLastError());
   return FDA_OK;
@@ -947,10 +895,6 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
   g_tcpool = d->tcpool;
   launch_unpack_add(d->recvb, d->xr_idx, d->outb, d->n_recv, s);
   const int nlev = (int)d->m2m.size();
-  if (d->use_tc)
-    for (int l = 0; l < nlev; ++l)
-      launch_split_states(d->outb, d->d_out_off, d->d_pout, d->lvl_T[l], d->lvl_Tp[l], d->out_lb[l],
-                          d->out_lb[l + 1], d->outp, s);
   CK(cudaEventRecord(d->ev_up[0], s));
   int k = 0;
   std::vector<int> nbr(nlev, 0);
@@ -964,8 +908,8 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
       if (c >= 0) {
         launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, sm);
       } else {
-        launch_stage(L.dense, d->pool, d->outb, d->inb, sm, d->outp);
-        launch_stage(L.a, d->pool, d->outb, d->tmpb, sm, d->outp);
+        launch_stage(L.dense, d->pool, d->outb, d->inb, sm);
+        launch_stage(L.a, d->pool, d->outb, d->tmpb, sm);
         launch_stage(L.b, d->pool, d->tmpb, d->inb, sm);
       }
       CK(cudaEventRecord(d->ev_m2l[l][nbr[l]++], sm));
@@ -973,10 +917,7 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
   }
   for (int l = 0; l < nlev; ++l) {
     for (int b = 0; b < nbr[l]; ++b) CK(cudaStreamWaitEvent(s, d->ev_m2l[l][b], 0));
-    if (d->use_tc)
-      launch_split_states(d->inb, d->d_in_off, d->d_pin, d->lvl_T[l], d->lvl_Tp[l], d->in_lb[l], d->in_lb[l + 1],
-                          d->inp, s);
-    launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s, d->inp);
+    launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
   }
   launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
   CK(cudaStreamWaitEvent(s, d->ev_join, 0));

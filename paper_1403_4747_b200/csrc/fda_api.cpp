@@ -131,13 +131,13 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
       int64_t off = 0;
       for (size_t s = 0; s < pl.out_states.size(); ++s) {
         pl.out_offset[s] = off;
-        off += ctx->t.levels[ctx->t.boxes[pl.out_states[s].box].level].rank;
+        off += (ctx->t.levels[ctx->t.boxes[pl.out_states[s].box].level].rank + 1) & ~1;   // 16-B aligned states
       }
       pl.out_size = off;
       off = 0;
       for (size_t s = 0; s < pl.in_states.size(); ++s) {
         pl.in_offset[s] = off;
-        off += ctx->t.levels[ctx->t.boxes[pl.in_states[s].box].level].rank;
+        off += (ctx->t.levels[ctx->t.boxes[pl.in_states[s].box].level].rank + 1) & ~1;
       }
       pl.in_size = off;
       build_operators(ctx->g, ctx->p, ctx->t, pl);

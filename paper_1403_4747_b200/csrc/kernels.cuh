@@ -55,17 +55,20 @@ struct LrTask {
   int32_t op_begin, op_count;
 };
 
-// tcgen05 translation task (kernels_tc.cu): ≤ 64 complex rows × ≤ 64 ops of one matrix;
-// A operand pre-laid-out per 64-row block and TC_KC-column chunk as [hi | lo] tiles of 128 × TC_KC floats
-constexpr int TC_KC = 16;
+// tcgen05 translation task (kernels_tc.cu): all rows of one matrix (R × C complex,
+// ntile = ⌈2R/128⌉ ≤ 3 tiles of the interleaved real matrix) × ≤ 128 or 256 ops sharing it.
+// The A operand is pre-laid-out per (tile, TC_KC-float K chunk) as [hi | lo] 128 × TC_KC tiles.
+constexpr int TC_KC = 16;   // floats of K per pipeline stage
+constexpr int TC_NV = 5;    // kernel variants (N, tiles): (128,1) (128,2) (128,3) (256,1) (256,2)
 struct TcTask {
-  int64_t a_off;      // float offset of this row block's pre-laid-out [chunk][hi|lo] A tiles
-  int32_t nkc;        // TC_KC-column chunks
+  int64_t a_off;      // float offset of the matrix's pre-laid-out A in the tensor-core pool
   int32_t R, C;       // matrix shape (complex)
-  int32_t row0;       // first complex row of the block
+  int32_t nkc;        // K chunks: ⌈2C / TC_KC⌉
+  int32_t ntile;      // 128-row tiles of the real matrix
   int32_t op_begin, op_count;
-  int32_t Tp;         // plane length of the (pre-split) source states
 };
+int tc_variant(int n, int tiles);
+int tc_variant_ops(int v);
 
 // leaf-level ops (S2M / L2T)
 struct LeafTask {
@@ -100,10 +103,9 @@ int m2l_lr_class(int r);
 int m2l_lr_ops(int cls);   // ops per CTA of a class
 constexpr int LR_MAX_R = 64;
 cudaError_t m2l_lr_prepare();
-void launch_xlate_tc(int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
-                     const float* tcpool, const float* srcp, float2* dst, cudaStream_t s);
-void launch_split_states(const float2* states, const int64_t* off, const int64_t* poff, int T, int Tp, int64_t s0,
-                         int64_t s1, float* planes, cudaStream_t s);
+// src / dst state offsets must be even (16-byte aligned complex64 states)
+void launch_xlate_tc(int variant, int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                     const float* tcpool, const float2* src, float2* dst, cudaStream_t s);
 cudaError_t tc_prepare();
 // GMRES / BLAS-1 helpers (fp64 accumulation)
 void launch_dots(const float2* V, int64_t ldv, int nv, const float2* w, int64_t n, double2* partial, int nchunks,

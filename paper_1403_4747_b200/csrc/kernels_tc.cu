@@ -1,22 +1,29 @@
 // Tensor-core (tcgen05, sm_100a) grouped complex GEMM for the dense FDA
-// translations (M2M, L2L, dense M2L).
+// translations (M2M, L2L, dense M2L):
+//   dst[:, op] += M · src[:, op]   for the ops of one task, all sharing M (R × C complex).
 //
-// For one task (one matrix M, R × C complex, ≤ 64 complex rows of it and ≤ 64
-// ops sharing it) the CTA computes D[:, n] = M_blk · S[:, n] and accumulates
-// D into the destination states with vector atomics, exactly like k_xlate.
-// Complex arithmetic is done on real planes:
-//   A = [M_r; M_i] (128 × C, real),  P = A·S_r,  Q = A·S_i  (128 × 64, TMEM)
-//   D_r = P_top - Q_bot,  D_i = Q_top + P_bot.
+// Complex arithmetic as one real GEMM with interleaved K and M: the complex
+// states are float2 arrays, i.e. a state is the real vector
+// (re₀, im₀, re₁, im₁, …); with the real 2R × 2C matrix
+//   A[2i][2j] = Re M_ij,  A[2i][2j+1] = −Im M_ij,  A[2i+1][2j] = Im M_ij,  A[2i+1][2j+1] = Re M_ij
+// the product A · state is the interleaved complex result, so the B operand
+// is the raw state memory (no pre-split planes) and the accumulator row 2i /
+// 2i+1 is Re / Im of output i.
+//
 // fp32 accuracy from TF32 tensor cores by the 3-term split (3xTF32):
-//   A·B ≈ A_hi·B_hi + A_hi·B_lo + A_lo·B_hi,  X_hi = tf32(X), X_lo = tf32(X - X_hi).
-// A is pre-split and pre-laid-out on the host in the canonical K-major
-// (no-swizzle) UMMA layout — core matrices of 8 rows × 16 bytes — per TC_KC-column
-// chunk; the sources are pre-split once per tree level (k_split_states) into
-// 16-byte-aligned planes, so the CTA streams both operands with 16-byte
-// cp.async and only issues MMAs.  One thread issues the MMAs
-// (tcgen05.mma.cta_group::1.kind::tf32, M = 128, N = 64, K = 8), completion is
-// tracked by tcgen05.commit on an mbarrier, two shared-memory stages overlap
-// the copy of chunk k+1 with the MMAs of chunk k.
+//   A·B ≈ A_hi·B_hi + A_hi·B_lo + A_lo·B_hi,  X_hi = tf32(X), X_lo = tf32(X − X_hi);
+// A is split and pre-laid-out on the host (engine.cu: tc_matrix) in the
+// canonical K-major no-swizzle UMMA layout — core matrices of 8 rows × 16 B —
+// per 128-row tile and KC-float K chunk, [hi | lo] contiguous, and streamed
+// with one bulk async copy (cp.async.bulk, TMA engine, mbarrier tx-count) per
+// tile and chunk; B (the gathered source states, 16-B cp.async per op and
+// k-group, zero-filled past the state end) is split into hi / lo in shared
+// memory.  S-stage ring: the copies of chunks c+1 … c+S-1 are in flight while
+// one thread issues the MMAs of chunk c (tcgen05.mma.cta_group::1.kind::tf32,
+// M = 128, N ∈ {128, 256}, K = 8) into TMEM accumulators (one 128 × N block
+// per row tile); tcgen05.commit on an mbarrier releases the stage.  Epilogue:
+// tcgen05.ld of each accumulator block, Re/Im lanes paired by shuffle, vector
+// atomics into the destination states (several tasks may share a destination).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -25,18 +32,11 @@
 namespace fda {
 
 namespace {
-constexpr int TC_N = 64;                     // ops per task (MMA N)
-constexpr int A_TILE = 128 * TC_KC;          // floats per (chunk, hi|lo) A tile
-constexpr int B_TILE = TC_N * TC_KC;         // floats per (chunk, plane) B tile
-constexpr uint32_t TMEM_COLS = 2 * TC_N;     // P and Q accumulators
+constexpr int KC = TC_KC;        // floats of K per stage (= 8 complex columns)
+constexpr int STAGES = 3;
+constexpr int A_TILE = 128 * KC;  // floats per (row tile, chunk, hi|lo)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
 
 // canonical K-major, no-swizzle UMMA shared-memory descriptor
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -45,13 +45,13 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
-  // base_offset = 0, lbo_mode = 0, layout_type = 0 (SWIZZLE_NONE)
   return d;
 }
 
-// instruction descriptor: kind::tf32, D = F32, A/B = TF32, both K-major, M = 128, N = TC_N
-__host__ __device__ constexpr uint32_t make_idesc() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// instruction descriptor: kind::tf32, D = F32, A/B = TF32, both K-major, M = 128, N
+template <int N>
+__device__ __forceinline__ constexpr uint32_t make_idesc() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -79,8 +79,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
-__device__ __forceinline__ void cp16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g));
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+// bulk async copy global → shared (TMA engine), completion counted on mbar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 16-byte cp.async with src-size (bytes beyond it are zero-filled)
+__device__ __forceinline__ void cp16z(void* s, const void* g, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(s)), "l"(g), "r"(bytes));
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
@@ -94,171 +109,211 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
+
+__host__ __device__ constexpr uint32_t tmem_cols(int n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 256 ? 256 : 512))); }
 }  // namespace
 
-// shared memory: 2 stages × (A hi, A lo, B r_hi, r_lo, i_hi, i_lo), 16-byte aligned
-constexpr int TC_STAGE_FLOATS = 2 * A_TILE + 4 * B_TILE;
-constexpr size_t TC_SMEM = (size_t)2 * TC_STAGE_FLOATS * sizeof(float) + 1024;
+template <int N, int TILES>
+struct TcCfg {
+  static constexpr int A_FL = TILES * 2 * A_TILE;   // A floats per stage
+  static constexpr int B_FL = 2 * N * KC;          // B floats per stage (hi, lo)
+  static constexpr int STAGE_FL = A_FL + B_FL;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_FL * 4 + 1024;
+  static_assert(TILES * N <= 512, "TMEM columns");
+};
 
-__global__ void __launch_bounds__(128, 3) k_xlate_tc(const TcTask* __restrict__ tasks,
+template <int N, int TILES>
+__global__ void __launch_bounds__(128, 1) k_xlate_tc(const TcTask* __restrict__ tasks,
                                                      const int64_t* __restrict__ src_off,
                                                      const int64_t* __restrict__ dst_off,
-                                                     const float* __restrict__ tcpool,
-                                                     const float* __restrict__ srcp, float2* __restrict__ dst) {
+                                                     const float* __restrict__ tcpool, const float2* __restrict__ src,
+                                                     float2* __restrict__ dst) {
+  using Cfg = TcCfg<N, TILES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* sbase = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t mbar[2];
+  __shared__ uint64_t mbar_a[STAGES], mbar_m[STAGES];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int64_t soff[TC_N];
+  __shared__ int64_t soff[N];   // float offset of the source state (-1: padding op)
+  __shared__ int64_t doff[N];   // complex offset of the destination state
   const TcTask t = tasks[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K2 = 2 * t.C;       // real K
 
-  for (int p = tid; p < TC_N; p += 128) soff[p] = p < t.op_count ? src_off[t.op_begin + p] : -1;
+  for (int p = tid; p < N; p += 128) {
+    const bool ok = p < t.op_count;
+    soff[p] = ok ? 2 * src_off[t.op_begin + p] : -1;
+    doff[p] = ok ? dst_off[t.op_begin + p] : -1;
+  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
-                 "r"(TMEM_COLS));
+                 "r"(tmem_cols(TILES * N)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
   }
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&mbar_a[s], 1);
+      mbar_init(&mbar_m[s], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t idesc = make_idesc();
   const int nkc = t.nkc;
+  const float* gA = tcpool + t.a_off;
 
-  for (int kc = 0; kc < nkc; ++kc) {
-    const int st = kc & 1;
-    if (kc >= 2) mbar_wait(&mbar[st], ((kc - 2) >> 1) & 1);   // MMAs of chunk kc-2 released this stage
-    float* sA = sbase + st * TC_STAGE_FLOATS;                 // [hi | lo], A_TILE each
-    float* sB = sA + 2 * A_TILE;                              // [r_hi | r_lo | i_hi | i_lo], B_TILE each
-    // A: contiguous 2 × A_TILE floats, pre-laid-out → 16-byte async copies
-    const float* gA = tcpool + t.a_off + (int64_t)kc * 2 * A_TILE;
-    for (int i = tid; i < 2 * A_TILE / 4; i += 128) cp16(sA + 4 * i, gA + 4 * i);
-    asm volatile("cp.async.commit_group;\n" ::);
-    // B: the sources were pre-split per state into 4 planes [r_hi | r_lo | i_hi | i_lo] of
-    // Tp floats each (k_split_states); a core-matrix row (op n, k-group kg) is 16 contiguous
-    // bytes of a plane → 16-byte async copies into ((kg·(N/8) + n/8)·8 + n%8)·4
-    for (int i = tid; i < 4 * (TC_KC / 4) * TC_N; i += 128) {
-      const int plane = i / ((TC_KC / 4) * TC_N), rem = i % ((TC_KC / 4) * TC_N);
-      const int kg = rem / TC_N, n = rem % TC_N;
-      float* dstp = sB + plane * B_TILE + ((kg * (TC_N / 8) + n / 8) * 8 + (n & 7)) * 4;
+  // stage layout: [A: tile][hi|lo][128 × KC] | [B hi: N × KC][B lo: N × KC]
+  auto issue = [&](int c) {
+    const int st = c % STAGES;
+    float* sA = sbase + st * Cfg::STAGE_FL;
+    float* sB = sA + Cfg::A_FL;
+    if (tid == 0) {
+      mbar_expect_tx(&mbar_a[st], (uint32_t)(TILES * 2 * A_TILE * 4));
+#pragma unroll
+      for (int ti = 0; ti < TILES; ++ti)
+        bulk_g2s(sA + ti * 2 * A_TILE, gA + ((int64_t)ti * nkc + c) * 2 * A_TILE, 2 * A_TILE * 4, &mbar_a[st]);
+    }
+    // B: op n, k-group kg (4 floats) → ((kg · N/8 + n/8) · 8 + n%8) · 4
+    for (int idx = tid; idx < N * (KC / 4); idx += 128) {
+      const int n = idx >> 2, kg = idx & 3;
+      const int k = c * KC + 4 * kg;
       const int64_t so = soff[n];
-      if (so >= 0) cp16(dstp, srcp + so + (int64_t)plane * t.Tp + kc * TC_KC + 4 * kg);
-      else *reinterpret_cast<float4*>(dstp) = make_float4(0.f, 0.f, 0.f, 0.f);
+      int bytes = so >= 0 ? 4 * min(4, max(0, K2 - k)) : 0;
+      const float* g = bytes ? reinterpret_cast<const float*>(src) + so + k : reinterpret_cast<const float*>(src);
+      cp16z(sB + ((kg * (N / 8) + (n >> 3)) * 8 + (n & 7)) * 4, g, bytes);
     }
     asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  };
+
+  for (int c = 0; c < STAGES - 1; ++c) {
+    if (c < nkc) issue(c);
+    else asm volatile("cp.async.commit_group;\n" ::);
+  }
+  for (int c = 0; c < nkc; ++c) {
+    const int st = c % STAGES;
+    const int cn = c + STAGES - 1;
+    if (cn < nkc) {
+      if (c >= 1) mbar_wait(&mbar_m[(c - 1) % STAGES], ((c - 1) / STAGES) & 1);   // MMAs of chunk c-1 done
+      issue(cn);
+    } else {
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 1) : "memory");
+    mbar_wait(&mbar_a[st], (c / STAGES) & 1);
+    __syncthreads();
+    float* sA = sbase + st * Cfg::STAGE_FL;
+    float* sB = sA + Cfg::A_FL;
+    // split B into tf32 hi (low 13 mantissa bits cleared, in place) and lo
+    {
+      float4* bh = reinterpret_cast<float4*>(sB);
+      float4* bl = reinterpret_cast<float4*>(sB + N * KC);
+      for (int i = tid; i < N * KC / 4; i += 128) {
+        const float4 v = bh[i];
+        const float4 h = make_float4(__uint_as_float(__float_as_uint(v.x) & 0xffffe000u),
+                                     __uint_as_float(__float_as_uint(v.y) & 0xffffe000u),
+                                     __uint_as_float(__float_as_uint(v.z) & 0xffffe000u),
+                                     __uint_as_float(__float_as_uint(v.w) & 0xffffe000u));
+        bh[i] = h;
+        bl[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+      }
+    }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-      const uint32_t a_hi = smem_u32(sA), a_lo = smem_u32(sA + A_TILE);
-      const uint32_t b0 = smem_u32(sB);
+      constexpr uint32_t idesc = make_idesc<N>();
+      const uint32_t b_hi = smem_u32(sB), b_lo = smem_u32(sB + N * KC);
 #pragma unroll
-      for (int s = 0; s < TC_KC / 8; ++s) {
-        // K = 8 per MMA: core-matrix k-groups 2s, 2s+1
-        const uint32_t ao = (uint32_t)(2 * s * 16 * 128), bo = (uint32_t)(2 * s * (TC_N / 8) * 128);
-        const uint64_t Ahi = make_desc(a_hi + ao, 16 * 128, 128), Alo = make_desc(a_lo + ao, 16 * 128, 128);
-        const uint64_t Brh = make_desc(b0 + bo, (TC_N / 8) * 128, 128);
-        const uint64_t Brl = make_desc(b0 + 4 * B_TILE + bo, (TC_N / 8) * 128, 128);
-        const uint64_t Bih = make_desc(b0 + 8 * B_TILE + bo, (TC_N / 8) * 128, 128);
-        const uint64_t Bil = make_desc(b0 + 12 * B_TILE + bo, (TC_N / 8) * 128, 128);
-        const uint32_t acc = (kc > 0 || s > 0) ? 1u : 0u;
-        mma_tf32(tmem, Ahi, Brh, idesc, acc);            // P = A · S_r
-        mma_tf32(tmem, Ahi, Brl, idesc, 1u);
-        mma_tf32(tmem, Alo, Brh, idesc, 1u);
-        mma_tf32(tmem + TC_N, Ahi, Bih, idesc, acc);     // Q = A · S_i
-        mma_tf32(tmem + TC_N, Ahi, Bil, idesc, 1u);
-        mma_tf32(tmem + TC_N, Alo, Bih, idesc, 1u);
+      for (int s = 0; s < KC / 8; ++s) {
+        const uint32_t bo = (uint32_t)(2 * s * (N / 8) * 128);
+        const uint64_t Bh = make_desc(b_hi + bo, (N / 8) * 128, 128);
+        const uint64_t Bl = make_desc(b_lo + bo, (N / 8) * 128, 128);
+#pragma unroll
+        for (int ti = 0; ti < TILES; ++ti) {
+          const uint32_t a_hi = smem_u32(sA + ti * 2 * A_TILE), a_lo = a_hi + A_TILE * 4;
+          const uint32_t ao = (uint32_t)(2 * s * 16 * 128);
+          const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
+          const uint32_t d = tmem + ti * N;
+          mma_tf32(d, Ah, Bh, idesc, (c > 0 || s > 0) ? 1u : 0u);
+          mma_tf32(d, Ah, Bl, idesc, 1u);
+          mma_tf32(d, Al, Bh, idesc, 1u);
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                       smem_u32(&mbar[st]))
+                       smem_u32(&mbar_m[st]))
                    : "memory");
     }
   }
-  mbar_wait(&mbar[(nkc - 1) & 1], ((nkc - 1) >> 1) & 1);
+  mbar_wait(&mbar_m[(nkc - 1) % STAGES], ((nkc - 1) / STAGES) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
 
-  // epilogue: warps 2,3 hold rows 64..127 (M_i·S) → shared; warps 0,1 combine and accumulate
-  float* sE = sbase;  // [64 rows][2 (P,Q)][TC_N + 1]
+  // epilogue: warp w holds accumulator rows 32w..32w+31 of each tile; row 2i / 2i+1 = Re / Im of output i
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-  if (warp >= 2) {
-    const int row = (warp - 2) * 32 + lane;
-    for (int c0 = 0; c0 < TC_N; c0 += 16) {
+  const bool even = (lane & 1) == 0;
+#pragma unroll 1
+  for (int ti = 0; ti < TILES; ++ti) {
+    const int out_i = (128 * ti + 32 * warp + lane) >> 1;
+#pragma unroll 1
+    for (int c0 = 0; c0 < N; c0 += 16) {
       float v[16];
-      tmem_ld16(tmem + lane_base + c0, v);
+      tmem_ld16(tmem + lane_base + ti * N + c0, v);
+      float w[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) sE[(row * 2 + 0) * (TC_N + 1) + c0 + j] = v[j];
-      tmem_ld16(tmem + lane_base + TC_N + c0, v);
+      for (int j = 0; j < 16; ++j) w[j] = __shfl_xor_sync(0xffffffffu, v[j], 1);
+      // even lane: ops c0 .. c0+7 with (re, im) = (v, w); odd lane: ops c0+8 .. c0+15 with (w, v)
+      if (out_i < t.R) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) sE[(row * 2 + 1) * (TC_N + 1) + c0 + j] = v[j];
-    }
-  }
-  __syncthreads();
-  if (warp < 2) {
-    const int row = warp * 32 + lane;       // complex row within the block
-    const int grow = t.row0 + row;
-    for (int c0 = 0; c0 < TC_N; c0 += 16) {
-      float p[16], q[16];
-      tmem_ld16(tmem + lane_base + c0, p);
-      tmem_ld16(tmem + lane_base + TC_N + c0, q);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int n = c0 + j;
-        if (n < t.op_count && grow < t.R) {
-          const float pb = sE[(row * 2 + 0) * (TC_N + 1) + n], qb = sE[(row * 2 + 1) * (TC_N + 1) + n];
-          atomicAdd(dst + dst_off[t.op_begin + n] + grow, make_float2(p[j] - qb, q[j] + pb));
+        for (int j = 0; j < 8; ++j) {
+          const int op = c0 + j + (even ? 0 : 8);
+          if (op < t.op_count) {
+            const float re = even ? v[j] : w[j + 8], im = even ? w[j] : v[j + 8];
+            atomicAdd(dst + doff[op] + out_i, make_float2(re, im));
+          }
         }
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols(TILES * N)));
 }
 
-size_t tc_smem_bytes() { return TC_SMEM; }
+namespace {
+template <int N, int TILES>
+cudaError_t tc_attr() {
+  return cudaFuncSetAttribute(k_xlate_tc<N, TILES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)TcCfg<N, TILES>::SMEM);
+}
+}  // namespace
 
 cudaError_t tc_prepare() {
-  return cudaFuncSetAttribute(k_xlate_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
+  cudaError_t e;
+  if ((e = tc_attr<128, 1>()) != cudaSuccess) return e;
+  if ((e = tc_attr<128, 2>()) != cudaSuccess) return e;
+  if ((e = tc_attr<128, 3>()) != cudaSuccess) return e;
+  if ((e = tc_attr<256, 1>()) != cudaSuccess) return e;
+  return tc_attr<256, 2>();
 }
 
-void launch_xlate_tc(int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
-                     const float* tcpool, const float* srcp, float2* dst, cudaStream_t s) {
+// variant = tc_variant(N, tiles): 0..4 = (128,1) (128,2) (128,3) (256,1) (256,2)
+int tc_variant(int n, int tiles) { return n == 256 ? 2 + tiles : tiles - 1; }
+int tc_variant_ops(int v) { return v >= 3 ? 256 : 128; }
+
+void launch_xlate_tc(int variant, int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                     const float* tcpool, const float2* src, float2* dst, cudaStream_t s) {
   if (ntask <= 0) return;
-  k_xlate_tc<<<ntask, 128, TC_SMEM, s>>>(tasks, src_off, dst_off, tcpool, srcp, dst);
-}
-
-// Pre-split states [s0, s1) for the tensor-core operand B: state s (T complex at
-// off[s]) → 4 planes of Tp floats at poff[s]: tf32 hi/lo of the real and the
-// imaginary parts, zero-padded to Tp (a multiple of TC_KC).
-__global__ void k_split_states(const float2* __restrict__ states, const int64_t* __restrict__ off,
-                               const int64_t* __restrict__ poff, int T, int Tp, int64_t s0, int64_t s1,
-                               float* __restrict__ planes) {
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t s = s0 + g / Tp;
-  const int k = (int)(g % Tp);
-  if (s >= s1) return;
-  float2 v = k < T ? states[off[s] + k] : make_float2(0.f, 0.f);
-  const uint32_t rh = to_tf32(v.x), ih = to_tf32(v.y);
-  const uint32_t rl = to_tf32(v.x - __uint_as_float(rh)), il = to_tf32(v.y - __uint_as_float(ih));
-  float* p = planes + poff[s];
-  p[k] = __uint_as_float(rh);
-  p[Tp + k] = __uint_as_float(rl);
-  p[2 * Tp + k] = __uint_as_float(ih);
-  p[3 * Tp + k] = __uint_as_float(il);
-}
-
-void launch_split_states(const float2* states, const int64_t* off, const int64_t* poff, int T, int Tp, int64_t s0,
-                         int64_t s1, float* planes, cudaStream_t s) {
-  if (s1 <= s0) return;
-  const int64_t n = (s1 - s0) * Tp;
-  k_split_states<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(states, off, poff, T, Tp, s0, s1, planes);
+#define TCL(NN, TT) \
+  k_xlate_tc<NN, TT><<<ntask, 128, TcCfg<NN, TT>::SMEM, s>>>(tasks, src_off, dst_off, tcpool, src, dst)
+  switch (variant) {
+    case 0: TCL(128, 1); break;
+    case 1: TCL(128, 2); break;
+    case 2: TCL(128, 3); break;
+    case 3: TCL(256, 1); break;
+    default: TCL(256, 2); break;
+  }
+#undef TCL
 }
 
 }  // namespace fda

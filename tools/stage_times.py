@@ -20,10 +20,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--tc", type=int, default=0, help="dense translations on tcgen05 (3xTF32)")
+    ap.add_argument("--lowrank", type=int, default=1, help="§4.2 second-stage SVD of K̃")
     a = ap.parse_args()
     c = CONFIGS[a.config]
     V, F = config_mesh(a.config)
-    f = FDA(V, F, c.k, c.alpha, c.eps, max_leaf=c.max_leaf)
+    f = FDA(V, F, c.k, c.alpha, c.eps, max_leaf=c.max_leaf, tensor_cores=a.tc, m2l_lowrank=a.lowrank)
     x = torch.from_numpy(random_density(len(F), c.x_seed).astype(np.complex64)).cuda()
     y = torch.empty_like(x)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
@@ -51,7 +53,7 @@ def main():
         ts.append(st.elapsed_time(en))
     out["graph_matvec"] = round(float(np.median(ts)), 4)
     out["y_checksum"] = [float(y.real.sum()), float(y.imag.sum()), float(y.abs().sum())]
-    print(json.dumps({"config": a.config, "env": {k: v for k, v in os.environ.items() if k.startswith("FDA_")},
+    print(json.dumps({"config": a.config, "tensor_cores": a.tc, "m2l_lowrank": a.lowrank,
                       "ms": out}))
 
 
