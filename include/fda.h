@@ -82,7 +82,9 @@ typedef struct {
   int32_t rhs_operator;  /* 1: also build the RHS pass B (fda_rhs_apply)        */
   int32_t rank;          /* this rank (0-based) when the operator is sharded over nranks GPUs */
   int32_t nranks;        /* ranks sharing the operator (1 = unsharded)                      */
-  int32_t tensor_cores;  /* 1: dense translations on tcgen05 tensor cores (3xTF32)          */
+  int32_t tensor_cores;  /* dense translations (M2M, L2L, dense M2L) on tcgen05 tensor cores,
+                            3xTF32: 0 never, 1 every eligible stage, 2 (default) stages of
+                            ≥ 1 GFLOP with ≥ 64 ops per matrix (CUDA cores elsewhere)     */
   int32_t reserved[2];
 } fda_options;
 

@@ -269,7 +269,17 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   });
   std::vector<int64_t> so, dof;
   std::vector<XTask> tasks[XV];
-  if (d->use_tc && atomic && tc_ok) {
+  bool tc = d->use_tc && atomic && tc_ok;
+  if (tc && ctx->p.opt.tensor_cores == 2) {   // auto: large, well-shared stages only
+    double flops = 0;
+    std::unordered_map<int64_t, int> nm;
+    for (const XOp& o : ops) {
+      flops += 8.0 * p.mats[o.mat].rows * p.mats[o.mat].cols;
+      nm[o.mat] = 1;
+    }
+    tc = flops >= 1e9 && (double)ops.size() >= 64.0 * (double)nm.size();
+  }
+  if (tc) {
     std::vector<TcTask> tct[TC_NV];
     for (size_t i = 0; i < ord.size();) {
       const int64_t m = ops[ord[i]].mat;
@@ -294,10 +304,31 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
         t.ntile = ntile;
         t.op_begin = base + (int32_t)c0;
         t.op_count = (int32_t)std::min<int64_t>(nmax, nops - c0);
+        t.kc0 = 0;
+        t.kc1 = t.nkc;
         tct[v].push_back(t);
       }
       i = j;
     }
+    // split-K for stages with fewer tasks than ~2 waves (one CTA per SM): ≥ 3 chunks per part
+    int64_t total = 0;
+    for (int v = 0; v < TC_NV; ++v) total += (int64_t)tct[v].size();
+    const int64_t target = 2 * 148;
+    if (total > 0 && total < target)
+      for (int v = 0; v < TC_NV; ++v) {
+        std::vector<TcTask> out;
+        for (const TcTask& t : tct[v]) {
+          const int parts = (int)std::max<int64_t>(1, std::min<int64_t>((target + total - 1) / total, t.nkc / 3));
+          const int per = (t.nkc + parts - 1) / parts;
+          for (int c = 0; c < t.nkc; c += per) {
+            TcTask u = t;
+            u.kc0 = c;
+            u.kc1 = std::min(t.nkc, c + per);
+            out.push_back(u);
+          }
+        }
+        tct[v].swap(out);
+      }
     for (int v = 0; v < TC_NV; ++v) {
       st.n_tc[v] = (int)tct[v].size();
       if (st.n_tc[v]) UP(&st.tc[v], tct[v].data(), tct[v].size());

@@ -63,9 +63,10 @@ constexpr int TC_NV = 5;    // kernel variants (N, tiles): (128,1) (128,2) (128,
 struct TcTask {
   int64_t a_off;      // float offset of the matrix's pre-laid-out A in the tensor-core pool
   int32_t R, C;       // matrix shape (complex)
-  int32_t nkc;        // K chunks: ⌈2C / TC_KC⌉
+  int32_t nkc;        // K chunks of the whole matrix: ⌈2C / TC_KC⌉ (layout stride of the A pool)
   int32_t ntile;      // 128-row tiles of the real matrix
   int32_t op_begin, op_count;
+  int32_t kc0, kc1;   // this task's K chunks (split-K: partial products accumulate atomically)
 };
 int tc_variant(int n, int tiles);
 int tc_variant_ops(int v);

@@ -160,24 +160,25 @@ __global__ void __launch_bounds__(128, 1) k_xlate_tc(const TcTask* __restrict__ 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
   const uint32_t tmem = tmem_base_sh;
-  const int nkc = t.nkc;
+  const int nkc = t.nkc, kc0 = t.kc0, nk = t.kc1 - t.kc0;   // this task: chunks kc0 … kc1-1
   const float* gA = tcpool + t.a_off;
 
   // stage layout: [A: tile][hi|lo][128 × KC] | [B hi: N × KC][B lo: N × KC]
-  auto issue = [&](int c) {
+  auto issue = [&](int c) {   // c: local chunk index (global chunk kc0 + c)
     const int st = c % STAGES;
+    const int cg = kc0 + c;
     float* sA = sbase + st * Cfg::STAGE_FL;
     float* sB = sA + Cfg::A_FL;
     if (tid == 0) {
       mbar_expect_tx(&mbar_a[st], (uint32_t)(TILES * 2 * A_TILE * 4));
 #pragma unroll
       for (int ti = 0; ti < TILES; ++ti)
-        bulk_g2s(sA + ti * 2 * A_TILE, gA + ((int64_t)ti * nkc + c) * 2 * A_TILE, 2 * A_TILE * 4, &mbar_a[st]);
+        bulk_g2s(sA + ti * 2 * A_TILE, gA + ((int64_t)ti * nkc + cg) * 2 * A_TILE, 2 * A_TILE * 4, &mbar_a[st]);
     }
     // B: op n, k-group kg (4 floats) → ((kg · N/8 + n/8) · 8 + n%8) · 4
     for (int idx = tid; idx < N * (KC / 4); idx += 128) {
       const int n = idx >> 2, kg = idx & 3;
-      const int k = c * KC + 4 * kg;
+      const int k = cg * KC + 4 * kg;
       const int64_t so = soff[n];
       int bytes = so >= 0 ? 4 * min(4, max(0, K2 - k)) : 0;
       const float* g = bytes ? reinterpret_cast<const float*>(src) + so + k : reinterpret_cast<const float*>(src);
@@ -187,13 +188,13 @@ __global__ void __launch_bounds__(128, 1) k_xlate_tc(const TcTask* __restrict__ 
   };
 
   for (int c = 0; c < STAGES - 1; ++c) {
-    if (c < nkc) issue(c);
+    if (c < nk) issue(c);
     else asm volatile("cp.async.commit_group;\n" ::);
   }
-  for (int c = 0; c < nkc; ++c) {
+  for (int c = 0; c < nk; ++c) {
     const int st = c % STAGES;
     const int cn = c + STAGES - 1;
-    if (cn < nkc) {
+    if (cn < nk) {
       if (c >= 1) mbar_wait(&mbar_m[(c - 1) % STAGES], ((c - 1) / STAGES) & 1);   // MMAs of chunk c-1 done
       issue(cn);
     } else {
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(128, 1) k_xlate_tc(const TcTask* __restrict__ 
                    : "memory");
     }
   }
-  mbar_wait(&mbar_m[(nkc - 1) % STAGES], ((nkc - 1) / STAGES) & 1);
+  mbar_wait(&mbar_m[(nk - 1) % STAGES], ((nk - 1) / STAGES) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
 
   // epilogue: warp w holds accumulator rows 32w..32w+31 of each tile; row 2i / 2i+1 = Re / Im of output i

@@ -44,7 +44,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", type=int, default=5)
     ap.add_argument("--rows", type=int, default=2000)
-    ap.add_argument("--tc", type=int, default=0)
+    ap.add_argument("--tc", type=int, default=2)
     ap.add_argument("--no-oracle", action="store_true")
     a = ap.parse_args()
     c = CONFIGS[a.cfg]
@@ -88,7 +88,7 @@ def main():
         err = float(np.linalg.norm(y[rows] - yo) / np.linalg.norm(yo))
     print(json.dumps({"config": a.cfg, "N": N, "k": c.k, "mesh_s": round(t_mesh, 1), "build_s": round(t_build, 1),
                       "matvec_ms": round(mv_ms, 3), "stages_ms": {k: round(v, 3) for k, v in stages.items()},
-                      "sampled_rows": len(rows), "rel_l2_sampled": err, "oracle_rows_s": t_or, "tensor_cores": bool(a.tc),
+                      "sampled_rows": len(rows), "rel_l2_sampled": err, "oracle_rows_s": t_or, "tensor_cores": a.tc,
                       "oracle_cores": fast.num_threads(), "levels": levels,
                       "tree": {k: st[k] for k in ("n_levels", "n_hf_levels", "n_leaves", "n_m2l_pairs",
                                                   "n_direct_element_pairs", "n_corrections", "table_bytes",

@@ -20,7 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--tc", type=int, default=0, help="dense translations on tcgen05 (3xTF32)")
+    ap.add_argument("--tc", type=int, default=2, help="tcgen05 translations: 0 off, 1 all eligible, 2 auto")
     ap.add_argument("--lowrank", type=int, default=1, help="§4.2 second-stage SVD of K̃")
     a = ap.parse_args()
     c = CONFIGS[a.config]
