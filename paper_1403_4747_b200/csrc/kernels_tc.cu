@@ -249,27 +249,42 @@ __global__ void __launch_bounds__(128, 1) k_xlate_tc(const TcTask* __restrict__ 
   mbar_wait(&mbar_m[(nk - 1) % STAGES], ((nk - 1) / STAGES) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
 
-  // epilogue: warp w holds accumulator rows 32w..32w+31 of each tile; row 2i / 2i+1 = Re / Im of output i
+  // epilogue: warp w holds accumulator rows 32w..32w+31 of each tile; rows 4q..4q+3 of a
+  // lane quad are (Re, Im) of outputs i, i+1 (i even).  A quad transpose (4 rounds of
+  // shuffles) gives lane p of the quad all four values of columns 4p..4p+3, added with
+  // one 16-byte vector atomic per column (states are 16-byte aligned and padded to an
+  // even length, so the pair (i, i+1 = R) writes a zero into the padding slot).
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-  const bool even = (lane & 1) == 0;
+  const int qp = lane & 3, qbase = lane & ~3;
 #pragma unroll 1
   for (int ti = 0; ti < TILES; ++ti) {
-    const int out_i = (128 * ti + 32 * warp + lane) >> 1;
+    const int out_i = (128 * ti + 32 * warp + qbase) >> 1;   // even
 #pragma unroll 1
     for (int c0 = 0; c0 < N; c0 += 16) {
       float v[16];
       tmem_ld16(tmem + lane_base + ti * N + c0, v);
-      float w[16];
+      float g[4][4];   // g[m][k]: component k (Re_i, Im_i, Re_i+1, Im_i+1) of column 4·qp + m
 #pragma unroll
-      for (int j = 0; j < 16; ++j) w[j] = __shfl_xor_sync(0xffffffffu, v[j], 1);
-      // even lane: ops c0 .. c0+7 with (re, im) = (v, w); odd lane: ops c0+8 .. c0+15 with (w, v)
+      for (int r = 0; r < 4; ++r) {
+        const int sidx = (qp - r) & 3;   // this lane sends column block sidx to lane (qp - r) & 3
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const float send = sidx == 0 ? v[m] : (sidx == 1 ? v[4 + m] : (sidx == 2 ? v[8 + m] : v[12 + m]));
+          const float recv = __shfl_sync(0xffffffffu, send, qbase + ((qp + r) & 3));
+          const int k = (qp + r) & 3;
+          g[m][0] = k == 0 ? recv : g[m][0];
+          g[m][1] = k == 1 ? recv : g[m][1];
+          g[m][2] = k == 2 ? recv : g[m][2];
+          g[m][3] = k == 3 ? recv : g[m][3];
+        }
+      }
       if (out_i < t.R) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int op = c0 + j + (even ? 0 : 8);
+        for (int m = 0; m < 4; ++m) {
+          const int op = c0 + 4 * qp + m;
           if (op < t.op_count) {
-            const float re = even ? v[j] : w[j + 8], im = even ? w[j] : v[j + 8];
-            atomicAdd(dst + doff[op] + out_i, make_float2(re, im));
+            float4* d4 = reinterpret_cast<float4*>(dst + doff[op] + out_i);
+            atomicAdd(d4, make_float4(g[m][0], g[m][1], g[m][2], g[m][3]));
           }
         }
       }

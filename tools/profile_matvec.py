@@ -19,10 +19,11 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--tc", type=int, default=2, help="tcgen05 translations: 0 off, 1 all eligible, 2 auto")
     a = ap.parse_args()
     c = CONFIGS[a.config]
     V, F = config_mesh(a.config)
-    f = FDA(V, F, c.k, c.alpha, c.eps, max_leaf=c.max_leaf)
+    f = FDA(V, F, c.k, c.alpha, c.eps, max_leaf=c.max_leaf, tensor_cores=a.tc)
     x = torch.from_numpy(random_density(len(F), c.x_seed).astype(np.complex64)).cuda()
     y = torch.empty_like(x)
     for _ in range(a.warmup + a.steps):
