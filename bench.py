@@ -125,6 +125,16 @@ def _stage_work(f, N):
     return work
 
 
+def _config(c, N, ws, args):
+    """The workload description shared by both arms (the same matvec)."""
+    return {"workload": f"config {c.cfg}: {c.name}, eps={c.eps}, leaf {c.max_leaf}, plane wave "
+                        f"{[float(v) for v in np.round(c.direction, 4)]}",
+            "N": N, "k": c.k, "alpha": "i/k", "eps": c.eps, "l2_flush": "256 MB write between steps",
+            "tensor_cores": args.tensor_cores, "m2l_lowrank": bool(args.m2l_lowrank),
+            "parallelism": (f"octree-sharded x{ws} (partial upward pass, NCCL exchange of outgoing states, "
+                            f"all-reduce of y)") if ws > 1 else "single GPU"}
+
+
 def _traffic(stage):
     """DRAM bytes (read + write) of one matvec's launches of `stage` from the
     committed ncu summary, or None when the stage's kernels are not uniquely named."""
@@ -253,11 +263,7 @@ def run_fda(args):
             "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "c64", "data": "synthetic",
-            "config": {"workload": f"config {c.cfg}: {c.name}, eps={c.eps}, leaf {c.max_leaf}, plane wave "
-                                   f"{list(np.round(c.direction, 4))}",
-                       "N": N, "k": c.k, "alpha": "i/k", "eps": c.eps, "l2_flush": "256 MB write between steps",
-                       "tensor_cores": args.tensor_cores, "m2l_lowrank": bool(args.m2l_lowrank),
-                       "parallelism": f"octree-sharded x{ws} (NCCL all-reduce of y)" if ws > 1 else "single GPU"},
+            "config": _config(c, N, ws, args),
             "matvecs_per_s": round(1e3 / ms, 2),
             "roofline": roof,
             "stages": stages,
@@ -329,7 +335,7 @@ def run_reference(args):
     return {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": "ms", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v, 2), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"config {c.cfg}: {c.name}", "N": N, "k": c.k, "eps": c.eps},
+            "config": _config(c, N, ws, args),
             "cpu_baseline": {"value": round(v, 2), "unit": "ms", "cores": fast.num_threads(), "kind": "oracle",
                              "sample": f"{args.ref_rows} seeded rows per step of the N={N} dense fp64 matvec, "
                                        f"scaled by N/rows"},

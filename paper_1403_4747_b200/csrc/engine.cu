@@ -258,7 +258,7 @@ static int64_t tc_matrix(Context* ctx, Dev* d, int64_t m) {
 // that pads the group least.  Stages with fewer CTAs than ~4 waves are split
 // along K (cols) so that small, latency-bound stages still fill the GPU.
 static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops, bool atomic, XStage& st,
-                               bool tc_ok = true) {
+                               bool tc_ok = true, bool force_tc = false) {
   const Plan& p = ctx->plan;
   st.atomic = atomic;
   if (ops.empty()) return FDA_OK;
@@ -270,7 +270,7 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   std::vector<int64_t> so, dof;
   std::vector<XTask> tasks[XV];
   bool tc = d->use_tc && atomic && tc_ok;
-  if (tc && ctx->p.opt.tensor_cores == 2) {   // auto: large, well-shared stages only
+  if (tc && ctx->p.opt.tensor_cores == 2 && !force_tc) {   // auto: large, well-shared stages only
     double flops = 0;
     std::unordered_map<int64_t, int> nm;
     for (const XOp& o : ops) {
@@ -609,11 +609,27 @@ fda_status engine_create(Context* ctx) {
   {
     // §4.2 factored ops: r ≤ 64 → fused kernel; r > 64 → tmp = V̂ src (atomic into a zeroed tmp
     // region, so small stages can be split along K) then in += Û tmp
+    // Levels whose factored ops are large, well-shared contractions go to the two
+    // stages instead, on the tensor cores (opt.tensor_cores; same rule as build_xstage).
     std::vector<std::vector<XOp>> a(nlev), b(nlev);
     std::vector<std::vector<LrOp>> fused(nlev);
+    std::vector<char> lr_tc(nlev, 0);
+    if (d->use_tc) {
+      std::vector<double> fl(nlev, 0.0);
+      std::vector<int64_t> nops(nlev, 0);
+      std::vector<std::unordered_map<int64_t, int>> nm(nlev);
+      for (const LrOp& o : p.m2l_lr) {
+        fl[o.level] += 16.0 * p.mats[o.matV].rows * p.mats[o.matV].cols;
+        ++nops[o.level];
+        nm[o.level][o.matV] = 1;
+      }
+      for (int l = 0; l < nlev; ++l)
+        lr_tc[l] = nops[l] > 0 && (ctx->p.opt.tensor_cores == 1 ||
+                                   (fl[l] >= 1e9 && (double)nops[l] >= 64.0 * (double)nm[l].size()));
+    }
     int64_t tmp_off = 0;
     for (const LrOp& o : p.m2l_lr) {
-      if (p.mats[o.matV].rows <= LR_MAX_R) {
+      if (p.mats[o.matV].rows <= LR_MAX_R && !lr_tc[o.level]) {
         fused[o.level].push_back(o);
         continue;
       }
@@ -665,8 +681,8 @@ fda_status engine_create(Context* ctx) {
         UP(&L.lr_src, ls.data(), ls.size());
         UP(&L.lr_dst, ld.data(), ld.size());
       }
-      if ((s = build_xstage(ctx, d, a[l], true, L.a)) != FDA_OK) return s;
-      if ((s = build_xstage(ctx, d, b[l], true, L.b, /*tc_ok=*/false)) != FDA_OK) return s;
+      if ((s = build_xstage(ctx, d, a[l], true, L.a, true, lr_tc[l] != 0)) != FDA_OK) return s;
+      if ((s = build_xstage(ctx, d, b[l], true, L.b, true, lr_tc[l] != 0)) != FDA_OK) return s;
     }
   }
   if (d->use_tc) {

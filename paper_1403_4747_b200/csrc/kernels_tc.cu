@@ -22,8 +22,9 @@
 // one thread issues the MMAs of chunk c (tcgen05.mma.cta_group::1.kind::tf32,
 // M = 128, N ∈ {128, 256}, K = 8) into TMEM accumulators (one 128 × N block
 // per row tile); tcgen05.commit on an mbarrier releases the stage.  Epilogue:
-// tcgen05.ld of each accumulator block, Re/Im lanes paired by shuffle, vector
-// atomics into the destination states (several tasks may share a destination).
+// tcgen05.ld of each accumulator block into shared memory (op-major), then
+// coalesced 16-byte vector atomics into the destination states (several tasks
+// may share a destination).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -249,46 +250,32 @@ __global__ void __launch_bounds__(128, 1) k_xlate_tc(const TcTask* __restrict__ 
   mbar_wait(&mbar_m[(nk - 1) % STAGES], ((nk - 1) / STAGES) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
 
-  // epilogue: warp w holds accumulator rows 32w..32w+31 of each tile; rows 4q..4q+3 of a
-  // lane quad are (Re, Im) of outputs i, i+1 (i even).  A quad transpose (4 rounds of
-  // shuffles) gives lane p of the quad all four values of columns 4p..4p+3, added with
-  // one 16-byte vector atomic per column (states are 16-byte aligned and padded to an
-  // even length, so the pair (i, i+1 = R) writes a zero into the padding slot).
+  // epilogue, per row tile: TMEM → shared memory column-major (column = op; rows 2i, 2i+1 =
+  // Re, Im of output i, so an op's outputs are contiguous float2), then each warp adds whole
+  // columns to the destination states with coalesced 16-byte vector atomics (2 outputs per
+  // lane; states are 16-byte aligned and padded to an even length, so the pair (i, i+1 = R)
+  // adds a zero into the padding slot).  The pipeline buffers are free here.
   const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-  const int qp = lane & 3, qbase = lane & ~3;
+  float* sE = sbase;                         // [N][128] floats
 #pragma unroll 1
   for (int ti = 0; ti < TILES; ++ti) {
-    const int out_i = (128 * ti + 32 * warp + qbase) >> 1;   // even
 #pragma unroll 1
     for (int c0 = 0; c0 < N; c0 += 16) {
       float v[16];
       tmem_ld16(tmem + lane_base + ti * N + c0, v);
-      float g[4][4];   // g[m][k]: component k (Re_i, Im_i, Re_i+1, Im_i+1) of column 4·qp + m
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int sidx = (qp - r) & 3;   // this lane sends column block sidx to lane (qp - r) & 3
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const float send = sidx == 0 ? v[m] : (sidx == 1 ? v[4 + m] : (sidx == 2 ? v[8 + m] : v[12 + m]));
-          const float recv = __shfl_sync(0xffffffffu, send, qbase + ((qp + r) & 3));
-          const int k = (qp + r) & 3;
-          g[m][0] = k == 0 ? recv : g[m][0];
-          g[m][1] = k == 1 ? recv : g[m][1];
-          g[m][2] = k == 2 ? recv : g[m][2];
-          g[m][3] = k == 3 ? recv : g[m][3];
-        }
-      }
-      if (out_i < t.R) {
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int op = c0 + 4 * qp + m;
-          if (op < t.op_count) {
-            float4* d4 = reinterpret_cast<float4*>(dst + doff[op] + out_i);
-            atomicAdd(d4, make_float4(g[m][0], g[m][1], g[m][2], g[m][3]));
-          }
-        }
+      for (int j = 0; j < 16; ++j) sE[(c0 + j) * 128 + 32 * warp + lane] = v[j];
+    }
+    __syncthreads();
+    const int i = 64 * ti + 2 * lane;        // this lane's first output of the tile
+#pragma unroll 4
+    for (int op = warp; op < N; op += 4) {
+      if (op < t.op_count && i < t.R) {
+        const float4 q = reinterpret_cast<const float4*>(sE + op * 128)[lane];
+        atomicAdd(reinterpret_cast<float4*>(dst + doff[op] + i), q);
       }
     }
+    __syncthreads();
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
