@@ -609,8 +609,9 @@ fda_status engine_create(Context* ctx) {
   {
     // §4.2 factored ops: r ≤ 64 → fused kernel; r > 64 → tmp = V̂ src (atomic into a zeroed tmp
     // region, so small stages can be split along K) then in += Û tmp
-    // Levels whose factored ops are large, well-shared contractions go to the two
-    // stages instead, on the tensor cores (opt.tensor_cores; same rule as build_xstage).
+    // With opt.tensor_cores = 1 the factored ops go to the two stages instead, on the
+    // tensor cores (V̂ then Û); the auto mode keeps the fused CUDA-core kernel, which is
+    // faster for these thin factors (config 5: 37 ms vs 49 ms).
     std::vector<std::vector<XOp>> a(nlev), b(nlev);
     std::vector<std::vector<LrOp>> fused(nlev);
     std::vector<char> lr_tc(nlev, 0);
@@ -624,8 +625,8 @@ fda_status engine_create(Context* ctx) {
         nm[o.level][o.matV] = 1;
       }
       for (int l = 0; l < nlev; ++l)
-        lr_tc[l] = nops[l] > 0 && (ctx->p.opt.tensor_cores == 1 ||
-                                   (fl[l] >= 1e9 && (double)nops[l] >= 64.0 * (double)nm[l].size()));
+        lr_tc[l] = nops[l] > 0 && ctx->p.opt.tensor_cores == 1;   // auto: the fused CUDA-core kernel
+                                                                   // measured faster (config 3/5)
     }
     int64_t tmp_off = 0;
     for (const LrOp& o : p.m2l_lr) {
