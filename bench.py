@@ -9,9 +9,10 @@ scatter) over device-resident inputs of the config-2
 workload (BASELINE configs[1]: icosphere s=6, N = 81,920, kD = 50, ε = 1e-4,
 leaf 64).  GMRES (row a9) and the build (row a0) are timed once and reported
 under "solve" and "build_s".  Under torchrun (N > 1) the operator is sharded
-over the ranks (leaves split by work, upward pass replicated, one NCCL
-all-reduce of y per matvec — DESIGN.md §7): strong scaling of one matvec, the
-time is the max over ranks.
+over the ranks (leaves split by work; each rank's upward pass covers its own
+elements, one grouped ncclSend/ncclRecv exchanges the partial outgoing states
+other ranks' interaction lists need, one all-reduce of y — DESIGN.md §7):
+strong scaling of one matvec, the time is the max over ranks.
 """
 from __future__ import annotations
 
@@ -165,7 +166,7 @@ def run_fda(args):
     N = len(F)
     t0 = time.perf_counter()
     if ws > 1:
-        # sharded operator: one NCCL all-reduce of y per matvec
+        # sharded operator: NCCL exchange of partial outgoing states + all-reduce of y
         threads = max(1, (os.cpu_count() or ws) // ws)
         f = FDA(V, F, c.k, c.alpha, c.eps, device=local, max_leaf=c.max_leaf, rank=rank, nranks=ws,
                 build_threads=threads, tensor_cores=args.tensor_cores, m2l_lowrank=args.m2l_lowrank)

@@ -144,12 +144,13 @@ struct Dev {
   // (fused kernel) and with r > 32 (two stages through tmp)
   struct M2LLevel {
     XStage dense, a, b;
-    LrTask* lr_tasks[3] = {};        // fused §4.2 tasks per phase-1 row class (m2l_lr_class)
-    int n_lr[3] = {};
+    LrTask* lr_tasks[LR_NCLS] = {};  // fused §4.2 tasks per phase-1 row class (m2l_lr_class)
+    int n_lr[LR_NCLS] = {};
     int64_t* lr_src = nullptr;
     int64_t* lr_dst = nullptr;
     bool any() const {
-      int n = n_lr[0] + n_lr[1] + n_lr[2];
+      int n = 0;
+      for (int c = 0; c < LR_NCLS; ++c) n += n_lr[c];
       for (int v = 0; v < TC_NV; ++v) n += dense.n_tc[v] + a.n_tc[v] + b.n_tc[v];
       for (int v = 0; v < XV; ++v) n += dense.ntask[v] + a.ntask[v] + b.ntask[v];
       return n > 0;
@@ -270,7 +271,7 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   std::vector<int64_t> so, dof;
   std::vector<XTask> tasks[XV];
   bool tc = d->use_tc && atomic && tc_ok;
-  if (tc && ctx->p.opt.tensor_cores == 2 && !force_tc) {   // auto: large, well-shared stages only
+  if (tc && ctx->p.opt.tensor_cores >= 2 && !force_tc) {   // auto: large, well-shared stages only
     double flops = 0;
     std::unordered_map<int64_t, int> nm;
     for (const XOp& o : ops) {
@@ -288,7 +289,10 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
       const int R = p.mats[m].rows, C = p.mats[m].cols, ntile = tc_tiles(R);
       if (ntile > 3) { ctx->err = "matrix too tall for the tensor-core path (rows > 192)"; return FDA_E_INTERNAL; }
       const int64_t nops = (int64_t)(j - i);
-      const int v = tc_variant(nops >= 160 && ntile <= 2 ? 256 : 128, ntile), nmax = tc_variant_ops(v);
+      // 2-stage variants with several CTAs per SM (default; measured faster on configs 3-5 than the
+      // 3-stage one-CTA-per-SM variants, which opt.tensor_cores = 3 selects for A/B runs)
+      const bool multi = ctx->p.opt.tensor_cores != 3;
+      const int v = tc_variant(!multi && nops >= 160 && ntile <= 2 ? 256 : 128, ntile, multi), nmax = tc_variant_ops(v);
       const int64_t off = tc_matrix(ctx, d, m);
       const int32_t base = (int32_t)so.size();
       for (size_t q = i; q < j; ++q) {
@@ -646,7 +650,7 @@ fda_status engine_create(Context* ctx) {
       std::stable_sort(F.begin(), F.end(), [](const LrOp& x, const LrOp& y) {
         return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
       });
-      std::vector<LrTask> lt[3];
+      std::vector<LrTask> lt[LR_NCLS];
       std::vector<int64_t> ls, ld;
       for (size_t i = 0; i < F.size();) {
         size_t j = i;
@@ -668,11 +672,11 @@ fda_status engine_create(Context* ctx) {
       }
       // longest CTAs first (phase-1 rows 16 / 32 / 64, phase-2 row tiles of 32)
       auto cost = [](const LrTask& t) {
-        const int r1 = 16 << m2l_lr_class(t.r);
+        const int r1 = m2l_lr_rows(m2l_lr_class(t.r));
         return (int64_t)(r1 * t.T + ((t.T + 31) / 32) * 32 * t.r) * t.op_count;
       };
       Dev::M2LLevel& L = d->m2lv[l];
-      for (int c = 0; c < 3; ++c) {
+      for (int c = 0; c < LR_NCLS; ++c) {
         std::stable_sort(lt[c].begin(), lt[c].end(),
                          [&](const LrTask& x, const LrTask& y) { return cost(x) > cost(y); });
         L.n_lr[c] = (int)lt[c].size();
@@ -726,7 +730,7 @@ fda_status engine_create(Context* ctx) {
   for (auto& st : d->l2l) cnt(st);
   for (auto& L : d->m2lv) {
     cnt(L.dense); cnt(L.a); cnt(L.b);
-    for (int c = 0; c < 3; ++c) nl += L.n_lr[c] > 0;
+    for (int c = 0; c < LR_NCLS; ++c) nl += L.n_lr[c] > 0;
   }
   ctx->launches_per_matvec = nl;
   CK(cudaStreamCreateWithFlags(&d->s_near, cudaStreamNonBlocking));
@@ -735,7 +739,7 @@ fda_status engine_create(Context* ctx) {
   d->ev_up.resize(nlev);
   d->ev_m2l.resize(nlev);
   for (auto& v : d->ev_m2l) {
-    v.resize(4);
+    v.resize(LR_NCLS + 1);
     for (auto& e : v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   for (auto& e : d->ev_up) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -834,7 +838,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   const int nlev = (int)d->m2m.size();
   auto m2l_level = [&](int l, cudaStream_t st) {
     const Dev::M2LLevel& L = d->m2lv[l];
-    for (int c = 2; c >= 0; --c)
+    for (int c = LR_NCLS - 1; c >= 0; --c)
       launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st);
     launch_stage(L.dense, d->pool, d->outb, d->inb, st);
     launch_stage(L.a, d->pool, d->outb, d->tmpb, st);
@@ -872,7 +876,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
         return FDA_OK;
       };
       fda_status bs;
-      for (int c = 2; c >= 0; --c)
+      for (int c = LR_NCLS - 1; c >= 0; --c)
         if (L.n_lr[c] &&
             (bs = branch([&](cudaStream_t sm) {
                launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, sm);
@@ -949,7 +953,7 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
   for (int l = nlev - 1; l >= 0; --l) {   // M2L branches of every level, concurrent
     const Dev::M2LLevel& L = d->m2lv[l];
     if (!L.any()) continue;
-    for (int c = 2; c >= -1; --c) {
+    for (int c = LR_NCLS - 1; c >= -1; --c) {
       if (c >= 0 && !L.n_lr[c]) continue;
       cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];
       CK(cudaStreamWaitEvent(sm, d->ev_up[0], 0));

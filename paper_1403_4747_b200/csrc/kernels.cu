@@ -123,7 +123,7 @@ __device__ __forceinline__ void lhs_eval(float3 X, float3 nx, float4 Y, float xn
   const float b = (Y.w - xny) * iq;                                  // ∂r/∂n_y = -(d·n_y)/|d|
   const float ab = a * b;
   const float g = fmaf(3.0f, ab, cn);               // 3ab + c
-  const float u1 = fmaf(3.0f - q2, ab, cn);         // (3 - q²) ab + c
+  const float u1 = fmaf(-q2, ab, g);                // (3 - q²) ab + c = g - q² ab
   float P, Q;
   if (PURE_IMAG) {
     P = fmaf(kp.ak_im, g, -b);
@@ -528,8 +528,8 @@ void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const
 // wavefront per load, ≤ RT1/2 + OT1/2 wavefronts per 4·RT1·OT1 FFMA.
 template <int R1, int O>
 struct LrCfg {
-  static constexpr int RT1 = R1 == 64 ? 8 : 4;
-  static constexpr int NR1 = R1 / RT1;        // 4, 8, 8
+  static constexpr int RT1 = R1 == 64 ? 8 : (R1 == 24 ? 6 : 4);
+  static constexpr int NR1 = R1 / RT1;        // 4, 4, 8, 8 for R1 = 16, 24, 32, 64
   static constexpr int NO1 = 128 / NR1;       // 32, 16, 16
   static constexpr int OT1 = O / NO1;
   static constexpr int SO = O + 2;            // padded sS row (conflict-free cp.async writes, 16-B aligned rows)
@@ -710,11 +710,13 @@ void launch_m2l_lr(int cls, int ntask, const LrTask* tasks, const int64_t* src_o
   if (ntask <= 0) return;
   switch (cls) {
     case 0: k_m2l_lr<16, 64><<<ntask, 128, LrCfg<16, 64>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
-    case 1: k_m2l_lr<32, 64><<<ntask, 128, LrCfg<32, 64>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+    case 1: k_m2l_lr<24, 64><<<ntask, 128, LrCfg<24, 64>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
+    case 2: k_m2l_lr<32, 64><<<ntask, 128, LrCfg<32, 64>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
     default: k_m2l_lr<64, 64><<<ntask, 128, LrCfg<64, 64>::SMEM, s>>>(tasks, src_off, dst_off, pool, src, dst); break;
   }
 }
-int m2l_lr_class(int r) { return r <= 16 ? 0 : (r <= 32 ? 1 : 2); }
+int m2l_lr_class(int r) { return r <= 16 ? 0 : (r <= 24 ? 1 : (r <= 32 ? 2 : 3)); }
+int m2l_lr_rows(int cls) { return cls == 0 ? 16 : (cls == 1 ? 24 : (cls == 2 ? 32 : 64)); }
 int m2l_lr_ops(int) { return 64; }
 cudaError_t m2l_lr_prepare() {
   return cudaFuncSetAttribute(k_m2l_lr<64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, LrCfg<64, 64>::SMEM);

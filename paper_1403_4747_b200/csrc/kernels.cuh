@@ -59,7 +59,7 @@ struct LrTask {
 // ntile = ⌈2R/128⌉ ≤ 3 tiles of the interleaved real matrix) × ≤ 128 or 256 ops sharing it.
 // The A operand is pre-laid-out per (tile, TC_KC-float K chunk) as [hi | lo] 128 × TC_KC tiles.
 constexpr int TC_KC = 16;   // floats of K per pipeline stage
-constexpr int TC_NV = 5;    // kernel variants (N, tiles): (128,1) (128,2) (128,3) (256,1) (256,2)
+constexpr int TC_NV = 7;    // kernel variants (N, tiles, stages, CTAs/SM), see kernels_tc.cu
 struct TcTask {
   int64_t a_off;      // float offset of the matrix's pre-laid-out A in the tensor-core pool
   int32_t R, C;       // matrix shape (complex)
@@ -68,7 +68,7 @@ struct TcTask {
   int32_t op_begin, op_count;
   int32_t kc0, kc1;   // this task's K chunks (split-K: partial products accumulate atomically)
 };
-int tc_variant(int n, int tiles);
+int tc_variant(int n, int tiles, bool multi);   // multi: the 2-stage, several-CTAs-per-SM variants
 int tc_variant_ops(int v);
 
 // leaf-level ops (S2M / L2T)
@@ -97,10 +97,12 @@ void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const floa
 void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s);
 void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const int64_t* src_off,
                   const int64_t* dst_off, const float2* pool, const float2* src, float2* dst, cudaStream_t s);
-// fused §4.2 M2L for r ≤ 64; cls = m2l_lr_class(r) (phase-1 rows 16 / 32 / 64)
+// fused §4.2 M2L for r ≤ 64; cls = m2l_lr_class(r) (phase-1 rows m2l_lr_rows(cls) = 16 / 24 / 32 / 64)
+constexpr int LR_NCLS = 4;
 void launch_m2l_lr(int cls, int ntask, const LrTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                    const float2* pool, const float2* src, float2* dst, cudaStream_t s);
 int m2l_lr_class(int r);
+int m2l_lr_rows(int cls);
 int m2l_lr_ops(int cls);   // ops per CTA of a class
 constexpr int LR_MAX_R = 64;
 cudaError_t m2l_lr_prepare();

@@ -34,7 +34,6 @@ namespace fda {
 
 namespace {
 constexpr int KC = TC_KC;        // floats of K per stage (= 8 complex columns)
-constexpr int STAGES = 3;
 constexpr int A_TILE = 128 * KC;  // floats per (row tile, chunk, hi|lo)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -114,22 +113,23 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 __host__ __device__ constexpr uint32_t tmem_cols(int n) { return n <= 32 ? 32 : (n <= 64 ? 64 : (n <= 128 ? 128 : (n <= 256 ? 256 : 512))); }
 }  // namespace
 
-template <int N, int TILES>
+template <int N, int TILES, int STAGES>
 struct TcCfg {
   static constexpr int A_FL = TILES * 2 * A_TILE;   // A floats per stage
   static constexpr int B_FL = 2 * N * KC;          // B floats per stage (hi, lo)
   static constexpr int STAGE_FL = A_FL + B_FL;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_FL * 4 + 1024;
+  static constexpr int SM_FL = STAGES * STAGE_FL > N * 128 ? STAGES * STAGE_FL : N * 128;   // + epilogue
+  static constexpr size_t SMEM = (size_t)SM_FL * 4 + 1024;
   static_assert(TILES * N <= 512, "TMEM columns");
 };
 
-template <int N, int TILES>
-__global__ void __launch_bounds__(128, 1) k_xlate_tc(const TcTask* __restrict__ tasks,
+template <int N, int TILES, int STAGES, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_xlate_tc(const TcTask* __restrict__ tasks,
                                                      const int64_t* __restrict__ src_off,
                                                      const int64_t* __restrict__ dst_off,
                                                      const float* __restrict__ tcpool, const float2* __restrict__ src,
                                                      float2* __restrict__ dst) {
-  using Cfg = TcCfg<N, TILES>;
+  using Cfg = TcCfg<N, TILES, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   float* sbase = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t mbar_a[STAGES], mbar_m[STAGES];
@@ -284,39 +284,43 @@ __global__ void __launch_bounds__(128, 1) k_xlate_tc(const TcTask* __restrict__ 
 }
 
 namespace {
-template <int N, int TILES>
+template <int N, int TILES, int S, int MB>
 cudaError_t tc_attr() {
-  return cudaFuncSetAttribute(k_xlate_tc<N, TILES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)TcCfg<N, TILES>::SMEM);
+  return cudaFuncSetAttribute(k_xlate_tc<N, TILES, S, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)TcCfg<N, TILES, S>::SMEM);
 }
 }  // namespace
 
+// variants (N, tiles, stages, CTAs per SM): 0 (128,1,3,1) 1 (128,2,3,1) 2 (128,3,3,1) 3 (256,1,3,1)
+// 4 (256,2,3,1); 5 (128,1,2,3) 6 (128,2,2,2) — the latter two trade pipeline depth for CTAs per SM
+#define TC_VARIANTS(X) X(0, 128, 1, 3, 1) X(1, 128, 2, 3, 1) X(2, 128, 3, 3, 1) X(3, 256, 1, 3, 1) \
+  X(4, 256, 2, 3, 1) X(5, 128, 1, 2, 3) X(6, 128, 2, 2, 2)
+
 cudaError_t tc_prepare() {
-  cudaError_t e;
-  if ((e = tc_attr<128, 1>()) != cudaSuccess) return e;
-  if ((e = tc_attr<128, 2>()) != cudaSuccess) return e;
-  if ((e = tc_attr<128, 3>()) != cudaSuccess) return e;
-  if ((e = tc_attr<256, 1>()) != cudaSuccess) return e;
-  return tc_attr<256, 2>();
+  cudaError_t e = cudaSuccess;
+#define TC_ATTR(V, NN, TT, SS, MB) \
+  if (e == cudaSuccess) e = tc_attr<NN, TT, SS, MB>();
+  TC_VARIANTS(TC_ATTR)
+#undef TC_ATTR
+  return e;
 }
 
-// variant = tc_variant(N, tiles): 0..4 = (128,1) (128,2) (128,3) (256,1) (256,2)
-int tc_variant(int n, int tiles) { return n == 256 ? 2 + tiles : tiles - 1; }
-int tc_variant_ops(int v) { return v >= 3 ? 256 : 128; }
+int tc_variant(int n, int tiles, bool multi) {
+  if (multi && n == 128 && tiles <= 2) return tiles == 1 ? 5 : 6;
+  return n == 256 ? 2 + tiles : tiles - 1;
+}
+int tc_variant_ops(int v) { return (v == 3 || v == 4) ? 256 : 128; }
 
 void launch_xlate_tc(int variant, int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                      const float* tcpool, const float2* src, float2* dst, cudaStream_t s) {
   if (ntask <= 0) return;
-#define TCL(NN, TT) \
-  k_xlate_tc<NN, TT><<<ntask, 128, TcCfg<NN, TT>::SMEM, s>>>(tasks, src_off, dst_off, tcpool, src, dst)
-  switch (variant) {
-    case 0: TCL(128, 1); break;
-    case 1: TCL(128, 2); break;
-    case 2: TCL(128, 3); break;
-    case 3: TCL(256, 1); break;
-    default: TCL(256, 2); break;
-  }
-#undef TCL
+#define TC_CASE(V, NN, TT, SS, MB)                                                                           \
+  case V:                                                                                                   \
+    k_xlate_tc<NN, TT, SS, MB><<<ntask, 128, TcCfg<NN, TT, SS>::SMEM, s>>>(tasks, src_off, dst_off, tcpool, src, \
+                                                                          dst);                              \
+    break;
+  switch (variant) { TC_VARIANTS(TC_CASE) }
+#undef TC_CASE
 }
 
 }  // namespace fda

@@ -302,15 +302,15 @@ def test_sharded_exchange_one_gpu(lib, R):
     assert _rel(bad, full) > 1e-3
 
 
-@pytest.mark.parametrize("lowrank", [1, 0])
-def test_tensor_core_translations(lib, lowrank):
+@pytest.mark.parametrize("lowrank,tc", [(1, 1), (0, 1), (0, 3)])
+def test_tensor_core_translations(lib, lowrank, tc):
     """tcgen05 3xTF32 translation path (opt.tensor_cores): same operator as the
     CUDA-core path to fp32 rounding, and within the gate vs the oracle."""
     V, F = icosphere(4, 0.5)
     k = 40.0
     x = random_density(len(F), 5)
     y0 = lib(V, F, k, 1j / k, 1e-4, max_leaf=16, m2l_lowrank=lowrank).matvec(x)
-    y1 = lib(V, F, k, 1j / k, 1e-4, max_leaf=16, m2l_lowrank=lowrank, tensor_cores=1).matvec(x)
+    y1 = lib(V, F, k, 1j / k, 1e-4, max_leaf=16, m2l_lowrank=lowrank, tensor_cores=tc).matvec(x)
     assert _rel(y1, y0) < 1e-5
     el = O.element_geometry(V, F)
     yo = fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k)
