@@ -667,12 +667,15 @@ fda_status engine_create(Context* ctx) {
           ls.push_back(p.out_offset[F[q].src]);
           ld.push_back(p.in_offset[F[q].dst]);
         }
-        lt[m2l_lr_class(tk.r)].push_back(tk);
+        // the R1 = 24 class only pays on large levels (fewer, fuller launches otherwise)
+        int cls = m2l_lr_class(tk.r);
+        if (cls == 1 && F.size() < 200000) cls = 2;
+        lt[cls].push_back(tk);
         i = j;
       }
       // longest CTAs first (phase-1 rows 16 / 32 / 64, phase-2 row tiles of 32)
       auto cost = [](const LrTask& t) {
-        const int r1 = m2l_lr_rows(m2l_lr_class(t.r));
+        const int r1 = m2l_lr_rows(m2l_lr_class(t.r));   // (the LPT key; class 1 → 2 merges change little)
         return (int64_t)(r1 * t.T + ((t.T + 31) / 32) * 32 * t.r) * t.op_count;
       };
       Dev::M2LLevel& L = d->m2lv[l];
@@ -905,20 +908,28 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
 // exchange of partial outgoing states → downward pass for the owned targets.
 // Eager launches; the near field runs on its own stream across the exchange.
 static fda_status run_sharded_up(Context* ctx, Dev* d, cudaStream_t s, int kind) {
+  // profiling mode serialises the near field on the main stream (stage times as in run_core)
+  const bool prof = ctx->profiling;
+  cudaStream_t sn = prof ? s : d->s_near;
   CK(cudaEventRecord(d->ev_fork, s));
-  CK(cudaStreamWaitEvent(d->s_near, d->ev_fork, 0));
+  CK(cudaStreamWaitEvent(sn, d->ev_fork, 0));
+  if (prof) CK(cudaEventRecord(d->ev_n0, sn));
   launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
               kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
-              kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, d->s_near);
-  CK(cudaEventRecord(d->ev_join, d->s_near));
+              kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, sn);
+  if (prof) CK(cudaEventRecord(d->ev_n1, sn));
+  CK(cudaEventRecord(d->ev_join, sn));
+  if (prof) CK(cudaEventRecord(d->ev[1], s));
   if (d->out_size) CK(cudaMemsetAsync(d->outb, 0, sizeof(float2) * d->out_size, s));
   if (d->in_size) CK(cudaMemsetAsync(d->inb, 0, sizeof(float2) * d->in_size, s));
   if (d->tmp_size) CK(cudaMemsetAsync(d->tmpb, 0, sizeof(float2) * d->tmp_size, s));
   if (kind) launch_s2m(d->n_s2m_rhs, d->s2m_rhs, d->pool, d->x_tree, d->outb, d->max_T, s);
   else launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s);
+  if (prof) CK(cudaEventRecord(d->ev[2], s));
   const int nlev = (int)d->m2m.size();
   for (int l = nlev - 1; l >= 0; --l) launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);   // partials
   launch_pack(d->outb, d->xs_idx, d->sendb, d->n_send, s);
+  if (prof) CK(cudaEventRecord(d->ev[3], s));
   CK(cudaGetLastError());
   return FDA_OK;
 }
@@ -967,11 +978,19 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
       CK(cudaEventRecord(d->ev_m2l[l][nbr[l]++], sm));
     }
   }
+  const bool prof = ctx->profiling;
+  if (prof) {   // M2L stage = exchange unpack + every M2L branch
+    for (int l = 0; l < nlev; ++l)
+      for (int b = 0; b < nbr[l]; ++b) CK(cudaStreamWaitEvent(s, d->ev_m2l[l][b], 0));
+    CK(cudaEventRecord(d->ev[4], s));
+  }
   for (int l = 0; l < nlev; ++l) {
     for (int b = 0; b < nbr[l]; ++b) CK(cudaStreamWaitEvent(s, d->ev_m2l[l][b], 0));
     launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
   }
+  if (prof) CK(cudaEventRecord(d->ev[5], s));
   launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
+  if (prof) CK(cudaEventRecord(d->ev[6], s));
   CK(cudaStreamWaitEvent(s, d->ev_join, 0));
   CK(cudaGetLastError());
   return FDA_OK;
@@ -1017,7 +1036,7 @@ static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind, int phase
 // device-pointer matvec in caller order (float2 in, float2 out)
 static fda_status matvec_dev(Context* ctx, Dev* d, const float2* x, float2* y, cudaStream_t s, int kind = 0,
                              bool local = false, int phase = 0) {
-  const bool prof = ctx->profiling && d->nranks <= 1;
+  const bool prof = ctx->profiling && (d->nranks <= 1 || phase == 0);
   if (prof) CK(cudaEventRecord(d->ev[0], s));
   if (phase != FDA_PHASE_DOWN) launch_gather_f32(x, d->perm, d->x_tree, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[1], s));
@@ -1050,7 +1069,7 @@ fda_status engine_apply(Context* ctx, const void* x, void* y, int32_t flags, voi
   if (flags & FDA_DEVICE)
     return matvec_dev(ctx, d, static_cast<const float2*>(x), static_cast<float2*>(y), s, kind, local, phase);
   // host complex128 in/out
-  const bool prof = ctx->profiling && d->nranks <= 1;
+  const bool prof = ctx->profiling && (d->nranks <= 1 || phase == 0);
   CK(cudaMemcpyAsync(d->xh, x, sizeof(double2) * d->n, cudaMemcpyHostToDevice, s));
   if (prof) CK(cudaEventRecord(d->ev[0], s));
   launch_gather_f64(d->xh, d->perm, d->x_tree, d->n, s);

@@ -183,6 +183,29 @@ def test_point_source_rhs_and_solve(cfg1):
     assert info["converged"] and err <= SOLVE_TOL and ser < 3e-2
 
 
+def test_eps_sweep_and_leaf_size(cfg1):
+    """the FDA error against the dense operator falls
+    with ε (roughly ∝ ε) and changing max_leaf (a different tree, other lists and
+    operators) moves the result by O(ε) only."""
+    V, F, c, el, A, f = cfg1
+    x = random_density(len(F), 21)
+    yo = A @ x
+    errs = []
+    for eps in (1e-2, 1e-3, 1e-4, 1e-5):
+        errs.append(_rel(lib_matvec(V, F, c, eps, 64, x), yo))
+    print("eps sweep:", ["%.2e" % e for e in errs])
+    assert all(errs[i + 1] < 0.5 * errs[i] for i in range(2)) and errs[3] <= errs[2] * 1.05
+    assert errs[1] < 1e-2 and errs[2] < 1e-3
+    y32 = lib_matvec(V, F, c, 1e-4, 32, x)
+    y64 = lib_matvec(V, F, c, 1e-4, 64, x)
+    assert _rel(y32, y64) < 10 * 1e-4
+
+
+def lib_matvec(V, F, c, eps, max_leaf, x):
+    from paper_1403_4747_b200 import FDA
+    return FDA(V, F, c.k, c.alpha, eps, max_leaf=max_leaf).matvec(x)
+
+
 def test_stage_times(cfg1):
     V, F, c, el, A, f = cfg1
     f.set_profiling(True)

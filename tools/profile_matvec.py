@@ -29,7 +29,7 @@ def main():
     for _ in range(a.warmup + a.steps):
         f.matvec(x, y)
     torch.cuda.synchronize()
-    print("ok", f.stats()["n_m2l_pairs"])
+    print("ok", f.stats()["n_m2l_pairs"], "launches_per_matvec", int(f.table("launches")[0]))
 
 
 if __name__ == "__main__":
