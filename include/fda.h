@@ -87,7 +87,11 @@ typedef struct {
                             2 (default) stages of ≥ 1 GFLOP with ≥ 64 ops per matrix (CUDA
                             cores elsewhere), 3 as 2 with the deep-pipeline one-CTA-per-SM
                             kernel variants (A/B)                                           */
-  int32_t reserved[2];
+  int32_t hf_leaves;     /* 0 (default): HF cubes are always split, all leaves are LF (reading
+                            C9); 1: the count rule at every level, leaves may be HF, with
+                            directional S2M / L2T per used wedge (PAPER.md P:344-346,
+                            P:449-454)                                                     */
+  int32_t reserved[1];
 } fda_options;
 
 typedef struct {

@@ -136,8 +136,8 @@ struct Dev {
   float2* pool = nullptr;
   float2 *outb = nullptr, *inb = nullptr;
   int64_t out_size = 0, in_size = 0;
-  LeafTask *s2m = nullptr, *l2t = nullptr;
-  int n_s2m = 0, n_l2t = 0, max_T = 0;
+  LeafTask *s2m = nullptr, *l2t = nullptr, *l2t_add = nullptr;
+  int n_s2m = 0, n_l2t = 0, n_l2t_add = 0, max_T = 0;
   std::vector<XStage> m2m, l2l;
   // M2L per level (levels are independent of each other; level l needs only
   // the outgoing states of level l): dense ops, §4.2 factored ops with r ≤ 32
@@ -580,6 +580,24 @@ fda_status engine_create(Context* ctx) {
     }
     l2t.push_back(lt);
   }
+  // HF leaves (opt.hf_leaves): one task per directional state; their L2T tasks accumulate
+  std::vector<LeafTask> l2t_add;
+  auto leaf_task = [&](const LeafOp& o, bool in) {
+    const Box& B = t.boxes[t.leaves[o.leaf]];
+    const int T = t.levels[B.level].rank;
+    return LeafTask{p.mats[o.mat].offset, in ? p.in_offset[o.state] : p.out_offset[o.state], (int32_t)B.begin,
+                    (int32_t)(B.end - B.begin), T, 0};
+  };
+  for (const LeafOp& o : p.hf_s2m) {
+    s2m.push_back(leaf_task(o, false));
+    d->max_T = std::max(d->max_T, s2m.back().T);
+  }
+  for (const LeafOp& o : p.hf_s2m_rhs) s2m_rhs.push_back(leaf_task(o, false));
+  for (const LeafOp& o : p.hf_l2t) l2t_add.push_back(leaf_task(o, true));
+  for (const LeafTask& lt : s2m)
+    if (lt.T > 320) { ctx->err = "rank above 320"; return FDA_E_INTERNAL; }
+  d->n_l2t_add = (int)l2t_add.size();
+  if (d->n_l2t_add) UP(&d->l2t_add, l2t_add.data(), l2t_add.size());
   d->n_s2m = (int)s2m.size();
   d->n_l2t = (int)l2t.size();
   UP(&d->s2m, s2m.data(), s2m.size());
@@ -724,7 +742,7 @@ fda_status engine_create(Context* ctx) {
     d->use_graph = false;   // the NCCL exchange sits between the passes: eager launches
   }
   // kernels per matvec: gather, near, s2m, every non-empty translation launch, l2t, scatter
-  int64_t nl = 4 + (d->n_s2m > 0);  // gather, near, l2t, scatter (+ s2m)
+  int64_t nl = 4 + (d->n_s2m > 0) + (d->n_l2t_add > 0);  // gather, near, l2t, scatter (+ s2m, HF-leaf L2T)
   auto cnt = [&](const XStage& st) {
     for (int v = 0; v < TC_NV; ++v) nl += st.n_tc[v] > 0;
     for (int v = 0; v < XV; ++v) nl += st.ntask[v] > 0;
@@ -898,6 +916,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
     }
   }
   launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
+  launch_l2t(d->n_l2t_add, d->l2t_add, d->pool, d->inb, d->y_far, s, /*accumulate=*/true);
   if (prof) CK(cudaEventRecord(d->ev[6], s));
   CK(cudaStreamWaitEvent(s, d->ev_join, 0));
   CK(cudaGetLastError());
@@ -990,6 +1009,7 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
   }
   if (prof) CK(cudaEventRecord(d->ev[5], s));
   launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
+  launch_l2t(d->n_l2t_add, d->l2t_add, d->pool, d->inb, d->y_far, s, /*accumulate=*/true);
   if (prof) CK(cudaEventRecord(d->ev[6], s));
   CK(cudaStreamWaitEvent(s, d->ev_join, 0));
   CK(cudaGetLastError());

@@ -44,6 +44,7 @@ fda_status fda_options_default(fda_options* opt) {
   opt->rank = 0;
   opt->nranks = 1;
   opt->tensor_cores = 2;
+  opt->hf_leaves = 0;
   return FDA_OK;
 }
 
@@ -97,7 +98,7 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
   }
   if (o.max_leaf < 1 || o.max_leaf > 128 || o.p_eq < 2 || o.p_chk_lf < 2 || o.p_chk_hf < 2 || !(o.eq_scale > 0) ||
       !(o.chk_scale_lf > o.eq_scale) || !(o.tier1_rho >= 0) || !(o.tier2_rho >= o.tier1_rho) ||
-      o.tensor_cores < 0 || o.tensor_cores > 3) {
+      o.tensor_cores < 0 || o.tensor_cores > 3 || o.hf_leaves < 0 || o.hf_leaves > 1) {
     g_build_error = "invalid fda_options";
     delete ctx;
     return FDA_E_INVALID_ARG;
@@ -336,6 +337,12 @@ fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int6
   if (nm == "out_offset") return put(p.out_offset, dst, count, eb);
   if (nm == "in_offset") return put(p.in_offset, dst, count, eb);
   if (nm == "sizes") return put(std::vector<int64_t>{p.out_size, p.in_size}, dst, count, eb);
+  if (nm == "hf_s2m" || nm == "hf_s2m_rhs" || nm == "hf_l2t") {   // (leaf, state, matrix) triples
+    const auto& L = nm == "hf_s2m" ? p.hf_s2m : (nm == "hf_s2m_rhs" ? p.hf_s2m_rhs : p.hf_l2t);
+    std::vector<int64_t> v;
+    for (const auto& o : L) { v.push_back(o.leaf); v.push_back(o.state); v.push_back(o.mat); }
+    return put(v, dst, count, eb);
+  }
   if (nm == "xsend" || nm == "xrecv") {   // per peer: count, sorted out-state ids
     const auto& L = nm == "xsend" ? p.xsend : p.xrecv;
     std::vector<int64_t> v;

@@ -99,6 +99,13 @@ struct LrOp {
   int level;
 };
 
+// leaf-level op of an HF leaf (opt.hf_leaves): one directional state of the leaf
+struct LeafOp {
+  int64_t leaf;      // leaf index
+  int64_t state;     // out-state (S2M) or in-state (L2T) id
+  int64_t mat;       // S̃_{B,u} (T × n_B) or T̃_{B,w} (n_B × T)
+};
+
 struct MatInfo {
   int64_t offset;    // complex64 elements into the matrix pool
   int32_t rows, cols;
@@ -156,6 +163,8 @@ struct Plan {
   std::vector<int64_t> corr_ptr_rhs, corr_col_rhs;
   std::vector<cf> corr_val_rhs;
   std::vector<int64_t> leaf_S_rhs;   // per leaf: S̃ with G sources (RHS pass), -1 = none
+  // HF leaves (opt.hf_leaves): directional S2M / L2T, one op per used wedge
+  std::vector<LeafOp> hf_s2m, hf_s2m_rhs, hf_l2t;
   // matrices
   std::vector<MatInfo> mats;
   std::vector<MatSpec> specs;    // parallel to mats

@@ -332,6 +332,8 @@ __global__ void __launch_bounds__(LEAF_MAXR) k_s2m(const LeafTask* __restrict__ 
 }
 
 // L2T: y_B = T̃_B ℓ̃_B (n_B × T column-major)   (Eq. 12; compressed T̃)
+// ADD: accumulate (HF leaves have one task per incoming wedge); else overwrite.
+template <bool ADD>
 __global__ void __launch_bounds__(LEAF_NT) k_l2t(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
                                                  const float2* __restrict__ in, float2* __restrict__ y) {
   __shared__ float2 sl[LEAF_MAXR];
@@ -339,7 +341,8 @@ __global__ void __launch_bounds__(LEAF_NT) k_l2t(const LeafTask* __restrict__ ta
   const LeafTask t = tasks[blockIdx.x];
   const int nb = t.elem_count;
   if (t.mat_off < 0) {
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) y[t.elem_begin + i] = make_float2(0.f, 0.f);
+    if (!ADD)
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) y[t.elem_begin + i] = make_float2(0.f, 0.f);
     return;
   }
   for (int c = threadIdx.x; c < t.T; c += blockDim.x) sl[c] = in[t.state_off + c];
@@ -356,7 +359,8 @@ __global__ void __launch_bounds__(LEAF_NT) k_l2t(const LeafTask* __restrict__ ta
       const float2 v = red[q * nb + threadIdx.x];
       s.x += v.x; s.y += v.y;
     }
-    y[t.elem_begin + threadIdx.x] = s;
+    if (ADD) atomicAdd(y + t.elem_begin + threadIdx.x, s);
+    else y[t.elem_begin + threadIdx.x] = s;
   }
 }
 
@@ -367,9 +371,11 @@ void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const floa
   bd = bd < LEAF_NT ? LEAF_NT : (bd > LEAF_MAXR ? LEAF_MAXR : bd);
   k_s2m<<<ntask, bd, 0, s>>>(tasks, pool, x, out);
 }
-void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s) {
+void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s,
+                bool accumulate) {
   if (ntask <= 0) return;
-  k_l2t<<<ntask, LEAF_NT, 0, s>>>(tasks, pool, in, y);
+  if (accumulate) k_l2t<true><<<ntask, LEAF_NT, 0, s>>>(tasks, pool, in, y);
+  else k_l2t<false><<<ntask, LEAF_NT, 0, s>>>(tasks, pool, in, y);
 }
 
 // ------------------------------------------------------------------ translations (a3 M2M, a4 M2L, a5 L2L)

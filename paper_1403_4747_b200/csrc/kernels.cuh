@@ -94,7 +94,8 @@ void launch_near(int ntask, const NearTask* tasks, const int2* slots, const floa
                  bool alpha_pure_imag, int kind, cudaStream_t s);
 void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const float2* x, float2* out, int max_rows,
                 cudaStream_t s);
-void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s);
+void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s,
+                bool accumulate = false);
 void launch_xlate(int variant, bool atomic, int ntask, const XTask* tasks, const int64_t* src_off,
                   const int64_t* dst_off, const float2* pool, const float2* src, float2* dst, cudaStream_t s);
 // fused §4.2 M2L for r ≤ 64; cls = m2l_lr_class(r) (phase-1 rows m2l_lr_rows(cls) = 16 / 24 / 32 / 64)

@@ -232,9 +232,29 @@ void build_lists(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
   // ---- leaves: S2M / L2T
   plan.leaf_S.assign(nleaf, -1); plan.leaf_T.assign(nleaf, -1); plan.leaf_S_rhs.assign(nleaf, -1);
   plan.leaf_out.assign(nleaf, -1); plan.leaf_in.assign(nleaf, -1);
+  plan.hf_s2m.clear(); plan.hf_s2m_rhs.clear(); plan.hf_l2t.clear();
   for (int64_t i = 0; i < nleaf; ++i) {
     const int64_t b = t.leaves[i];
     const int l = t.boxes[b].level;
+    if (t.levels[l].hf) {
+      // HF leaf (opt.hf_leaves): directional S2M for every used outgoing wedge u and
+      // L2T for every incoming wedge w (Algorithm Step 2/3 leaf branches)
+      auto lo = std::lower_bound(out_need[l].begin(), out_need[l].end(), std::make_pair(b, -1));
+      for (auto it = lo; it != out_need[l].end() && it->first == b; ++it) {
+        const int u = it->second;
+        const int64_t s = out_id.at(skey(b, u));
+        plan.hf_s2m.push_back({i, s, reg.get({MK_S2M, b, u}, MatSpec{MK_S2M, l, 0, u, b, 0, 0, 0})});
+        if (p.opt.rhs_operator)
+          plan.hf_s2m_rhs.push_back(
+              {i, s, reg.get({MK_S2M_RHS, b, u}, MatSpec{MK_S2M_RHS, l, 0, u, b, 0, 0, 0})});
+      }
+      auto li = std::lower_bound(in_need[l].begin(), in_need[l].end(), std::make_pair(b, -1));
+      for (auto it = li; it != in_need[l].end() && it->first == b; ++it) {
+        const int w = it->second;
+        plan.hf_l2t.push_back({i, in_id.at(skey(b, w)), reg.get({MK_L2T, b, w}, MatSpec{MK_L2T, l, 0, w, b, 0, 0, 0})});
+      }
+      continue;
+    }
     auto io = out_id.find(skey(b, -1));
     if (io != out_id.end()) {
       plan.leaf_out[i] = io->second;

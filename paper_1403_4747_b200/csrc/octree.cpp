@@ -7,7 +7,8 @@
 //      extent·(1+2⁻²⁰); split while a cube owns > max_leaf elements; elements
 //      owned by centroid; Morton order of centroids = internal "tree order".
 //  C8  HF ⇔ w ≥ λ = 2π/k.
-//  C9  HF cubes are always split (all leaves are LF).
+//  C9  HF cubes are always split (all leaves are LF) — unless opt.hf_leaves,
+//      the paper's rule: split while > max_leaf elements at every level (HF leaves).
 //  C10 wedges: 6·4^j face-grid squares, j = ⌈log₂(w/λ)⌉; the wedge of v is
 //      the square hit on its dominant face; ties → lowest index; child map =
 //      face index >> 1.
@@ -105,7 +106,7 @@ void build_tree(Geometry& g, const Params& p, Tree& t) {
     for (int64_t b = lvl_begin; b < lvl_end; ++b) {
       Box& B = t.boxes[b];
       int64_t cnt = B.end - B.begin;
-      bool split = L.hf ? (cnt > 0) : (cnt > p.opt.max_leaf);
+      bool split = (L.hf && !p.opt.hf_leaves) ? (cnt > 0) : (cnt > p.opt.max_leaf);   // C9 / P:344-346
       if (!split) continue;
       int64_t s = B.begin;
       for (int o = 0; o < 8; ++o) {

@@ -140,10 +140,12 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
         const Box& B = t.boxes[s.leaf];
         const int nb = (int)(B.end - B.begin);
         E.resize((size_t)m * nb);
+        // HF leaf (s.dir ≥ 0): the check cloud of wedge u, R_u^T chk (as for M2M)
+        const Mat3 Rs = out_frame(L, s.dir);
         for (int j = 0; j < nb; ++j) {
           const int64_t e = B.begin + j;
           for (int c = 0; c < m; ++c) {
-            Vec3 xc = B.center + L.chk[c];
+            Vec3 xc = B.center + (s.dir >= 0 ? Rs.apply_t(L.chk[c]) : L.chk[c]);
             cd acc = 0.0;
             for (int q = 0; q < 3; ++q) {
               Vec3 y = g.v0[e] * Q3_BARY[q][0] + g.v1[e] * Q3_BARY[q][1] + g.v2[e] * Q3_BARY[q][2];
@@ -163,8 +165,10 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
         const Box& B = t.boxes[s.leaf];
         const int nb = (int)(B.end - B.begin);
         E.resize((size_t)nb * m);
+        // HF leaf (s.dir = incoming wedge w ≥ 0): IN_EQUIV of w, R^T (−chk) in the frame of anti(w) (as for L2L)
+        const Mat3 Qs = in_frame(L, s.dir);
         for (int j = 0; j < m; ++j) {
-          Vec3 y = B.center - L.chk[j];
+          Vec3 y = B.center + (s.dir >= 0 ? Qs.apply_t(-L.chk[j]) : -L.chk[j]);
           for (int i = 0; i < nb; ++i) {
             const int64_t e = B.begin + i;
             E[(size_t)j * nb + i] = G(g.centroid[e], y, p.k) + p.alpha * dGdnx(g.centroid[e], g.normal[e], y, p.k);

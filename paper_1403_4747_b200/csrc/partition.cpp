@@ -129,6 +129,15 @@ void apply_partition(const Params& p, const Tree& t, Plan& plan) {
       plan.leaf_S[i] = -1;
       if (!plan.leaf_S_rhs.empty()) plan.leaf_S_rhs[i] = -1;
     }
+  auto own_ops = [&](std::vector<LeafOp>& v) {
+    std::vector<LeafOp> keep;
+    for (const LeafOp& o : v)
+      if (o.leaf >= plan.own_leaf0 && o.leaf < plan.own_leaf1) keep.push_back(o);
+    v.swap(keep);
+  };
+  own_ops(plan.hf_s2m);
+  own_ops(plan.hf_s2m_rhs);
+  own_ops(plan.hf_l2t);
   for (auto& lev : plan.m2m) {
     std::vector<Op> keep;
     for (const Op& o : lev) if (mine_out(o.src)) keep.push_back(o);

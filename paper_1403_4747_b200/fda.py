@@ -55,7 +55,7 @@ class fda_options(ctypes.Structure):
                 ("device", ctypes.c_int32), ("build_threads", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("verbose", ctypes.c_int32), ("m2l_lowrank", ctypes.c_int32),
                 ("rhs_operator", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("tensor_cores", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
+                ("tensor_cores", ctypes.c_int32), ("hf_leaves", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class fda_solve_info(ctypes.Structure):
@@ -316,7 +316,8 @@ class FDA:
                "near_idx": np.int64, "corr_ptr": np.int64, "corr_col": np.int64, "corr_val": np.complex64,
                "out_states": np.int64, "in_states": np.int64, "boxes": np.int64, "box_center": np.float64,
                "levels": np.float64, "root": np.float64, "launches": np.int64, "owned": np.int64,
-               "xsend": np.int64, "xrecv": np.int64}
+               "xsend": np.int64, "xrecv": np.int64, "hf_s2m": np.int64, "hf_s2m_rhs": np.int64,
+               "hf_l2t": np.int64}
 
     def table(self, name: str) -> np.ndarray:
         """A host-side build table (host-logic tests only)."""

@@ -83,6 +83,8 @@ def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bo
             if lS[i] >= 0:
                 s = lo[i]
                 ob[oo[s]:oo[s] + T_out(s)] = _mat(pool, mats, lS[i]) @ xt[lr[i, 0]:lr[i, 1]]
+        for (i, s, m) in f.table("hf_s2m" + sfx).reshape(-1, 3):    # HF leaves: one op per wedge
+            ob[oo[s]:oo[s] + T_out(s)] = _mat(pool, mats, m) @ xt[lr[i, 0]:lr[i, 1]]
         m2m = f.table("m2m").reshape(-1, 4)
         for l in sorted(set(m2m[:, 0]), reverse=True):
             for (_, s, d, m) in m2m[m2m[:, 0] == l]:
@@ -101,6 +103,8 @@ def apply_tables(f, x: np.ndarray, far: bool = True, near: bool = True, corr: bo
             if lT[i] >= 0:
                 s = li[i]
                 y[lr[i, 0]:lr[i, 1]] += _mat(pool, mats, lT[i]) @ ib[io[s]:io[s] + T_in(s)]
+        for (i, s, m) in f.table("hf_l2t").reshape(-1, 3):           # HF leaves: one op per wedge
+            y[lr[i, 0]:lr[i, 1]] += _mat(pool, mats, m) @ ib[io[s]:io[s] + T_in(s)]
     out = np.empty(n, dtype=np.complex128)
     out[perm] = y
     return out

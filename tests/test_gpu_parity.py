@@ -183,6 +183,27 @@ def test_point_source_rhs_and_solve(cfg1):
     assert info["converged"] and err <= SOLVE_TOL and ser < 3e-2
 
 
+def test_hf_leaves_parity(lib):
+    """Paper-faithful adaptivity (opt.hf_leaves = 1, PAPER.md P:344-346,
+    P:449-454): HF leaves with directional S2M / L2T; LHS matvec and the RHS
+    pass vs the oracle."""
+    V, F = icosphere(4, 0.5)
+    k = 80.0
+    f = lib(V, F, k, 1j / k, 1e-4, max_leaf=64, hf_leaves=1, rhs_operator=1)
+    assert len(f.table("hf_s2m")) > 0
+    x = random_density(len(F), 8)
+    el = O.element_geometry(V, F)
+    rows = np.arange(0, len(F), 2)
+    y = f.matvec(x)
+    yo = fast.matvec_rows(el, rows, x, k, 1j / k)
+    err = _rel(y[rows], yo)
+    b = f.rhs_apply(x)
+    bo = fast.matvec_rows(el, rows, x, k, 1j / k, kind="rhs")
+    errb = _rel(b[rows], bo)
+    print(f"hf_leaves: LHS rel-L2 {err:.3e}, RHS {errb:.3e}")
+    assert err <= MATVEC_TOL and errb <= MATVEC_TOL
+
+
 def test_eps_sweep_and_leaf_size(cfg1):
     """the FDA error against the dense operator falls
     with ε (roughly ∝ ε) and changing max_leaf (a different tree, other lists and

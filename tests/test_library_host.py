@@ -105,12 +105,16 @@ def _coverage(f):
     return cov
 
 
-@pytest.mark.parametrize("s,k,ml", [(3, 60.0, 8), (3, 120.0, 4), (2, 10.0, 4)])
-def test_pair_coverage_exact(s, k, ml):
+@pytest.mark.parametrize("s,k,ml,hfl", [(3, 60.0, 8, 0), (3, 120.0, 4, 0), (2, 10.0, 4, 0), (3, 60.0, 64, 1),
+                                         (3, 120.0, 16, 1)])
+def test_pair_coverage_exact(s, k, ml, hfl):
     """Every ordered element pair is covered exactly once (reading C11;
-    SURVEY A.13)."""
+    SURVEY A.13), with HF boxes split (C9) or kept as HF leaves (hfl = 1,
+    PAPER.md P:344-346)."""
     V, F = icosphere(s, 0.5)
-    f = FDA(V, F, k, 1j / k, 1e-3, device=-1, max_leaf=ml)
+    f = FDA(V, F, k, 1j / k, 1e-3, device=-1, max_leaf=ml, hf_leaves=hfl)
+    if hfl:
+        assert len(f.table("hf_s2m")) > 0 and len(f.table("hf_l2t")) > 0
     assert (_coverage(f) == 1).all()
 
 
@@ -135,6 +139,21 @@ def test_config1_tables_match_oracle():
     # direct path alone (near + corrections, no far field) is NOT the operator
     yn = apply_tables(f, x, far=False)
     assert np.linalg.norm(yn - yo) / np.linalg.norm(yo) > 1e-3
+
+
+def test_hf_leaf_tables_match_oracle():
+    """Paper-faithful adaptivity (opt.hf_leaves): HF
+    leaves with directional S2M / L2T per used wedge, applied from the
+    exported tables vs the dense oracle."""
+    V, F = icosphere(3, 0.5)
+    k = 60.0
+    f = FDA(V, F, k, 1j / k, 1e-4, device=-1, max_leaf=64, hf_leaves=1)
+    assert len(f.table("hf_s2m")) // 3 > 100      # many (leaf, wedge) S2M ops
+    x = random_density(len(F), 4)
+    y = apply_tables(f, x)
+    el = O.element_geometry(V, F)
+    yo = fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k)
+    assert np.linalg.norm(y - yo) / np.linalg.norm(yo) < 1e-3
 
 
 def test_hf_tables_match_oracle():
