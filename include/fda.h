@@ -210,6 +210,12 @@ fda_status fda_exchange_local(fda_ctx** ctxs, int32_t n);
  * fda_set_profiling(ctx, 1): [gather, near, s2m, m2m, m2l, l2l, l2t, scatter].
  * n = capacity of ms; returns the number of stages written in *n. */
 fda_status fda_set_profiling(fda_ctx* ctx, int32_t on);
+/* Device time (ms) of the near-field kernel (row a7) in the last fda_matvec /
+ * fda_rhs_apply, from CUDA events recorded on its own stream inside the
+ * captured graph, i.e. while it runs concurrently with the far field (no
+ * profiling mode needed).  Synchronises on that event.  FDA_E_STATE before
+ * the first matvec. */
+fda_status fda_near_time(fda_ctx* ctx, double* ms);
 fda_status fda_stage_times(fda_ctx* ctx, double* ms, int32_t* n);
 
 /* Copy a named host-side build table (for host-logic tests; see

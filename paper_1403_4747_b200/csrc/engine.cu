@@ -109,6 +109,8 @@ struct Dev {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev[8] = {};
   cudaEvent_t ev_n0 = nullptr, ev_n1 = nullptr;
+  cudaEvent_t ev_l0 = nullptr, ev_l1 = nullptr;   // near kernel of the last matvec, recorded on its stream
+  bool live = false;                                // ev_l0/ev_l1 hold a completed-or-pending matvec
   int32_t* perm = nullptr;
   float4 *tgt_pos = nullptr, *tgt_nrm = nullptr;
   SrcElem* src = nullptr;
@@ -769,6 +771,8 @@ fda_status engine_create(Context* ctx) {
   CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
   for (auto& e : d->ev) CK(cudaEventCreate(&e));
   CK(cudaEventCreate(&d->ev_n0));
+  CK(cudaEventCreate(&d->ev_l0));
+  CK(cudaEventCreate(&d->ev_l1));
   CK(cudaEventCreate(&d->ev_n1));
   CK(cudaDeviceSynchronize());
   return FDA_OK;
@@ -828,6 +832,8 @@ void engine_destroy(Context* ctx) {
   if (d->ev_join) cudaEventDestroy(d->ev_join);
   for (auto& e : d->ev) if (e) cudaEventDestroy(e);
   if (d->ev_n0) cudaEventDestroy(d->ev_n0);
+  if (d->ev_l0) cudaEventDestroy(d->ev_l0);
+  if (d->ev_l1) cudaEventDestroy(d->ev_l1);
   if (d->ev_n1) cudaEventDestroy(d->ev_n1);
   delete d;
   ctx->dev = nullptr;
@@ -843,9 +849,12 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   CK(cudaEventRecord(d->ev_fork, s));
   CK(cudaStreamWaitEvent(sn, d->ev_fork, 0));
   if (prof) CK(cudaEventRecord(d->ev_n0, sn));
+  CK(cudaEventRecord(d->ev_l0, sn));
   launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
               kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
               kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, sn);
+  CK(cudaEventRecord(d->ev_l1, sn));
+  d->live = true;
   if (prof) CK(cudaEventRecord(d->ev_n1, sn));
   CK(cudaEventRecord(d->ev_join, sn));
 
@@ -933,9 +942,12 @@ static fda_status run_sharded_up(Context* ctx, Dev* d, cudaStream_t s, int kind)
   CK(cudaEventRecord(d->ev_fork, s));
   CK(cudaStreamWaitEvent(sn, d->ev_fork, 0));
   if (prof) CK(cudaEventRecord(d->ev_n0, sn));
+  CK(cudaEventRecord(d->ev_l0, sn));
   launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
               kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
               kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, sn);
+  CK(cudaEventRecord(d->ev_l1, sn));
+  d->live = true;
   if (prof) CK(cudaEventRecord(d->ev_n1, sn));
   CK(cudaEventRecord(d->ev_join, sn));
   if (prof) CK(cudaEventRecord(d->ev[1], s));
@@ -1128,6 +1140,19 @@ fda_status engine_exchange_local(Context** ctxs, int n) {
       }
     }
   }
+  return FDA_OK;
+}
+
+// device time of the near-field kernel in the last matvec (events on its own
+// stream, recorded inside the captured graph: the kernel as it runs
+// concurrently with the far field)
+fda_status engine_near_time(Context* ctx, double* ms) {
+  Dev* d = static_cast<Dev*>(ctx->dev);
+  if (!d->live) { ctx->err = "no matvec yet"; return FDA_E_STATE; }
+  CK(cudaEventSynchronize(d->ev_l1));
+  float v = 0.f;
+  CK(cudaEventElapsedTime(&v, d->ev_l0, d->ev_l1));
+  *ms = v;
   return FDA_OK;
 }
 

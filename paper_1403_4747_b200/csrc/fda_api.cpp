@@ -300,6 +300,12 @@ fda_status fda_set_profiling(fda_ctx* ctx, int32_t on) {
   return FDA_OK;
 }
 
+fda_status fda_near_time(fda_ctx* ctx, double* ms) {
+  if (!ctx || !ms) return FDA_E_INVALID_ARG;
+  if (!ctx->dev) { ctx->err = "context was built host-only"; return FDA_E_STATE; }
+  return engine_near_time(ctx, ms);
+}
+
 fda_status fda_stage_times(fda_ctx* ctx, double* ms, int32_t* n) {
   if (!ctx || !ms || !n) return FDA_E_INVALID_ARG;
   if (!ctx->dev) return FDA_E_STATE;

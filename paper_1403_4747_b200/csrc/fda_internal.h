@@ -226,6 +226,7 @@ fda_status engine_rhs_point_source(Context* ctx, const double src[3], void* b, i
 fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int32_t max_iter, int32_t restart,
                         fda_solve_info* info, int32_t flags);
 fda_status engine_stage_times(Context* ctx, double* ms, int32_t* n);
+fda_status engine_near_time(Context* ctx, double* ms);
 fda_status engine_comm_init(Context* ctx, const void* id128);
 fda_status engine_exchange_local(Context** ctxs, int n);
 fda_status nccl_unique_id(void* id128, std::string& err);

@@ -32,7 +32,7 @@ STATUS = {0: "FDA_OK", 1: "FDA_E_INVALID_ARG", 2: "FDA_E_MESH", 3: "FDA_E_NOMEM"
 EXPORTS = ["fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_point_source",
            "fda_rhs_apply", "bm_solve",
            "fda_stats", "fda_nccl_unique_id", "fda_comm_init", "fda_exchange_local",
-           "fda_set_profiling", "fda_stage_times", "fda_debug_table", "fda_last_error", "fda_status_string",
+           "fda_set_profiling", "fda_stage_times", "fda_near_time", "fda_debug_table", "fda_last_error", "fda_status_string",
            "fda_free"]
 
 STAGES = ["gather", "near", "s2m", "m2m", "m2l", "l2l", "l2t", "scatter"]
@@ -107,6 +107,7 @@ def load_library(path: str = LIB_PATH):
     lib.fda_comm_init.argtypes = [vp, vp]
     lib.fda_exchange_local.argtypes = [ctypes.POINTER(vp), i32]
     lib.fda_set_profiling.argtypes = [vp, i32]
+    lib.fda_near_time.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
     lib.fda_stage_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)]
     lib.fda_debug_table.argtypes = [vp, ctypes.c_char_p, vp, ctypes.POINTER(i64), ctypes.POINTER(i32)]
     lib.fda_last_error.argtypes = [vp]
@@ -118,7 +119,7 @@ def load_library(path: str = LIB_PATH):
     for name in ("fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_point_source",
                  "fda_rhs_apply", "bm_solve",
                  "fda_stats", "fda_nccl_unique_id", "fda_comm_init", "fda_exchange_local", "fda_exchange_local",
-                 "fda_set_profiling", "fda_stage_times", "fda_debug_table"):
+                 "fda_set_profiling", "fda_stage_times", "fda_near_time", "fda_debug_table"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -301,6 +302,12 @@ class FDA:
 
     def set_profiling(self, on: bool = True):
         self._check(self.lib.fda_set_profiling(self.ctx, 1 if on else 0))
+
+    def near_time(self) -> float:
+        """fda_near_time: ms of the near-field kernel in the last matvec (live, in the graph)."""
+        ms = ctypes.c_double()
+        self._check(self.lib.fda_near_time(self.ctx, ctypes.byref(ms)))
+        return ms.value
 
     def stage_times(self) -> dict:
         ms = (ctypes.c_double * 8)()
