@@ -102,8 +102,19 @@ struct XStage {
   int64_t* dst = nullptr;
 };
 
+// GMRES workspace (engine_solve; cached per context)
+struct Gm {
+  float2 *V = nullptr, *w = nullptr, *b = nullptr, *x = nullptr;
+  double2 *partial = nullptr, *hbuf = nullptr;   // hbuf: [h1 (m+1) | h2 (m+1) | y (m+1)]
+  double *np = nullptr, *nrm = nullptr;
+  int m = 0;
+};
+
 struct Dev {
   int device = 0;
+  Gm gm;
+  int gm_cap = 0;                   // Krylov vectors the cached workspace holds
+  std::vector<void*> gm_allocs;
   int n = 0, nleaf = 0;
   cudaStream_t s_near = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -819,6 +830,7 @@ void engine_destroy(Context* ctx) {
     if (a.ok) a.commDestroy(d->comm);
   }
   for (void* a : d->allocs) cudaFree(a);
+  for (void* a : d->gm_allocs) cudaFree(a);
   for (auto& ge : d->graph_exec)
     if (ge) cudaGraphExecDestroy(ge);
   if (d->s_near) cudaStreamDestroy(d->s_near);
@@ -1213,14 +1225,6 @@ fda_status engine_rhs_point_source(Context* ctx, const double src[3], void* b, i
 // caller order.  Arnoldi with classical Gram-Schmidt applied twice (CGS2),
 // fp64 accumulation of every inner product, coefficients kept on the device;
 // one small device→host copy per iteration feeds the Givens rotations.
-namespace {
-struct Gm {
-  float2 *V = nullptr, *w = nullptr, *b = nullptr, *x = nullptr;
-  double2 *partial = nullptr, *hbuf = nullptr;   // hbuf: [h1 (m+1) | h2 (m+1) | y (m+1)]
-  double *np = nullptr, *nrm = nullptr;
-  int m = 0;
-};
-}  // namespace
 
 static const int kChunks = 128;
 
@@ -1245,29 +1249,35 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
   auto t0 = std::chrono::steady_clock::now();
   const int64_t n = d->n;
   const int m = restart > 0 ? std::min(restart, max_iter) : max_iter;
-  Gm gm;
-  gm.m = m;
-  std::vector<void*> mine;
-  auto cleanup = [&]() {
-    for (void* p : mine) cudaFree(p);
-  };
-  auto A = [&](void** p, size_t bytes) -> bool {
-    if (cudaMalloc(p, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
+  // workspace cached in the context (allocated on the first solve, grown on demand)
+  if (d->gm_cap < m + 1) {
+    for (void* q : d->gm_allocs) cudaFree(q);
+    d->gm_allocs.clear();
+    d->gm_cap = 0;
+    auto A = [&](void** q, size_t bytes) -> bool {
+      if (cudaMalloc(q, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      d->gm_allocs.push_back(*q);
+      return true;
+    };
+    Gm& w = d->gm;
+    if (!A((void**)&w.V, sizeof(float2) * n * (m + 1)) || !A((void**)&w.w, sizeof(float2) * n) ||
+        !A((void**)&w.b, sizeof(float2) * n) || !A((void**)&w.x, sizeof(float2) * n) ||
+        !A((void**)&w.partial, sizeof(double2) * kChunks * (m + 1)) ||
+        !A((void**)&w.hbuf, sizeof(double2) * 3 * (m + 1)) || !A((void**)&w.np, sizeof(double) * kChunks) ||
+        !A((void**)&w.nrm, sizeof(double))) {
+      for (void* q : d->gm_allocs) cudaFree(q);
+      d->gm_allocs.clear();
+      ctx->err = "device allocation for the GMRES workspace failed";
+      return FDA_E_NOMEM;
     }
-    mine.push_back(*p);
-    return true;
-  };
-  if (!A((void**)&gm.V, sizeof(float2) * n * (m + 1)) || !A((void**)&gm.w, sizeof(float2) * n) ||
-      !A((void**)&gm.b, sizeof(float2) * n) || !A((void**)&gm.x, sizeof(float2) * n) ||
-      !A((void**)&gm.partial, sizeof(double2) * kChunks * (m + 1)) ||
-      !A((void**)&gm.hbuf, sizeof(double2) * 3 * (m + 1)) || !A((void**)&gm.np, sizeof(double) * kChunks) ||
-      !A((void**)&gm.nrm, sizeof(double))) {
-    cleanup();
-    ctx->err = "device allocation for the GMRES workspace failed";
-    return FDA_E_NOMEM;
+    d->gm_cap = m + 1;
   }
+  Gm gm = d->gm;
+  gm.m = m;
+  auto cleanup = []() {};
   fda_status st = FDA_OK;
 #define GCK(expr)       \
   do {                  \
@@ -1331,8 +1341,7 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
       launch_reduce_norm(gm.np, kChunks, gm.nrm, 0);
       launch_scale_by_inv(gm.V + (int64_t)(j + 1) * n, gm.w, gm.nrm, n, 0);
       // one copy: h1, h2 and the norm
-      GCU(cudaMemcpy(hh.data(), h1, sizeof(double2) * (j + 1), cudaMemcpyDeviceToHost));
-      GCU(cudaMemcpy(hh.data() + (m + 1), h2, sizeof(double2) * (j + 1), cudaMemcpyDeviceToHost));
+      GCU(cudaMemcpy(hh.data(), h1, sizeof(double2) * (m + 1 + j + 1), cudaMemcpyDeviceToHost));   // h1 | h2
       double hn;
       GCU(cudaMemcpy(&hn, gm.nrm, sizeof(double), cudaMemcpyDeviceToHost));
       for (int i = 0; i <= j; ++i)
