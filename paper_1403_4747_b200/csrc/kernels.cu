@@ -489,16 +489,21 @@ __global__ void __launch_bounds__(128) k_xlate(const XTask* __restrict__ tasks, 
     __syncthreads();
     buf ^= 1;
   }
+  // rows (2tr, 2tr+1) + 2·NR·i are pairs: one 16-byte vector atomic per pair (states and
+  // the tmp buffer are 16-byte aligned and padded to an even length; rows ≥ t.rows hold
+  // zeros since M rows ≥ t.rows were zero-filled)
 #pragma unroll
   for (int j = 0; j < OT; ++j) {
     const int op = 2 * to + (j & 1) + 2 * NO * (j >> 1);
     if (op >= t.op_count) continue;
     float2* d = dst + dst_off[t.op_begin + op];
 #pragma unroll
-    for (int i = 0; i < RT; ++i) {
-      const int row = t.row0 + 2 * tr + (i & 1) + 2 * NR * (i >> 1);
+    for (int i = 0; i < RT; i += 2) {
+      const int row = t.row0 + 2 * tr + 2 * NR * (i >> 1);
       if (row < t.rows) {
-        if (ATOMIC) atomicAdd(d + row, acc[i][j]);
+        const float4 v = make_float4(acc[i][j].x, acc[i][j].y, acc[i + 1][j].x, acc[i + 1][j].y);
+        if (ATOMIC) atomicAdd(reinterpret_cast<float4*>(d + row), v);
+        else if (row + 1 < t.rows) *reinterpret_cast<float4*>(d + row) = v;
         else d[row] = acc[i][j];
       }
     }
@@ -693,15 +698,20 @@ __global__ void __launch_bounds__(128) k_m2l_lr(const LrTask* __restrict__ tasks
 #pragma unroll
         for (int j = 0; j < 4; ++j) cmac(a2[i][j], m[i], v[j]);
     }
+    // rows (2·tr2, 2·tr2+1) are a pair: one 16-byte vector atomic per pair (states are
+    // 16-byte aligned and padded to an even length; rows ≥ T hold zeros since Û rows ≥ T
+    // were zero-filled, so the pair (T-1, T) adds a zero into the padding slot)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int op = oh + 2 * to2 + (j & 1) + 32 * (j >> 1);
       if (op >= t.op_count) continue;
       float2* d = dst + doff[op] + r0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int row = 2 * tr2 + (i & 1) + 16 * (i >> 1);
-        if (r0 + row < t.T) atomicAdd(d + row, a2[i][j]);
+      for (int i = 0; i < 4; i += 2) {
+        const int row = 2 * tr2 + 16 * (i >> 1);
+        if (r0 + row < t.T)
+          atomicAdd(reinterpret_cast<float4*>(d + row),
+                    make_float4(a2[i][j].x, a2[i][j].y, a2[i + 1][j].x, a2[i + 1][j].y));
       }
     }
     __syncthreads();
