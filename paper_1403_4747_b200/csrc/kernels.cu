@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include "f32x2.cuh"
 #include "kernels.cuh"
 
 namespace fda {
@@ -103,58 +104,74 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
   return y;
 }
 
-// One Q3 point of the LHS kernel, accumulated into ks (without the weight):
-//   ks += (r²/k²)·[∂G/∂n_y + α ∂²G/∂n_x∂n_y](x, y) · 4π ... i.e. ks += e^{iq}(P + iQ)/q²
+// One Q3 point of the LHS kernel for TWO targets at once (the lanes of the
+// packed fp32 pairs, f32x2.cuh), accumulated into (kr, ki) without the weight:
+//   k += (r²/k²)·4π·[∂G/∂n_y + α ∂²G/∂n_x∂n_y](x, y) = e^{iq}(P + iQ)/q²
 // With q = kr, a = ∂r/∂n_x, b = ∂r/∂n_y, c = n_x·n_y, g = 3ab + c, u1 = (3 - q²)ab + c:
 //   4π r² e^{-iq} ∂G/∂n_y          = (iq - 1) b
 //   4π r² e^{-iq} ∂²G/∂n_x∂n_y     = (1/r) [ u1 - iq g ]
 // so for α = i α_i (PURE_IMAG; α = i/k):  P = -b + α_i k g,  Q = q b + α_i k (1/q) u1.
-// d = X - Y (wave units); xny = X·n_y, cy = Y·n_y, so d·n_y = xny - cy.
+// d = X - Y (wave units), s = d·n_x, t = Y·n_y - X·n_y = -(d·n_y) (Y.w = Y·n_y), ι = 1/q:
+// a = sι, b = tι, ab = st ι², q²ab = st, qb = t — so u1 = g - st and Q = t + α_i k ι u1.
+// The source point Y is the same for both lanes (a broadcast operand); MUFU
+// work (rsqrt, sin, cos) stays per lane.
 template <bool PURE_IMAG>
-__device__ __forceinline__ void lhs_eval(float3 X, float3 nx, float4 Y, float xny, float cn, const KernelParams& kp,
-                                         float2& ks) {
-  const float dx = X.x - Y.x, dy = X.y - Y.y, dz = X.z - Y.z;
-  const float q2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-  const float iq = rsqrt_ftz(q2);
-  const float q = q2 * iq;
-  float sn, cs;
-  __sincosf(q, &sn, &cs);  // MUFU sin/cos; argument error ≤ ulp(q/2π)
-  const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * iq;   // ∂r/∂n_x
-  const float b = (Y.w - xny) * iq;                                  // ∂r/∂n_y = -(d·n_y)/|d|
-  const float ab = a * b;
-  const float g = fmaf(3.0f, ab, cn);               // 3ab + c
-  const float u1 = fmaf(-q2, ab, g);                // (3 - q²) ab + c = g - q² ab
-  float P, Q;
+__device__ __forceinline__ void lhs_eval2(const f2x* X, const f2x* nx, float4 Y, f2x xny, f2x cn,
+                                          const KernelParams& kp, f2x& kr, f2x& ki) {
+  const f2x dx = sub2(X[0], bcast2(Y.x)), dy = sub2(X[1], bcast2(Y.y)), dz = sub2(X[2], bcast2(Y.z));
+  const f2x q2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+  float q2a, q2b;
+  unpack2(q2, q2a, q2b);
+  const f2x iq = pack2(rsqrt_ftz(q2a), rsqrt_ftz(q2b));
+  const f2x q = mul2(q2, iq);
+  float qa, qb, sa, ca, sb, cb;
+  unpack2(q, qa, qb);
+  __sincosf(qa, &sa, &ca);  // MUFU sin/cos; argument error ≤ ulp(q/2π)
+  __sincosf(qb, &sb, &cb);
+  const f2x sd = fma2(dx, nx[0], fma2(dy, nx[1], mul2(dz, nx[2])));   // s = d·n_x
+  const f2x t = sub2(bcast2(Y.w), xny);                              // t = -(d·n_y)
+  const f2x iq2 = mul2(iq, iq);
+  const f2x st = mul2(sd, t);
+  const f2x g = fma2(bcast2(3.0f), mul2(st, iq2), cn);   // 3ab + c
+  const f2x u1 = sub2(g, st);                            // (3 - q²) ab + c
+  const f2x b = mul2(t, iq);
+  f2x P, Q;
   if (PURE_IMAG) {
-    P = fmaf(kp.ak_im, g, -b);
-    Q = fmaf(q, b, (kp.ak_im * iq) * u1);
+    P = fma2(bcast2(kp.ak_im), g, neg2(b));
+    Q = fma2(mul2(bcast2(kp.ak_im), iq), u1, t);
   } else {
-    const float u2 = -q * g;
-    P = fmaf(iq, kp.ak_re * u1 - kp.ak_im * u2, -b);
-    Q = fmaf(iq, kp.ak_re * u2 + kp.ak_im * u1, q * b);
+    // P = ι (α_r k u1 - α_i k u2) - b,  Q = ι (α_r k u2 + α_i k u1) + qb,  u2 = -q g
+    const f2x u2 = neg2(mul2(q, g));
+    P = fma2(iq, fma2(bcast2(kp.ak_re), u1, mul2(bcast2(-kp.ak_im), u2)), neg2(b));
+    Q = fma2(iq, fma2(bcast2(kp.ak_re), u2, mul2(bcast2(kp.ak_im), u1)), t);
   }
-  const float iq2 = iq * iq;
-  const float Er = iq2 * cs, Ei = iq2 * sn;
-  ks.x = fmaf(Er, P, fmaf(-Ei, Q, ks.x));
-  ks.y = fmaf(Er, Q, fmaf(Ei, P, ks.y));
+  const f2x Er = mul2(iq2, pack2(ca, cb)), Ei = mul2(iq2, pack2(sa, sb));
+  kr = fma2(Er, P, fma2(neg2(Ei), Q, kr));
+  ki = fma2(Er, Q, fma2(Ei, P, ki));
 }
 
-// One Q3 point of the RHS kernel (Eq. 4 right side), without the weight:
+// One Q3 point of the RHS kernel (Eq. 4 right side) for two targets, without the weight:
 //   4π r² e^{-iq} (G + α ∂G/∂n_x) = r + α (iq - 1) a,   r = q/k
-__device__ __forceinline__ void rhs_eval(float3 X, float3 nx, float4 Y, const KernelParams& kp, float2& ks) {
-  const float dx = X.x - Y.x, dy = X.y - Y.y, dz = X.z - Y.z;
-  const float q2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-  const float iq = rsqrt_ftz(q2);
-  const float q = q2 * iq;
-  const float a = fmaf(dx, nx.x, fmaf(dy, nx.y, dz * nx.z)) * iq;
-  float sn, cs;
-  __sincosf(q, &sn, &cs);
-  const float P = fmaf(q, kp.inv_k, -a * fmaf(kp.alpha_im, q, kp.alpha_re));   // r - a (α_r + α_i q)
-  const float Q = a * fmaf(kp.alpha_re, q, -kp.alpha_im);                      // a (α_r q - α_i)
-  const float iq2 = iq * iq;
-  const float Er = iq2 * cs, Ei = iq2 * sn;
-  ks.x = fmaf(Er, P, fmaf(-Ei, Q, ks.x));
-  ks.y = fmaf(Er, Q, fmaf(Ei, P, ks.y));
+__device__ __forceinline__ void rhs_eval2(const f2x* X, const f2x* nx, float4 Y, const KernelParams& kp, f2x& kr,
+                                          f2x& ki) {
+  const f2x dx = sub2(X[0], bcast2(Y.x)), dy = sub2(X[1], bcast2(Y.y)), dz = sub2(X[2], bcast2(Y.z));
+  const f2x q2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+  float q2a, q2b;
+  unpack2(q2, q2a, q2b);
+  const f2x iq = pack2(rsqrt_ftz(q2a), rsqrt_ftz(q2b));
+  const f2x q = mul2(q2, iq);
+  float qa, qb, sa, ca, sb, cb;
+  unpack2(q, qa, qb);
+  __sincosf(qa, &sa, &ca);
+  __sincosf(qb, &sb, &cb);
+  const f2x a = mul2(fma2(dx, nx[0], fma2(dy, nx[1], mul2(dz, nx[2]))), iq);
+  // P = r - a (α_r + α_i q),  Q = a (α_r q - α_i)
+  const f2x P = fma2(q, bcast2(kp.inv_k), neg2(mul2(a, fma2(bcast2(kp.alpha_im), q, bcast2(kp.alpha_re)))));
+  const f2x Q = mul2(a, fma2(bcast2(kp.alpha_re), q, bcast2(-kp.alpha_im)));
+  const f2x iq2 = mul2(iq, iq);
+  const f2x Er = mul2(iq2, pack2(ca, cb)), Ei = mul2(iq2, pack2(sa, sb));
+  kr = fma2(Er, P, fma2(neg2(Ei), Q, kr));
+  ki = fma2(Er, Q, fma2(Ei, P, ki));
 }
 
 // y_i = Σ_{j ∈ direct(i)} A^{Q3}_ij x_j + Σ_{j: ρ_ij<3} C_ij x_j   (a7)
@@ -162,10 +179,12 @@ __device__ __forceinline__ void rhs_eval(float3 X, float3 nx, float4 Y, const Ke
 // elements of all its direct leaves are listed in a build-time slot table
 // (element, index of its source leaf in the near list → k(c_B − c_C)), so the
 // CTA stages them through shared memory in chunks of NEAR_MAXS with one
-// coalesced table load per slot.  P = ⌊NT/n_B⌋ threads share one target and
-// split the sources; partial sums are reduced in shared memory.  Staged per
-// source element: the three Q3 points with Y_q·n_y in .w (wave units, shifted
-// into the target leaf's frame), the normal, and w_j = x_j·k²A_j/(12π).
+// coalesced table load per slot.  Each thread owns a PAIR of targets (the two
+// lanes of its packed fp32 registers); P = ⌊NT/⌈n_B/2⌉⌋ threads share one
+// pair and split the sources; partial sums are reduced in shared memory.
+// Staged per source element: the three Q3 points with Y_q·n_y in .w (wave
+// units, shifted into the target leaf's frame), the normal, and
+// w_j = x_j·k²A_j/(12π).
 // KIND 0: LHS operator A (Eq. 5); KIND 1: RHS operator B (G sources).
 template <int KIND, bool PURE_IMAG>
 __global__ void __launch_bounds__(NEAR_NT) k_near(
@@ -175,20 +194,23 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
     const float2* __restrict__ corr_val, const float2* __restrict__ x, float2* __restrict__ y, KernelParams kp) {
   // staged source element s: st[5s..5s+4] = Y0, Y1, Y2 (with Y_q·n_y in .w), (n_y, -), (w_j, -, -)
   __shared__ float4 st[NEAR_MAXS * 5];
-  __shared__ float2 sred[NEAR_NT];
+  __shared__ float4 sred[NEAR_NT];
   const NearTask t = tasks[blockIdx.x];
   const int tb = t.tb, nt = t.nt;
-  const int P = max(1, NEAR_NT / nt);
+  const int np = (nt + 1) >> 1;   // target pairs
+  const int P = max(1, NEAR_NT / np);
   const int tid = threadIdx.x;
-  const int ti = tid % nt, part = tid / nt;
-  const bool active = part < P && ti < nt;
-  float3 X = make_float3(0.f, 0.f, 0.f), nx = X;
-  if (active) {
-    float4 p = tgt_pos[tb + ti], q = tgt_nrm[tb + ti];
-    X = make_float3(p.x, p.y, p.z);
-    nx = make_float3(q.x, q.y, q.z);
+  const int tp = tid % np, part = tid / np;
+  const bool active = part < P;
+  const int j0 = 2 * tp, j1 = min(j0 + 1, nt - 1);   // odd n_B: the last lane duplicates a target (discarded)
+  f2x X[3], N[3];
+  {
+    const float4 p0 = tgt_pos[tb + j0], p1 = tgt_pos[tb + j1];
+    const float4 n0 = tgt_nrm[tb + j0], n1 = tgt_nrm[tb + j1];
+    X[0] = pack2(p0.x, p1.x); X[1] = pack2(p0.y, p1.y); X[2] = pack2(p0.z, p1.z);
+    N[0] = pack2(n0.x, n1.x); N[1] = pack2(n0.y, n1.y); N[2] = pack2(n0.z, n1.z);
   }
-  float2 acc = make_float2(0.f, 0.f);
+  f2x ar = zero2(), ai = zero2();
   for (int base = t.s0; base < t.s1; base += NEAR_MAXS) {
     const int ns = min(NEAR_MAXS, t.s1 - base);
     __syncthreads();
@@ -217,44 +239,55 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
         const float4* e = st + 5 * s;
         const float4 A = e[0], B = e[1], C = e[2];
         const float4 w = e[4];
-        float2 ks = make_float2(0.f, 0.f);
+        f2x kr = zero2(), ki = zero2();
         if (KIND == 0) {
           const float4 ny = e[3];
-          const float cn = fmaf(nx.x, ny.x, fmaf(nx.y, ny.y, nx.z * ny.z));
-          const float xny = fmaf(X.x, ny.x, fmaf(X.y, ny.y, X.z * ny.z));
-          lhs_eval<PURE_IMAG>(X, nx, A, xny, cn, kp, ks);
-          lhs_eval<PURE_IMAG>(X, nx, B, xny, cn, kp, ks);
-          lhs_eval<PURE_IMAG>(X, nx, C, xny, cn, kp, ks);
+          const f2x cn = fma2(N[0], bcast2(ny.x), fma2(N[1], bcast2(ny.y), mul2(N[2], bcast2(ny.z))));
+          const f2x xny = fma2(X[0], bcast2(ny.x), fma2(X[1], bcast2(ny.y), mul2(X[2], bcast2(ny.z))));
+          lhs_eval2<PURE_IMAG>(X, N, A, xny, cn, kp, kr, ki);
+          lhs_eval2<PURE_IMAG>(X, N, B, xny, cn, kp, kr, ki);
+          lhs_eval2<PURE_IMAG>(X, N, C, xny, cn, kp, kr, ki);
         } else {
-          rhs_eval(X, nx, A, kp, ks);
-          rhs_eval(X, nx, B, kp, ks);
-          rhs_eval(X, nx, C, kp, ks);
+          rhs_eval2(X, N, A, kp, kr, ki);
+          rhs_eval2(X, N, B, kp, kr, ki);
+          rhs_eval2(X, N, C, kp, kr, ki);
         }
-        acc.x = fmaf(ks.x, w.x, fmaf(-ks.y, w.y, acc.x));
-        acc.y = fmaf(ks.x, w.y, fmaf(ks.y, w.x, acc.y));
+        ar = fma2(kr, bcast2(w.x), fma2(neg2(ki), bcast2(w.y), ar));
+        ai = fma2(kr, bcast2(w.y), fma2(ki, bcast2(w.x), ai));
       }
     }
   }
+  float4 acc;
+  unpack2(ar, acc.x, acc.z);
+  unpack2(ai, acc.y, acc.w);
   // correction SpMV, rows split over the P parts
   if (active) {
-    const int i = tb + ti;
-    const int cb = corr_ptr[i], ce = corr_ptr[i + 1];
-    for (int e = cb + part; e < ce; e += P) {
-      const float2 v = corr_val[e];
-      const float2 xv = x[corr_col[e]];
-      acc.x = fmaf(v.x, xv.x, fmaf(-v.y, xv.y, acc.x));
-      acc.y = fmaf(v.x, xv.y, fmaf(v.y, xv.x, acc.y));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (j0 + h >= nt) break;
+      const int i = tb + j0 + h;
+      const int cb = corr_ptr[i], ce = corr_ptr[i + 1];
+      float2 c = make_float2(0.f, 0.f);
+      for (int e = cb + part; e < ce; e += P) {
+        const float2 v = corr_val[e];
+        const float2 xv = x[corr_col[e]];
+        c.x = fmaf(v.x, xv.x, fmaf(-v.y, xv.y, c.x));
+        c.y = fmaf(v.x, xv.y, fmaf(v.y, xv.x, c.y));
+      }
+      if (h == 0) { acc.x += c.x; acc.y += c.y; }
+      else { acc.z += c.x; acc.w += c.y; }
     }
   }
-  sred[tid] = active ? acc : make_float2(0.f, 0.f);
+  sred[tid] = active ? acc : make_float4(0.f, 0.f, 0.f, 0.f);
   __syncthreads();
-  if (tid < nt) {
-    float2 s = make_float2(0.f, 0.f);
+  if (tid < np) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int p = 0; p < P; ++p) {
-      float2 v = sred[p * nt + tid];
-      s.x += v.x; s.y += v.y;
+      const float4 v = sred[p * np + tid];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
     }
-    y[tb + tid] = s;
+    y[tb + 2 * tid] = make_float2(s.x, s.y);
+    if (2 * tid + 1 < nt) y[tb + 2 * tid + 1] = make_float2(s.z, s.w);
   }
 }
 
