@@ -161,8 +161,11 @@ struct Dev {
     int n_lr[LR_NCLS] = {};
     int64_t* lr_src = nullptr;
     int64_t* lr_dst = nullptr;
+    LrTcTask* lrtc = nullptr;        // fused §4.2 tasks on the tensor cores (k_m2l_tc)
+    int n_lrtc = 0;
+    size_t lrtc_smem = 0;
     bool any() const {
-      int n = 0;
+      int n = n_lrtc;
       for (int c = 0; c < LR_NCLS; ++c) n += n_lr[c];
       for (int v = 0; v < TC_NV; ++v) n += dense.n_tc[v] + a.n_tc[v] + b.n_tc[v];
       for (int v = 0; v < XV; ++v) n += dense.ntask[v] + a.ntask[v] + b.ntask[v];
@@ -189,6 +192,7 @@ struct Dev {
   bool use_tc = false;
   std::vector<float> tc_host;
   std::unordered_map<int64_t, int64_t> tc_off;   // matrix id → float offset
+  std::unordered_map<int64_t, int64_t> tc_boff;  // matrix id → float offset of its k_m2l_tc B operand
   float* tcpool = nullptr;
 };
 
@@ -264,6 +268,42 @@ static int64_t tc_matrix(Context* ctx, Dev* d, int64_t m) {
       }
     }
   d->tc_off.emplace(m, off);
+  return off;
+}
+
+// B operand of k_m2l_tc: the real 2R × 2C form of matrix m (as in tc_matrix) as
+// nrp ≥ 2R rows × K = 2C (zero-padded to nkc 16-float chunks), per chunk
+// [hi: nrp × 16 | lo: nrp × 16] in the canonical K-major no-swizzle layout
+// (core matrices of 8 rows × 16 B; the rows of one 4-float k-group contiguous)
+static int64_t tc_bop(Context* ctx, Dev* d, int64_t m, int nrp, int nkc) {
+  auto it = d->tc_boff.find(m);
+  if (it != d->tc_boff.end()) return it->second;
+  const Plan& p = ctx->plan;
+  const MatInfo& mi = p.mats[m];
+  const int R = mi.rows, C = mi.cols;
+  const int64_t off = (int64_t)d->tc_host.size();
+  const size_t blk = (size_t)nrp * TC_KC;
+  d->tc_host.resize(d->tc_host.size() + (size_t)nkc * 2 * blk, 0.0f);
+  float* base = d->tc_host.data() + off;
+  const cf* M = p.pool.data() + mi.offset;
+  for (int kc = 0; kc < nkc; ++kc) {
+    float* hi = base + (size_t)kc * 2 * blk;
+    float* lo = hi + blk;
+    for (int gr = 0; gr < 2 * R && gr < nrp; ++gr) {
+      const int i = gr >> 1;
+      for (int k = 0; k < TC_KC; ++k) {
+        const int gk = kc * TC_KC + k, j = gk >> 1;
+        if (j >= C) continue;
+        const cf v = M[(size_t)j * R + i];
+        const float x = (gr & 1) == 0 ? ((gk & 1) == 0 ? v.real() : -v.imag()) : ((gk & 1) == 0 ? v.imag() : v.real());
+        const float h = tf32_rna(x), l = tf32_rna(x - h);
+        const size_t idx = ((size_t)((k >> 2) * (nrp / 8) + (gr >> 3)) * 8 + (gr & 7)) * 4 + (k & 3);
+        hi[idx] = h;
+        lo[idx] = l;
+      }
+    }
+  }
+  d->tc_boff.emplace(m, off);
   return off;
 }
 
@@ -456,6 +496,7 @@ fda_status engine_create(Context* ctx) {
   d->kp.inv_k = (float)(1.0 / ctx->p.k);
   d->use_tc = ctx->p.opt.tensor_cores != 0;
   if (d->use_tc) CK(tc_prepare());
+  if (d->use_tc) CK(m2l_tc_prepare());
   CK(m2l_lr_prepare());
 
   // leaf-local element data in wave units (fp32 k·(offset from the owning leaf
@@ -663,8 +704,27 @@ fda_status engine_create(Context* ctx) {
         lr_tc[l] = nops[l] > 0 && ctx->p.opt.tensor_cores == 1;   // auto: the fused CUDA-core kernel
                                                                    // measured faster (config 3/5)
     }
+    // fused tensor-core kernel (opt.lr_tensor_cores): per level, the ops with r ≤ 32, T ≤ 224
+    std::vector<char> lr_f(nlev, 0);
+    if (d->use_tc && ctx->p.opt.lr_tensor_cores != 0) {
+      std::vector<int64_t> nops(nlev, 0);
+      std::vector<std::unordered_map<int64_t, int>> nm(nlev);
+      for (const LrOp& o : p.m2l_lr) {
+        if (p.mats[o.matV].rows > LRTC_MAX_R || p.mats[o.matV].cols > LRTC_MAX_T) continue;
+        ++nops[o.level];
+        nm[o.level][o.matV] = 1;
+      }
+      for (int l = 0; l < nlev; ++l)
+        lr_f[l] = nops[l] > 0 && !lr_tc[l] &&
+                  (ctx->p.opt.lr_tensor_cores == 1 || (double)nops[l] >= 64.0 * (double)nm[l].size());
+    }
+    std::vector<std::vector<LrOp>> ftc(nlev);
     int64_t tmp_off = 0;
     for (const LrOp& o : p.m2l_lr) {
+      if (lr_f[o.level] && p.mats[o.matV].rows <= LRTC_MAX_R && p.mats[o.matV].cols <= LRTC_MAX_T) {
+        ftc[o.level].push_back(o);
+        continue;
+      }
       if (p.mats[o.matV].rows <= LR_MAX_R && !lr_tc[o.level]) {
         fused[o.level].push_back(o);
         continue;
@@ -710,6 +770,38 @@ fda_status engine_create(Context* ctx) {
         return (int64_t)(r1 * t.T + ((t.T + 31) / 32) * 32 * t.r) * t.op_count;
       };
       Dev::M2LLevel& L = d->m2lv[l];
+      {   // tensor-core tasks: ≤ 128 ops per factored K̃, op offsets appended to ls / ld
+        auto& Ft = ftc[l];
+        std::stable_sort(Ft.begin(), Ft.end(), [](const LrOp& x, const LrOp& y) {
+          return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
+        });
+        std::vector<LrTcTask> tt;
+        for (size_t i = 0; i < Ft.size();) {
+          size_t j = i;
+          while (j < Ft.size() && Ft[j].matV == Ft[i].matV && j - i < 128) ++j;
+          const int r = p.mats[Ft[i].matV].rows, T = p.mats[Ft[i].matV].cols;
+          LrTcTask tk;
+          tk.T = T;
+          tk.r = r;
+          tk.n1 = 2 * ((r + 7) / 8) * 8;
+          tk.n2 = 2 * ((T + 7) / 8) * 8;
+          tk.nk1 = (2 * T + TC_KC - 1) / TC_KC;
+          tk.stage_fl = m2l_tc_stage_fl(tk.n1, tk.n2);
+          tk.b1_off = tc_bop(ctx, d, Ft[i].matV, tk.n1, tk.nk1);
+          tk.b2_off = tc_bop(ctx, d, Ft[i].matU, tk.n2, tk.n1 / TC_KC);
+          tk.op_begin = (int32_t)ls.size();
+          tk.op_count = (int32_t)(j - i);
+          for (size_t q = i; q < j; ++q) {
+            ls.push_back(p.out_offset[Ft[q].src]);
+            ld.push_back(p.in_offset[Ft[q].dst]);
+          }
+          L.lrtc_smem = std::max(L.lrtc_smem, m2l_tc_smem(tk.n1, tk.n2, T));
+          tt.push_back(tk);
+          i = j;
+        }
+        L.n_lrtc = (int)tt.size();
+        if (L.n_lrtc) UP(&L.lrtc, tt.data(), tt.size());
+      }
       for (int c = 0; c < LR_NCLS; ++c) {
         std::stable_sort(lt[c].begin(), lt[c].end(),
                          [&](const LrTask& x, const LrTask& y) { return cost(x) > cost(y); });
@@ -765,6 +857,7 @@ fda_status engine_create(Context* ctx) {
   for (auto& L : d->m2lv) {
     cnt(L.dense); cnt(L.a); cnt(L.b);
     for (int c = 0; c < LR_NCLS; ++c) nl += L.n_lr[c] > 0;
+    nl += L.n_lrtc > 0;
   }
   ctx->launches_per_matvec = nl;
   CK(cudaStreamCreateWithFlags(&d->s_near, cudaStreamNonBlocking));
@@ -773,7 +866,7 @@ fda_status engine_create(Context* ctx) {
   d->ev_up.resize(nlev);
   d->ev_m2l.resize(nlev);
   for (auto& v : d->ev_m2l) {
-    v.resize(LR_NCLS + 1);
+    v.resize(LR_NCLS + 2);
     for (auto& e : v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   for (auto& e : d->ev_up) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -880,6 +973,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   const int nlev = (int)d->m2m.size();
   auto m2l_level = [&](int l, cudaStream_t st) {
     const Dev::M2LLevel& L = d->m2lv[l];
+    launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, st);
     for (int c = LR_NCLS - 1; c >= 0; --c)
       launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st);
     launch_stage(L.dense, d->pool, d->outb, d->inb, st);
@@ -918,6 +1012,11 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
         return FDA_OK;
       };
       fda_status bs;
+      if (L.n_lrtc &&
+          (bs = branch([&](cudaStream_t sm) {
+             launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, sm);
+           })) != FDA_OK)
+        return bs;
       for (int c = LR_NCLS - 1; c >= 0; --c)
         if (L.n_lr[c] &&
             (bs = branch([&](cudaStream_t sm) {
@@ -1007,6 +1106,12 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
   for (int l = nlev - 1; l >= 0; --l) {   // M2L branches of every level, concurrent
     const Dev::M2LLevel& L = d->m2lv[l];
     if (!L.any()) continue;
+    if (L.n_lrtc) {
+      cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];
+      CK(cudaStreamWaitEvent(sm, d->ev_up[0], 0));
+      launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, sm);
+      CK(cudaEventRecord(d->ev_m2l[l][nbr[l]++], sm));
+    }
     for (int c = LR_NCLS - 1; c >= -1; --c) {
       if (c >= 0 && !L.n_lr[c]) continue;
       cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];

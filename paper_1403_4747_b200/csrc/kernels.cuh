@@ -68,7 +68,26 @@ struct TcTask {
   int32_t op_begin, op_count;
   int32_t kc0, kc1;   // this task's K chunks (split-K: partial products accumulate atomically)
 };
-int tc_variant(int n, int tiles, bool multi);   // multi: the 2-stage, several-CTAs-per-SM variants
+int tc_variant(int n, int tiles, bool multi);
+
+// fused §4.2 M2L on the tensor cores (kernels_tc.cu, k_m2l_tc): ≤ 128 ops sharing K̃ ≈ Û V̂
+// with r ≤ 32; B operands pre-laid-out in the tensor-core pool (engine.cu: tc_bop)
+struct LrTcTask {
+  int64_t b1_off;     // float offset of A_Vᵀ: n1 rows × 2T (padded to nk1·16) K, per 16-float chunk [hi | lo]
+  int64_t b2_off;     // float offset of A_Uᵀ: n2 rows × n1 K
+  int32_t T, r;
+  int32_t n1, n2;     // 2·⌈r/8⌉·8 and 2·⌈T/8⌉·8
+  int32_t nk1;        // ⌈2T / 16⌉
+  int32_t stage_fl;   // floats per ring stage (m2l_tc_stage_fl)
+  int32_t op_begin, op_count;
+};
+constexpr int LRTC_MAX_R = 32;
+constexpr int LRTC_MAX_T = 224;
+size_t m2l_tc_smem(int n1, int n2, int T);
+int m2l_tc_stage_fl(int n1, int n2);
+cudaError_t m2l_tc_prepare();
+void launch_m2l_tc(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off, const float* tcpool,
+                   const float2* src, float2* dst, size_t smem, cudaStream_t s);   // multi: the 2-stage, several-CTAs-per-SM variants
 int tc_variant_ops(int v);
 
 // leaf-level ops (S2M / L2T)

@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace fda {
@@ -281,6 +283,241 @@ __global__ void __launch_bounds__(128, MINB) k_xlate_tc(const TcTask* __restrict
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols(TILES * N)));
+}
+
+// ---------------------------------------------------------------------------
+// Fused §4.2 M2L on the tensor cores (§4.2):
+//   dst[:, op] += Û (V̂ src[:, op])   for ≤ 128 ops sharing one factored K̃ ≈ Û V̂.
+// The ops are the M = 128 rows (TMEM lanes) of both products, in the interleaved
+// real form of the kernel above transposed (row op = the op's state as a real
+// vector of length 2T):
+//   phase 1  D1 (128 × 2R1p) = S (128 × 2T) · A_Vᵀ,   A_V = real 2r × 2T form of V̂;
+//   phase 2  D2 (128 × 2Tp)  = D1 (128 × 2R1p) · A_Uᵀ, A_U = real 2T × 2r form of Û,
+// so the B operands (A_Vᵀ, A_Uᵀ) are pre-laid-out constants (host, engine.cu:
+// tc_bop) streamed by the TMA engine, the A operand of phase 1 is the gathered
+// source states (each thread loads its op's K chunk, splits it into tf32
+// hi / lo in registers and stores both into the canonical K-major layout),
+// and the A operand of phase 2 is phase 1's accumulator read back from TMEM
+// (tcgen05.ld) and split the same way — the r-vector tmp never leaves the SM.
+// 3xTF32 throughout (hi·hi + hi·lo + lo·hi).  Epilogue: each thread holds its
+// op's whole output state (tcgen05.ld of its TMEM lane) and adds it to the
+// destination state with 16-byte vector atomics.
+namespace {
+constexpr int LRTC_STAGES = 3;
+__device__ __forceinline__ uint32_t idesc_n(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ float4 tf32_hi4(float4 v) {
+  return make_float4(__uint_as_float(__float_as_uint(v.x) & 0xffffe000u), __uint_as_float(__float_as_uint(v.y) & 0xffffe000u),
+                     __uint_as_float(__float_as_uint(v.z) & 0xffffe000u), __uint_as_float(__float_as_uint(v.w) & 0xffffe000u));
+}
+// A operand row `row` (0…127), k-group kg (4 floats) of a [hi | lo] 128 × 16-float chunk
+__device__ __forceinline__ void put_a(float* chunk, int row, int kg, float4 v) {
+  const float4 h = tf32_hi4(v);
+  const int idx = ((kg * 16 + (row >> 3)) * 8 + (row & 7)) * 4;
+  *reinterpret_cast<float4*>(chunk + idx) = h;
+  *reinterpret_cast<float4*>(chunk + 128 * TC_KC + idx) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+}
+}  // namespace
+
+__global__ void __launch_bounds__(128, 1) k_m2l_tc(const LrTcTask* __restrict__ tasks,
+                                                   const int64_t* __restrict__ src_off,
+                                                   const int64_t* __restrict__ dst_off,
+                                                   const float* __restrict__ tcpool, const float2* __restrict__ src,
+                                                   float2* __restrict__ dst) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* sbase = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t mbar_b[LRTC_STAGES], mbar_m[LRTC_STAGES];
+  __shared__ uint32_t tmem_base_sh;
+  const LrTcTask t = tasks[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int N1 = t.n1, N2 = t.n2;                 // D1 / D2 columns (2·R1p, 2·Tp)
+  const int nk1 = t.nk1, nk2 = N1 / TC_KC;        // K chunks of phase 1 (⌈2T/16⌉) and phase 2
+  const int stage_fl = t.stage_fl;                // floats per ring stage
+  float* sA2 = sbase + LRTC_STAGES * stage_fl;    // phase-2 A operand: nk2 × [hi | lo] 128 × 16
+  const uint32_t ncols = tmem_cols(N1 > N2 ? N1 : N2);   // D1 and (after it is read) D2 at column 0
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  if (tid == 0) {
+    for (int q = 0; q < LRTC_STAGES; ++q) {
+      mbar_init(&mbar_b[q], 1);
+      mbar_init(&mbar_m[q], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  const bool valid = tid < t.op_count;
+  const float* sp = valid ? reinterpret_cast<const float*>(src) + 2 * src_off[t.op_begin + tid] : nullptr;
+  const int K2 = 2 * t.T;
+  const float* gB1 = tcpool + t.b1_off;
+  const float* gB2 = tcpool + t.b2_off;
+  const uint32_t b1_bytes = (uint32_t)N1 * TC_KC * 2 * 4, b2_bytes = (uint32_t)N2 * TC_KC * 2 * 4;
+
+  // ---- phase 1: S-stage ring over the K chunks of the states.  issue(c): each
+  // thread copies its op's 16 floats of chunk c (4 × 16-B cp.async, zero-filled
+  // past 2T) straight into the stage's A-hi slot of the canonical layout; thread 0
+  // streams the B1 chunk with the TMA engine.  Chunk c is split in place into
+  // tf32 hi / lo by the thread that owns the row (no barrier needed between the
+  // copy and the split), then one thread issues its 6 MMAs.
+  auto issue = [&](int c) {
+    const int st = c % LRTC_STAGES;
+    float* sA = sbase + st * stage_fl;
+    if (tid == 0) {
+      mbar_expect_tx(&mbar_b[st], b1_bytes);
+      bulk_g2s(sA + 2 * 128 * TC_KC, gB1 + (int64_t)c * N1 * TC_KC * 2, b1_bytes, &mbar_b[st]);
+    }
+#pragma unroll
+    for (int kg = 0; kg < 4; ++kg) {
+      const int k = c * TC_KC + 4 * kg;
+      const int bytes = valid ? 4 * min(4, max(0, K2 - k)) : 0;
+      cp16z(sA + ((kg * 16 + (tid >> 3)) * 8 + (tid & 7)) * 4, bytes ? (const void*)(sp + k) : (const void*)src, bytes);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  for (int c = 0; c < LRTC_STAGES - 1; ++c) {
+    if (c < nk1) issue(c);
+    else asm volatile("cp.async.commit_group;\n" ::);
+  }
+  for (int c = 0; c < nk1; ++c) {
+    const int st = c % LRTC_STAGES;
+    const int cn = c + LRTC_STAGES - 1;
+    if (cn < nk1) {
+      if (c >= 1) mbar_wait(&mbar_m[(c - 1) % LRTC_STAGES], ((c - 1) / LRTC_STAGES) & 1);   // stage of cn is free
+      issue(cn);
+    } else {
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(LRTC_STAGES - 1) : "memory");
+    float* sA = sbase + st * stage_fl;
+    float* sB = sA + 2 * 128 * TC_KC;
+#pragma unroll
+    for (int kg = 0; kg < 4; ++kg) {
+      const int idx = ((kg * 16 + (tid >> 3)) * 8 + (tid & 7)) * 4;
+      put_a(sA, tid, kg, *reinterpret_cast<const float4*>(sA + idx));
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(&mbar_b[st], (c / LRTC_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      const uint32_t idesc = idesc_n(N1);
+      const uint32_t a_hi = smem_u32(sA), a_lo = a_hi + 128 * TC_KC * 4;
+      const uint32_t b_hi = smem_u32(sB), b_lo = b_hi + N1 * TC_KC * 4;
+#pragma unroll
+      for (int s = 0; s < TC_KC / 8; ++s) {
+        const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (N1 / 8) * 128);
+        const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
+        const uint64_t Bh = make_desc(b_hi + bo, (N1 / 8) * 128, 128), Bl = make_desc(b_lo + bo, (N1 / 8) * 128, 128);
+        mma_tf32(tmem, Ah, Bh, idesc, (c > 0 || s > 0) ? 1u : 0u);
+        mma_tf32(tmem, Ah, Bl, idesc, 1u);
+        mma_tf32(tmem, Al, Bh, idesc, 1u);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                       smem_u32(&mbar_m[st]))
+                   : "memory");
+    }
+  }
+  mbar_wait(&mbar_m[(nk1 - 1) % LRTC_STAGES], ((nk1 - 1) / LRTC_STAGES) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+
+  // ---- tmp: D1 row (this thread's op) → phase-2 A operand (tf32 hi / lo, K-major)
+  for (int c0 = 0; c0 < N1; c0 += 16) {
+    float w[16];
+    tmem_ld16(tmem + lane_base + c0, w);
+    float* ch = sA2 + (c0 / TC_KC) * 2 * 128 * TC_KC;
+#pragma unroll
+    for (int kg = 0; kg < 4; ++kg) put_a(ch, tid, kg, make_float4(w[4 * kg], w[4 * kg + 1], w[4 * kg + 2], w[4 * kg + 3]));
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+
+  // ---- phase 2 (one thread): B2 chunks through the same ring (global chunk
+  // index nk1 + c2), MMAs into D2 — TMEM columns 0 … N2-1, D1 has been read
+  if (tid == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    auto load_b2 = [&](int c2) {
+      const int cc = nk1 + c2, st = cc % LRTC_STAGES;
+      if (cc >= LRTC_STAGES) mbar_wait(&mbar_m[st], ((cc - LRTC_STAGES) / LRTC_STAGES) & 1);
+      mbar_expect_tx(&mbar_b[st], b2_bytes);
+      bulk_g2s(sbase + st * stage_fl, gB2 + (int64_t)c2 * N2 * TC_KC * 2, b2_bytes, &mbar_b[st]);
+    };
+    for (int c2 = 0; c2 < nk2 && c2 < LRTC_STAGES - 1; ++c2) load_b2(c2);
+    for (int c2 = 0; c2 < nk2; ++c2) {
+      const int cc = nk1 + c2, st = cc % LRTC_STAGES;
+      if (c2 + LRTC_STAGES - 1 < nk2) load_b2(c2 + LRTC_STAGES - 1);
+      mbar_wait(&mbar_b[st], (cc / LRTC_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      const uint32_t b_hi = smem_u32(sbase + st * stage_fl), b_lo = b_hi + N2 * TC_KC * 4;
+      const uint32_t a_hi = smem_u32(sA2 + c2 * 2 * 128 * TC_KC), a_lo = a_hi + 128 * TC_KC * 4;
+#pragma unroll
+      for (int s = 0; s < TC_KC / 8; ++s) {
+        const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (N2 / 8) * 128);
+        const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
+        for (int n0 = 0; n0 < N2; n0 += 256) {
+          const int nn = min(256, N2 - n0);
+          const uint32_t idesc = idesc_n(nn);
+          const uint32_t no = (uint32_t)((n0 / 8) * 128);
+          const uint64_t Bh = make_desc(b_hi + bo + no, (N2 / 8) * 128, 128);
+          const uint64_t Bl = make_desc(b_lo + bo + no, (N2 / 8) * 128, 128);
+          const uint32_t d = tmem + n0;
+          mma_tf32(d, Ah, Bh, idesc, (c2 > 0 || s > 0) ? 1u : 0u);
+          mma_tf32(d, Ah, Bl, idesc, 1u);
+          mma_tf32(d, Al, Bh, idesc, 1u);
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                       smem_u32(&mbar_m[st]))
+                   : "memory");
+    }
+  }
+  __syncthreads();
+  {
+    const int cl = nk1 + nk2 - 1;
+    mbar_wait(&mbar_m[cl % LRTC_STAGES], (cl / LRTC_STAGES) & 1);
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+
+  // ---- epilogue: this thread's TMEM lane holds its op's output state (interleaved re / im)
+  float2* d = valid ? dst + dst_off[t.op_begin + tid] : nullptr;
+  for (int c0 = 0; c0 < N2; c0 += 16) {
+    float w[16];
+    tmem_ld16(tmem + lane_base + c0, w);
+    if (valid) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int row = c0 / 2 + 2 * q;   // complex rows (row, row+1); row+1 ≤ T is padding when = T
+        if (row < t.T) atomicAdd(reinterpret_cast<float4*>(d + row), make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
+}
+
+size_t m2l_tc_smem(int n1, int n2, int T) {
+  const size_t stage = std::max<size_t>(2 * 128 * TC_KC + (size_t)n1 * TC_KC * 2, (size_t)n2 * TC_KC * 2);
+  (void)T;
+  return (LRTC_STAGES * stage + (size_t)(n1 / TC_KC) * 2 * 128 * TC_KC) * 4 + 1024;
+}
+int m2l_tc_stage_fl(int n1, int n2) {
+  return (int)std::max<size_t>(2 * 128 * TC_KC + (size_t)n1 * TC_KC * 2, (size_t)n2 * TC_KC * 2);
+}
+cudaError_t m2l_tc_prepare() {
+  return cudaFuncSetAttribute(k_m2l_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+void launch_m2l_tc(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off, const float* tcpool,
+                   const float2* src, float2* dst, size_t smem, cudaStream_t s) {
+  if (ntask <= 0) return;
+  k_m2l_tc<<<ntask, 128, smem, s>>>(tasks, src_off, dst_off, tcpool, src, dst);
 }
 
 namespace {

@@ -55,7 +55,7 @@ class fda_options(ctypes.Structure):
                 ("device", ctypes.c_int32), ("build_threads", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("verbose", ctypes.c_int32), ("m2l_lowrank", ctypes.c_int32),
                 ("rhs_operator", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("tensor_cores", ctypes.c_int32), ("hf_leaves", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
+                ("tensor_cores", ctypes.c_int32), ("hf_leaves", ctypes.c_int32), ("lr_tensor_cores", ctypes.c_int32)]
 
 
 class fda_solve_info(ctypes.Structure):

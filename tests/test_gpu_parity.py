@@ -359,3 +359,22 @@ def test_tensor_core_translations(lib, lowrank, tc):
     el = O.element_geometry(V, F)
     yo = fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k)
     assert _rel(y1, yo) <= MATVEC_TOL
+
+
+@pytest.mark.parametrize("mesh_s,k,ml", [(4, 40.0, 16), (5, 30.0, 32)])
+def test_tensor_core_fused_m2l(lib, mesh_s, k, ml):
+    """Fused tcgen05 §4.2 M2L (opt.lr_tensor_cores = 1: both factors on the
+    tensor cores, tmp kept on chip): same operator as the fused CUDA-core
+    kernel to fp32 rounding (3xTF32), and within the gate vs the oracle on
+    the full matvec (mesh_s = 4) or 600 sampled rows (mesh_s = 5)."""
+    V, F = icosphere(mesh_s, 0.5)
+    x = random_density(len(F), 6)
+    y0 = lib(V, F, k, 1j / k, 1e-4, max_leaf=ml, lr_tensor_cores=0).matvec(x)
+    f1 = lib(V, F, k, 1j / k, 1e-4, max_leaf=ml, lr_tensor_cores=1)
+    assert int(f1.table("launches")[0]) > 0
+    y1 = f1.matvec(x)
+    assert _rel(y1, y0) < 1e-5
+    el = O.element_geometry(V, F)
+    rows = np.arange(len(F)) if mesh_s == 4 else sampled_rows(len(F), 600, 7)
+    yo = fast.matvec_rows(el, rows, x, k, 1j / k)
+    assert _rel(y1[rows], yo) <= MATVEC_TOL
