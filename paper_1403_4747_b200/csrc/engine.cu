@@ -860,9 +860,15 @@ fda_status engine_create(Context* ctx) {
     nl += L.n_lrtc > 0;
   }
   ctx->launches_per_matvec = nl;
-  CK(cudaStreamCreateWithFlags(&d->s_near, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&d->s_cap, cudaStreamNonBlocking));
-  for (auto& sm : d->s_m2l) CK(cudaStreamCreateWithFlags(&sm, cudaStreamNonBlocking));
+  // priorities: the far-field chain (S2M → M2M → M2L → L2L → L2T, captured
+  // from s_cap and the M2L branch streams) is the critical path of the graph;
+  // the near field (no dependencies until the final join) runs at the lowest
+  // priority and fills the SMs the chain leaves idle
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CK(cudaStreamCreateWithPriority(&d->s_near, cudaStreamNonBlocking, prio_lo));
+  CK(cudaStreamCreateWithPriority(&d->s_cap, cudaStreamNonBlocking, prio_hi));
+  for (auto& sm : d->s_m2l) CK(cudaStreamCreateWithPriority(&sm, cudaStreamNonBlocking, prio_hi));
   d->ev_up.resize(nlev);
   d->ev_m2l.resize(nlev);
   for (auto& v : d->ev_m2l) {
@@ -1170,7 +1176,7 @@ static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind, int phase
       ctx->err = std::string("graph capture failed: ") + cudaGetErrorString(e);
       return FDA_E_CUDA;
     }
-    e = cudaGraphInstantiate(&ge, g, 0);
+    e = cudaGraphInstantiate(&ge, g, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
       ge = nullptr;

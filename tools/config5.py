@@ -46,6 +46,9 @@ def main():
     ap.add_argument("--rows", type=int, default=2000)
     ap.add_argument("--tc", type=int, default=2)
     ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--solve", action="store_true", help="also bm_solve the plane-wave system (GMRES tol 1e-4)")
+    ap.add_argument("--max-iter", type=int, default=400)
+    ap.add_argument("--restart", type=int, default=0)
     a = ap.parse_args()
     c = CONFIGS[a.cfg]
     t0 = time.perf_counter()
@@ -86,7 +89,23 @@ def main():
         yo = fast.matvec_rows(el, rows, x, c.k, c.alpha)
         t_or = time.perf_counter() - t0
         err = float(np.linalg.norm(y[rows] - yo) / np.linalg.norm(yo))
+    solve = None
+    if a.solve:
+        # bm_solve (GMRES, tol 1e-4) of the plane-wave system; parity where a dense
+        # solve is infeasible: the oracle's rows A_S on the sampled
+        # rows give the sampled residual ‖A_S u − b_S‖/‖b_S‖ of the GPU solution;
+        # the rigid-sphere series is a discretisation sanity check only
+        el = O.element_geometry(V, F)
+        b = O.plane_wave_rhs(el.centroid, el.normal, c.k, c.alpha, c.direction)
+        u, info = f.solve(b, tol=c.gmres_tol, max_iter=a.max_iter, restart=a.restart, check=False)
+        solve = {"tol": c.gmres_tol, **info}
+        if not a.no_oracle:
+            Au = fast.matvec_rows(el, rows, u, c.k, c.alpha)
+            solve["sampled_residual"] = float(np.linalg.norm(Au - b[rows]) / np.linalg.norm(b[rows]))
+            ser = O.rigid_sphere_total(el.centroid[rows], c.k, 0.5, c.direction)
+            solve["rel_l2_vs_series_sampled"] = float(np.linalg.norm(u[rows] - ser) / np.linalg.norm(ser))
     print(json.dumps({"config": a.cfg, "N": N, "k": c.k, "mesh_s": round(t_mesh, 1), "build_s": round(t_build, 1),
+                      "solve": solve,
                       "matvec_ms": round(mv_ms, 3), "stages_ms": {k: round(v, 3) for k, v in stages.items()},
                       "sampled_rows": len(rows), "rel_l2_sampled": err, "oracle_rows_s": t_or, "tensor_cores": a.tc,
                       "oracle_cores": fast.num_threads(), "levels": levels,
