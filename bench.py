@@ -130,7 +130,7 @@ def _config(c, N, ws, args):
     """The workload description shared by both arms (the same matvec)."""
     return {"workload": f"config {c.cfg}: {c.name}, eps={c.eps}, leaf {c.max_leaf}, plane wave "
                         f"{[float(v) for v in np.round(c.direction, 4)]}",
-            "N": N, "k": c.k, "alpha": "i/k", "eps": c.eps, "l2_flush": "256 MB write between steps",
+            "N": N, "k": c.k, "alpha": "-i/k (the paper's i/k, reading C25)", "eps": c.eps, "l2_flush": "256 MB write between steps",
             "tensor_cores": args.tensor_cores, "m2l_lowrank": bool(args.m2l_lowrank),
             "parallelism": (f"octree-sharded x{ws} (partial upward pass, NCCL exchange of outgoing states, "
                             f"all-reduce of y)") if ws > 1 else "single GPU"}

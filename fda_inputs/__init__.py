@@ -12,4 +12,4 @@ N = 8·4^n, k = π·2^(n-3)).
 """
 from .meshes import icosphere, octasphere, graded_spheroid, geodesic_sphere  # noqa: F401
 from .vectors import random_density, sampled_rows, plane_wave_direction  # noqa: F401
-from .configs import CONFIGS, config_mesh, WorkloadConfig, POINT_SOURCE, point_source_mesh  # noqa: F401
+from .configs import CONFIGS, config_mesh, WorkloadConfig, POINT_SOURCE, point_source_mesh, bm_alpha  # noqa: F401

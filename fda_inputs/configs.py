@@ -10,6 +10,19 @@ from .meshes import icosphere, graded_spheroid, geodesic_sphere
 from .vectors import plane_wave_direction
 
 
+def bm_alpha(k: float) -> complex:
+    """The paper's Burton-Miller coupling α = i/k expressed in the
+    convention of this code and its oracle (G = e^{ikr}/4πr, normals into the
+    body): α = −i/k.  DESIGN.md reading C25: the paper's printed formulas are
+    the complex conjugates of the e^{ikr} ones (reading C2), and only this sign
+    reproduces the paper's GMRES iteration counts (14 at ka = 201, P:1058-1068;
+    3-6 in Table 2) — with +i/k GMRES needs 10× more iterations at ka = 30
+    on the dense oracle operator (tests/test_oracle_dense.py) and does not
+    converge at kD = 1000.  Both signs give a uniquely solvable system with
+    the same solution; a seeded input choice, not arithmetic of the method."""
+    return -1j / k
+
+
 @dataclass(frozen=True)
 class WorkloadConfig:
     cfg: int
@@ -22,8 +35,10 @@ class WorkloadConfig:
 
     @property
     def alpha(self) -> complex:
-        """Burton-Miller coupling α = i/k."""
-        return 1j / self.k
+        """Burton-Miller coupling: the paper's α = i/k in this
+        code's convention (G = e^{ikr}/4πr, kernel normal into the body, reading
+        C1), i.e. α = −i/k — DESIGN.md reading C25."""
+        return bm_alpha(self.k)
 
     @property
     def direction(self) -> np.ndarray:

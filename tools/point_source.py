@@ -26,7 +26,7 @@ PAPER_T_IT = {5.0: 2.15, 50.0: 12.38}   # Table 3, "Present", 1 Xeon core (P:103
 def main():
     import torch
     import oracle as O
-    from fda_inputs import POINT_SOURCE, point_source_mesh
+    from fda_inputs import POINT_SOURCE, point_source_mesh, bm_alpha
     from paper_1403_4747_b200 import FDA
     ap = argparse.ArgumentParser()
     ap.add_argument("--nu", type=int, default=POINT_SOURCE["nu"])
@@ -37,7 +37,7 @@ def main():
     xs = POINT_SOURCE["source"]
     for k in POINT_SOURCE["ks"]:
         t0 = time.perf_counter()
-        f = FDA(V, F, k, 1j / k, POINT_SOURCE["eps"], max_leaf=POINT_SOURCE["max_leaf"])
+        f = FDA(V, F, k, bm_alpha(k), POINT_SOURCE["eps"], max_leaf=POINT_SOURCE["max_leaf"])
         t_build = time.perf_counter() - t0
         b = f.rhs_point_source(xs, device=True)
         y = torch.empty_like(b)

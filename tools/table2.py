@@ -34,7 +34,7 @@ PAPER = {  # (N): (k/π, eps=1e-3: T_it, N_it, err ; eps=1e-4: T_it, N_it, err) 
 
 def main():
     import torch
-    from fda_inputs import octasphere
+    from fda_inputs import octasphere, bm_alpha
     from paper_1403_4747_b200 import FDA
     ap = argparse.ArgumentParser()
     ap.add_argument("--nmin", type=int, default=3)
@@ -50,7 +50,7 @@ def main():
         N = len(F)
         k = np.pi * 2.0 ** (n - 3)
         t0 = time.perf_counter()
-        f = FDA(V, F, k, 1j / k, a.eps, **opts)
+        f = FDA(V, F, k, bm_alpha(k), a.eps, **opts)
         t_build = time.perf_counter() - t0
         ones = torch.ones(N, dtype=torch.complex64, device="cuda")
         b = f.rhs_apply(ones)
