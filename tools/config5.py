@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--solve", action="store_true", help="also bm_solve the plane-wave system (GMRES tol 1e-4)")
     ap.add_argument("--max-iter", type=int, default=400)
     ap.add_argument("--restart", type=int, default=0)
+    ap.add_argument("--lrtc", type=int, default=0, help="opt.lr_tensor_cores (fused tcgen05 factored M2L)")
     a = ap.parse_args()
     c = CONFIGS[a.cfg]
     t0 = time.perf_counter()
@@ -56,7 +57,7 @@ def main():
     t_mesh = time.perf_counter() - t0
     N = len(F)
     t0 = time.perf_counter()
-    f = FDA(V, F, c.k, c.alpha, c.eps, verbose=1, tensor_cores=a.tc)
+    f = FDA(V, F, c.k, c.alpha, c.eps, verbose=1, tensor_cores=a.tc, lr_tensor_cores=a.lrtc)
     t_build = time.perf_counter() - t0
     st = f.stats()
     levels = _level_stats(f)
@@ -108,6 +109,7 @@ def main():
                       "solve": solve,
                       "matvec_ms": round(mv_ms, 3), "stages_ms": {k: round(v, 3) for k, v in stages.items()},
                       "sampled_rows": len(rows), "rel_l2_sampled": err, "oracle_rows_s": t_or, "tensor_cores": a.tc,
+                      "lr_tensor_cores": a.lrtc, "alpha": str(c.alpha),
                       "oracle_cores": fast.num_threads(), "levels": levels,
                       "tree": {k: st[k] for k in ("n_levels", "n_hf_levels", "n_leaves", "n_m2l_pairs",
                                                   "n_direct_element_pairs", "n_corrections", "table_bytes",
