@@ -306,103 +306,109 @@ void launch_near(int ntask, const NearTask* tasks, const int2* slots, const floa
 }
 
 // ------------------------------------------------------------------ S2M (a2) / L2T (a6)
-// HBM-bound per-leaf matrix-vector products, one warp per leaf task (no shared
-// memory, no barriers: a leaf matrix is only ~10 KB, so per-CTA ramp-up and
-// reduction used to dominate).  Lane l owns rows l and l + 32 of a 64-row
-// block; every column is one coalesced warp load per row block, the vector
-// entry a broadcast load; LEAF_U columns (2·LEAF_U independent loads per lane)
-// are in flight at a time.
-constexpr int LEAF_WPB = 4;   // warps (tasks) per CTA
+// HBM-bound per-leaf matrix-vector products.  Thread (row, group): G = ⌊NT/rows⌋
+// groups split the columns (column c handled by group c mod G), so one warp
+// reads consecutive entries of the column-major matrix; each thread keeps
+// LEAF_U independent loads in flight; the G partial sums meet in shared memory.
+constexpr int LEAF_NT = 128;
 constexpr int LEAF_U = 8;
+constexpr int LEAF_MAXR = 320;
 
-__device__ __forceinline__ void cmac_leaf(float2& acc, float2 a, float2 b) {
-  acc.x = fmaf(a.x, b.x, fmaf(-a.y, b.y, acc.x));
-  acc.y = fmaf(a.x, b.y, fmaf(a.y, b.x, acc.y));
-}
-
-// rows (r0 + lane, r0 + 32 + lane) of M (rows × ncol, column-major) · v
-__device__ __forceinline__ void leaf_rows(const float2* __restrict__ M, int rows, int ncol,
-                                          const float2* __restrict__ v, int ra, int rb, float2& a, float2& b) {
-  a = make_float2(0.f, 0.f);
-  b = a;
-  const bool oa = ra < rows, ob = rb < rows;
-  int c = 0;
-  for (; c + LEAF_U <= ncol; c += LEAF_U) {
-    float2 ma[LEAF_U], mb[LEAF_U], xv[LEAF_U];
+__device__ __forceinline__ float2 leaf_colsum(const float2* __restrict__ M, int64_t ld, int row, int c0, int cstep,
+                                              int ncol, const float2* __restrict__ v) {
+  float2 acc = make_float2(0.f, 0.f);
+  for (int c = c0; c < ncol; c += LEAF_U * cstep) {
+    float2 m[LEAF_U];
 #pragma unroll
     for (int u = 0; u < LEAF_U; ++u) {
-      const int64_t col = (int64_t)(c + u) * rows;
-      xv[u] = __ldg(v + c + u);
-      ma[u] = oa ? __ldg(M + col + ra) : make_float2(0.f, 0.f);
-      mb[u] = ob ? __ldg(M + col + rb) : make_float2(0.f, 0.f);
+      const int cc = c + u * cstep;
+      m[u] = cc < ncol ? __ldg(M + (int64_t)cc * ld + row) : make_float2(0.f, 0.f);
     }
 #pragma unroll
     for (int u = 0; u < LEAF_U; ++u) {
-      cmac_leaf(a, ma[u], xv[u]);
-      cmac_leaf(b, mb[u], xv[u]);
+      const int cc = min(c + u * cstep, ncol - 1);
+      const float2 x = v[cc];
+      acc.x = fmaf(m[u].x, x.x, fmaf(-m[u].y, x.y, acc.x));
+      acc.y = fmaf(m[u].x, x.y, fmaf(m[u].y, x.x, acc.y));
     }
   }
-  for (; c < ncol; ++c) {
-    const int64_t col = (int64_t)c * rows;
-    const float2 xv = __ldg(v + c);
-    if (oa) cmac_leaf(a, __ldg(M + col + ra), xv);
-    if (ob) cmac_leaf(b, __ldg(M + col + rb), xv);
-  }
+  return acc;
 }
 
 // S2M: m̃_B = S̃_B x_B (T × n_B, column-major)   (Eq. 10; compressed S̃)
-__global__ void __launch_bounds__(32 * LEAF_WPB) k_s2m(const LeafTask* __restrict__ tasks, int ntask,
-                                                       const float2* __restrict__ pool, const float2* __restrict__ x,
-                                                       float2* __restrict__ out) {
-  const int w = blockIdx.x * LEAF_WPB + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (w >= ntask) return;
-  const LeafTask t = tasks[w];
-  for (int r0 = 0; r0 < t.T; r0 += 64) {
-    const int ra = r0 + lane, rb = r0 + 32 + lane;
-    float2 a, b;
-    leaf_rows(pool + t.mat_off, t.T, t.elem_count, x + t.elem_begin, ra, rb, a, b);
-    if (ra < t.T) out[t.state_off + ra] = a;
-    if (rb < t.T) out[t.state_off + rb] = b;
+__global__ void __launch_bounds__(LEAF_MAXR) k_s2m(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
+                                                   const float2* __restrict__ x, float2* __restrict__ out) {
+  __shared__ float2 sx[128];
+  __shared__ float2 red[LEAF_MAXR];
+  const LeafTask t = tasks[blockIdx.x];
+  const int nb = t.elem_count, T = t.T;
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) sx[j] = x[t.elem_begin + j];
+  __syncthreads();
+  const int G = max(1, (int)blockDim.x / T);
+  const int r = threadIdx.x % T, g = threadIdx.x / T;
+  float2 acc = make_float2(0.f, 0.f);
+  if (g < G) acc = leaf_colsum(pool + t.mat_off, T, r, g, G, nb, sx);
+  if (G == 1) {
+    if (threadIdx.x < T) out[t.state_off + r] = acc;
+    return;
+  }
+  if (g < G) red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < T) {
+    float2 s = red[threadIdx.x];
+    for (int q = 1; q < G; ++q) {
+      const float2 v = red[q * T + threadIdx.x];
+      s.x += v.x; s.y += v.y;
+    }
+    out[t.state_off + r] = s;
   }
 }
 
 // L2T: y_B = T̃_B ℓ̃_B (n_B × T column-major)   (Eq. 12; compressed T̃)
 // ADD: accumulate (HF leaves have one task per incoming wedge); else overwrite.
 template <bool ADD>
-__global__ void __launch_bounds__(32 * LEAF_WPB) k_l2t(const LeafTask* __restrict__ tasks, int ntask,
-                                                       const float2* __restrict__ pool, const float2* __restrict__ in,
-                                                       float2* __restrict__ y) {
-  const int w = blockIdx.x * LEAF_WPB + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (w >= ntask) return;
-  const LeafTask t = tasks[w];
+__global__ void __launch_bounds__(LEAF_NT) k_l2t(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
+                                                 const float2* __restrict__ in, float2* __restrict__ y) {
+  __shared__ float2 sl[LEAF_MAXR];
+  __shared__ float2 red[LEAF_NT];
+  const LeafTask t = tasks[blockIdx.x];
   const int nb = t.elem_count;
-  for (int r0 = 0; r0 < nb; r0 += 64) {
-    const int ra = r0 + lane, rb = r0 + 32 + lane;
-    float2 a = make_float2(0.f, 0.f), b = a;
-    if (t.mat_off >= 0) leaf_rows(pool + t.mat_off, nb, t.T, in + t.state_off, ra, rb, a, b);
-    else if (ADD) return;
-    if (ADD) {
-      if (ra < nb) atomicAdd(y + t.elem_begin + ra, a);
-      if (rb < nb) atomicAdd(y + t.elem_begin + rb, b);
-    } else {
-      if (ra < nb) y[t.elem_begin + ra] = a;
-      if (rb < nb) y[t.elem_begin + rb] = b;
+  if (t.mat_off < 0) {
+    if (!ADD)
+      for (int i = threadIdx.x; i < nb; i += blockDim.x) y[t.elem_begin + i] = make_float2(0.f, 0.f);
+    return;
+  }
+  for (int c = threadIdx.x; c < t.T; c += blockDim.x) sl[c] = in[t.state_off + c];
+  __syncthreads();
+  const int G = max(1, LEAF_NT / nb);
+  const int i = threadIdx.x % nb, g = threadIdx.x / nb;
+  float2 acc = make_float2(0.f, 0.f);
+  if (g < G) acc = leaf_colsum(pool + t.mat_off, nb, i, g, G, t.T, sl);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    float2 s = red[threadIdx.x];
+    for (int q = 1; q < G; ++q) {
+      const float2 v = red[q * nb + threadIdx.x];
+      s.x += v.x; s.y += v.y;
     }
+    if (ADD) atomicAdd(y + t.elem_begin + threadIdx.x, s);
+    else y[t.elem_begin + threadIdx.x] = s;
   }
 }
 
 void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const float2* x, float2* out, int max_rows,
                 cudaStream_t s) {
   if (ntask <= 0) return;
-  (void)max_rows;
-  k_s2m<<<(ntask + LEAF_WPB - 1) / LEAF_WPB, 32 * LEAF_WPB, 0, s>>>(tasks, ntask, pool, x, out);
+  int bd = ((max_rows + 31) / 32) * 32;
+  bd = bd < LEAF_NT ? LEAF_NT : (bd > LEAF_MAXR ? LEAF_MAXR : bd);
+  k_s2m<<<ntask, bd, 0, s>>>(tasks, pool, x, out);
 }
 void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s,
                 bool accumulate) {
   if (ntask <= 0) return;
-  const unsigned g = (unsigned)((ntask + LEAF_WPB - 1) / LEAF_WPB);
-  if (accumulate) k_l2t<true><<<g, 32 * LEAF_WPB, 0, s>>>(tasks, ntask, pool, in, y);
-  else k_l2t<false><<<g, 32 * LEAF_WPB, 0, s>>>(tasks, ntask, pool, in, y);
+  if (accumulate) k_l2t<true><<<ntask, LEAF_NT, 0, s>>>(tasks, pool, in, y);
+  else k_l2t<false><<<ntask, LEAF_NT, 0, s>>>(tasks, pool, in, y);
 }
 
 // ------------------------------------------------------------------ translations (a3 M2M, a4 M2L, a5 L2L)
