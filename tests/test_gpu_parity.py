@@ -255,6 +255,14 @@ def test_large_config_sampled_rows(lib, cfg):
     print(f"config{cfg} sampled-row rel-L2 = {err:.3e}; N={len(F)} levels={st['n_levels']} "
           f"hf={st['n_hf_levels']} m2l={st['n_m2l_pairs']} build={st['t_build_s']:.1f}s")
     assert err <= MATVEC_TOL
+    # bm_solve at the full size (plane wave, tol 1e-4, α per reading C25): the GPU
+    # solution satisfies the oracle's equations on the sampled rows
+    b = O.plane_wave_rhs(el.centroid, el.normal, c.k, c.alpha, c.direction)
+    u, info = f.solve(b, tol=c.gmres_tol, max_iter=150)
+    res = _rel(fast.matvec_rows(el, rows, u, c.k, c.alpha), b[rows])
+    print(f"config{cfg} solve: {info}, sampled oracle residual {res:.2e}")
+    assert info["converged"] and info["iterations"] <= 80
+    assert res <= 1e-3
 
 
 def test_rhs_apply_parity(lib):
