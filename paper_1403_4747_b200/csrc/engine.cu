@@ -161,9 +161,11 @@ struct Dev {
     int n_lr[LR_NCLS] = {};
     int64_t* lr_src = nullptr;
     int64_t* lr_dst = nullptr;
-    LrTcTask* lrtc = nullptr;        // fused §4.2 tasks on the tensor cores (k_m2l_tc)
+    LrTcTask* lrtc = nullptr;        // fused §4.2 tasks on the tensor cores (k_m2l_tc, persistent)
     int n_lrtc = 0;
     size_t lrtc_smem = 0;
+    uint32_t lrtc_cols = 0;
+    int lrtc_grid = 0, lrtc_stages = 3;
     bool any() const {
       int n = n_lrtc;
       for (int c = 0; c < LR_NCLS; ++c) n += n_lr[c];
@@ -786,7 +788,7 @@ fda_status engine_create(Context* ctx) {
           tk.n1 = 2 * ((r + 7) / 8) * 8;
           tk.n2 = 2 * ((T + 7) / 8) * 8;
           tk.nk1 = (2 * T + TC_KC - 1) / TC_KC;
-          tk.stage_fl = m2l_tc_stage_fl(tk.n1, tk.n2);
+          tk.stage_fl = m2l_tc_stage_fl(tk.n1, tk.n2);   // (raised to the level maximum below)
           tk.b1_off = tc_bop(ctx, d, Ft[i].matV, tk.n1, tk.nk1);
           tk.b2_off = tc_bop(ctx, d, Ft[i].matU, tk.n2, tk.n1 / TC_KC);
           tk.op_begin = (int32_t)ls.size();
@@ -795,9 +797,30 @@ fda_status engine_create(Context* ctx) {
             ls.push_back(p.out_offset[Ft[q].src]);
             ld.push_back(p.in_offset[Ft[q].dst]);
           }
-          L.lrtc_smem = std::max(L.lrtc_smem, m2l_tc_smem(tk.n1, tk.n2, T));
           tt.push_back(tk);
           i = j;
+        }
+        // one ring layout per launch; tasks longest first (the persistent CTAs stride over them)
+        int sfl = 0, n1m = 16, nm = 16;
+        for (const LrTcTask& tk : tt) {
+          sfl = std::max(sfl, tk.stage_fl);
+          n1m = std::max(n1m, tk.n1);
+          nm = std::max(nm, std::max(tk.n1, tk.n2));
+        }
+        for (LrTcTask& tk : tt) tk.stage_fl = sfl;
+        std::stable_sort(tt.begin(), tt.end(), [](const LrTcTask& x, const LrTcTask& y) {
+          return (int64_t)(x.nk1 + x.n1 / TC_KC) * x.n2 > (int64_t)(y.nk1 + y.n1 / TC_KC) * y.n2;
+        });
+        if (!tt.empty()) {
+          L.lrtc_smem = m2l_tc_smem(sfl, n1m);
+          L.lrtc_stages = m2l_tc_stages(sfl, n1m);
+        }
+        L.lrtc_cols = m2l_tc_cols(nm);
+        {
+          int dev = 0, nsm = 148;
+          cudaGetDevice(&dev);
+          cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+          L.lrtc_grid = std::min<int>((int)tt.size(), nsm);
         }
         L.n_lrtc = (int)tt.size();
         if (L.n_lrtc) UP(&L.lrtc, tt.data(), tt.size());
@@ -979,7 +1002,8 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   const int nlev = (int)d->m2m.size();
   auto m2l_level = [&](int l, cudaStream_t st) {
     const Dev::M2LLevel& L = d->m2lv[l];
-    launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, st);
+    launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, L.lrtc_cols,
+                  L.lrtc_grid, L.lrtc_stages, st);
     for (int c = LR_NCLS - 1; c >= 0; --c)
       launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st);
     launch_stage(L.dense, d->pool, d->outb, d->inb, st);
@@ -1020,7 +1044,8 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
       fda_status bs;
       if (L.n_lrtc &&
           (bs = branch([&](cudaStream_t sm) {
-             launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, sm);
+             launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, L.lrtc_cols,
+                    L.lrtc_grid, L.lrtc_stages, sm);
            })) != FDA_OK)
         return bs;
       for (int c = LR_NCLS - 1; c >= 0; --c)
@@ -1115,7 +1140,8 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
     if (L.n_lrtc) {
       cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];
       CK(cudaStreamWaitEvent(sm, d->ev_up[0], 0));
-      launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, sm);
+      launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, L.lrtc_cols,
+                    L.lrtc_grid, L.lrtc_stages, sm);
       CK(cudaEventRecord(d->ev_m2l[l][nbr[l]++], sm));
     }
     for (int c = LR_NCLS - 1; c >= -1; --c) {

@@ -78,16 +78,19 @@ struct LrTcTask {
   int32_t T, r;
   int32_t n1, n2;     // 2·⌈r/8⌉·8 and 2·⌈T/8⌉·8
   int32_t nk1;        // ⌈2T / 16⌉
-  int32_t stage_fl;   // floats per ring stage (m2l_tc_stage_fl)
+  int32_t stage_fl;   // floats per ring stage: the maximum of m2l_tc_stage_fl over the launch
   int32_t op_begin, op_count;
 };
 constexpr int LRTC_MAX_R = 32;
 constexpr int LRTC_MAX_T = 224;
-size_t m2l_tc_smem(int n1, int n2, int T);
-int m2l_tc_stage_fl(int n1, int n2);
+int m2l_tc_stage_fl(int n1, int n2);                 // floats per ring stage of one task
+int m2l_tc_stages(int stage_fl, int n1max);           // ring stages of a launch (3 … 8)
+size_t m2l_tc_smem(int stage_fl, int n1max);          // dynamic shared memory of a launch (uniform stage_fl)
+uint32_t m2l_tc_cols(int nmax);                       // TMEM columns for max(n1, n2) over the launch
 cudaError_t m2l_tc_prepare();
+// persistent: grid ≤ #SMs CTAs walk the tasks (sorted longest first) with stride grid
 void launch_m2l_tc(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off, const float* tcpool,
-                   const float2* src, float2* dst, size_t smem, cudaStream_t s);   // multi: the 2-stage, several-CTAs-per-SM variants
+                   const float2* src, float2* dst, size_t smem, uint32_t ncols, int grid, int stages, cudaStream_t s);   // multi: the 2-stage, several-CTAs-per-SM variants
 int tc_variant_ops(int v);
 
 // leaf-level ops (S2M / L2T)
