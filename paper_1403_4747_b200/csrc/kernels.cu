@@ -94,8 +94,8 @@ void launch_scatter_f64(const float2* yn, const float2* yf, const int32_t* perm,
 // constant k of α·k into KernelParams.  Per (target, source element) the
 // kernel values of the three Q3 points are summed first and multiplied by
 // w_j once.
-constexpr int NEAR_NT = 128;
-constexpr int NEAR_MAXS = 256;
+constexpr int NEAR_NT = 256;
+constexpr int NEAR_MAXS = 512;
 
 // MUFU.RSQ without the denormal guard of rsqrtf (q² ≥ 1e-12 here, never denormal)
 __device__ __forceinline__ float rsqrt_ftz(float x) {
