@@ -152,9 +152,23 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
       pl.tmp_size = 0;
       for (size_t l = 0; l < pl.m2l.size(); ++l) {
         std::vector<Op> dense;
+        // levels where a factored K̃ is shared by fewer than 16 ops on average (the
+        // coarse HF levels: ~10 at config 2 L2) keep the dense K̃ — the grouped dense
+        // translation kernel tiles 16 ops per CTA, the fused factored one 64
+        bool use_lr = !pl.lr_V.empty();
+        if (use_lr) {
+          std::unordered_map<int64_t, int> nm;
+          int64_t nf = 0;
+          for (const Op& op : pl.m2l[l])
+            if (pl.lr_V[op.mat] >= 0) {
+              ++nf;
+              nm[op.mat] = 1;
+            }
+          use_lr = nf >= 16 * (int64_t)nm.size();
+        }
         for (const Op& op : pl.m2l[l]) {
           ++pl.n_m2l_total;
-          if (!pl.lr_V.empty() && pl.lr_V[op.mat] >= 0) {
+          if (use_lr && pl.lr_V[op.mat] >= 0) {
             LrOp lo{op.src, op.dst, pl.lr_V[op.mat], pl.lr_U[op.mat], pl.tmp_size, (int)l};
             pl.tmp_size += pl.mats[pl.lr_V[op.mat]].rows;
             pl.m2l_lr.push_back(lo);
