@@ -91,7 +91,7 @@ typedef struct {
                             C9); 1: the count rule at every level, leaves may be HF, with
                             directional S2M / L2T per used wedge (PAPER.md P:344-346,
                             P:449-454)                                                     */
-  int32_t lr_tensor_cores;  /* §4.2 factored M2L (r ≤ 32, T ≤ 224) on the fused tcgen05 kernel
+  int32_t lr_tensor_cores;  /* §4.2 factored M2L (r ≤ 32, T ≤ 160) on the fused tcgen05 kernel
                             (both products on the tensor cores, 3xTF32, tmp kept on chip):
                             0 (default) never — the fused CUDA-core kernel is faster on B200
                             today (latency-bound at 1 CTA/SM); 1 always; 2 on

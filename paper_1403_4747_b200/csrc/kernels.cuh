@@ -82,7 +82,7 @@ struct LrTcTask {
   int32_t op_begin, op_count;
 };
 constexpr int LRTC_MAX_R = 32;
-constexpr int LRTC_MAX_T = 224;
+constexpr int LRTC_MAX_T = 160;   // keeps 3 ring stages + the phase-2 A region ≤ 220 KB (n1 ≤ 64, n2 ≤ 320)
 int m2l_tc_stage_fl(int n1, int n2);                 // floats per ring stage of one task
 int m2l_tc_stages(int stage_fl, int n1max);           // ring stages of a launch (3 … 8)
 size_t m2l_tc_smem(int stage_fl, int n1max);          // dynamic shared memory of a launch (uniform stage_fl)
