@@ -166,6 +166,7 @@ struct Dev {
     size_t lrtc_smem = 0;
     uint32_t lrtc_cols = 0;
     int lrtc_grid = 0, lrtc_stages = 3;
+    LrTcPlan lrtc_plan;
     bool any() const {
       int n = n_lrtc;
       for (int c = 0; c < LR_NCLS; ++c) n += n_lr[c];
@@ -499,6 +500,7 @@ fda_status engine_create(Context* ctx) {
   d->use_tc = ctx->p.opt.tensor_cores != 0;
   if (d->use_tc) CK(tc_prepare());
   if (d->use_tc) CK(m2l_tc_prepare());
+  if (d->use_tc) CK(m2l_tcw_prepare());
   CK(m2l_lr_prepare());
 
   // leaf-local element data in wave units (fp32 k·(offset from the owning leaf
@@ -814,6 +816,9 @@ fda_status engine_create(Context* ctx) {
         if (!tt.empty()) {
           L.lrtc_smem = m2l_tc_smem(sfl, n1m);
           L.lrtc_stages = m2l_tc_stages(sfl, n1m);
+          int n2m = 16;
+          for (const LrTcTask& tk : tt) n2m = std::max(n2m, tk.n2);
+          L.lrtc_plan = m2l_tcw_plan(n1m, n2m);
         }
         L.lrtc_cols = m2l_tc_cols(nm);
         {
@@ -1002,8 +1007,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   const int nlev = (int)d->m2m.size();
   auto m2l_level = [&](int l, cudaStream_t st) {
     const Dev::M2LLevel& L = d->m2lv[l];
-    launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, L.lrtc_cols,
-                  L.lrtc_grid, L.lrtc_stages, st);
+    launch_m2l_tcw(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_plan, L.lrtc_grid, st);
     for (int c = LR_NCLS - 1; c >= 0; --c)
       launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st);
     launch_stage(L.dense, d->pool, d->outb, d->inb, st);
@@ -1044,8 +1048,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
       fda_status bs;
       if (L.n_lrtc &&
           (bs = branch([&](cudaStream_t sm) {
-             launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, L.lrtc_cols,
-                    L.lrtc_grid, L.lrtc_stages, sm);
+             launch_m2l_tcw(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_plan, L.lrtc_grid, sm);
            })) != FDA_OK)
         return bs;
       for (int c = LR_NCLS - 1; c >= 0; --c)
@@ -1140,8 +1143,7 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
     if (L.n_lrtc) {
       cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];
       CK(cudaStreamWaitEvent(sm, d->ev_up[0], 0));
-      launch_m2l_tc(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_smem, L.lrtc_cols,
-                    L.lrtc_grid, L.lrtc_stages, sm);
+      launch_m2l_tcw(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_plan, L.lrtc_grid, sm);
       CK(cudaEventRecord(d->ev_m2l[l][nbr[l]++], sm));
     }
     for (int c = LR_NCLS - 1; c >= -1; --c) {

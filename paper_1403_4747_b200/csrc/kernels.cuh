@@ -88,6 +88,17 @@ int m2l_tc_stages(int stage_fl, int n1max);           // ring stages of a launch
 size_t m2l_tc_smem(int stage_fl, int n1max);          // dynamic shared memory of a launch (uniform stage_fl)
 uint32_t m2l_tc_cols(int nmax);                       // TMEM columns for max(n1, n2) over the launch
 cudaError_t m2l_tc_prepare();
+// warp-specialised persistent variant (k_m2l_tcw): launch plan from the level's max n1 / n2
+struct LrTcPlan {
+  int stages = 3, stage_fl = 0, b2_fl = 0, n1max = 16;
+  uint32_t ncols = 32;
+  size_t smem = 0;
+};
+LrTcPlan m2l_tcw_plan(int n1max, int n2max);
+cudaError_t m2l_tcw_prepare();
+void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                    const float* tcpool, const float2* src, float2* dst, const LrTcPlan& pl, int grid,
+                    cudaStream_t s);
 // persistent: grid ≤ #SMs CTAs walk the tasks (sorted longest first) with stride grid
 void launch_m2l_tc(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off, const float* tcpool,
                    const float2* src, float2* dst, size_t smem, uint32_t ncols, int grid, int stages, cudaStream_t s);   // multi: the 2-stage, several-CTAs-per-SM variants

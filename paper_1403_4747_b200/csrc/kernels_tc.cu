@@ -81,6 +81,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -537,6 +541,286 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const LrTcTask* __restrict__ 
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised persistent form (k_m2l_tcw, the default tensor-core M2L):
+//   warps 0-3 (the "row" warps, thread t = op t = TMEM lane t): gather the
+//     states of phase-1 ring jobs (16-B cp.async, issued S1 − 2 jobs ahead),
+//     split them hi / lo in place, arrive on a_full; at each task boundary
+//     drain the previous task's D2 (TMEM → 16-B vector atomics) and turn D1
+//     into the phase-2 A operand;
+//   warp 4 (one lane): issues every MMA and commits (frees ring stages,
+//     signals D1 / D2 complete);
+//   warp 5 (one lane): streams the B1 and B2 operands with the TMA engine.
+// TMEM: D1 in columns [0, n1max), D2 in [n1max, n1max + n2max), so the MMAs of
+// task i+1's phase 1 run while the row warps drain D2 of task i.  Barriers
+// (phase parity = use count & 1): a_full[s] (128 arrivals) + b_full[s] (TMA)
+// → MMA; empty[s] (MMA commit) → refill; b2_full / b2_empty (2-stage B2 ring);
+// d1_full, a2_full (128), d2_full, y_free (128) once per task.
+template <int S1>
+__global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__ tasks, int ntask,
+                                                    const int64_t* __restrict__ src_off,
+                                                    const int64_t* __restrict__ dst_off,
+                                                    const float* __restrict__ tcpool, const float2* __restrict__ src,
+                                                    float2* __restrict__ dst, int stage_fl, int b2_fl, int n1max,
+                                                    uint32_t ncols) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* sbase = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t a_full[S1], b_full[S1], empty[S1], b2_full[2], b2_empty[2];
+  __shared__ uint64_t d1_full, a2_full, d2_full, y_free;
+  __shared__ uint32_t tmem_base_sh;
+  constexpr int LA = S1 - 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x;
+  float* sB2 = sbase + S1 * stage_fl;              // [2][b2_fl]
+  float* sA2 = sB2 + 2 * b2_fl;                    // phase-2 A operand: (n1/16) × [hi | lo] 128 × 16
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  if (tid == 0) {
+    for (int q = 0; q < S1; ++q) {
+      mbar_init(&a_full[q], 128);
+      mbar_init(&b_full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&b2_full[q], 1);
+      mbar_init(&b2_empty[q], 1);
+    }
+    mbar_init(&d1_full, 1);
+    mbar_init(&a2_full, 128);
+    mbar_init(&d2_full, 1);
+    mbar_init(&y_free, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t tY = tmem + (uint32_t)n1max;      // D2 region
+
+  if (warp == 5) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int j = 0, b2j = 0;
+      for (int ct = blockIdx.x; ct < ntask; ct += G) {
+        const LrTcTask t = tasks[ct];
+        for (int c = 0; c < t.nk1; ++c, ++j) {
+          const int st = j % S1;
+          if (j >= S1) mbar_wait(&empty[st], ((j / S1) - 1) & 1);
+          const uint32_t bytes = (uint32_t)t.n1 * TC_KC * 2 * 4;
+          mbar_expect_tx(&b_full[st], bytes);
+          bulk_g2s(sbase + st * stage_fl + 2 * 128 * TC_KC, tcpool + t.b1_off + (int64_t)c * t.n1 * TC_KC * 2, bytes,
+                   &b_full[st]);
+        }
+        const int nk2 = t.n1 / TC_KC;
+        for (int c2 = 0; c2 < nk2; ++c2, ++b2j) {
+          const int st = b2j & 1;
+          if (b2j >= 2) mbar_wait(&b2_empty[st], ((b2j >> 1) - 1) & 1);
+          const uint32_t bytes = (uint32_t)t.n2 * TC_KC * 2 * 4;
+          mbar_expect_tx(&b2_full[st], bytes);
+          bulk_g2s(sB2 + st * b2_fl, tcpool + t.b2_off + (int64_t)c2 * t.n2 * TC_KC * 2, bytes, &b2_full[st]);
+        }
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      int j = 0, b2j = 0, i = 0;
+      for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
+        const LrTcTask t = tasks[ct];
+        const int N1 = t.n1, N2 = t.n2, nk2 = N1 / TC_KC;
+        const uint32_t idesc1 = idesc_n(N1);
+        for (int c = 0; c < t.nk1; ++c, ++j) {
+          const int st = j % S1;
+          mbar_wait(&a_full[st], (j / S1) & 1);
+          mbar_wait(&b_full[st], (j / S1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+          float* sA = sbase + st * stage_fl;
+          const uint32_t a_hi = smem_u32(sA), a_lo = a_hi + 128 * TC_KC * 4;
+          const uint32_t b_hi = smem_u32(sA + 2 * 128 * TC_KC), b_lo = b_hi + N1 * TC_KC * 4;
+#pragma unroll
+          for (int s = 0; s < TC_KC / 8; ++s) {
+            const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (N1 / 8) * 128);
+            const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
+            const uint64_t Bh = make_desc(b_hi + bo, (N1 / 8) * 128, 128), Bl = make_desc(b_lo + bo, (N1 / 8) * 128, 128);
+            mma_tf32(tmem, Ah, Bh, idesc1, (c > 0 || s > 0) ? 1u : 0u);
+            mma_tf32(tmem, Ah, Bl, idesc1, 1u);
+            mma_tf32(tmem, Al, Bh, idesc1, 1u);
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           smem_u32(&empty[st]))
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&d1_full))
+                     : "memory");
+        mbar_wait(&a2_full, i & 1);                   // tmp is in shared memory (and D1 was read)
+        if (i >= 1) mbar_wait(&y_free, (i - 1) & 1);  // D2 of the previous task was drained
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        for (int c2 = 0; c2 < nk2; ++c2, ++b2j) {
+          const int st = b2j & 1;
+          mbar_wait(&b2_full[st], (b2j >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+          const uint32_t b_hi = smem_u32(sB2 + st * b2_fl), b_lo = b_hi + N2 * TC_KC * 4;
+          const uint32_t a_hi = smem_u32(sA2 + c2 * 2 * 128 * TC_KC), a_lo = a_hi + 128 * TC_KC * 4;
+#pragma unroll
+          for (int s = 0; s < TC_KC / 8; ++s) {
+            const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (N2 / 8) * 128);
+            const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
+            for (int n0 = 0; n0 < N2; n0 += 256) {
+              const int nn = min(256, N2 - n0);
+              const uint32_t idesc = idesc_n(nn);
+              const uint32_t no = (uint32_t)((n0 / 8) * 128);
+              const uint64_t Bh = make_desc(b_hi + bo + no, (N2 / 8) * 128, 128);
+              const uint64_t Bl = make_desc(b_lo + bo + no, (N2 / 8) * 128, 128);
+              mma_tf32(tY + n0, Ah, Bh, idesc, (c2 > 0 || s > 0) ? 1u : 0u);
+              mma_tf32(tY + n0, Ah, Bl, idesc, 1u);
+              mma_tf32(tY + n0, Al, Bh, idesc, 1u);
+            }
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           smem_u32(&b2_empty[st]))
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&d2_full))
+                     : "memory");
+      }
+    }
+  } else {
+    // ---------------- row warps (tid < 128)
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    int it = blockIdx.x, ic = 0, js = 0;          // issue cursor over phase-1 jobs
+    LrTcTask ti = tasks[it];
+    const float* isp = tid < ti.op_count ? reinterpret_cast<const float*>(src) + 2 * src_off[ti.op_begin + tid] : nullptr;
+    auto issue_next = [&]() {
+      if (it < ntask) {
+        const int st = js % S1;
+        if (js >= S1) mbar_wait(&empty[st], ((js / S1) - 1) & 1);
+        float* sA = sbase + st * stage_fl;
+        const int K2 = 2 * ti.T;
+#pragma unroll
+        for (int kg = 0; kg < 4; ++kg) {
+          const int k = ic * TC_KC + 4 * kg;
+          const int nb = isp ? 4 * min(4, max(0, K2 - k)) : 0;
+          cp16z(sA + ((kg * 16 + (tid >> 3)) * 8 + (tid & 7)) * 4, nb ? (const void*)(isp + k) : (const void*)src, nb);
+        }
+        ++js;
+        if (++ic == ti.nk1) {
+          ic = 0;
+          it += G;
+          if (it < ntask) {
+            ti = tasks[it];
+            isp = tid < ti.op_count ? reinterpret_cast<const float*>(src) + 2 * src_off[ti.op_begin + tid] : nullptr;
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    };
+    for (int q = 0; q < LA; ++q) issue_next();
+    int jc = 0, i = 0;
+    LrTcTask tp{};                                 // previous task (its D2 is drained at the next boundary)
+    auto drain = [&](const LrTcTask& t) {
+      float2* d = tid < t.op_count ? dst + dst_off[t.op_begin + tid] : nullptr;
+      for (int c0 = 0; c0 < t.n2; c0 += 16) {
+        float w[16];
+        tmem_ld16(tY + lane_base + c0, w);
+        if (d) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int row = c0 / 2 + 2 * q;   // complex rows (row, row+1); row+1 = T is the padding slot
+            if (row < t.T)
+              atomicAdd(reinterpret_cast<float4*>(d + row), make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      mbar_arrive(&y_free);
+    };
+    for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
+      const LrTcTask t = tasks[ct];
+      for (int c = 0; c < t.nk1; ++c, ++jc) {
+        issue_next();
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(LA) : "memory");
+        float* sA = sbase + (jc % S1) * stage_fl;
+#pragma unroll
+        for (int kg = 0; kg < 4; ++kg) {
+          const int idx = ((kg * 16 + (tid >> 3)) * 8 + (tid & 7)) * 4;
+          put_a(sA, tid, kg, *reinterpret_cast<const float4*>(sA + idx));
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive(&a_full[jc % S1]);
+      }
+      if (i >= 1) {                                // D2 of the previous task → destination states
+        mbar_wait(&d2_full, (i - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        drain(tp);
+      }
+      mbar_wait(&d1_full, i & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      for (int c0 = 0; c0 < t.n1; c0 += 16) {
+        float w[16];
+        tmem_ld16(tmem + lane_base + c0, w);
+        float* ch = sA2 + (c0 / TC_KC) * 2 * 128 * TC_KC;
+#pragma unroll
+        for (int kg = 0; kg < 4; ++kg)
+          put_a(ch, tid, kg, make_float4(w[4 * kg], w[4 * kg + 1], w[4 * kg + 2], w[4 * kg + 3]));
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      mbar_arrive(&a2_full);
+      tp = t;
+    }
+    if (i >= 1) {
+      mbar_wait(&d2_full, (i - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      drain(tp);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
+}
+
+// warp-specialised plan for one launch: ring stages S1 (3 … 6) of one 16-float K
+// chunk (A hi|lo + B1 hi|lo), a 2-stage B2 ring and the phase-2 A region ≤ 220 KB
+LrTcPlan m2l_tcw_plan(int n1max, int n2max) {
+  LrTcPlan pl;
+  pl.stage_fl = 2 * 128 * TC_KC + n1max * TC_KC * 2;
+  pl.b2_fl = n2max * TC_KC * 2;
+  const size_t a2 = (size_t)(n1max / TC_KC) * 2 * 128 * TC_KC;
+  const size_t cap = (220 * 1024 - 1024) / 4 - 2 * (size_t)pl.b2_fl - a2;
+  const int s = (int)(cap / pl.stage_fl);
+  pl.stages = s >= 6 ? 6 : (s >= 4 ? 4 : 3);
+  pl.smem = ((size_t)pl.stages * pl.stage_fl + 2 * (size_t)pl.b2_fl + a2) * 4 + 1024;
+  pl.ncols = tmem_cols(n1max + n2max);
+  pl.n1max = n1max;
+  return pl;
+}
+cudaError_t m2l_tcw_prepare() {
+  cudaError_t e = cudaFuncSetAttribute(k_m2l_tcw<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_tcw<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_tcw<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  return e;
+}
+void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                    const float* tcpool, const float2* src, float2* dst, const LrTcPlan& pl, int grid,
+                    cudaStream_t s) {
+  if (ntask <= 0) return;
+#define TCW(S)                                                                                                   \
+  k_m2l_tcw<S><<<grid, 192, pl.smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst, pl.stage_fl, pl.b2_fl, \
+                                          pl.n1max, pl.ncols)
+  switch (pl.stages) {
+    case 6: TCW(6); break;
+    case 4: TCW(4); break;
+    default: TCW(3); break;
+  }
+#undef TCW
 }
 
 int m2l_tc_stage_fl(int n1, int n2) {
