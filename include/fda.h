@@ -93,9 +93,10 @@ typedef struct {
                             P:449-454)                                                     */
   int32_t lr_tensor_cores;  /* §4.2 factored M2L (r ≤ 32, T ≤ 160) on the fused tcgen05 kernel
                             (both products on the tensor cores, 3xTF32, tmp kept on chip):
-                            0 (default) never — the fused CUDA-core kernel is faster on B200
-                            today (latency-bound at 1 CTA/SM); 1 always; 2 on
-                            levels with ≥ 64 ops per factored K̃; needs tensor_cores ≠ 0  */
+                            (persistent, warp-specialised k_m2l_tcw): 0 never (fused CUDA-core
+                            kernel), 1 always, 2 (default) on levels with ≥ 64 ops per factored
+                            K̃ and ≥ 10 GFLOP of factored work; needs
+                            tensor_cores ≠ 0                                               */
 } fda_options;
 
 typedef struct {

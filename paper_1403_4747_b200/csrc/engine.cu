@@ -708,19 +708,26 @@ fda_status engine_create(Context* ctx) {
         lr_tc[l] = nops[l] > 0 && ctx->p.opt.tensor_cores == 1;   // auto: the fused CUDA-core kernel
                                                                    // measured faster (config 3/5)
     }
-    // fused tensor-core kernel (opt.lr_tensor_cores): per level, the ops with r ≤ 32, T ≤ 224
+    // fused tensor-core kernel (opt.lr_tensor_cores): per level, the ops with r ≤ 32, T ≤ LRTC_MAX_T.
+    // Auto (2): levels with ≥ 64 ops per factored K̃ and ≥ 10 GFLOP of factored work — the
+    // persistent kernel owns every SM while it runs, which pays on large levels (config 5:
+    // M2L 32.6 vs 34.9 ms) but not on small ones that share the GPU with the near field
+    // inside the graph (config 2: matvec 0.481 vs 0.471 ms)
     std::vector<char> lr_f(nlev, 0);
     if (d->use_tc && ctx->p.opt.lr_tensor_cores != 0) {
       std::vector<int64_t> nops(nlev, 0);
+      std::vector<double> fl(nlev, 0.0);
       std::vector<std::unordered_map<int64_t, int>> nm(nlev);
       for (const LrOp& o : p.m2l_lr) {
         if (p.mats[o.matV].rows > LRTC_MAX_R || p.mats[o.matV].cols > LRTC_MAX_T) continue;
         ++nops[o.level];
+        fl[o.level] += 16.0 * p.mats[o.matV].rows * p.mats[o.matV].cols;
         nm[o.level][o.matV] = 1;
       }
       for (int l = 0; l < nlev; ++l)
         lr_f[l] = nops[l] > 0 && !lr_tc[l] &&
-                  (ctx->p.opt.lr_tensor_cores == 1 || (double)nops[l] >= 64.0 * (double)nm[l].size());
+                  (ctx->p.opt.lr_tensor_cores == 1 ||
+                   ((double)nops[l] >= 64.0 * (double)nm[l].size() && fl[l] >= 1e10));
     }
     std::vector<std::vector<LrOp>> ftc(nlev);
     int64_t tmp_off = 0;

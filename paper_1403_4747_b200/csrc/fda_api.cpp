@@ -45,7 +45,7 @@ fda_status fda_options_default(fda_options* opt) {
   opt->nranks = 1;
   opt->tensor_cores = 2;
   opt->hf_leaves = 0;
-  opt->lr_tensor_cores = 0;
+  opt->lr_tensor_cores = 2;
   return FDA_OK;
 }
 
