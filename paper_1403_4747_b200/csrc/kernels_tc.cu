@@ -558,8 +558,10 @@ __global__ void __launch_bounds__(128, 1) k_m2l_tc(const LrTcTask* __restrict__ 
 // (phase parity = use count & 1): a_full[s] (128 arrivals) + b_full[s] (TMA)
 // → MMA; empty[s] (MMA commit) → refill; b2_full / b2_empty (2-stage B2 ring);
 // d1_full, a2_full (128), d2_full, y_free (128) once per task.
+constexpr int TCW_RW = 8;                   // row warps (two threads per op row)
+constexpr int TCW_NT = 32 * (TCW_RW + 2);   // + MMA warp + TMA warp
 template <int S1>
-__global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__ tasks, int ntask,
+__global__ void __launch_bounds__(TCW_NT, 1) k_m2l_tcw(const LrTcTask* __restrict__ tasks, int ntask,
                                                     const int64_t* __restrict__ src_off,
                                                     const int64_t* __restrict__ dst_off,
                                                     const float* __restrict__ tcpool, const float2* __restrict__ src,
@@ -570,7 +572,7 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
   __shared__ uint64_t a_full[S1], b_full[S1], empty[S1], b2_full[2], b2_empty[2];
   __shared__ uint64_t d1_full, a2_full, d2_full, y_free;
   __shared__ uint32_t tmem_base_sh;
-  constexpr int LA = S1 - 2;
+  constexpr int LA = S1 > 4 ? S1 - 3 : S1 - 2;   // lookahead of the gathers; the rest is MMA-completion slack
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x;
   float* sB2 = sbase + S1 * stage_fl;              // [2][b2_fl]
@@ -582,7 +584,7 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
   }
   if (tid == 0) {
     for (int q = 0; q < S1; ++q) {
-      mbar_init(&a_full[q], 128);
+      mbar_init(&a_full[q], 32 * TCW_RW);
       mbar_init(&b_full[q], 1);
       mbar_init(&empty[q], 1);
     }
@@ -591,9 +593,9 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
       mbar_init(&b2_empty[q], 1);
     }
     mbar_init(&d1_full, 1);
-    mbar_init(&a2_full, 128);
+    mbar_init(&a2_full, 32 * TCW_RW);
     mbar_init(&d2_full, 1);
-    mbar_init(&y_free, 128);
+    mbar_init(&y_free, 32 * TCW_RW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
@@ -602,7 +604,7 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
   const uint32_t tmem = tmem_base_sh;
   const uint32_t tY = tmem + (uint32_t)n1max;      // D2 region
 
-  if (warp == 5) {
+  if (warp == TCW_RW + 1) {
     // ---------------- TMA producer
     if (lane == 0) {
       int j = 0, b2j = 0;
@@ -626,7 +628,7 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
         }
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == TCW_RW) {
     // ---------------- MMA issuer
     if (lane == 0) {
       int j = 0, b2j = 0, i = 0;
@@ -692,11 +694,14 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
       }
     }
   } else {
-    // ---------------- row warps (tid < 128)
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    // ---------------- row warps: thread (row = tid & 127, half h = tid >> 7); warp w reads TMEM
+    // lanes 32·(w & 3) …; half h copies and splits k-groups {2h, 2h+1} of each chunk and
+    // converts / drains the 16-column blocks b ≡ h (mod 2)
+    const int row = tid & 127, h = tid >> 7;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     int it = blockIdx.x, ic = 0, js = 0;          // issue cursor over phase-1 jobs
     LrTcTask ti = tasks[it];
-    const float* isp = tid < ti.op_count ? reinterpret_cast<const float*>(src) + 2 * src_off[ti.op_begin + tid] : nullptr;
+    const float* isp = row < ti.op_count ? reinterpret_cast<const float*>(src) + 2 * src_off[ti.op_begin + row] : nullptr;
     auto issue_next = [&]() {
       if (it < ntask) {
         const int st = js % S1;
@@ -704,10 +709,11 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
         float* sA = sbase + st * stage_fl;
         const int K2 = 2 * ti.T;
 #pragma unroll
-        for (int kg = 0; kg < 4; ++kg) {
+        for (int q = 0; q < 2; ++q) {
+          const int kg = 2 * h + q;
           const int k = ic * TC_KC + 4 * kg;
           const int nb = isp ? 4 * min(4, max(0, K2 - k)) : 0;
-          cp16z(sA + ((kg * 16 + (tid >> 3)) * 8 + (tid & 7)) * 4, nb ? (const void*)(isp + k) : (const void*)src, nb);
+          cp16z(sA + ((kg * 16 + (row >> 3)) * 8 + (row & 7)) * 4, nb ? (const void*)(isp + k) : (const void*)src, nb);
         }
         ++js;
         if (++ic == ti.nk1) {
@@ -715,7 +721,7 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
           it += G;
           if (it < ntask) {
             ti = tasks[it];
-            isp = tid < ti.op_count ? reinterpret_cast<const float*>(src) + 2 * src_off[ti.op_begin + tid] : nullptr;
+            isp = row < ti.op_count ? reinterpret_cast<const float*>(src) + 2 * src_off[ti.op_begin + row] : nullptr;
           }
         }
       }
@@ -725,16 +731,16 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
     int jc = 0, i = 0;
     LrTcTask tp{};                                 // previous task (its D2 is drained at the next boundary)
     auto drain = [&](const LrTcTask& t) {
-      float2* d = tid < t.op_count ? dst + dst_off[t.op_begin + tid] : nullptr;
-      for (int c0 = 0; c0 < t.n2; c0 += 16) {
+      float2* d = row < t.op_count ? dst + dst_off[t.op_begin + row] : nullptr;
+      for (int c0 = 16 * h; c0 < t.n2; c0 += 32) {
         float w[16];
         tmem_ld16(tY + lane_base + c0, w);
         if (d) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int row = c0 / 2 + 2 * q;   // complex rows (row, row+1); row+1 = T is the padding slot
-            if (row < t.T)
-              atomicAdd(reinterpret_cast<float4*>(d + row), make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
+            const int r = c0 / 2 + 2 * q;   // complex rows (r, r+1); r+1 = T is the padding slot
+            if (r < t.T)
+              atomicAdd(reinterpret_cast<float4*>(d + r), make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
           }
         }
       }
@@ -748,9 +754,10 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
         asm volatile("cp.async.wait_group %0;\n" ::"n"(LA) : "memory");
         float* sA = sbase + (jc % S1) * stage_fl;
 #pragma unroll
-        for (int kg = 0; kg < 4; ++kg) {
-          const int idx = ((kg * 16 + (tid >> 3)) * 8 + (tid & 7)) * 4;
-          put_a(sA, tid, kg, *reinterpret_cast<const float4*>(sA + idx));
+        for (int q = 0; q < 2; ++q) {
+          const int kg = 2 * h + q;
+          const int idx = ((kg * 16 + (row >> 3)) * 8 + (row & 7)) * 4;
+          put_a(sA, row, kg, *reinterpret_cast<const float4*>(sA + idx));
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_arrive(&a_full[jc % S1]);
@@ -762,13 +769,13 @@ __global__ void __launch_bounds__(192, 1) k_m2l_tcw(const LrTcTask* __restrict__
       }
       mbar_wait(&d1_full, i & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-      for (int c0 = 0; c0 < t.n1; c0 += 16) {
+      for (int c0 = 16 * h; c0 < t.n1; c0 += 32) {
         float w[16];
         tmem_ld16(tmem + lane_base + c0, w);
         float* ch = sA2 + (c0 / TC_KC) * 2 * 128 * TC_KC;
 #pragma unroll
         for (int kg = 0; kg < 4; ++kg)
-          put_a(ch, tid, kg, make_float4(w[4 * kg], w[4 * kg + 1], w[4 * kg + 2], w[4 * kg + 3]));
+          put_a(ch, row, kg, make_float4(w[4 * kg], w[4 * kg + 1], w[4 * kg + 2], w[4 * kg + 3]));
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
@@ -813,7 +820,7 @@ void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, co
                     cudaStream_t s) {
   if (ntask <= 0) return;
 #define TCW(S)                                                                                                   \
-  k_m2l_tcw<S><<<grid, 192, pl.smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst, pl.stage_fl, pl.b2_fl, \
+  k_m2l_tcw<S><<<grid, TCW_NT, pl.smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst, pl.stage_fl, pl.b2_fl, \
                                           pl.n1max, pl.ncols)
   switch (pl.stages) {
     case 6: TCW(6); break;
