@@ -49,7 +49,7 @@ def main():
     ap.add_argument("--solve", action="store_true", help="also bm_solve the plane-wave system (GMRES tol 1e-4)")
     ap.add_argument("--max-iter", type=int, default=400)
     ap.add_argument("--restart", type=int, default=0)
-    ap.add_argument("--lrtc", type=int, default=0, help="opt.lr_tensor_cores (fused tcgen05 factored M2L)")
+    ap.add_argument("--lrtc", type=int, default=2, help="opt.lr_tensor_cores (fused tcgen05 factored M2L; 2 = library default)")
     a = ap.parse_args()
     c = CONFIGS[a.cfg]
     t0 = time.perf_counter()
