@@ -130,6 +130,7 @@ struct Dev {
   int2* near_slots = nullptr;      // per task: (source element, index into near_off) of every direct source
   bool alpha_pure_imag = false;
   int n_near = 0;                  // near-field CTAs (owned leaves)
+  bool near_wide = true;           // near CTA shape: 256 threads / 512 staged sources (else 128 / 256)
   int e0 = 0, e1 = 0;              // owned element range (tree order)
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
@@ -575,6 +576,8 @@ fda_status engine_create(Context* ctx) {
     ntask.push_back(nt);
   }
   d->n_near = (int)order.size();
+  // 256-thread near CTAs pay when a target leaf sees many direct sources (kernels.cu)
+  d->near_wide = d->n_near > 0 && (double)slots.size() >= 400.0 * (double)d->n_near;
   d->e0 = (int)p.own_e0;
   d->e1 = (int)p.own_e1;
   d->nranks = ctx->p.opt.nranks;
@@ -998,7 +1001,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   CK(cudaEventRecord(d->ev_l0, sn));
   launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
               kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
-              kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, sn);
+              kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, d->near_wide, sn);
   CK(cudaEventRecord(d->ev_l1, sn));
   d->live = true;
   if (prof) CK(cudaEventRecord(d->ev_n1, sn));
@@ -1097,7 +1100,7 @@ static fda_status run_sharded_up(Context* ctx, Dev* d, cudaStream_t s, int kind)
   CK(cudaEventRecord(d->ev_l0, sn));
   launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
               kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
-              kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, sn);
+              kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, d->near_wide, sn);
   CK(cudaEventRecord(d->ev_l1, sn));
   d->live = true;
   if (prof) CK(cudaEventRecord(d->ev_n1, sn));

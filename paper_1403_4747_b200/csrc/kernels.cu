@@ -94,8 +94,11 @@ void launch_scatter_f64(const float2* yn, const float2* yf, const int32_t* perm,
 // constant k of α·k into KernelParams.  Per (target, source element) the
 // kernel values of the three Q3 points are summed first and multiplied by
 // w_j once.
-constexpr int NEAR_NT = 256;
-constexpr int NEAR_MAXS = 512;
+// CTA shape (threads, staged sources per chunk): (256, 512) when target leaves see many
+// direct sources (config 2: 530 per target, near 0.188 → 0.182 ms), (128, 256) otherwise
+// (config 5: 268 per target, 6.2 → 5.6 ms); launch_near's `wide` picks the variant
+constexpr int NEAR_NT_WIDE = 256, NEAR_MAXS_WIDE = 512;
+constexpr int NEAR_NT_NARROW = 128, NEAR_MAXS_NARROW = 256;
 
 // MUFU.RSQ without the denormal guard of rsqrtf (q² ≥ 1e-12 here, never denormal)
 __device__ __forceinline__ float rsqrt_ftz(float x) {
@@ -186,7 +189,7 @@ __device__ __forceinline__ void rhs_eval2(const f2x* X, const f2x* nx, float4 Y,
 // units, shifted into the target leaf's frame), the normal, and
 // w_j = x_j·k²A_j/(12π).
 // KIND 0: LHS operator A (Eq. 5); KIND 1: RHS operator B (G sources).
-template <int KIND, bool PURE_IMAG>
+template <int KIND, bool PURE_IMAG, int NEAR_NT, int NEAR_MAXS>
 __global__ void __launch_bounds__(NEAR_NT) k_near(
     const NearTask* __restrict__ tasks, const int2* __restrict__ slots, const float4* __restrict__ near_off,
     const float4* __restrict__ tgt_pos, const float4* __restrict__ tgt_nrm, const SrcElem* __restrict__ src,
@@ -294,14 +297,20 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
 void launch_near(int ntask, const NearTask* tasks, const int2* slots, const float4* near_off, const float4* tgt_pos,
                  const float4* tgt_nrm, const SrcElem* src, const float* src_w, const int32_t* corr_ptr,
                  const int32_t* corr_col, const float2* corr_val, const float2* x, float2* y, KernelParams kp,
-                 bool alpha_pure_imag, int kind, cudaStream_t s) {
+                 bool alpha_pure_imag, int kind, bool wide, cudaStream_t s) {
   if (ntask <= 0) return;
-#define NEAR(K, PI)                                                                                              \
-  k_near<K, PI><<<ntask, NEAR_NT, 0, s>>>(tasks, slots, near_off, tgt_pos, tgt_nrm, src, src_w, corr_ptr, corr_col, \
-                                          corr_val, x, y, kp)
-  if (kind == 1) NEAR(1, false);
-  else if (alpha_pure_imag) NEAR(0, true);
-  else NEAR(0, false);
+#define NEAR(K, PI, NT, MS)                                                                                       \
+  k_near<K, PI, NT, MS><<<ntask, NT, 0, s>>>(tasks, slots, near_off, tgt_pos, tgt_nrm, src, src_w, corr_ptr,     \
+                                             corr_col, corr_val, x, y, kp)
+  if (wide) {
+    if (kind == 1) NEAR(1, false, NEAR_NT_WIDE, NEAR_MAXS_WIDE);
+    else if (alpha_pure_imag) NEAR(0, true, NEAR_NT_WIDE, NEAR_MAXS_WIDE);
+    else NEAR(0, false, NEAR_NT_WIDE, NEAR_MAXS_WIDE);
+  } else {
+    if (kind == 1) NEAR(1, false, NEAR_NT_NARROW, NEAR_MAXS_NARROW);
+    else if (alpha_pure_imag) NEAR(0, true, NEAR_NT_NARROW, NEAR_MAXS_NARROW);
+    else NEAR(0, false, NEAR_NT_NARROW, NEAR_MAXS_NARROW);
+  }
 #undef NEAR
 }
 

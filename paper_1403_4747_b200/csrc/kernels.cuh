@@ -124,7 +124,7 @@ void launch_scatter_f64(const float2* y_near, const float2* y_far, const int32_t
 void launch_near(int ntask, const NearTask* tasks, const int2* slots, const float4* near_off, const float4* tgt_pos,
                  const float4* tgt_nrm, const SrcElem* src, const float* src_w, const int32_t* corr_ptr,
                  const int32_t* corr_col, const float2* corr_val, const float2* x, float2* y, KernelParams kp,
-                 bool alpha_pure_imag, int kind, cudaStream_t s);
+                 bool alpha_pure_imag, int kind, bool wide, cudaStream_t s);   // wide: 256-thread CTAs
 void launch_s2m(int ntask, const LeafTask* tasks, const float2* pool, const float2* x, float2* out, int max_rows,
                 cudaStream_t s);
 void launch_l2t(int ntask, const LeafTask* tasks, const float2* pool, const float2* in, float2* y, cudaStream_t s,
