@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_tcw(const LrTcTask* __restric
   __shared__ uint64_t a_full[S1], b_full[S1], empty[S1], b2_full[2], b2_empty[2];
   __shared__ uint64_t d1_full, a2_full, d2_full, y_free;
   __shared__ uint32_t tmem_base_sh;
-  constexpr int LA = S1 > 4 ? S1 - 3 : S1 - 2;   // lookahead of the gathers; the rest is MMA-completion slack
+  constexpr int LA = S1 >= 8 ? S1 - 4 : (S1 > 4 ? S1 - 3 : S1 - 2);   // gather lookahead; the rest is MMA-completion slack
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x;
   float* sB2 = sbase + S1 * stage_fl;              // [2][b2_fl]
@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_tcw(const LrTcTask* __restric
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
 }
 
-// warp-specialised plan for one launch: ring stages S1 (3 … 6) of one 16-float K
+// warp-specialised plan for one launch: ring stages S1 (3 … 8) of one 16-float K
 // chunk (A hi|lo + B1 hi|lo), a 2-stage B2 ring and the phase-2 A region ≤ 220 KB
 LrTcPlan m2l_tcw_plan(int n1max, int n2max) {
   LrTcPlan pl;
@@ -803,7 +803,7 @@ LrTcPlan m2l_tcw_plan(int n1max, int n2max) {
   const size_t a2 = (size_t)(n1max / TC_KC) * 2 * 128 * TC_KC;
   const size_t cap = (220 * 1024 - 1024) / 4 - 2 * (size_t)pl.b2_fl - a2;
   const int s = (int)(cap / pl.stage_fl);
-  pl.stages = s >= 6 ? 6 : (s >= 4 ? 4 : 3);
+  pl.stages = s >= 8 ? 8 : (s >= 6 ? 6 : (s >= 5 ? 5 : (s >= 4 ? 4 : 3)));
   pl.smem = ((size_t)pl.stages * pl.stage_fl + 2 * (size_t)pl.b2_fl + a2) * 4 + 1024;
   pl.ncols = tmem_cols(n1max + n2max);
   pl.n1max = n1max;
@@ -812,7 +812,9 @@ LrTcPlan m2l_tcw_plan(int n1max, int n2max) {
 cudaError_t m2l_tcw_prepare() {
   cudaError_t e = cudaFuncSetAttribute(k_m2l_tcw<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_tcw<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_tcw<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_tcw<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_tcw<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   return e;
 }
 void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
@@ -823,7 +825,9 @@ void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, co
   k_m2l_tcw<S><<<grid, TCW_NT, pl.smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst, pl.stage_fl, pl.b2_fl, \
                                           pl.n1max, pl.ncols)
   switch (pl.stages) {
+    case 8: TCW(8); break;
     case 6: TCW(6); break;
+    case 5: TCW(5); break;
     case 4: TCW(4); break;
     default: TCW(3); break;
   }

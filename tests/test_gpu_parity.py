@@ -411,3 +411,21 @@ def test_config2_solve_sampled_residual(lib):
     print(f"config2 solve: {info}, sampled oracle residual {res:.2e}, vs series {_rel(u[rows], ser):.2e}")
     assert res <= 5e-4
     assert _rel(u[rows], ser) < 1.5e-2
+
+
+def test_tensor_core_fused_m2l_persistent_config2(lib):
+    """Config 2 with every factored level on the warp-specialised persistent
+    tensor-core kernel (opt.lr_tensor_cores = 1): ~1,800 tasks over 148 CTAs,
+    so each CTA pipelines several tasks (the next task's gathers and phase-1
+    MMAs overlap the previous task's drain).  Same operator as the CUDA-core
+    path to fp32 rounding; within the gate vs the oracle on sampled rows."""
+    V, F = config_mesh(2)
+    c = CONFIGS[2]
+    x = random_density(len(F), c.x_seed)
+    y0 = lib(V, F, c.k, c.alpha, c.eps, lr_tensor_cores=0).matvec(x)
+    y1 = lib(V, F, c.k, c.alpha, c.eps, lr_tensor_cores=1).matvec(x)
+    assert _rel(y1, y0) < 1e-5
+    rows = sampled_rows(len(F), 500, c.rows_seed)
+    el = O.element_geometry(V, F)
+    yo = fast.matvec_rows(el, rows, x, c.k, c.alpha)
+    assert _rel(y1[rows], yo) <= MATVEC_TOL
