@@ -95,7 +95,7 @@ typedef struct {
                             (both products on the tensor cores, 3xTF32, tmp kept on chip):
                             (persistent, warp-specialised k_m2l_tcw): 0 never (fused CUDA-core
                             kernel), 1 always, 2 (default) on levels with ≥ 64 ops per factored
-                            K̃ and ≥ 10 GFLOP of factored work; needs
+                            K̃ and ≥ 3 GFLOP of factored work; needs
                             tensor_cores ≠ 0                                               */
 } fda_options;
 

@@ -712,10 +712,11 @@ fda_status engine_create(Context* ctx) {
                                                                    // measured faster (config 3/5)
     }
     // fused tensor-core kernel (opt.lr_tensor_cores): per level, the ops with r ≤ 32, T ≤ LRTC_MAX_T.
-    // Auto (2): levels with ≥ 64 ops per factored K̃ and ≥ 10 GFLOP of factored work — the
+    // Auto (2): levels with ≥ 64 ops per factored K̃ and ≥ 3 GFLOP of factored work — the
     // persistent kernel owns every SM while it runs, which pays on large levels (config 5:
-    // M2L 32.6 vs 34.9 ms) but not on small ones that share the GPU with the near field
-    // inside the graph (config 2: matvec 0.481 vs 0.471 ms)
+    // M2L 32.0 vs 35.0 ms; config 3: matvec 1.735 vs 1.767 ms) but not on small ones that
+    // share the GPU with the near field inside the graph (config 2, largest level 1.6 GFLOP:
+    // matvec 0.473 vs 0.471 ms at a 1.5 GFLOP threshold)
     std::vector<char> lr_f(nlev, 0);
     if (d->use_tc && ctx->p.opt.lr_tensor_cores != 0) {
       std::vector<int64_t> nops(nlev, 0);
@@ -730,7 +731,7 @@ fda_status engine_create(Context* ctx) {
       for (int l = 0; l < nlev; ++l)
         lr_f[l] = nops[l] > 0 && !lr_tc[l] &&
                   (ctx->p.opt.lr_tensor_cores == 1 ||
-                   ((double)nops[l] >= 64.0 * (double)nm[l].size() && fl[l] >= 1e10));
+                   ((double)nops[l] >= 64.0 * (double)nm[l].size() && fl[l] >= 3e9));
     }
     std::vector<std::vector<LrOp>> ftc(nlev);
     int64_t tmp_off = 0;
