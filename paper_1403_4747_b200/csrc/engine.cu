@@ -96,6 +96,8 @@ struct XStage {
   bool atomic = true;
   TcTask* tc[TC_NV] = {};          // tensor-core tasks per kernel variant (opt.tensor_cores)
   int n_tc[TC_NV] = {};
+  TcTask* tcw[2] = {};             // warp-specialised persistent kernel, 1 / 2 row tiles (opt.tensor_cores = 4)
+  int n_tcw[2] = {}, grid_tcw[2] = {};
   XTask* tasks[XV] = {};
   int ntask[XV] = {};
   int64_t* src = nullptr;
@@ -172,6 +174,7 @@ struct Dev {
       int n = n_lrtc;
       for (int c = 0; c < LR_NCLS; ++c) n += n_lr[c];
       for (int v = 0; v < TC_NV; ++v) n += dense.n_tc[v] + a.n_tc[v] + b.n_tc[v];
+      for (int q = 0; q < 2; ++q) n += dense.n_tcw[q] + a.n_tcw[q] + b.n_tcw[q];
       for (int v = 0; v < XV; ++v) n += dense.ntask[v] + a.ntask[v] + b.ntask[v];
       return n > 0;
     }
@@ -390,6 +393,25 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
         }
         tct[v].swap(out);
       }
+    if (ctx->p.opt.tensor_cores == 4) {   // N = 128, ≤ 2 tiles → the warp-specialised persistent kernel
+      std::vector<TcTask> w[2];
+      for (int v = 0; v < TC_NV; ++v) {
+        if (tc_variant_ops(v) != 128) continue;
+        std::vector<TcTask> keep;
+        for (const TcTask& t : tct[v]) (t.ntile <= 2 ? w[t.ntile - 1] : keep).push_back(t);
+        tct[v].swap(keep);
+      }
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      for (int q = 0; q < 2; ++q) {
+        std::stable_sort(w[q].begin(), w[q].end(),
+                         [](const TcTask& x, const TcTask& y) { return x.kc1 - x.kc0 > y.kc1 - y.kc0; });
+        st.n_tcw[q] = (int)w[q].size();
+        st.grid_tcw[q] = std::min<int>(st.n_tcw[q], nsm);
+        if (st.n_tcw[q]) UP(&st.tcw[q], w[q].data(), w[q].size());
+      }
+    }
     for (int v = 0; v < TC_NV; ++v) {
       st.n_tc[v] = (int)tct[v].size();
       if (st.n_tc[v]) UP(&st.tc[v], tct[v].data(), tct[v].size());
@@ -467,6 +489,8 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
 static const float* g_tcpool = nullptr;   // set per context before launches (single-threaded use)
 
 static void launch_stage(const XStage& st, const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
+  for (int q = 0; q < 2; ++q)
+    if (st.n_tcw[q]) launch_xlate_tcw(q + 1, st.n_tcw[q], st.tcw[q], st.src, st.dst, g_tcpool, src, dst, st.grid_tcw[q], s);
   for (int v = 0; v < TC_NV; ++v)
     if (st.n_tc[v]) launch_xlate_tc(v, st.n_tc[v], st.tc[v], st.src, st.dst, g_tcpool, src, dst, s);
   for (int v = 0; v < XV; ++v)
@@ -500,6 +524,7 @@ fda_status engine_create(Context* ctx) {
   d->kp.inv_k = (float)(1.0 / ctx->p.k);
   d->use_tc = ctx->p.opt.tensor_cores != 0;
   if (d->use_tc) CK(tc_prepare());
+  if (d->use_tc) CK(xlate_tcw_prepare());
   if (d->use_tc) CK(m2l_tc_prepare());
   if (d->use_tc) CK(m2l_tcw_prepare());
   CK(m2l_lr_prepare());
@@ -888,6 +913,7 @@ fda_status engine_create(Context* ctx) {
   // kernels per matvec: gather, near, s2m, every non-empty translation launch, l2t, scatter
   int64_t nl = 4 + (d->n_s2m > 0) + (d->n_l2t_add > 0);  // gather, near, l2t, scatter (+ s2m, HF-leaf L2T)
   auto cnt = [&](const XStage& st) {
+    for (int q = 0; q < 2; ++q) nl += st.n_tcw[q] > 0;
     for (int v = 0; v < TC_NV; ++v) nl += st.n_tc[v] > 0;
     for (int v = 0; v < XV; ++v) nl += st.ntask[v] > 0;
   };

@@ -99,7 +99,7 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
   }
   if (o.max_leaf < 1 || o.max_leaf > 128 || o.p_eq < 2 || o.p_chk_lf < 2 || o.p_chk_hf < 2 || !(o.eq_scale > 0) ||
       !(o.chk_scale_lf > o.eq_scale) || !(o.tier1_rho >= 0) || !(o.tier2_rho >= o.tier1_rho) ||
-      o.tensor_cores < 0 || o.tensor_cores > 3 || o.hf_leaves < 0 || o.hf_leaves > 1 ||
+      o.tensor_cores < 0 || o.tensor_cores > 4 || o.hf_leaves < 0 || o.hf_leaves > 1 ||
       o.lr_tensor_cores < 0 || o.lr_tensor_cores > 2) {
     g_build_error = "invalid fda_options";
     delete ctx;

@@ -144,6 +144,10 @@ cudaError_t m2l_lr_prepare();
 void launch_xlate_tc(int variant, int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                      const float* tcpool, const float2* src, float2* dst, cudaStream_t s);
 cudaError_t tc_prepare();
+// warp-specialised persistent translation kernel (N = 128 ops per task, tiles ≤ 2)
+cudaError_t xlate_tcw_prepare();
+void launch_xlate_tcw(int tiles, int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                      const float* tcpool, const float2* src, float2* dst, int grid, cudaStream_t s);
 // GMRES / BLAS-1 helpers (fp64 accumulation)
 void launch_dots(const float2* V, int64_t ldv, int nv, const float2* w, int64_t n, double2* partial, int nchunks,
                  cudaStream_t s);

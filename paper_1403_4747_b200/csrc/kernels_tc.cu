@@ -834,6 +834,226 @@ void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, co
 #undef TCW
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised persistent form of the translation kernel (k_xlate_tcw):
+// the same product (dst[:, op] += M · src[:, op] in interleaved real form,
+// 3xTF32, N = 128 ops per task, TILES ≤ 2 row tiles) with the roles of
+// k_m2l_tcw — row warps 0-7 gather the B operand (two threads per op, two
+// k-groups each), split it in place and drain the accumulators; warp 8 issues
+// the MMAs; warp 9 streams the A tiles with the TMA engine.  TMEM holds two
+// accumulator sets (2 × TILES × 128 columns), so task i+1's MMAs run while
+// the row warps drain task i: a warp reads 32 real rows × 16 ops per
+// tcgen05.ld, pairs (Re, Im) of a complex row with one shuffle and adds them
+// with 8-byte atomics, 16 lanes covering 16 consecutive complex rows of one op.
+template <int S, int TILES>
+__global__ void __launch_bounds__(TCW_NT, 1) k_xlate_tcw(const TcTask* __restrict__ tasks, int ntask,
+                                                       const int64_t* __restrict__ src_off,
+                                                       const int64_t* __restrict__ dst_off,
+                                                       const float* __restrict__ tcpool,
+                                                       const float2* __restrict__ src, float2* __restrict__ dst) {
+  constexpr int N = 128;
+  constexpr int A_FL = TILES * 2 * A_TILE;         // A floats per stage (hi | lo per tile)
+  constexpr int STAGE_FL = A_FL + 2 * N * KC;      // + B hi | lo
+  constexpr int LA = S >= 6 ? S - 3 : S - 2;
+  constexpr uint32_t NCOLS = tmem_cols(2 * TILES * N);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  float* sbase = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t a_full[S], b_full[S], empty[S], d_full[2], y_free[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(NCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) {
+      mbar_init(&a_full[q], 1);
+      mbar_init(&b_full[q], 32 * TCW_RW);
+      mbar_init(&empty[q], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&d_full[q], 1);
+      mbar_init(&y_free[q], 32 * TCW_RW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == TCW_RW + 1) {
+    // ---------------- TMA producer: the A tiles of every job
+    if (lane == 0) {
+      int j = 0;
+      for (int ct = blockIdx.x; ct < ntask; ct += G) {
+        const TcTask t = tasks[ct];
+        for (int cg = t.kc0; cg < t.kc1; ++cg, ++j) {
+          const int st = j % S;
+          if (j >= S) mbar_wait(&empty[st], ((j / S) - 1) & 1);
+          mbar_expect_tx(&a_full[st], (uint32_t)(TILES * 2 * A_TILE * 4));
+#pragma unroll
+          for (int ti = 0; ti < TILES; ++ti)
+            bulk_g2s(sbase + st * STAGE_FL + ti * 2 * A_TILE, tcpool + t.a_off + ((int64_t)ti * t.nkc + cg) * 2 * A_TILE,
+                     2 * A_TILE * 4, &a_full[st]);
+        }
+      }
+    }
+  } else if (warp == TCW_RW) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc<N>();
+      int j = 0, i = 0;
+      for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
+        const TcTask t = tasks[ct];
+        const int b = i & 1;
+        if (i >= 2) mbar_wait(&y_free[b], ((i >> 1) - 1) & 1);   // task i-2's accumulators drained
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        for (int cg = t.kc0; cg < t.kc1; ++cg, ++j) {
+          const int st = j % S;
+          mbar_wait(&a_full[st], (j / S) & 1);
+          mbar_wait(&b_full[st], (j / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+          float* sA = sbase + st * STAGE_FL;
+          const uint32_t b_hi = smem_u32(sA + A_FL), b_lo = b_hi + N * KC * 4;
+#pragma unroll
+          for (int s = 0; s < KC / 8; ++s) {
+            const uint32_t bo = (uint32_t)(2 * s * (N / 8) * 128);
+            const uint64_t Bh = make_desc(b_hi + bo, (N / 8) * 128, 128), Bl = make_desc(b_lo + bo, (N / 8) * 128, 128);
+#pragma unroll
+            for (int ti = 0; ti < TILES; ++ti) {
+              const uint32_t a_hi = smem_u32(sA + ti * 2 * A_TILE), a_lo = a_hi + A_TILE * 4;
+              const uint32_t ao = (uint32_t)(2 * s * 16 * 128);
+              const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
+              const uint32_t d = tmem + (uint32_t)((b * TILES + ti) * N);
+              mma_tf32(d, Ah, Bh, idesc, (cg > t.kc0 || s > 0) ? 1u : 0u);
+              mma_tf32(d, Ah, Bl, idesc, 1u);
+              mma_tf32(d, Al, Bh, idesc, 1u);
+            }
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           smem_u32(&empty[st]))
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&d_full[b]))
+                     : "memory");
+      }
+    }
+  } else {
+    // ---------------- row warps: op = tid & 127, half h = tid >> 7 (k-groups 2h, 2h+1)
+    const int op = tid & 127, h = tid >> 7;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    int it = blockIdx.x, js = 0;
+    TcTask ti = tasks[it];
+    int cg_i = ti.kc0;
+    const float* isp = op < ti.op_count ? reinterpret_cast<const float*>(src) + 2 * src_off[ti.op_begin + op] : nullptr;
+    auto issue_next = [&]() {
+      if (it < ntask) {
+        const int st = js % S;
+        if (js >= S) mbar_wait(&empty[st], ((js / S) - 1) & 1);
+        float* sB = sbase + st * STAGE_FL + A_FL;
+        const int K2 = 2 * ti.C;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int kg = 2 * h + q;
+          const int k = cg_i * KC + 4 * kg;
+          const int nb = isp ? 4 * min(4, max(0, K2 - k)) : 0;
+          cp16z(sB + ((kg * (N / 8) + (op >> 3)) * 8 + (op & 7)) * 4, nb ? (const void*)(isp + k) : (const void*)src, nb);
+        }
+        ++js;
+        if (++cg_i == ti.kc1) {
+          it += G;
+          if (it < ntask) {
+            ti = tasks[it];
+            cg_i = ti.kc0;
+            isp = op < ti.op_count ? reinterpret_cast<const float*>(src) + 2 * src_off[ti.op_begin + op] : nullptr;
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    };
+    for (int q = 0; q < LA; ++q) issue_next();
+    auto drain = [&](const TcTask& t, int b) {
+      // lane = real row rr of the tile: complex row rr >> 1, Re (even) / Im (odd)
+      for (int tt = 0; tt < t.ntile; ++tt)
+        for (int c0 = 16 * h; c0 < N; c0 += 32) {
+          float w[16];
+          tmem_ld16(tmem + lane_base + (uint32_t)((b * TILES + tt) * N + c0), w);
+          const int ci = (128 * tt + 32 * (warp & 3) + lane) >> 1;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float im = __shfl_xor_sync(0xffffffffu, w[q], 1);
+            const int o = c0 + q;
+            if ((lane & 1) == 0 && o < t.op_count && ci < t.R)
+              atomicAdd(dst + dst_off[t.op_begin + o] + ci, make_float2(w[q], im));
+          }
+        }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      mbar_arrive(&y_free[b]);
+    };
+    int jc = 0, i = 0;
+    TcTask tp{};
+    for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
+      const TcTask t = tasks[ct];
+      for (int cg = t.kc0; cg < t.kc1; ++cg, ++jc) {
+        issue_next();
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(LA) : "memory");
+        float* sB = sbase + (jc % S) * STAGE_FL + A_FL;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int kg = 2 * h + q;
+          const int idx = ((kg * (N / 8) + (op >> 3)) * 8 + (op & 7)) * 4;
+          const float4 v = *reinterpret_cast<const float4*>(sB + idx);
+          const float4 hv = tf32_hi4(v);
+          *reinterpret_cast<float4*>(sB + idx) = hv;
+          *reinterpret_cast<float4*>(sB + N * KC + idx) = make_float4(v.x - hv.x, v.y - hv.y, v.z - hv.z, v.w - hv.w);
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive(&b_full[jc % S]);
+      }
+      if (i >= 1) {
+        mbar_wait(&d_full[(i - 1) & 1], ((i - 1) >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        drain(tp, (i - 1) & 1);
+      }
+      tp = t;
+    }
+    if (i >= 1) {
+      mbar_wait(&d_full[(i - 1) & 1], ((i - 1) >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      drain(tp, (i - 1) & 1);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(NCOLS));
+}
+
+template <int S, int TILES>
+size_t xlate_tcw_smem() {
+  return (size_t)S * (TILES * 2 * A_TILE + 2 * 128 * KC) * 4 + 1024;
+}
+cudaError_t xlate_tcw_prepare() {
+  cudaError_t e = cudaFuncSetAttribute(k_xlate_tcw<6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)xlate_tcw_smem<6, 1>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_xlate_tcw<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xlate_tcw_smem<4, 2>());
+  return e;
+}
+// persistent: grid = min(ntask, #SMs); tasks sorted longest first on the host
+void launch_xlate_tcw(int tiles, int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                      const float* tcpool, const float2* src, float2* dst, int grid, cudaStream_t s) {
+  if (ntask <= 0) return;
+  if (tiles == 1)
+    k_xlate_tcw<6, 1><<<grid, TCW_NT, xlate_tcw_smem<6, 1>(), s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst);
+  else
+    k_xlate_tcw<4, 2><<<grid, TCW_NT, xlate_tcw_smem<4, 2>(), s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst);
+}
+
 int m2l_tc_stage_fl(int n1, int n2) {
   return (int)std::max<size_t>(LRTC_CPJ * (2 * 128 * TC_KC + (size_t)n1 * TC_KC * 2), (size_t)n2 * TC_KC * 2);
 }

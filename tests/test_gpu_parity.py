@@ -356,7 +356,7 @@ def test_sharded_exchange_one_gpu(lib, R):
     assert _rel(bad, full) > 1e-3
 
 
-@pytest.mark.parametrize("lowrank,tc", [(1, 1), (0, 1), (0, 3)])
+@pytest.mark.parametrize("lowrank,tc", [(1, 1), (0, 1), (0, 3), (0, 4), (1, 4)])
 def test_tensor_core_translations(lib, lowrank, tc):
     """tcgen05 3xTF32 translation path (opt.tensor_cores): same operator as the
     CUDA-core path to fp32 rounding, and within the gate vs the oracle."""
