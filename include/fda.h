@@ -86,7 +86,8 @@ typedef struct {
                             3xTF32: 0 never, 1 every eligible stage (factored M2L too),
                             2 (default) stages of ≥ 1 GFLOP with ≥ 64 ops per matrix (CUDA
                             cores elsewhere), 3 as 2 with the deep-pipeline one-CTA-per-SM
-                            kernel variants (A/B)                                           */
+                            kernel variants (A/B), 4 as 2 with the warp-specialised
+                            persistent kernel for ≤ 2 row tiles (A/B)                      */
   int32_t hf_leaves;     /* 0 (default): HF cubes are always split, all leaves are LF (reading
                             C9); 1: the count rule at every level, leaves may be HF, with
                             directional S2M / L2T per used wedge (PAPER.md P:344-346,
