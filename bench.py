@@ -47,7 +47,10 @@ def _peaks():
     hbm = mp.get("hbm_gbs", 6650.0)
     clk = mp.get("sm_max_mhz", 1965.0)
     fp32 = SMS * FP32_LANES * 2 * clk * 1e6 / 1e12    # TFLOP/s, derived from unit counts × max clock
-    return hbm, fp32, ("measured" if "hbm_gbs" in mp else "fallback")
+    src = ("derived: 148 SMs x 128 FP32 lanes x 2 flops x the max SM clock "
+           f"({clk:.0f} MHz, {'MEASURED_PEAKS.json' if 'sm_max_mhz' in mp else 'fallback'}); "
+           f"HBM peak {'measured (MEASURED_PEAKS.json)' if 'hbm_gbs' in mp else 'fallback'}")
+    return hbm, fp32, src
 
 
 def _dist():
