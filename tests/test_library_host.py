@@ -201,3 +201,22 @@ def test_rhs_pass_tables_match_oracle():
         y = apply_tables(f, x, kind=kind)
         yo = fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k, kind=kind)
         assert np.linalg.norm(y - yo) / np.linalg.norm(yo) < 1e-4, kind
+
+
+def test_m2l_routing_dense_on_low_sharing_levels():
+    """§4.2 factored K̃ (r < T/2) on every level where a factored K̃ is
+    shared by ≥ 16 ops; the coarse HF level of config 2 (L2: ~10 ops per K̃)
+    keeps the dense K̃.  Every M2L pair is routed exactly once."""
+    V, F = config_mesh(2)
+    c = CONFIGS[2]
+    f = FDA(V, F, c.k, c.alpha, c.eps, device=-1)
+    dense = f.table("m2l").reshape(-1, 4)
+    lr = f.table("m2l_lr").reshape(-1, 6)
+    assert len(dense) + len(lr) == f.stats()["n_m2l_pairs"]
+    lr_levels = set(lr[:, 0].tolist())
+    dense_levels = set(dense[:, 0].tolist())
+    assert 2 in dense_levels and 2 not in lr_levels
+    assert {3, 4, 5} <= lr_levels
+    for l in lr_levels:
+        o = lr[lr[:, 0] == l]
+        assert len(o) >= 16 * len(set(o[:, 3].tolist()))
