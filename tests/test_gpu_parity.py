@@ -309,8 +309,8 @@ def test_pulsating_table2_on_gpu(lib, row):
     assert _rel(u, u_ref) <= SOLVE_TOL
 
 
-@pytest.mark.parametrize("R", [2, 3])
-def test_sharded_exchange_one_gpu(lib, R):
+@pytest.mark.parametrize("R,lrtc", [(2, 0), (3, 0), (2, 1)])
+def test_sharded_exchange_one_gpu(lib, R, lrtc):
     """Sharded build in fake-partition mode: R rank contexts on
     this GPU run the partial upward pass (FDA_PHASE_UP), exchange their partial
     outgoing states through fda_exchange_local (the copies the grouped
@@ -323,7 +323,8 @@ def test_sharded_exchange_one_gpu(lib, R):
     k = 40.0
     x = random_density(len(F), 9)
     full = lib(V, F, k, 1j / k, 1e-4, max_leaf=16).matvec(x)
-    ranks = [lib(V, F, k, 1j / k, 1e-4, max_leaf=16, rank=r, nranks=R) for r in range(R)]
+    # lrtc = 1: the ranks' factored M2L on the persistent tensor-core kernel (sharded launch path)
+    ranks = [lib(V, F, k, 1j / k, 1e-4, max_leaf=16, rank=r, nranks=R, lr_tensor_cores=lrtc) for r in range(R)]
     xd = torch.from_numpy(x.astype(np.complex64)).cuda()
     ys = [torch.empty_like(xd) for _ in range(R)]
     for f, y in zip(ranks, ys):
