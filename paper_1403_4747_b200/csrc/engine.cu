@@ -166,9 +166,7 @@ struct Dev {
     int64_t* lr_dst = nullptr;
     LrTcTask* lrtc = nullptr;        // fused §4.2 tasks on the tensor cores (k_m2l_tc, persistent)
     int n_lrtc = 0;
-    size_t lrtc_smem = 0;
-    uint32_t lrtc_cols = 0;
-    int lrtc_grid = 0, lrtc_stages = 3;
+    int lrtc_grid = 0;
     LrTcPlan lrtc_plan;
     bool any() const {
       int n = n_lrtc;
@@ -525,7 +523,6 @@ fda_status engine_create(Context* ctx) {
   d->use_tc = ctx->p.opt.tensor_cores != 0;
   if (d->use_tc) CK(tc_prepare());
   if (d->use_tc) CK(xlate_tcw_prepare());
-  if (d->use_tc) CK(m2l_tc_prepare());
   if (d->use_tc) CK(m2l_tcw_prepare());
   CK(m2l_lr_prepare());
 
@@ -839,24 +836,20 @@ fda_status engine_create(Context* ctx) {
           i = j;
         }
         // one ring layout per launch; tasks longest first (the persistent CTAs stride over them)
-        int sfl = 0, n1m = 16, nm = 16;
+        int sfl = 0, n1m = 16;
         for (const LrTcTask& tk : tt) {
           sfl = std::max(sfl, tk.stage_fl);
           n1m = std::max(n1m, tk.n1);
-          nm = std::max(nm, std::max(tk.n1, tk.n2));
         }
         for (LrTcTask& tk : tt) tk.stage_fl = sfl;
         std::stable_sort(tt.begin(), tt.end(), [](const LrTcTask& x, const LrTcTask& y) {
           return (int64_t)(x.nk1 + x.n1 / TC_KC) * x.n2 > (int64_t)(y.nk1 + y.n1 / TC_KC) * y.n2;
         });
         if (!tt.empty()) {
-          L.lrtc_smem = m2l_tc_smem(sfl, n1m);
-          L.lrtc_stages = m2l_tc_stages(sfl, n1m);
           int n2m = 16;
           for (const LrTcTask& tk : tt) n2m = std::max(n2m, tk.n2);
           L.lrtc_plan = m2l_tcw_plan(n1m, n2m);
         }
-        L.lrtc_cols = m2l_tc_cols(nm);
         {
           int dev = 0, nsm = 148;
           cudaGetDevice(&dev);

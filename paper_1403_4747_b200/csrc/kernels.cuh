@@ -83,11 +83,7 @@ struct LrTcTask {
 };
 constexpr int LRTC_MAX_R = 32;
 constexpr int LRTC_MAX_T = 160;   // keeps 3 ring stages + the phase-2 A region ≤ 220 KB (n1 ≤ 64, n2 ≤ 320)
-int m2l_tc_stage_fl(int n1, int n2);                 // floats per ring stage of one task
-int m2l_tc_stages(int stage_fl, int n1max);           // ring stages of a launch (3 … 8)
-size_t m2l_tc_smem(int stage_fl, int n1max);          // dynamic shared memory of a launch (uniform stage_fl)
-uint32_t m2l_tc_cols(int nmax);                       // TMEM columns for max(n1, n2) over the launch
-cudaError_t m2l_tc_prepare();
+int m2l_tc_stage_fl(int n1, int n2);                 // floats of one phase-1 ring stage of k_m2l_tcw
 // warp-specialised persistent variant (k_m2l_tcw): launch plan from the level's max n1 / n2
 struct LrTcPlan {
   int stages = 3, stage_fl = 0, b2_fl = 0, n1max = 16;
@@ -99,9 +95,7 @@ cudaError_t m2l_tcw_prepare();
 void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                     const float* tcpool, const float2* src, float2* dst, const LrTcPlan& pl, int grid,
                     cudaStream_t s);
-// persistent: grid ≤ #SMs CTAs walk the tasks (sorted longest first) with stride grid
-void launch_m2l_tc(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off, const float* tcpool,
-                   const float2* src, float2* dst, size_t smem, uint32_t ncols, int grid, int stages, cudaStream_t s);   // multi: the 2-stage, several-CTAs-per-SM variants
+  // multi: the 2-stage, several-CTAs-per-SM variants
 int tc_variant_ops(int v);
 
 // leaf-level ops (S2M / L2T)

@@ -323,226 +323,6 @@ __device__ __forceinline__ void put_a(float* chunk, int row, int kg, float4 v) {
 }
 }  // namespace
 
-// Persistent form: one CTA per SM walks its tasks (b, b + G, b + 2G, … in
-// the host's longest-first order) as ONE stream of ring jobs — per task its
-// nk1 phase-1 chunks (states by 16-B cp.async into the stage's A slot, B1 by
-// the TMA engine) then its nk2 phase-2 B2 chunks (TMA) — issued
-// S − 2 jobs ahead of consumption (S = 3 … 8 stages, as many as fit in shared
-// memory; the stage refilled was consumed two jobs earlier, so the refill
-// never waits for MMAs just issued), so the gathers of the next task
-// are in flight while the current one finishes phase 2 and drains its
-// accumulator.  Job j uses stage j mod S; its TMA and MMA completions are
-// counted on mbar_b / mbar_m of that stage (phase parity (j / S) & 1); every
-// thread commits one cp.async group per job (empty for B2 jobs), so
-// cp.async.wait_group(S − 2) at the consumption of job j means "my copies of
-// job j have landed".
-constexpr int LRTC_CPJ = 2;   // 16-float K chunks per ring job
-template <int S>
-__global__ void __launch_bounds__(128, 1) k_m2l_tc(const LrTcTask* __restrict__ tasks, int ntask,
-                                                   const int64_t* __restrict__ src_off,
-                                                   const int64_t* __restrict__ dst_off,
-                                                   const float* __restrict__ tcpool, const float2* __restrict__ src,
-                                                   float2* __restrict__ dst, uint32_t ncols) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  float* sbase = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t mbar_b[S], mbar_m[S];
-  __shared__ uint32_t tmem_base_sh;
-  constexpr int LA = S - 2;   // issue lookahead: the stage refilled was consumed two jobs ago
-  constexpr int CPJ = LRTC_CPJ;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int G = gridDim.x;
-  if ((int)blockIdx.x >= ntask) return;
-  const int stage_fl = tasks[0].stage_fl;          // uniform over the launch (host)
-  float* sA2 = sbase + S * stage_fl;               // phase-2 A operand: nk2 × [hi | lo] 128 × 16
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
-                 "r"(ncols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
-  }
-  if (tid == 0) {
-    for (int q = 0; q < S; ++q) {
-      mbar_init(&mbar_b[q], 1);
-      mbar_init(&mbar_m[q], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-  const uint32_t tmem = tmem_base_sh;
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-
-  // ---- issue cursor: task it, job ic within it (0 … nk1 + nk2 − 1), global job js
-  int it = blockIdx.x, ic = 0, js = 0;
-  LrTcTask ti = tasks[it];
-  const float* isp = nullptr;   // this thread's source state (issue task)
-  auto issue_set = [&]() {
-    isp = tid < ti.op_count ? reinterpret_cast<const float*>(src) + 2 * src_off[ti.op_begin + tid] : nullptr;
-  };
-  issue_set();
-  // a phase-1 job covers CPJ consecutive 16-float K chunks: stage = [A chunk q: hi | lo] × CPJ,
-  // then the B1 chunks (contiguous in the pool, one bulk copy); a B2 job is one B2 chunk
-  auto issue_next = [&]() {
-    if (it >= ntask) {
-      asm volatile("cp.async.commit_group;\n" ::);
-      return;
-    }
-    const int st = js % S;
-    if (js >= S) mbar_wait(&mbar_m[st], ((js - S) / S) & 1);   // the stage's previous job is consumed
-    float* sA = sbase + st * stage_fl;
-    const int nj1 = (ti.nk1 + CPJ - 1) / CPJ, nk2 = ti.n1 / TC_KC, nj2 = nk2;   // B2 jobs: one chunk
-    if (ic < nj1) {
-      const int c0 = ic * CPJ, nc = min(CPJ, ti.nk1 - c0);
-      const uint32_t bytes = (uint32_t)(nc * ti.n1 * TC_KC * 2 * 4);
-      if (tid == 0) {
-        mbar_expect_tx(&mbar_b[st], bytes);
-        bulk_g2s(sA + CPJ * 2 * 128 * TC_KC, tcpool + ti.b1_off + (int64_t)c0 * ti.n1 * TC_KC * 2, bytes, &mbar_b[st]);
-      }
-      const int K2 = 2 * ti.T;
-      for (int q = 0; q < nc; ++q)
-#pragma unroll
-        for (int kg = 0; kg < 4; ++kg) {
-          const int k = (c0 + q) * TC_KC + 4 * kg;
-          const int nb = isp ? 4 * min(4, max(0, K2 - k)) : 0;
-          cp16z(sA + q * 2 * 128 * TC_KC + ((kg * 16 + (tid >> 3)) * 8 + (tid & 7)) * 4,
-                nb ? (const void*)(isp + k) : (const void*)src, nb);
-        }
-    } else if (tid == 0) {
-      const int c0 = ic - nj1, nc = 1;
-      const uint32_t bytes = (uint32_t)(nc * ti.n2 * TC_KC * 2 * 4);
-      mbar_expect_tx(&mbar_b[st], bytes);
-      bulk_g2s(sA, tcpool + ti.b2_off + (int64_t)c0 * ti.n2 * TC_KC * 2, bytes, &mbar_b[st]);
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-    ++js;
-    if (++ic == nj1 + nj2) {
-      ic = 0;
-      it += G;
-      if (it < ntask) {
-        ti = tasks[it];
-        issue_set();
-      }
-    }
-  };
-  for (int q = 0; q < LA; ++q) issue_next();
-
-  int jc = 0;   // consume cursor (global job index)
-  for (int ct = blockIdx.x; ct < ntask; ct += G) {
-    const LrTcTask t = tasks[ct];
-    const int N1 = t.n1, N2 = t.n2, nk1 = t.nk1, nk2 = N1 / TC_KC;
-    const int nj1 = (nk1 + CPJ - 1) / CPJ, nj2 = nk2;
-    // phase 1: D1 (128 × N1) = S · A_Vᵀ
-    for (int j = 0; j < nj1; ++j, ++jc) {
-      issue_next();
-      asm volatile("cp.async.wait_group %0;\n" ::"n"(LA) : "memory");
-      const int st = jc % S;
-      const int c0 = j * CPJ, nc = min(CPJ, nk1 - c0);
-      float* sA = sbase + st * stage_fl;
-      float* sB = sA + CPJ * 2 * 128 * TC_KC;
-      for (int q = 0; q < nc; ++q)
-#pragma unroll
-        for (int kg = 0; kg < 4; ++kg) {
-          float* ch = sA + q * 2 * 128 * TC_KC;
-          const int idx = ((kg * 16 + (tid >> 3)) * 8 + (tid & 7)) * 4;
-          put_a(ch, tid, kg, *reinterpret_cast<const float4*>(ch + idx));
-        }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncthreads();
-      if (tid == 0) {
-        mbar_wait(&mbar_b[st], (jc / S) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-        const uint32_t idesc = idesc_n(N1);
-        for (int q = 0; q < nc; ++q) {
-          const uint32_t a_hi = smem_u32(sA + q * 2 * 128 * TC_KC), a_lo = a_hi + 128 * TC_KC * 4;
-          const uint32_t b_hi = smem_u32(sB + q * N1 * TC_KC * 2), b_lo = b_hi + N1 * TC_KC * 4;
-#pragma unroll
-          for (int s = 0; s < TC_KC / 8; ++s) {
-            const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (N1 / 8) * 128);
-            const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
-            const uint64_t Bh = make_desc(b_hi + bo, (N1 / 8) * 128, 128), Bl = make_desc(b_lo + bo, (N1 / 8) * 128, 128);
-            mma_tf32(tmem, Ah, Bh, idesc, (c0 + q > 0 || s > 0) ? 1u : 0u);
-            mma_tf32(tmem, Ah, Bl, idesc, 1u);
-            mma_tf32(tmem, Al, Bh, idesc, 1u);
-          }
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                         smem_u32(&mbar_m[st]))
-                     : "memory");
-      }
-    }
-    mbar_wait(&mbar_m[(jc - 1) % S], ((jc - 1) / S) & 1);   // D1 complete
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-    // tmp: D1 row → phase-2 A operand (tf32 hi / lo, K-major)
-    for (int c0 = 0; c0 < N1; c0 += 16) {
-      float w[16];
-      tmem_ld16(tmem + lane_base + c0, w);
-      float* ch = sA2 + (c0 / TC_KC) * 2 * 128 * TC_KC;
-#pragma unroll
-      for (int kg = 0; kg < 4; ++kg)
-        put_a(ch, tid, kg, make_float4(w[4 * kg], w[4 * kg + 1], w[4 * kg + 2], w[4 * kg + 3]));
-    }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
-    __syncthreads();
-    // phase 2: D2 (128 × N2) = tmp · A_Uᵀ, into TMEM columns 0 … N2-1 (D1 has been read)
-    for (int j = 0; j < nj2; ++j, ++jc) {
-      issue_next();
-      asm volatile("cp.async.wait_group %0;\n" ::"n"(LA) : "memory");
-      const int st = jc % S;
-      const int c0 = j, nc = 1;
-      if (tid == 0) {
-        mbar_wait(&mbar_b[st], (jc / S) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-        for (int q = 0; q < nc; ++q) {
-          const uint32_t b_hi = smem_u32(sbase + st * stage_fl + q * N2 * TC_KC * 2), b_lo = b_hi + N2 * TC_KC * 4;
-          const uint32_t a_hi = smem_u32(sA2 + (c0 + q) * 2 * 128 * TC_KC), a_lo = a_hi + 128 * TC_KC * 4;
-#pragma unroll
-          for (int s = 0; s < TC_KC / 8; ++s) {
-            const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (N2 / 8) * 128);
-            const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
-            for (int n0 = 0; n0 < N2; n0 += 256) {
-              const int nn = min(256, N2 - n0);
-              const uint32_t idesc = idesc_n(nn);
-              const uint32_t no = (uint32_t)((n0 / 8) * 128);
-              const uint64_t Bh = make_desc(b_hi + bo + no, (N2 / 8) * 128, 128);
-              const uint64_t Bl = make_desc(b_lo + bo + no, (N2 / 8) * 128, 128);
-              const uint32_t d = tmem + n0;
-              mma_tf32(d, Ah, Bh, idesc, (c0 + q > 0 || s > 0) ? 1u : 0u);
-              mma_tf32(d, Ah, Bl, idesc, 1u);
-              mma_tf32(d, Al, Bh, idesc, 1u);
-            }
-          }
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                         smem_u32(&mbar_m[st]))
-                     : "memory");
-      }
-    }
-    mbar_wait(&mbar_m[(jc - 1) % S], ((jc - 1) / S) & 1);   // D2 complete
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-    // epilogue: this thread's TMEM lane holds its op's output state (interleaved re / im)
-    float2* d = tid < t.op_count ? dst + dst_off[t.op_begin + tid] : nullptr;
-    for (int c0 = 0; c0 < N2; c0 += 16) {
-      float w[16];
-      tmem_ld16(tmem + lane_base + c0, w);
-      if (d) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int row = c0 / 2 + 2 * q;   // complex rows (row, row+1); row+1 = T is the padding slot
-          if (row < t.T)
-            atomicAdd(reinterpret_cast<float4*>(d + row), make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
-        }
-      }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
-    __syncthreads();   // TMEM column 0 is free for the next task's D1
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
-}
-
 // ---------------------------------------------------------------------------
 // Warp-specialised persistent form (k_m2l_tcw, the default tensor-core M2L):
 //   warps 0-3 (the "row" warps, thread t = op t = TMEM lane t): gather the
@@ -1054,36 +834,9 @@ void launch_xlate_tcw(int tiles, int ntask, const TcTask* tasks, const int64_t* 
     k_xlate_tcw<4, 2><<<grid, TCW_NT, xlate_tcw_smem<4, 2>(), s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst);
 }
 
-int m2l_tc_stage_fl(int n1, int n2) {
-  return (int)std::max<size_t>(LRTC_CPJ * (2 * 128 * TC_KC + (size_t)n1 * TC_KC * 2), (size_t)n2 * TC_KC * 2);
-}
-// ring stages that fit next to the phase-2 A region (≤ 220 KB), 3 … 8
-int m2l_tc_stages(int stage_fl, int n1max) {
-  const size_t a2 = (size_t)(n1max / TC_KC) * 2 * 128 * TC_KC * 4;
-  const size_t cap = 220 * 1024 - 1024 - a2;
-  const int s = (int)(cap / ((size_t)stage_fl * 4));
-  return s >= 8 ? 8 : (s >= 6 ? 6 : (s >= 4 ? 4 : 3));
-}
-size_t m2l_tc_smem(int stage_fl, int n1max) {
-  return ((size_t)m2l_tc_stages(stage_fl, n1max) * stage_fl + (size_t)(n1max / TC_KC) * 2 * 128 * TC_KC) * 4 + 1024;
-}
-uint32_t m2l_tc_cols(int nmax) { return tmem_cols(nmax); }
-cudaError_t m2l_tc_prepare() {
-  cudaError_t e = cudaFuncSetAttribute(k_m2l_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_tc<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  return e;
-}
-void launch_m2l_tc(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off, const float* tcpool,
-                   const float2* src, float2* dst, size_t smem, uint32_t ncols, int grid, int stages, cudaStream_t s) {
-  if (ntask <= 0) return;
-  switch (stages) {
-    case 8: k_m2l_tc<8><<<grid, 128, smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst, ncols); break;
-    case 6: k_m2l_tc<6><<<grid, 128, smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst, ncols); break;
-    case 4: k_m2l_tc<4><<<grid, 128, smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst, ncols); break;
-    default: k_m2l_tc<3><<<grid, 128, smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst, ncols); break;
-  }
+int m2l_tc_stage_fl(int n1, int n2) {   // floats of one phase-1 ring stage of k_m2l_tcw (A hi|lo + B1 hi|lo)
+  (void)n2;
+  return 2 * 128 * TC_KC + n1 * TC_KC * 2;
 }
 
 
