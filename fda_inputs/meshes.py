@@ -220,8 +220,8 @@ def graded_spheroid(a: float = 0.5, b: float = 0.125, h_eq: float = 2.4809e-3,
                 adv_a = False
             elif ib >= nb:
                 adv_a = True
-            else:
-                adv_a = np.linalg.norm(P[a1] - P[b0]) <= np.linalg.norm(P[a0] - P[b1])
+            else:      # the shorter diagonal (squared lengths, plain floats: same order as the norms)
+                adv_a = _d2(verts[a1], verts[b0]) <= _d2(verts[a0], verts[b1])
             if adv_a:
                 faces.append((a0, a1, b0))
                 ia += 1
@@ -235,11 +235,15 @@ def graded_spheroid(a: float = 0.5, b: float = 0.125, h_eq: float = 2.4809e-3,
     return _finish(P, faces)
 
 
+def _d2(p, q):
+    dx, dy, dz = p[0] - q[0], p[1] - q[1], p[2] - q[2]
+    return dx * dx + dy * dy + dz * dz
+
+
 def _orient_outward_convex(P, faces):
-    out = []
-    for (a, b, c) in faces:
-        pa, pb, pc = P[a], P[b], P[c]
-        if np.dot(np.cross(pb - pa, pc - pa), pa + pb + pc) < 0:
-            b, c = c, b
-        out.append((a, b, c))
-    return out
+    """Flip faces whose CCW normal points towards the origin (convex, origin inside)."""
+    Fa = np.asarray(faces, dtype=np.int64)
+    pa, pb, pc = P[Fa[:, 0]], P[Fa[:, 1]], P[Fa[:, 2]]
+    flip = np.einsum("ij,ij->i", np.cross(pb - pa, pc - pa), pa + pb + pc) < 0
+    Fa[flip, 1], Fa[flip, 2] = Fa[flip, 2], Fa[flip, 1].copy()
+    return [tuple(f) for f in Fa.tolist()]

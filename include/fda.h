@@ -43,7 +43,7 @@ typedef enum {
   FDA_E_MESH = 2,          /* degenerate triangle, repeated vertex, open/inconsistent mesh */
   FDA_E_NOMEM = 3,         /* host or device allocation failed */
   FDA_E_CUDA = 4,          /* CUDA runtime error (message has the CUDA error string) */
-  FDA_E_NCCL = 5,          /* reserved: multi-GPU communication error */
+  FDA_E_NCCL = 5,          /* NCCL load / communicator / collective error (sharded contexts) */
   FDA_E_NOT_CONVERGED = 6, /* bm_solve hit max_iter; u holds the best iterate */
   FDA_E_STATE = 7,         /* call not valid in this state (e.g. matvec on a host-only build) */
   FDA_E_INTERNAL = 8
@@ -85,9 +85,10 @@ typedef struct {
   int32_t tensor_cores;  /* dense translations (M2M, L2L, dense M2L) on tcgen05 tensor cores,
                             3xTF32: 0 never, 1 every eligible stage (factored M2L too),
                             2 (default) stages of ≥ 1 GFLOP with ≥ 64 ops per matrix (CUDA
-                            cores elsewhere), 3 as 2 with the deep-pipeline one-CTA-per-SM
-                            kernel variants (A/B), 4 as 2 with the warp-specialised
-                            persistent kernel for ≤ 2 row tiles (A/B)                      */
+                            cores elsewhere); A/B variants on every eligible stage (dense
+                            ones; the factored M2L keeps its fused kernels): 3 the
+                            deep-pipeline one-CTA-per-SM kernels, 4 the warp-specialised
+                            persistent kernel for ≤ 2 row tiles                            */
   int32_t hf_leaves;     /* 0 (default): HF cubes are always split, all leaves are LF (reading
                             C9); 1: the count rule at every level, leaves may be HF, with
                             directional S2M / L2T per used wedge (PAPER.md P:344-346,
@@ -98,6 +99,11 @@ typedef struct {
                             kernel), 1 always, 2 (default) on levels with ≥ 64 ops per factored
                             K̃ and ≥ 3 GFLOP of factored work; needs
                             tensor_cores ≠ 0                                               */
+  int32_t build_on_device;  /* 1 (default): the fp64 operator and correction tables of
+                            fda_build are computed on opt.device (build_dev.cu: kernel-matrix
+                            generation, batched fp64 complex GEMMs, tier quadrature), the
+                            same definitions as the host build; 0: host C++/OpenMP only.
+                            Ignored (host) when opt.device = -1                             */
 } fda_options;
 
 typedef struct {
@@ -223,6 +229,14 @@ fda_status fda_set_profiling(fda_ctx* ctx, int32_t on);
  * the first matvec. */
 fda_status fda_near_time(fda_ctx* ctx, double* ms);
 fda_status fda_stage_times(fda_ctx* ctx, double* ms, int32_t* n);
+/* Per-kernel-family device time (ms, CUDA events around every launch on the
+ * one stream of a profiled, serialised matvec: fda_set_profiling(ctx, 1) then
+ * fda_matvec(..., FDA_DEVICE, ...) on an unsharded context), summed over the
+ * family's launches, in the order [k_gather, k_near, k_s2m, k_xlate,
+ * k_xlate_tc, k_xlate_tcw, k_m2l_lr, k_m2l_tcw, k_l2t, k_scatter, memset] —
+ * the launch-list share of each __global__ function.  n = capacity; returns
+ * the count written in *n.  FDA_E_STATE before such a matvec. */
+fda_status fda_kernel_times(fda_ctx* ctx, double* ms, int32_t* n);
 
 /* Copy a named host-side build table (for host-logic tests; see
  * paper_1403_4747_b200/fda.py for the names).  If dst is NULL only *count

@@ -6,7 +6,7 @@
  * seconds.  Off-diagonal entries only: the self entry (tier T0, closed form,
  * reading C5) is added by oracle/selfterms.py on the Python side.
  * Rows are independent; OpenMP parallelises over rows.  Pinned by agreement
- * with oracle/dense.py (tests/test_oracle_c.py).  Shares nothing with the
+ * with oracle/dense.py (tests/test_oracle_dense.py).  Shares nothing with the
  * CUDA path.
  */
 #include <complex.h>

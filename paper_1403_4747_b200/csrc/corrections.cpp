@@ -1,5 +1,5 @@
 // Near-field correction tables C (LHS) and C_rhs (RHS operator, kind 1)
-// (host, fp64 → complex64 CSR in tree order).
+// (fp64 → complex64 CSR in tree order).
 //
 // The device applies the 3-point rule Q3 to every element pair, either on the
 // fly (direct leaf pairs, near kernel) or folded into S2M (far pairs).  The
@@ -8,7 +8,9 @@
 //   C_ij = A^tier_ij - A^Q3_ij   (ρ_ij < 3, including i = j)
 // where A^tier_ii = ½ + α H_ii (closed-form self term, reading C5) and the
 // Q3 value of the self pair is the (regular) 3-point sum on Δ_i.  The pair
-// search is a tree-independent radius search (uniform hash grid).
+// search is a tree-independent radius search (uniform hash grid) on the host;
+// the entries are evaluated here (host build) or by build_dev.cu (device build,
+// the same definitions in fp64 on the GPU).
 #include <algorithm>
 #include <cmath>
 #include <unordered_map>
@@ -17,7 +19,8 @@
 
 namespace fda {
 
-void build_corrections(const Geometry& g, const Params& p, Plan& plan, int kind) {
+void correction_pairs(const Geometry& g, const Params& p, std::vector<int64_t>& ptr, std::vector<int64_t>& col,
+                      std::vector<int8_t>& tier) {
   const int64_t n = g.n;
   const double t1 = p.opt.tier1_rho, t2 = p.opt.tier2_rho;
   double hmax = 0;
@@ -40,8 +43,9 @@ void build_corrections(const Geometry& g, const Params& p, Plan& plan, int kind)
     cidx(g.centroid[j], a, b, d);
     grid[hkey(a, b, d)].push_back(j);
   }
-  std::vector<std::vector<std::pair<int64_t, cf>>> rows(n);
-#pragma omp parallel for schedule(dynamic, 64)
+  std::vector<int64_t> cnt(n + 1, 0);
+  std::vector<std::vector<std::pair<int64_t, int8_t>>> rows(n);
+#pragma omp parallel for schedule(dynamic, 256)
   for (int64_t i = 0; i < n; ++i) {
     const Vec3& x = g.centroid[i];
     int64_t a, b, d;
@@ -53,34 +57,50 @@ void build_corrections(const Geometry& g, const Params& p, Plan& plan, int kind)
           auto it = grid.find(hkey(a + da, b + db, d + dd));
           if (it == grid.end()) continue;
           for (int64_t j : it->second) {
-            double rho = (x - g.centroid[j]).norm() / g.hmax[j];
+            const double rho = (x - g.centroid[j]).norm() / g.hmax[j];
             if (!(rho < t2)) continue;
-            cd q3 = entry_rule(3, x, g.normal[i], g.v0[j], g.v1[j], g.v2[j], g.normal[j], g.area[j], p.k, p.alpha,
-                               kind);
-            cd exact;
-            if (j == i)
-              exact = kind == 0 ? self_lhs(g.v0[i], g.v1[i], g.v2[i], p.k, p.alpha)
-                                : self_rhs(g.v0[i], g.v1[i], g.v2[i], p.k, p.alpha);
-            else exact = entry_rule(rho < t1 ? 1 : 2, x, g.normal[i], g.v0[j], g.v1[j], g.v2[j], g.normal[j],
-                                    g.area[j], p.k, p.alpha, kind);
-            cd c = exact - q3;
-            row.push_back({j, cf((float)c.real(), (float)c.imag())});
+            row.push_back({j, (int8_t)(j == i ? 0 : (rho < t1 ? 1 : 2))});
           }
         }
     std::sort(row.begin(), row.end(), [](const auto& u, const auto& v) { return u.first < v.first; });
   }
-  auto& ptr = kind == 0 ? plan.corr_ptr : plan.corr_ptr_rhs;
-  auto& col = kind == 0 ? plan.corr_col : plan.corr_col_rhs;
-  auto& val = kind == 0 ? plan.corr_val : plan.corr_val_rhs;
   ptr.assign(n + 1, 0);
   for (int64_t i = 0; i < n; ++i) ptr[i + 1] = ptr[i] + (int64_t)rows[i].size();
   col.resize(ptr[n]);
-  val.resize(ptr[n]);
+  tier.resize(ptr[n]);
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) {
     int64_t o = ptr[i];
     for (size_t e = 0; e < rows[i].size(); ++e) {
       col[o + e] = rows[i][e].first;
-      val[o + e] = rows[i][e].second;
+      tier[o + e] = rows[i][e].second;
+    }
+    std::vector<std::pair<int64_t, int8_t>>().swap(rows[i]);
+  }
+}
+
+void build_corrections(const Geometry& g, const Params& p, Plan& plan, int kind) {
+  auto& ptr = kind == 0 ? plan.corr_ptr : plan.corr_ptr_rhs;
+  auto& col = kind == 0 ? plan.corr_col : plan.corr_col_rhs;
+  auto& val = kind == 0 ? plan.corr_val : plan.corr_val_rhs;
+  std::vector<int8_t> tier;
+  correction_pairs(g, p, ptr, col, tier);
+  const int64_t n = g.n;
+  val.resize(ptr[n]);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t i = 0; i < n; ++i) {
+    const Vec3& x = g.centroid[i];
+    for (int64_t e = ptr[i]; e < ptr[i + 1]; ++e) {
+      const int64_t j = col[e];
+      cd q3 = entry_rule(3, x, g.normal[i], g.v0[j], g.v1[j], g.v2[j], g.normal[j], g.area[j], p.k, p.alpha, kind);
+      cd exact;
+      if (tier[e] == 0)
+        exact = kind == 0 ? self_lhs(g.v0[i], g.v1[i], g.v2[i], p.k, p.alpha)
+                          : self_rhs(g.v0[i], g.v1[i], g.v2[i], p.k, p.alpha);
+      else exact = entry_rule(tier[e], x, g.normal[i], g.v0[j], g.v1[j], g.v2[j], g.normal[j], g.area[j], p.k,
+                              p.alpha, kind);
+      const cd c = exact - q3;
+      val[e] = cf((float)c.real(), (float)c.imag());
     }
   }
 }

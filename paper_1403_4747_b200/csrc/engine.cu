@@ -102,6 +102,7 @@ struct XStage {
   int ntask[XV] = {};
   int64_t* src = nullptr;
   int64_t* dst = nullptr;
+  double fl[3] = {0, 0, 0};        // algorithmic flops (8·rows·cols per op) on k_xlate / k_xlate_tc / k_xlate_tcw
 };
 
 // GMRES workspace (engine_solve; cached per context)
@@ -164,10 +165,11 @@ struct Dev {
     int n_lr[LR_NCLS] = {};
     int64_t* lr_src = nullptr;
     int64_t* lr_dst = nullptr;
-    LrTcTask* lrtc = nullptr;        // fused §4.2 tasks on the tensor cores (k_m2l_tc, persistent)
+    LrTcTask* lrtc = nullptr;        // fused §4.2 tasks on the tensor cores (k_m2l_tcw, persistent)
     int n_lrtc = 0;
     int lrtc_grid = 0;
     LrTcPlan lrtc_plan;
+    double fl_lr = 0, fl_lrtc = 0;   // algorithmic flops (16·r·T per factored op) on k_m2l_lr / k_m2l_tcw
     bool any() const {
       int n = n_lrtc;
       for (int c = 0; c < LR_NCLS; ++c) n += n_lr[c];
@@ -197,9 +199,37 @@ struct Dev {
   bool use_tc = false;
   std::vector<float> tc_host;
   std::unordered_map<int64_t, int64_t> tc_off;   // matrix id → float offset
-  std::unordered_map<int64_t, int64_t> tc_boff;  // matrix id → float offset of its k_m2l_tc B operand
+  std::unordered_map<int64_t, int64_t> tc_boff;  // matrix id → float offset of its k_m2l_tcw B operand
   float* tcpool = nullptr;
+  // per-kernel-family device times of a profiled (serialised) matvec: event marks
+  // recorded around every launch on the one stream (fda_kernel_times)
+  bool kt_on = false;
+  std::vector<cudaEvent_t> kt_ev;
+  std::vector<int> kt_fam;        // family of the launch that ends at mark i (-1: a start mark)
+  int kt_n = 0;
 };
+
+// kernel families of fda_kernel_times (include/fda.h)
+enum KFam { KF_GATHER = 0, KF_NEAR, KF_S2M, KF_XLATE, KF_XLATE_TC, KF_XLATE_TCW, KF_M2L_LR, KF_M2L_TCW, KF_L2T,
+            KF_SCATTER, KF_MEMSET, KF_COUNT };
+
+static void kt_mark(Dev* d, cudaStream_t s, int fam) {
+  if (!d->kt_on) return;
+  if (d->kt_n >= (int)d->kt_ev.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) { d->kt_on = false; return; }
+    d->kt_ev.push_back(e);
+    d->kt_fam.push_back(-1);
+  }
+  d->kt_fam[d->kt_n] = fam;
+  cudaEventRecord(d->kt_ev[d->kt_n++], s);
+}
+#define KT(fam, s, ...)       \
+  do {                        \
+    kt_mark(d, s, -1);        \
+    __VA_ARGS__;              \
+    kt_mark(d, s, fam);       \
+  } while (0)
 
 template <class T>
 static fda_status upload(Context* ctx, Dev* d, T** dst, const T* src, size_t count) {
@@ -276,7 +306,7 @@ static int64_t tc_matrix(Context* ctx, Dev* d, int64_t m) {
   return off;
 }
 
-// B operand of k_m2l_tc: the real 2R × 2C form of matrix m (as in tc_matrix) as
+// B operand of k_m2l_tcw: the real 2R × 2C form of matrix m (as in tc_matrix) as
 // nrp ≥ 2R rows × K = 2C (zero-padded to nkc 16-float chunks), per chunk
 // [hi: nrp × 16 | lo: nrp × 16] in the canonical K-major no-swizzle layout
 // (core matrices of 8 rows × 16 B; the rows of one 4-float k-group contiguous)
@@ -329,7 +359,7 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   std::vector<int64_t> so, dof;
   std::vector<XTask> tasks[XV];
   bool tc = d->use_tc && atomic && tc_ok;
-  if (tc && ctx->p.opt.tensor_cores >= 2 && !force_tc) {   // auto: large, well-shared stages only
+  if (tc && ctx->p.opt.tensor_cores == 2 && !force_tc) {   // auto: large, well-shared stages only
     double flops = 0;
     std::unordered_map<int64_t, int> nm;
     for (const XOp& o : ops) {
@@ -391,6 +421,7 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
         }
         tct[v].swap(out);
       }
+    auto tfl = [](const TcTask& t) { return 8.0 * t.R * t.C * t.op_count * (double)(t.kc1 - t.kc0) / t.nkc; };
     if (ctx->p.opt.tensor_cores == 4) {   // N = 128, ≤ 2 tiles → the warp-specialised persistent kernel
       std::vector<TcTask> w[2];
       for (int v = 0; v < TC_NV; ++v) {
@@ -407,11 +438,13 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
                          [](const TcTask& x, const TcTask& y) { return x.kc1 - x.kc0 > y.kc1 - y.kc0; });
         st.n_tcw[q] = (int)w[q].size();
         st.grid_tcw[q] = std::min<int>(st.n_tcw[q], nsm);
+        for (const TcTask& t : w[q]) st.fl[2] += tfl(t);
         if (st.n_tcw[q]) UP(&st.tcw[q], w[q].data(), w[q].size());
       }
     }
     for (int v = 0; v < TC_NV; ++v) {
       st.n_tc[v] = (int)tct[v].size();
+      for (const TcTask& t : tct[v]) st.fl[1] += tfl(t);
       if (st.n_tc[v]) UP(&st.tc[v], tct[v].data(), tct[v].size());
     }
     UP(&st.src, so.data(), so.size());
@@ -477,6 +510,7 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   }
   for (int v = 0; v < XV; ++v) {
     st.ntask[v] = (int)tasks[v].size();
+    for (const XTask& t : tasks[v]) st.fl[0] += 8.0 * std::min(xvar_rows(v), t.rows - t.row0) * (t.k_end - t.k_begin) * t.op_count;
     if (st.ntask[v]) UP(&st.tasks[v], tasks[v].data(), tasks[v].size());
   }
   UP(&st.src, so.data(), so.size());
@@ -484,15 +518,18 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   return FDA_OK;
 }
 
-static const float* g_tcpool = nullptr;   // set per context before launches (single-threaded use)
-
-static void launch_stage(const XStage& st, const float2* pool, const float2* src, float2* dst, cudaStream_t s) {
+// one translation stage: its tensor-core tasks read the context's own operand pool (d->tcpool)
+static void launch_stage(Dev* d, const XStage& st, const float2* src, float2* dst, cudaStream_t s) {
+  const float2* pool = d->pool;
+  const float* tcpool = d->tcpool;
   for (int q = 0; q < 2; ++q)
-    if (st.n_tcw[q]) launch_xlate_tcw(q + 1, st.n_tcw[q], st.tcw[q], st.src, st.dst, g_tcpool, src, dst, st.grid_tcw[q], s);
+    if (st.n_tcw[q])
+      KT(KF_XLATE_TCW, s, launch_xlate_tcw(q + 1, st.n_tcw[q], st.tcw[q], st.src, st.dst, tcpool, src, dst, st.grid_tcw[q], s));
   for (int v = 0; v < TC_NV; ++v)
-    if (st.n_tc[v]) launch_xlate_tc(v, st.n_tc[v], st.tc[v], st.src, st.dst, g_tcpool, src, dst, s);
+    if (st.n_tc[v]) KT(KF_XLATE_TC, s, launch_xlate_tc(v, st.n_tc[v], st.tc[v], st.src, st.dst, tcpool, src, dst, s));
   for (int v = 0; v < XV; ++v)
-    if (st.ntask[v]) launch_xlate(v, st.atomic, st.ntask[v], st.tasks[v], st.src, st.dst, pool, src, dst, s);
+    if (st.ntask[v])
+      KT(KF_XLATE, s, launch_xlate(v, st.atomic, st.ntask[v], st.tasks[v], st.src, st.dst, pool, src, dst, s));
 }
 
 fda_status engine_create(Context* ctx) {
@@ -823,7 +860,6 @@ fda_status engine_create(Context* ctx) {
           tk.n1 = 2 * ((r + 7) / 8) * 8;
           tk.n2 = 2 * ((T + 7) / 8) * 8;
           tk.nk1 = (2 * T + TC_KC - 1) / TC_KC;
-          tk.stage_fl = m2l_tc_stage_fl(tk.n1, tk.n2);   // (raised to the level maximum below)
           tk.b1_off = tc_bop(ctx, d, Ft[i].matV, tk.n1, tk.nk1);
           tk.b2_off = tc_bop(ctx, d, Ft[i].matU, tk.n2, tk.n1 / TC_KC);
           tk.op_begin = (int32_t)ls.size();
@@ -836,12 +872,8 @@ fda_status engine_create(Context* ctx) {
           i = j;
         }
         // one ring layout per launch; tasks longest first (the persistent CTAs stride over them)
-        int sfl = 0, n1m = 16;
-        for (const LrTcTask& tk : tt) {
-          sfl = std::max(sfl, tk.stage_fl);
-          n1m = std::max(n1m, tk.n1);
-        }
-        for (LrTcTask& tk : tt) tk.stage_fl = sfl;
+        int n1m = 16;
+        for (const LrTcTask& tk : tt) n1m = std::max(n1m, tk.n1);
         std::stable_sort(tt.begin(), tt.end(), [](const LrTcTask& x, const LrTcTask& y) {
           return (int64_t)(x.nk1 + x.n1 / TC_KC) * x.n2 > (int64_t)(y.nk1 + y.n1 / TC_KC) * y.n2;
         });
@@ -857,12 +889,14 @@ fda_status engine_create(Context* ctx) {
           L.lrtc_grid = std::min<int>((int)tt.size(), nsm);
         }
         L.n_lrtc = (int)tt.size();
+        for (const LrTcTask& tk : tt) L.fl_lrtc += 16.0 * tk.r * tk.T * tk.op_count;
         if (L.n_lrtc) UP(&L.lrtc, tt.data(), tt.size());
       }
       for (int c = 0; c < LR_NCLS; ++c) {
         std::stable_sort(lt[c].begin(), lt[c].end(),
                          [&](const LrTask& x, const LrTask& y) { return cost(x) > cost(y); });
         L.n_lr[c] = (int)lt[c].size();
+        for (const LrTask& tk : lt[c]) L.fl_lr += 16.0 * tk.r * tk.T * tk.op_count;
         if (L.n_lr[c]) UP(&L.lr_tasks[c], lt[c].data(), lt[c].size());
       }
       if (!ls.empty()) {
@@ -918,6 +952,30 @@ fda_status engine_create(Context* ctx) {
     nl += L.n_lrtc > 0;
   }
   ctx->launches_per_matvec = nl;
+  // CTA tasks per translation kernel family (fda_debug_table "kernel_tasks"; lets the tests
+  // assert where the translations were routed): [k_xlate, k_xlate_tc, k_xlate_tcw, k_m2l_lr,
+  // k_m2l_tcw], each split into M2M | M2L | L2L
+  {
+    int64_t* kt = ctx->kernel_tasks;
+    for (int i = 0; i < 15; ++i) kt[i] = 0;
+    double* kf = ctx->kernel_flops;
+    for (int i = 0; i < 15; ++i) kf[i] = 0;
+    auto add = [&](const XStage& st, int which) {
+      for (int v = 0; v < XV; ++v) kt[0 * 3 + which] += st.ntask[v];
+      for (int v = 0; v < TC_NV; ++v) kt[1 * 3 + which] += st.n_tc[v];
+      for (int q = 0; q < 2; ++q) kt[2 * 3 + which] += st.n_tcw[q];
+      for (int f = 0; f < 3; ++f) kf[f * 3 + which] += st.fl[f];
+    };
+    for (auto& st : d->m2m) add(st, 0);
+    for (auto& st : d->l2l) add(st, 2);
+    for (auto& L : d->m2lv) {
+      add(L.dense, 1); add(L.a, 1); add(L.b, 1);
+      for (int c = 0; c < LR_NCLS; ++c) kt[3 * 3 + 1] += L.n_lr[c];
+      kt[4 * 3 + 1] += L.n_lrtc;
+      kf[3 * 3 + 1] += L.fl_lr;
+      kf[4 * 3 + 1] += L.fl_lrtc;
+    }
+  }
   // priorities: the far-field chain (S2M → M2M → M2L → L2L → L2T, captured
   // from s_cap and the M2L branch streams) is the critical path of the graph;
   // the near field (no dependencies until the final join) runs at the lowest
@@ -1004,13 +1062,13 @@ void engine_destroy(Context* ctx) {
   if (d->ev_l0) cudaEventDestroy(d->ev_l0);
   if (d->ev_l1) cudaEventDestroy(d->ev_l1);
   if (d->ev_n1) cudaEventDestroy(d->ev_n1);
+  for (auto& e : d->kt_ev) cudaEventDestroy(e);
   delete d;
   ctx->dev = nullptr;
 }
 
 // the device part of one matvec: x_tree → y_near, y_far (tree order)
 static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
-  g_tcpool = d->tcpool;
   // profiling mode serialises the near field on the main stream so that every
   // stage time is the isolated duration of its kernels
   const bool prof = ctx->profiling;
@@ -1018,42 +1076,54 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   CK(cudaEventRecord(d->ev_fork, s));
   CK(cudaStreamWaitEvent(sn, d->ev_fork, 0));
   if (prof) CK(cudaEventRecord(d->ev_n0, sn));
-  CK(cudaEventRecord(d->ev_l0, sn));
-  launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
-              kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
-              kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, d->near_wide, sn);
-  CK(cudaEventRecord(d->ev_l1, sn));
+  // near-kernel timing events: external event nodes when captured (so every graph replay
+  // re-timestamps them), plain records in eager runs (the flag is only valid under capture)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(sn, &cap));
+  const unsigned evf = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  CK(cudaEventRecordWithFlags(d->ev_l0, sn, evf));
+  KT(KF_NEAR, sn,
+     launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
+                 kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
+                 kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind,
+                 d->near_wide, sn));
+  CK(cudaEventRecordWithFlags(d->ev_l1, sn, evf));
   d->live = true;
   if (prof) CK(cudaEventRecord(d->ev_n1, sn));
   CK(cudaEventRecord(d->ev_join, sn));
 
   if (prof) CK(cudaEventRecord(d->ev[1], s));
+  kt_mark(d, s, -1);
   if (d->out_size) CK(cudaMemsetAsync(d->outb, 0, sizeof(float2) * d->out_size, s));
   if (d->in_size) CK(cudaMemsetAsync(d->inb, 0, sizeof(float2) * d->in_size, s));
   if (d->tmp_size) CK(cudaMemsetAsync(d->tmpb, 0, sizeof(float2) * d->tmp_size, s));
-  if (kind) launch_s2m(d->n_s2m_rhs, d->s2m_rhs, d->pool, d->x_tree, d->outb, d->max_T, s);
-  else launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s);
+  kt_mark(d, s, KF_MEMSET);
+  if (kind) KT(KF_S2M, s, launch_s2m(d->n_s2m_rhs, d->s2m_rhs, d->pool, d->x_tree, d->outb, d->max_T, s));
+  else KT(KF_S2M, s, launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s));
   if (prof) CK(cudaEventRecord(d->ev[2], s));
   const int nlev = (int)d->m2m.size();
   auto m2l_level = [&](int l, cudaStream_t st) {
     const Dev::M2LLevel& L = d->m2lv[l];
-    launch_m2l_tcw(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_plan, L.lrtc_grid, st);
+    if (L.n_lrtc)
+      KT(KF_M2L_TCW, st,
+         launch_m2l_tcw(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_plan, L.lrtc_grid, st));
     for (int c = LR_NCLS - 1; c >= 0; --c)
-      launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st);
-    launch_stage(L.dense, d->pool, d->outb, d->inb, st);
-    launch_stage(L.a, d->pool, d->outb, d->tmpb, st);
-    launch_stage(L.b, d->pool, d->tmpb, d->inb, st);
+      if (L.n_lr[c])
+        KT(KF_M2L_LR, st, launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st));
+    launch_stage(d, L.dense, d->outb, d->inb, st);
+    launch_stage(d, L.a, d->outb, d->tmpb, st);
+    launch_stage(d, L.b, d->tmpb, d->inb, st);
   };
   if (prof) {
     // serialised: every stage time is the isolated duration of its kernels
     for (int l = nlev - 1; l >= 0; --l) {
-      launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);
+      launch_stage(d, d->m2m[l], d->outb, d->outb, s);
     }
     CK(cudaEventRecord(d->ev[3], s));
     for (int l = 0; l < nlev; ++l) m2l_level(l, s);
     CK(cudaEventRecord(d->ev[4], s));
     for (int l = 0; l < nlev; ++l) {
-      launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
+      launch_stage(d, d->l2l[l], d->inb, d->inb, s);
     }
     CK(cudaEventRecord(d->ev[5], s));
   } else {
@@ -1064,7 +1134,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
     int k = 0;
     std::vector<int> nbr(nlev, 0);
     for (int l = nlev - 1; l >= 0; --l) {
-      launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);   // writes level-l out-states
+      launch_stage(d, d->m2m[l], d->outb, d->outb, s);   // writes level-l out-states
       if (!d->m2lv[l].any()) continue;
       const Dev::M2LLevel& L = d->m2lv[l];
       CK(cudaEventRecord(d->ev_up[l], s));
@@ -1088,19 +1158,19 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
              })) != FDA_OK)
           return bs;
       if ((bs = branch([&](cudaStream_t sm) {
-             launch_stage(L.dense, d->pool, d->outb, d->inb, sm);
-             launch_stage(L.a, d->pool, d->outb, d->tmpb, sm);
-             launch_stage(L.b, d->pool, d->tmpb, d->inb, sm);
+             launch_stage(d, L.dense, d->outb, d->inb, sm);
+             launch_stage(d, L.a, d->outb, d->tmpb, sm);
+             launch_stage(d, L.b, d->tmpb, d->inb, sm);
            })) != FDA_OK)
         return bs;
     }
     for (int l = 0; l < nlev; ++l) {
       for (int b = 0; b < nbr[l]; ++b) CK(cudaStreamWaitEvent(s, d->ev_m2l[l][b], 0));
-      launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
+      launch_stage(d, d->l2l[l], d->inb, d->inb, s);
     }
   }
-  launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
-  launch_l2t(d->n_l2t_add, d->l2t_add, d->pool, d->inb, d->y_far, s, /*accumulate=*/true);
+  KT(KF_L2T, s, launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s));
+  if (d->n_l2t_add) KT(KF_L2T, s, launch_l2t(d->n_l2t_add, d->l2t_add, d->pool, d->inb, d->y_far, s, /*accumulate=*/true));
   if (prof) CK(cudaEventRecord(d->ev[6], s));
   CK(cudaStreamWaitEvent(s, d->ev_join, 0));
   CK(cudaGetLastError());
@@ -1117,11 +1187,16 @@ static fda_status run_sharded_up(Context* ctx, Dev* d, cudaStream_t s, int kind)
   CK(cudaEventRecord(d->ev_fork, s));
   CK(cudaStreamWaitEvent(sn, d->ev_fork, 0));
   if (prof) CK(cudaEventRecord(d->ev_n0, sn));
-  CK(cudaEventRecord(d->ev_l0, sn));
+  // near-kernel timing events: external event nodes when captured (so every graph replay
+  // re-timestamps them), plain records in eager runs (the flag is only valid under capture)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(sn, &cap));
+  const unsigned evf = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  CK(cudaEventRecordWithFlags(d->ev_l0, sn, evf));
   launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
               kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
               kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, d->near_wide, sn);
-  CK(cudaEventRecord(d->ev_l1, sn));
+  CK(cudaEventRecordWithFlags(d->ev_l1, sn, evf));
   d->live = true;
   if (prof) CK(cudaEventRecord(d->ev_n1, sn));
   CK(cudaEventRecord(d->ev_join, sn));
@@ -1133,7 +1208,7 @@ static fda_status run_sharded_up(Context* ctx, Dev* d, cudaStream_t s, int kind)
   else launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s);
   if (prof) CK(cudaEventRecord(d->ev[2], s));
   const int nlev = (int)d->m2m.size();
-  for (int l = nlev - 1; l >= 0; --l) launch_stage(d->m2m[l], d->pool, d->outb, d->outb, s);   // partials
+  for (int l = nlev - 1; l >= 0; --l) launch_stage(d, d->m2m[l], d->outb, d->outb, s);   // partials
   launch_pack(d->outb, d->xs_idx, d->sendb, d->n_send, s);
   if (prof) CK(cudaEventRecord(d->ev[3], s));
   CK(cudaGetLastError());
@@ -1161,7 +1236,6 @@ static fda_status exchange_nccl(Context* ctx, Dev* d, cudaStream_t s) {
 }
 
 static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
-  g_tcpool = d->tcpool;
   launch_unpack_add(d->recvb, d->xr_idx, d->outb, d->n_recv, s);
   const int nlev = (int)d->m2m.size();
   CK(cudaEventRecord(d->ev_up[0], s));
@@ -1183,9 +1257,9 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
       if (c >= 0) {
         launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, sm);
       } else {
-        launch_stage(L.dense, d->pool, d->outb, d->inb, sm);
-        launch_stage(L.a, d->pool, d->outb, d->tmpb, sm);
-        launch_stage(L.b, d->pool, d->tmpb, d->inb, sm);
+        launch_stage(d, L.dense, d->outb, d->inb, sm);
+        launch_stage(d, L.a, d->outb, d->tmpb, sm);
+        launch_stage(d, L.b, d->tmpb, d->inb, sm);
       }
       CK(cudaEventRecord(d->ev_m2l[l][nbr[l]++], sm));
     }
@@ -1198,7 +1272,7 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
   }
   for (int l = 0; l < nlev; ++l) {
     for (int b = 0; b < nbr[l]; ++b) CK(cudaStreamWaitEvent(s, d->ev_m2l[l][b], 0));
-    launch_stage(d->l2l[l], d->pool, d->inb, d->inb, s);
+    launch_stage(d, d->l2l[l], d->inb, d->inb, s);
   }
   if (prof) CK(cudaEventRecord(d->ev[5], s));
   launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
@@ -1250,13 +1324,16 @@ static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind, int phase
 static fda_status matvec_dev(Context* ctx, Dev* d, const float2* x, float2* y, cudaStream_t s, int kind = 0,
                              bool local = false, int phase = 0) {
   const bool prof = ctx->profiling && (d->nranks <= 1 || phase == 0);
+  d->kt_on = prof && d->nranks <= 1;
+  d->kt_n = 0;
   if (prof) CK(cudaEventRecord(d->ev[0], s));
-  if (phase != FDA_PHASE_DOWN) launch_gather_f32(x, d->perm, d->x_tree, d->n, s);
+  if (phase != FDA_PHASE_DOWN) KT(KF_GATHER, s, launch_gather_f32(x, d->perm, d->x_tree, d->n, s));
   if (prof) CK(cudaEventRecord(d->ev[1], s));
   fda_status st = core(ctx, d, s, kind, phase);
   if (st != FDA_OK) return st;
   if (phase == FDA_PHASE_UP) return FDA_OK;
-  launch_scatter_f32(d->y_near, d->y_far, d->perm, y, d->n, d->e0, d->e1, s);
+  KT(KF_SCATTER, s, launch_scatter_f32(d->y_near, d->y_far, d->perm, y, d->n, d->e0, d->e1, s));
+  d->kt_on = false;
   if (prof) CK(cudaEventRecord(d->ev[7], s));
   d->timed = prof;
   CK(cudaGetLastError());
@@ -1334,6 +1411,26 @@ fda_status engine_near_time(Context* ctx, double* ms) {
   float v = 0.f;
   CK(cudaEventElapsedTime(&v, d->ev_l0, d->ev_l1));
   *ms = v;
+  return FDA_OK;
+}
+
+fda_status engine_kernel_times(Context* ctx, double* ms, int32_t* n) {
+  Dev* d = static_cast<Dev*>(ctx->dev);
+  if (!d->timed || d->kt_n == 0) {
+    ctx->err = "no profiled device-pointer matvec yet (fda_set_profiling(ctx, 1), then fda_matvec with FDA_DEVICE)";
+    return FDA_E_STATE;
+  }
+  CK(cudaEventSynchronize(d->kt_ev[d->kt_n - 1]));
+  double acc[KF_COUNT] = {0};
+  for (int i = 1; i < d->kt_n; ++i) {
+    if (d->kt_fam[i] < 0 || d->kt_fam[i - 1] >= 0) continue;
+    float v = 0.f;
+    CK(cudaEventElapsedTime(&v, d->kt_ev[i - 1], d->kt_ev[i]));
+    acc[d->kt_fam[i]] += v;
+  }
+  const int m = std::min<int>(*n, KF_COUNT);
+  for (int i = 0; i < m; ++i) ms[i] = acc[i];
+  *n = m;
   return FDA_OK;
 }
 

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <new>
+#include <stdexcept>
 #include <omp.h>
 
 #include "fda_internal.h"
@@ -46,6 +47,7 @@ fda_status fda_options_default(fda_options* opt) {
   opt->tensor_cores = 2;
   opt->hf_leaves = 0;
   opt->lr_tensor_cores = 2;
+  opt->build_on_device = 1;
   return FDA_OK;
 }
 
@@ -144,7 +146,18 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
         off += (ctx->t.levels[ctx->t.boxes[pl.in_states[s].box].level].rank + 1) & ~1;
       }
       pl.in_size = off;
-      build_operators(ctx->g, ctx->p, ctx->t, pl);
+      // operator tables: the device build (fp64 on opt.device) where possible, the host for
+      // the rest (HF-leaf S2M / L2T) and for host-only contexts
+      const bool on_dev = o.build_on_device != 0 && o.device >= 0;
+      operator_layout(ctx->t, pl);
+      std::vector<char> done;
+      LowRank lr;
+      if (on_dev) {
+        st = build_operators_device(ctx, done, lr);
+        if (st != FDA_OK) throw std::runtime_error(ctx->err);
+        phase("operators (device)");
+      }
+      build_operators(ctx->g, ctx->p, ctx->t, pl, done, lr);
       phase("operators");
       // §4.2: route the M2L ops whose K̃ was factored (r < T/2) to the two-stage path
       pl.n_m2l_total = 0;
@@ -178,8 +191,14 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
         }
         pl.m2l[l].swap(dense);
       }
-      build_corrections(ctx->g, ctx->p, pl, 0);
-      if (o.rhs_operator) build_corrections(ctx->g, ctx->p, pl, 1);
+      for (int kind = 0; kind <= (o.rhs_operator ? 1 : 0); ++kind) {
+        if (on_dev) {
+          st = build_corrections_device(ctx, kind);
+          if (st != FDA_OK) throw std::runtime_error(ctx->err);
+        } else {
+          build_corrections(ctx->g, ctx->p, pl, kind);
+        }
+      }
       phase("corrections");
       apply_partition(ctx->p, ctx->t, pl);
     }
@@ -328,6 +347,12 @@ fda_status fda_stage_times(fda_ctx* ctx, double* ms, int32_t* n) {
   return engine_stage_times(ctx, ms, n);
 }
 
+fda_status fda_kernel_times(fda_ctx* ctx, double* ms, int32_t* n) {
+  if (!ctx || !ms || !n) return FDA_E_INVALID_ARG;
+  if (!ctx->dev) return FDA_E_STATE;
+  return engine_kernel_times(ctx, ms, n);
+}
+
 fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int64_t* count, int32_t* eb) {
   if (!ctx || !name || !count || !eb) return FDA_E_INVALID_ARG;
   const Plan& p = ctx->plan;
@@ -430,6 +455,10 @@ fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int6
   if (nm == "owned")
     return put(std::vector<int64_t>{p.own_leaf0, p.own_leaf1, p.own_e0, p.own_e1}, dst, count, eb);
   if (nm == "launches") return put(std::vector<int64_t>{ctx->launches_per_matvec}, dst, count, eb);
+  if (nm == "kernel_tasks")
+    return put(std::vector<int64_t>(ctx->kernel_tasks, ctx->kernel_tasks + 15), dst, count, eb);
+  if (nm == "kernel_flops")
+    return put(std::vector<double>(ctx->kernel_flops, ctx->kernel_flops + 15), dst, count, eb);
   if (nm == "root") {
     return put(std::vector<double>{t.root_center.x, t.root_center.y, t.root_center.z, t.root_width, t.lambda},
                dst, count, eb);

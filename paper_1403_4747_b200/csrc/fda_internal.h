@@ -12,6 +12,7 @@
 
 namespace fda {
 
+struct Context;
 using cd = std::complex<double>;
 using cf = std::complex<float>;
 
@@ -191,9 +192,25 @@ int child_dir(int dir, int nf);
 Vec3 dir_center(int dir, int nf);
 Mat3 rotation_to_z(const Vec3& u);
 // operators.cpp
+struct LowRank {                       // §4.2 factors K̃ ≈ Û V̂ per M2L matrix id (R = -1: dense)
+  std::vector<int> R;
+  std::vector<std::vector<cd>> U, V;
+};
 void build_clouds_and_svd(const Params& p, Tree& t, const std::vector<bool>& need);
-void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan);
-// corrections.cpp
+void operator_layout(const Tree& t, Plan& plan);   // plan.mats (offset, rows, cols) + zeroed pool
+Mat3 out_frame(const Level& L, int dir);
+Mat3 in_frame(const Level& L, int dir);
+Vec3 octant_offset(int o, double wc);
+void lowrank_one(const Params& p, int64_t id, int T, const cd* M, LowRank& lr);
+// every spec with done[id] == 0 (done empty: all) on the host, then the §4.2 factors appended
+void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan, const std::vector<char>& done,
+                     LowRank& lr);
+// build_dev.cu: the same tables computed on the device in fp64 (opt.device >= 0, opt.build_on_device)
+fda_status build_operators_device(Context* ctx, std::vector<char>& done, LowRank& lr);
+fda_status build_corrections_device(Context* ctx, int kind);
+// corrections.cpp: pair search (CSR, tier 0 self / 1 / 2 per entry) and the host evaluation
+void correction_pairs(const Geometry& g, const Params& p, std::vector<int64_t>& ptr, std::vector<int64_t>& col,
+                      std::vector<int8_t>& tier);
 void build_corrections(const Geometry& g, const Params& p, Plan& plan, int kind = 0);
 // partition.cpp
 void apply_partition(const Params& p, const Tree& t, Plan& plan);
@@ -209,6 +226,8 @@ cd G(const Vec3& x, const Vec3& y, double k);
 cd dGdnx(const Vec3& x, const Vec3& nx, const Vec3& y, double k);
 cd dGdny(const Vec3& x, const Vec3& y, const Vec3& ny, double k);
 extern const double Q3_BARY[3][3];
+// rule tables for the device build: T1 448 × (b0, b1, b2, w), Q6 6 × (b0, b1, b2, w), GL20 20 × (x, w)
+void quad_tables(std::vector<double>& t1, std::vector<double>& q6, std::vector<double>& gl);
 // linalg.cpp
 void svd_jacobi(int m, int n, std::vector<cd>& A /*col-major m×n, overwritten*/, std::vector<double>& S,
                 std::vector<cd>& V /*n×n col-major*/);
@@ -226,6 +245,7 @@ fda_status engine_rhs_point_source(Context* ctx, const double src[3], void* b, i
 fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int32_t max_iter, int32_t restart,
                         fda_solve_info* info, int32_t flags);
 fda_status engine_stage_times(Context* ctx, double* ms, int32_t* n);
+fda_status engine_kernel_times(Context* ctx, double* ms, int32_t* n);
 fda_status engine_near_time(Context* ctx, double* ms);
 fda_status engine_comm_init(Context* ctx, const void* id128);
 fda_status engine_exchange_local(Context** ctxs, int n);
@@ -241,6 +261,8 @@ struct Context {
   fda_build_info info{};
   void* dev = nullptr;   // engine-owned device state
   int64_t launches_per_matvec = 0;
+  int64_t kernel_tasks[15] = {};   // CTA tasks per translation kernel family × (M2M, M2L, L2L)
+  double kernel_flops[15] = {};    // their algorithmic flops (complex-equivalent, 8·rows·cols per op)
   bool profiling = false;
 };
 

@@ -68,9 +68,9 @@ struct TcTask {
   int32_t op_begin, op_count;
   int32_t kc0, kc1;   // this task's K chunks (split-K: partial products accumulate atomically)
 };
-int tc_variant(int n, int tiles, bool multi);
+int tc_variant(int n, int tiles, bool multi);   // multi: the 2-stage, several-CTAs-per-SM variants
 
-// fused §4.2 M2L on the tensor cores (kernels_tc.cu, k_m2l_tc): ≤ 128 ops sharing K̃ ≈ Û V̂
+// fused §4.2 M2L on the tensor cores (kernels_tc.cu, k_m2l_tcw): ≤ 128 ops sharing K̃ ≈ Û V̂
 // with r ≤ 32; B operands pre-laid-out in the tensor-core pool (engine.cu: tc_bop)
 struct LrTcTask {
   int64_t b1_off;     // float offset of A_Vᵀ: n1 rows × 2T (padded to nk1·16) K, per 16-float chunk [hi | lo]
@@ -78,12 +78,10 @@ struct LrTcTask {
   int32_t T, r;
   int32_t n1, n2;     // 2·⌈r/8⌉·8 and 2·⌈T/8⌉·8
   int32_t nk1;        // ⌈2T / 16⌉
-  int32_t stage_fl;   // floats per ring stage: the maximum of m2l_tc_stage_fl over the launch
   int32_t op_begin, op_count;
 };
 constexpr int LRTC_MAX_R = 32;
 constexpr int LRTC_MAX_T = 160;   // keeps 3 ring stages + the phase-2 A region ≤ 220 KB (n1 ≤ 64, n2 ≤ 320)
-int m2l_tc_stage_fl(int n1, int n2);                 // floats of one phase-1 ring stage of k_m2l_tcw
 // warp-specialised persistent variant (k_m2l_tcw): launch plan from the level's max n1 / n2
 struct LrTcPlan {
   int stages = 3, stage_fl = 0, b2_fl = 0, n1max = 16;
@@ -95,7 +93,6 @@ cudaError_t m2l_tcw_prepare();
 void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                     const float* tcpool, const float2* src, float2* dst, const LrTcPlan& pl, int grid,
                     cudaStream_t s);
-  // multi: the 2-stage, several-CTAs-per-SM variants
 int tc_variant_ops(int v);
 
 // leaf-level ops (S2M / L2T)

@@ -834,10 +834,6 @@ void launch_xlate_tcw(int tiles, int ntask, const TcTask* tasks, const int64_t* 
     k_xlate_tcw<4, 2><<<grid, TCW_NT, xlate_tcw_smem<4, 2>(), s>>>(tasks, ntask, src_off, dst_off, tcpool, src, dst);
 }
 
-int m2l_tc_stage_fl(int n1, int n2) {   // floats of one phase-1 ring stage of k_m2l_tcw (A hi|lo + B1 hi|lo)
-  (void)n2;
-  return 2 * 128 * TC_KC + n1 * TC_KC * 2;
-}
 
 
 namespace {

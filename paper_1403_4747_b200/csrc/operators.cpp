@@ -78,15 +78,15 @@ void build_clouds_and_svd(const Params& p, Tree& t, const std::vector<bool>& nee
 }
 
 // frame rotation of an out-state (dir u) or in-state (dir w: frame of anti(w))
-static Mat3 out_frame(const Level& L, int dir) {
+Mat3 out_frame(const Level& L, int dir) {
   if (dir < 0) return rotation_to_z(Vec3(0, 0, 1));
   return rotation_to_z(dir_center(dir, L.nf));
 }
-static Mat3 in_frame(const Level& L, int dir) {
+Mat3 in_frame(const Level& L, int dir) {
   if (dir < 0) return rotation_to_z(Vec3(0, 0, 1));
   return rotation_to_z(dir_center(anti_dir(dir, L.nf), L.nf));
 }
-static Vec3 octant_offset(int o, double wc) {
+Vec3 octant_offset(int o, double wc) {
   return Vec3(((o & 1) ? 0.5 : -0.5) * wc, ((o >> 1) & 1 ? 0.5 : -0.5) * wc, ((o >> 2) & 1 ? 0.5 : -0.5) * wc);
 }
 
@@ -95,12 +95,9 @@ static void store(Plan& plan, int64_t id, int rows, int cols, const std::vector<
   for (size_t i = 0; i < (size_t)rows * cols; ++i) dst[i] = cf((float)M[i].real(), (float)M[i].imag());
 }
 
-void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
+void operator_layout(const Tree& t, Plan& plan) {
   const int64_t nm = (int64_t)plan.specs.size();
   plan.mats.resize(nm);
-  // leaf index of a leaf box
-  std::vector<int64_t> leaf_of_box(t.boxes.size(), -1);
-  for (size_t i = 0; i < plan.leaf_box.size(); ++i) leaf_of_box[plan.leaf_box[i]] = (int64_t)i;
   int64_t off = 0;
   for (int64_t id = 0; id < nm; ++id) {
     const MatSpec& s = plan.specs[id];
@@ -123,11 +120,30 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
     off += (int64_t)rows * cols;
   }
   plan.pool.assign(off, cf(0, 0));
-  std::vector<std::vector<cd>> lrU(nm), lrV(nm);
-  std::vector<int> lrR(nm, -1);
+}
 
+// §4.2: K̃ ≈ Û V̂ of one T × T M2L matrix, kept when r < T/2
+void lowrank_one(const Params& p, int64_t id, int T, const cd* M, LowRank& lr) {
+  std::vector<cd> Uh, Vh;
+  const int r = lowrank_factor(T, T, M, p.eps, Uh, Vh);
+  if (r > 0 && 2 * r < T) {
+    lr.R[id] = r;
+    lr.U[id].swap(Uh);
+    lr.V[id].swap(Vh);
+  }
+}
+
+// every spec not already computed on the device (done[id] = 1), then the §4.2 factors
+void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan, const std::vector<char>& done,
+                     LowRank& lr) {
+  const int64_t nm = (int64_t)plan.specs.size();
+  if ((int64_t)lr.R.size() != nm) { lr.R.assign(nm, -1); lr.U.assign(nm, {}); lr.V.assign(nm, {}); }
+  std::vector<int>& lrR = lr.R;
+  std::vector<std::vector<cd>>& lrU = lr.U;
+  std::vector<std::vector<cd>>& lrV = lr.V;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t id = 0; id < nm; ++id) {
+    if (!done.empty() && done[id]) continue;
     const MatSpec& s = plan.specs[id];
     const Level& L = t.levels[s.level];
     const int m = (int)L.chk.size(), n = (int)L.eq.size(), T = L.rank;
@@ -245,16 +261,7 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan) {
         M.resize((size_t)T * T);
         zgemm_cm(T, T, n, Vc.data(), n, X.data(), n, M.data(), T, true);  // V^T (K V)
         store(plan, id, T, T, M);
-        if (p.opt.m2l_lowrank) {
-          // §4.2: K̃ ≈ Û V̂, used when r < T/2
-          std::vector<cd> Uh, Vh;
-          const int r = lowrank_factor(T, T, M.data(), p.eps, Uh, Vh);
-          if (r > 0 && 2 * r < T) {
-            lrR[id] = r;
-            lrU[id].swap(Uh);
-            lrV[id].swap(Vh);
-          }
-        }
+        if (p.opt.m2l_lowrank) lowrank_one(p, id, T, M.data(), lr);
       } break;
     }
   }

@@ -101,6 +101,14 @@ const Rules& rules() {
 }
 }  // namespace
 
+void quad_tables(std::vector<double>& t1, std::vector<double>& q6, std::vector<double>& gl) {
+  const Rules& R = rules();
+  t1.clear(); q6.clear(); gl.clear();
+  for (int q = 0; q < 448; ++q) { t1.insert(t1.end(), {R.t1[q][0], R.t1[q][1], R.t1[q][2], R.wt1[q]}); }
+  for (int q = 0; q < 6; ++q) { q6.insert(q6.end(), {R.q6[q][0], R.q6[q][1], R.q6[q][2], R.w6[q]}); }
+  for (int i = 0; i < 20; ++i) { gl.push_back(R.gl_x[i]); gl.push_back(R.gl_w[i]); }
+}
+
 cd G(const Vec3& x, const Vec3& y, double k) {
   double r = (x - y).norm();
   return std::polar(1.0, k * r) / (4.0 * kPi * r);

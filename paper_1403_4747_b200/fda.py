@@ -32,10 +32,12 @@ STATUS = {0: "FDA_OK", 1: "FDA_E_INVALID_ARG", 2: "FDA_E_MESH", 3: "FDA_E_NOMEM"
 EXPORTS = ["fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_point_source",
            "fda_rhs_apply", "bm_solve",
            "fda_stats", "fda_nccl_unique_id", "fda_comm_init", "fda_exchange_local",
-           "fda_set_profiling", "fda_stage_times", "fda_near_time", "fda_debug_table", "fda_last_error", "fda_status_string",
-           "fda_free"]
+           "fda_set_profiling", "fda_stage_times", "fda_kernel_times", "fda_near_time", "fda_debug_table",
+           "fda_last_error", "fda_status_string", "fda_free"]
 
 STAGES = ["gather", "near", "s2m", "m2m", "m2l", "l2l", "l2t", "scatter"]
+KERNELS = ["k_gather", "k_near", "k_s2m", "k_xlate", "k_xlate_tc", "k_xlate_tcw", "k_m2l_lr", "k_m2l_tcw", "k_l2t",
+           "k_scatter", "memset"]
 
 
 class FdaError(RuntimeError):
@@ -55,7 +57,8 @@ class fda_options(ctypes.Structure):
                 ("device", ctypes.c_int32), ("build_threads", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("verbose", ctypes.c_int32), ("m2l_lowrank", ctypes.c_int32),
                 ("rhs_operator", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("tensor_cores", ctypes.c_int32), ("hf_leaves", ctypes.c_int32), ("lr_tensor_cores", ctypes.c_int32)]
+                ("tensor_cores", ctypes.c_int32), ("hf_leaves", ctypes.c_int32), ("lr_tensor_cores", ctypes.c_int32),
+                ("build_on_device", ctypes.c_int32)]
 
 
 class fda_solve_info(ctypes.Structure):
@@ -109,6 +112,7 @@ def load_library(path: str = LIB_PATH):
     lib.fda_set_profiling.argtypes = [vp, i32]
     lib.fda_near_time.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
     lib.fda_stage_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)]
+    lib.fda_kernel_times.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)]
     lib.fda_debug_table.argtypes = [vp, ctypes.c_char_p, vp, ctypes.POINTER(i64), ctypes.POINTER(i32)]
     lib.fda_last_error.argtypes = [vp]
     lib.fda_last_error.restype = ctypes.c_char_p
@@ -119,7 +123,7 @@ def load_library(path: str = LIB_PATH):
     for name in ("fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave", "fda_rhs_point_source",
                  "fda_rhs_apply", "bm_solve",
                  "fda_stats", "fda_nccl_unique_id", "fda_comm_init", "fda_exchange_local", "fda_exchange_local",
-                 "fda_set_profiling", "fda_stage_times", "fda_near_time", "fda_debug_table"):
+                 "fda_set_profiling", "fda_stage_times", "fda_kernel_times", "fda_near_time", "fda_debug_table"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -315,6 +319,13 @@ class FDA:
         self._check(self.lib.fda_stage_times(self.ctx, ms, ctypes.byref(n)))
         return {STAGES[i]: ms[i] for i in range(n.value)}
 
+    def kernel_times(self) -> dict:
+        """fda_kernel_times: ms per kernel family of the last profiled device matvec."""
+        ms = (ctypes.c_double * len(KERNELS))()
+        n = ctypes.c_int32(len(KERNELS))
+        self._check(self.lib.fda_kernel_times(self.ctx, ms, ctypes.byref(n)))
+        return {KERNELS[i]: ms[i] for i in range(n.value)}
+
     _DTYPES = {"perm": np.int64, "verts": np.float64, "leaf_range": np.int64, "leaf_S": np.int64,
                "leaf_T": np.int64, "leaf_S_rhs": np.int64, "corr_ptr_rhs": np.int64, "corr_col_rhs": np.int64,
                "corr_val_rhs": np.complex64, "leaf_out": np.int64, "leaf_in": np.int64, "out_offset": np.int64,
@@ -324,7 +335,23 @@ class FDA:
                "out_states": np.int64, "in_states": np.int64, "boxes": np.int64, "box_center": np.float64,
                "levels": np.float64, "root": np.float64, "launches": np.int64, "owned": np.int64,
                "xsend": np.int64, "xrecv": np.int64, "hf_s2m": np.int64, "hf_s2m_rhs": np.int64,
-               "hf_l2t": np.int64}
+               "hf_l2t": np.int64, "kernel_tasks": np.int64, "kernel_flops": np.float64}
+
+    KERNEL_FAMILIES = ("k_xlate", "k_xlate_tc", "k_xlate_tcw", "k_m2l_lr", "k_m2l_tcw")
+
+    def kernel_tasks(self) -> dict:
+        """CTA tasks per translation kernel family and stage ("k_xlate_tc/m2m", …):
+        where the build routed the translations (fda_debug_table "kernel_tasks")."""
+        t = self.table("kernel_tasks").reshape(5, 3)
+        return {f"{f}/{s}": int(t[i, j]) for i, f in enumerate(self.KERNEL_FAMILIES)
+                for j, s in enumerate(("m2m", "m2l", "l2l"))}
+
+    def kernel_flops(self) -> dict:
+        """Algorithmic flops per translation kernel family and stage (complex-equivalent,
+        8·rows·cols per op; 16·r·T per factored M2L op)."""
+        t = self.table("kernel_flops").reshape(5, 3)
+        return {f"{f}/{s}": float(t[i, j]) for i, f in enumerate(self.KERNEL_FAMILIES)
+                for j, s in enumerate(("m2m", "m2l", "l2l"))}
 
     def table(self, name: str) -> np.ndarray:
         """A host-side build table (host-logic tests only)."""

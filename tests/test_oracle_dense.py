@@ -154,3 +154,32 @@ def test_bm_coupling_sign_reading_c25():
         b = O.plane_wave_rhs(el.centroid, el.normal, k, a, np.array([0.0, 0.0, 1.0]))
         its[sg] = O.gmres(lambda v: A @ v, b, tol=1e-4, max_iter=200)[1]
     assert its[-1] <= 15 and its[1] >= 3 * its[-1], its
+
+
+def test_tier_uses_source_element_size():
+    """Reading C6 pins ρ_ij = |x_i − c_j| / h_j with h_j the SOURCE element's
+    longest edge.  A large source triangle (h = 1) and a tiny target triangle
+    (h = 0.01) one unit apart: row i sees j at ρ = 1 (tier T1, 448 points), row
+    j sees i at ρ = 100 (tier T3).  Swapping h_i for h_j (a misreading near-
+    uniform spheres cannot expose) flips both tiers; the T1 entry must also
+    match brute-force quadrature (depth-6 Radon, 28,672 points) where Q3 would
+    be off by O(1e-2).  Both the numpy definition and the C evaluator."""
+    V = np.array([[0.0, 0, 0], [1.0, 0, 0], [0.5, np.sqrt(3) / 2, 0],          # big source j = 0
+                  [0.0, 0, 1.0], [0.01, 0, 1.0], [0.005, 0.01 * np.sqrt(3) / 2, 1.0]])  # tiny target i = 1
+    F = np.array([[0, 1, 2], [3, 4, 5]], dtype=np.int32)
+    el = O.element_geometry(V, F)
+    el.centroid[1] = el.centroid[0] + np.array([0.0, 0.0, 1.0])     # |x_i − c_j| = 1 exactly
+    el.verts[1] = el.verts[1] - el.verts[1].mean(0) + el.centroid[1]
+    assert O.tier_of(el, 1)[0] == 1 and O.tier_of(el, 0)[1] == 3
+    k = 3.0
+    brute = subdivided_rule(RULE_Q7, 6)
+    P, W = brute
+    Y = P @ el.verts[0]
+    ref = el.area[0] * np.sum(W * O.lhs_kernel(el.centroid[1][None], el.normal[1][None], Y, el.normal[0][None],
+                                               k, 1j / k))
+    for a in (O.lhs_rows(el, [1], k, 1j / k)[0, 0], fast.dense_rows(el, [1], k, 1j / k, "lhs")[0, 0]):
+        assert abs(a - ref) <= 1e-6 * abs(ref)
+    P3, W3 = O.RULE_Q3
+    q3 = el.area[0] * np.sum(W3 * O.lhs_kernel(el.centroid[1][None], el.normal[1][None], P3 @ el.verts[0],
+                                               el.normal[0][None], k, 1j / k))
+    assert abs(q3 - ref) > 1e-3 * abs(ref)      # the wrong tier would be visible
