@@ -20,7 +20,7 @@
 namespace fda {
 
 void correction_pairs(const Geometry& g, const Params& p, std::vector<int64_t>& ptr, std::vector<int64_t>& col,
-                      std::vector<int8_t>& tier) {
+                      std::vector<int8_t>& tier, int64_t row0, int64_t row1) {
   const int64_t n = g.n;
   const double t1 = p.opt.tier1_rho, t2 = p.opt.tier2_rho;
   double hmax = 0;
@@ -43,10 +43,10 @@ void correction_pairs(const Geometry& g, const Params& p, std::vector<int64_t>& 
     cidx(g.centroid[j], a, b, d);
     grid[hkey(a, b, d)].push_back(j);
   }
-  std::vector<int64_t> cnt(n + 1, 0);
   std::vector<std::vector<std::pair<int64_t, int8_t>>> rows(n);
 #pragma omp parallel for schedule(dynamic, 256)
   for (int64_t i = 0; i < n; ++i) {
+    if (i < row0 || i >= row1) continue;   // another rank's row (sharded build)
     const Vec3& x = g.centroid[i];
     int64_t a, b, d;
     cidx(x, a, b, d);
@@ -84,7 +84,7 @@ void build_corrections(const Geometry& g, const Params& p, Plan& plan, int kind)
   auto& col = kind == 0 ? plan.corr_col : plan.corr_col_rhs;
   auto& val = kind == 0 ? plan.corr_val : plan.corr_val_rhs;
   std::vector<int8_t> tier;
-  correction_pairs(g, p, ptr, col, tier);
+  correction_pairs(g, p, ptr, col, tier, plan.own_e0, plan.own_e1);
   const int64_t n = g.n;
   val.resize(ptr[n]);
 #pragma omp parallel for schedule(dynamic, 64)

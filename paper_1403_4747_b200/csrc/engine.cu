@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <unordered_map>
 #include <vector>
@@ -197,7 +198,8 @@ struct Dev {
   std::vector<void*> allocs;
   // tensor-core operand pool: per matrix, per 128-row tile, per TC_KC-float K chunk: [hi | lo] A tiles
   bool use_tc = false;
-  std::vector<float> tc_host;
+  int64_t tc_size = 0;                           // floats of the tensor-core operand pool
+  std::vector<TcLayoutJob> tc_jobs;              // its contents, laid out on the device (k_tc_layout)
   std::unordered_map<int64_t, int64_t> tc_off;   // matrix id → float offset
   std::unordered_map<int64_t, int64_t> tc_boff;  // matrix id → float offset of its k_m2l_tcw B operand
   float* tcpool = nullptr;
@@ -260,84 +262,34 @@ static fda_status alloc(Context* ctx, Dev* d, T** dst, size_t count) {
 // interleaved rows / columns (A[2i][2j] = Re M, A[2i][2j+1] = −Im M, A[2i+1][2j] = Im M,
 // A[2i+1][2j+1] = Re M), TF32 hi/lo, per 128-row tile and TC_KC-float K chunk, canonical
 // K-major core matrices: element (r, k) of a 128 × TC_KC tile at ((k/4 · 16 + r/8) · 8 + r%8) · 4 + k%4
-static inline float tf32_rna(float x) {
-  uint32_t u;
-  std::memcpy(&u, &x, 4);
-  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;  // round to nearest, ties away
-  float y;
-  std::memcpy(&y, &u, 4);
-  return y;
-}
 
 static int tc_tiles(int rows) { return (2 * rows + 127) / 128; }
 
+// A operand of the tensor-core translation kernels: the real interleaved 2R × 2C form of
+// matrix m, TF32 hi / lo, per 128-row tile and TC_KC-float K chunk (layout in
+// kernels_tc.cu: k_tc_layout, built on the device from the complex64 pool)
 static int64_t tc_matrix(Context* ctx, Dev* d, int64_t m) {
   auto it = d->tc_off.find(m);
   if (it != d->tc_off.end()) return it->second;
-  const Plan& p = ctx->plan;
-  const MatInfo& mi = p.mats[m];
-  const int R = mi.rows, C = mi.cols, ntile = tc_tiles(R), nkc = (2 * C + TC_KC - 1) / TC_KC;
-  const int TILE = 128 * TC_KC;
-  const int64_t off = (int64_t)d->tc_host.size();
-  d->tc_host.resize(d->tc_host.size() + (size_t)ntile * nkc * 2 * TILE, 0.0f);
-  float* base = d->tc_host.data() + off;
-  const cf* M = p.pool.data() + mi.offset;
-  for (int ti = 0; ti < ntile; ++ti)
-    for (int kc = 0; kc < nkc; ++kc) {
-      float* hi = base + ((size_t)ti * nkc + kc) * 2 * TILE;
-      float* lo = hi + TILE;
-      for (int r = 0; r < 128; ++r) {
-        const int gr = 128 * ti + r, i = gr >> 1;
-        for (int k = 0; k < TC_KC; ++k) {
-          const int gk = kc * TC_KC + k, j = gk >> 1;
-          float x = 0.0f;
-          if (i < R && j < C) {
-            const cf v = M[(size_t)j * R + i];
-            x = (gr & 1) == 0 ? ((gk & 1) == 0 ? v.real() : -v.imag()) : ((gk & 1) == 0 ? v.imag() : v.real());
-          }
-          const float h = tf32_rna(x), l = tf32_rna(x - h);
-          const int idx = (((k >> 2) * 16 + (r >> 3)) * 8 + (r & 7)) * 4 + (k & 3);
-          hi[idx] = h;
-          lo[idx] = l;
-        }
-      }
-    }
+  const MatInfo& mi = ctx->plan.mats[m];
+  const int ntile = tc_tiles(mi.rows), nkc = (2 * mi.cols + TC_KC - 1) / TC_KC;
+  const int64_t off = d->tc_size;
+  d->tc_size += (int64_t)ntile * nkc * 2 * 128 * TC_KC;
+  d->tc_jobs.push_back(TcLayoutJob{off, mi.offset, mi.rows, mi.cols, ntile, nkc, 0, 0});
   d->tc_off.emplace(m, off);
   return off;
 }
 
-// B operand of k_m2l_tcw: the real 2R × 2C form of matrix m (as in tc_matrix) as
-// nrp ≥ 2R rows × K = 2C (zero-padded to nkc 16-float chunks), per chunk
-// [hi: nrp × 16 | lo: nrp × 16] in the canonical K-major no-swizzle layout
-// (core matrices of 8 rows × 16 B; the rows of one 4-float k-group contiguous)
+// B operand of k_m2l_tcw: the real 2R × 2C form of matrix m as nrp ≥ 2R rows × K = 2C
+// (zero-padded to nkc 16-float chunks), per chunk [hi: nrp × 16 | lo: nrp × 16] in the
+// canonical K-major no-swizzle layout (core matrices of 8 rows × 16 B)
 static int64_t tc_bop(Context* ctx, Dev* d, int64_t m, int nrp, int nkc) {
   auto it = d->tc_boff.find(m);
   if (it != d->tc_boff.end()) return it->second;
-  const Plan& p = ctx->plan;
-  const MatInfo& mi = p.mats[m];
-  const int R = mi.rows, C = mi.cols;
-  const int64_t off = (int64_t)d->tc_host.size();
-  const size_t blk = (size_t)nrp * TC_KC;
-  d->tc_host.resize(d->tc_host.size() + (size_t)nkc * 2 * blk, 0.0f);
-  float* base = d->tc_host.data() + off;
-  const cf* M = p.pool.data() + mi.offset;
-  for (int kc = 0; kc < nkc; ++kc) {
-    float* hi = base + (size_t)kc * 2 * blk;
-    float* lo = hi + blk;
-    for (int gr = 0; gr < 2 * R && gr < nrp; ++gr) {
-      const int i = gr >> 1;
-      for (int k = 0; k < TC_KC; ++k) {
-        const int gk = kc * TC_KC + k, j = gk >> 1;
-        if (j >= C) continue;
-        const cf v = M[(size_t)j * R + i];
-        const float x = (gr & 1) == 0 ? ((gk & 1) == 0 ? v.real() : -v.imag()) : ((gk & 1) == 0 ? v.imag() : v.real());
-        const float h = tf32_rna(x), l = tf32_rna(x - h);
-        const size_t idx = ((size_t)((k >> 2) * (nrp / 8) + (gr >> 3)) * 8 + (gr & 7)) * 4 + (k & 3);
-        hi[idx] = h;
-        lo[idx] = l;
-      }
-    }
-  }
+  const MatInfo& mi = ctx->plan.mats[m];
+  const int64_t off = d->tc_size;
+  d->tc_size += (int64_t)nkc * 2 * nrp * TC_KC;
+  d->tc_jobs.push_back(TcLayoutJob{off, mi.offset, mi.rows, mi.cols, nrp, nkc, 1, 0});
   d->tc_boff.emplace(m, off);
   return off;
 }
@@ -544,6 +496,13 @@ fda_status engine_create(Context* ctx) {
   ctx->dev = d;
   d->device = ctx->p.opt.device;
   CK(cudaSetDevice(d->device));
+  auto tp = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    auto now = std::chrono::steady_clock::now();
+    if (ctx->p.opt.verbose)
+      fprintf(stderr, "[engine_create] %-14s %8.3f s\n", name, std::chrono::duration<double>(now - tp).count());
+    tp = now;
+  };
   const Geometry& g = ctx->g;
   const Tree& t = ctx->t;
   const Plan& p = ctx->plan;
@@ -725,6 +684,7 @@ fda_status engine_create(Context* ctx) {
   UP(&d->s2m_rhs, s2m_rhs.data(), s2m_rhs.size());
   UP(&d->l2t, l2t.data(), l2t.size());
 
+  phase("leaf tables");
   const int nlev = (int)t.levels.size();
   d->m2m.resize(nlev); d->l2l.resize(nlev);
   auto xops = [&](const std::vector<Op>& ops, const std::vector<int64_t>& so, const std::vector<int64_t>& dof,
@@ -907,9 +867,20 @@ fda_status engine_create(Context* ctx) {
       if ((s = build_xstage(ctx, d, b[l], true, L.b, true, lr_tc[l] != 0)) != FDA_OK) return s;
     }
   }
+  phase("translations");
   if (d->use_tc) {
-    UP(&d->tcpool, d->tc_host.data(), d->tc_host.size());
-    std::vector<float>().swap(d->tc_host);
+    AL(&d->tcpool, (size_t)std::max<int64_t>(1, d->tc_size));
+    CK(cudaMemset(d->tcpool, 0, sizeof(float) * std::max<int64_t>(1, d->tc_size)));
+    if (!d->tc_jobs.empty()) {
+      TcLayoutJob* dj = nullptr;
+      CK(cudaMalloc((void**)&dj, sizeof(TcLayoutJob) * d->tc_jobs.size()));
+      CK(cudaMemcpy(dj, d->tc_jobs.data(), sizeof(TcLayoutJob) * d->tc_jobs.size(), cudaMemcpyHostToDevice));
+      launch_tc_layout((int)d->tc_jobs.size(), dj, d->pool, d->tcpool, 0);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+      cudaFree(dj);
+    }
+    std::vector<TcLayoutJob>().swap(d->tc_jobs);
   }
   // sharded: packed exchange lists (partition.cpp xsend / xrecv)
   d->rank = ctx->p.opt.rank;
@@ -995,6 +966,7 @@ fda_status engine_create(Context* ctx) {
   d->use_graph = ctx->p.opt.use_graph != 0 && d->nranks <= 1;
   CK(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming));
+  phase("upload/exchange");
   for (auto& e : d->ev) CK(cudaEventCreate(&e));
   CK(cudaEventCreate(&d->ev_n0));
   CK(cudaEventCreate(&d->ev_l0));

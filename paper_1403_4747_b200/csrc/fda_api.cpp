@@ -148,8 +148,12 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
       pl.in_size = off;
       // operator tables: the device build (fp64 on opt.device) where possible, the host for
       // the rest (HF-leaf S2M / L2T) and for host-only contexts
+      // sharding (opt.nranks > 1): own leaves, exchange plan, pruned ops and the matrices this
+      // rank needs, decided before any table is built (partition.cpp)
+      std::vector<char> needed;
+      apply_partition(ctx->p, ctx->t, pl, needed);
       const bool on_dev = o.build_on_device != 0 && o.device >= 0;
-      operator_layout(ctx->t, pl);
+      operator_layout(ctx->t, pl, needed);
       std::vector<char> done;
       LowRank lr;
       if (on_dev) {
@@ -200,7 +204,6 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
         }
       }
       phase("corrections");
-      apply_partition(ctx->p, ctx->t, pl);
     }
   } catch (const std::bad_alloc&) {
     ctx->err = "host allocation failed during build";

@@ -197,7 +197,8 @@ struct LowRank {                       // §4.2 factors K̃ ≈ Û V̂ per M2L m
   std::vector<std::vector<cd>> U, V;
 };
 void build_clouds_and_svd(const Params& p, Tree& t, const std::vector<bool>& need);
-void operator_layout(const Tree& t, Plan& plan);   // plan.mats (offset, rows, cols) + zeroed pool
+// plan.mats (offset, rows, cols) + zeroed pool; matrices with needed[id] = 0 get no storage
+void operator_layout(const Tree& t, Plan& plan, const std::vector<char>& needed);
 Mat3 out_frame(const Level& L, int dir);
 Mat3 in_frame(const Level& L, int dir);
 Vec3 octant_offset(int o, double wc);
@@ -209,11 +210,13 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan, co
 fda_status build_operators_device(Context* ctx, std::vector<char>& done, LowRank& lr);
 fda_status build_corrections_device(Context* ctx, int kind);
 // corrections.cpp: pair search (CSR, tier 0 self / 1 / 2 per entry) and the host evaluation
+// rows outside [row0, row1) (other ranks' elements) are left empty
 void correction_pairs(const Geometry& g, const Params& p, std::vector<int64_t>& ptr, std::vector<int64_t>& col,
-                      std::vector<int8_t>& tier);
+                      std::vector<int8_t>& tier, int64_t row0, int64_t row1);
 void build_corrections(const Geometry& g, const Params& p, Plan& plan, int kind = 0);
 // partition.cpp
-void apply_partition(const Params& p, const Tree& t, Plan& plan);
+// before the operator tables: own leaves / elements, exchange plan, pruned ops, needed[matrix id]
+void apply_partition(const Params& p, const Tree& t, Plan& plan, std::vector<char>& needed);
 // quad.cpp (fp64 kernels and rules)
 cd lhs_kernel(const Vec3& x, const Vec3& nx, const Vec3& y, const Vec3& ny, double k, cd alpha);
 cd rhs_kernel(const Vec3& x, const Vec3& nx, const Vec3& y, double k, cd alpha);

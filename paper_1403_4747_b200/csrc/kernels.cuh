@@ -135,6 +135,18 @@ cudaError_t m2l_lr_prepare();
 void launch_xlate_tc(int variant, int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                      const float* tcpool, const float2* src, float2* dst, cudaStream_t s);
 cudaError_t tc_prepare();
+// device layout of the tensor-core operand pool from the complex64 matrix pool (engine.cu:
+// tc_matrix / tc_bop record one job per matrix and operand form)
+struct TcLayoutJob {
+  int64_t dst;        // float offset in the tensor-core pool
+  int64_t src;        // complex offset of the matrix (R × C, column-major) in the pool
+  int32_t R, C;
+  int32_t a;          // kind 0: row tiles of 128; kind 1: padded row count nrp
+  int32_t nkc;        // TC_KC-float K chunks
+  int32_t kind;       // 0: A tiles [tile][chunk][hi | lo] 128 × TC_KC; 1: B operand [chunk][hi | lo] nrp × TC_KC
+  int32_t pad;
+};
+void launch_tc_layout(int njob, const TcLayoutJob* jobs, const float2* pool, float* tcpool, cudaStream_t s);
 // warp-specialised persistent translation kernel (N = 128 ops per task, tiles ≤ 2)
 cudaError_t xlate_tcw_prepare();
 void launch_xlate_tcw(int tiles, int ntask, const TcTask* tasks, const int64_t* src_off, const int64_t* dst_off,

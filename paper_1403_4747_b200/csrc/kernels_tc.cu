@@ -836,6 +836,58 @@ void launch_xlate_tcw(int tiles, int ntask, const TcTask* tasks, const int64_t* 
 
 
 
+// tensor-core operand layout (one CTA per matrix job): the real interleaved form of a
+// complex matrix M (A[2i][2j] = Re M, A[2i][2j+1] = −Im M, A[2i+1][2j] = Im M,
+// A[2i+1][2j+1] = Re M) split into TF32 hi = rna(x) and lo = rna(x − hi), written into the
+// canonical K-major no-swizzle UMMA layout (core matrices of 8 rows × 16 B)
+__device__ __forceinline__ float tf32_rna_dev(float x) {
+  uint32_t u = __float_as_uint(x);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;   // round to nearest, ties away
+  return __uint_as_float(u);
+}
+__global__ void k_tc_layout(const TcLayoutJob* __restrict__ jobs, const float2* __restrict__ pool,
+                            float* __restrict__ tcpool) {
+  const TcLayoutJob jb = jobs[blockIdx.x];
+  const float2* M = pool + jb.src;
+  float* base = tcpool + jb.dst;
+  if (jb.kind == 0) {
+    const int64_t total = (int64_t)jb.a * jb.nkc * 128 * TC_KC;
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+      const int k = (int)(e % TC_KC), r = (int)((e / TC_KC) % 128);
+      const int kc = (int)((e / (128 * TC_KC)) % jb.nkc), ti = (int)(e / ((int64_t)128 * TC_KC * jb.nkc));
+      const int gr = 128 * ti + r, i = gr >> 1, gk = kc * TC_KC + k, j = gk >> 1;
+      float x = 0.0f;
+      if (i < jb.R && j < jb.C) {
+        const float2 v = M[(int64_t)j * jb.R + i];
+        x = (gr & 1) == 0 ? ((gk & 1) == 0 ? v.x : -v.y) : ((gk & 1) == 0 ? v.y : v.x);
+      }
+      const float h = tf32_rna_dev(x), l = tf32_rna_dev(x - h);
+      float* hi = base + ((int64_t)ti * jb.nkc + kc) * 2 * 128 * TC_KC;
+      const int idx = (((k >> 2) * 16 + (r >> 3)) * 8 + (r & 7)) * 4 + (k & 3);
+      hi[idx] = h;
+      hi[128 * TC_KC + idx] = l;
+    }
+  } else {
+    const int nrp = jb.a;
+    const int64_t total = (int64_t)jb.nkc * nrp * TC_KC;
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+      const int k = (int)(e % TC_KC), gr = (int)((e / TC_KC) % nrp), kc = (int)(e / ((int64_t)TC_KC * nrp));
+      const int i = gr >> 1, gk = kc * TC_KC + k, j = gk >> 1;
+      if (gr >= 2 * jb.R || j >= jb.C) continue;
+      const float2 v = M[(int64_t)j * jb.R + i];
+      const float x = (gr & 1) == 0 ? ((gk & 1) == 0 ? v.x : -v.y) : ((gk & 1) == 0 ? v.y : v.x);
+      const float h = tf32_rna_dev(x), l = tf32_rna_dev(x - h);
+      float* hi = base + (int64_t)kc * 2 * nrp * TC_KC;
+      const int64_t idx = ((int64_t)((k >> 2) * (nrp / 8) + (gr >> 3)) * 8 + (gr & 7)) * 4 + (k & 3);
+      hi[idx] = h;
+      hi[(int64_t)nrp * TC_KC + idx] = l;
+    }
+  }
+}
+void launch_tc_layout(int njob, const TcLayoutJob* jobs, const float2* pool, float* tcpool, cudaStream_t s) {
+  if (njob > 0) k_tc_layout<<<njob, 256, 0, s>>>(jobs, pool, tcpool);
+}
+
 namespace {
 template <int N, int TILES, int S, int MB>
 cudaError_t tc_attr() {

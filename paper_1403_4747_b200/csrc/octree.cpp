@@ -104,14 +104,15 @@ void build_tree(Geometry& g, const Params& p, Tree& t) {
     int64_t next_begin = (int64_t)t.boxes.size();
     const int shift = kMortonBits - 1 - l;  // bit giving the child octant at level l+1
     for (int64_t b = lvl_begin; b < lvl_end; ++b) {
-      Box& B = t.boxes[b];
-      int64_t cnt = B.end - B.begin;
+      // copies, not a reference: t.boxes grows (and may reallocate) inside the loop
+      const int64_t b_begin = t.boxes[b].begin, b_end = t.boxes[b].end;
+      int64_t cnt = b_end - b_begin;
       bool split = (L.hf && !p.opt.hf_leaves) ? (cnt > 0) : (cnt > p.opt.max_leaf);   // C9 / P:344-346
       if (!split) continue;
-      int64_t s = B.begin;
+      int64_t s = b_begin;
       for (int o = 0; o < 8; ++o) {
         int64_t e = s;
-        while (e < B.end) {
+        while (e < b_end) {
           int oo = (int)(((ix[e] >> shift) & 1) | (((iy[e] >> shift) & 1) << 1) | (((iz[e] >> shift) & 1) << 2));
           if (oo != o) break;
           ++e;

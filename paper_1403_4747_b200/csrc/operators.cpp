@@ -95,7 +95,7 @@ static void store(Plan& plan, int64_t id, int rows, int cols, const std::vector<
   for (size_t i = 0; i < (size_t)rows * cols; ++i) dst[i] = cf((float)M[i].real(), (float)M[i].imag());
 }
 
-void operator_layout(const Tree& t, Plan& plan) {
+void operator_layout(const Tree& t, Plan& plan, const std::vector<char>& needed) {
   const int64_t nm = (int64_t)plan.specs.size();
   plan.mats.resize(nm);
   int64_t off = 0;
@@ -116,6 +116,7 @@ void operator_layout(const Tree& t, Plan& plan) {
       case MK_L2L: rows = t.levels[s.level + 1].rank; cols = t.levels[s.level].rank; break;
       case MK_M2L: rows = cols = t.levels[s.level].rank; break;
     }
+    if (!needed.empty() && !needed[id]) rows = cols = 0;   // another rank's matrix (sharded build)
     plan.mats[id] = {off, rows, cols};
     off += (int64_t)rows * cols;
   }
@@ -144,6 +145,7 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan, co
 #pragma omp parallel for schedule(dynamic, 1)
   for (int64_t id = 0; id < nm; ++id) {
     if (!done.empty() && done[id]) continue;
+    if (plan.mats[id].rows == 0) continue;   // not needed on this rank
     const MatSpec& s = plan.specs[id];
     const Level& L = t.levels[s.level];
     const int m = (int)L.chk.size(), n = (int)L.eq.size(), T = L.rank;

@@ -87,6 +87,8 @@ def _worker(rank, world, port, out):
     dist.all_reduce(t0)
     plans = [None] * world
     dist.all_gather_object(plans, (xsend, xrecv))
+    tb = [None] * world
+    dist.all_gather_object(tb, int(f.stats()["table_bytes"]))
     owned = torch.from_numpy(f.table("owned").astype(np.int64))
     allowned = [torch.zeros_like(owned) for _ in range(world)]
     dist.all_gather(allowned, owned)
@@ -96,10 +98,11 @@ def _worker(rank, world, port, out):
         np.save(out + ".own.npy", torch.stack(allowned).numpy())
         ok = all(plans[a][0][b] == plans[b][1][a] for a in range(world) for b in range(world) if a != b)
         np.save(out + ".plan_ok.npy", np.array([ok, sum(len(v) for p in plans for v in p[0])]))
+        np.save(out + ".tb.npy", np.array(tb))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [3])
+@pytest.mark.parametrize("world", [3, 8])
 def test_gloo_sharded_matvec(tmp_path, world):
     import oracle as O
     from oracle import fast
@@ -123,3 +126,10 @@ def test_gloo_sharded_matvec(tmp_path, world):
     assert np.linalg.norm(y - yo) / np.linalg.norm(yo) < 1e-3
     # the exchange is needed: without it the far field changes by O(1)
     assert np.linalg.norm(y_noex) / np.linalg.norm(yo) > 1e-2
+    # each rank built only its share of the operator tables (partition.cpp: needed matrices,
+    # own correction rows): the largest shard is well below the unsharded table size
+    from paper_1403_4747_b200 import FDA
+    full = FDA(V, F, k, 1j / k, 1e-4, device=-1, max_leaf=16).stats()["table_bytes"]
+    tb = np.load(out + ".tb.npy")
+    print(f"world {world}: table bytes per rank / unsharded = {np.round(tb / full, 3).tolist()}")
+    assert tb.max() < (0.75 if world == 3 else 0.45) * full

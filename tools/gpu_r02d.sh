@@ -1,0 +1,8 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests -m gpu -q -rP -k "device_build" > gpurun_out/r02d_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/r02d_pytest.log
+FDA_VERBOSE=2 timeout 900 python tools/build_times.py --configs 5 4 > gpurun_out/r02d_build.jsonl 2> gpurun_out/r02d_build.err
+echo "build rc=$?" >> gpurun_out/r02d_build.err
+tail -3 gpurun_out/r02d_pytest.log
