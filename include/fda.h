@@ -104,6 +104,10 @@ typedef struct {
                             generation, batched fp64 complex GEMMs, tier quadrature), the
                             same definitions as the host build; 0: host C++/OpenMP only.
                             Ignored (host) when opt.device = -1                             */
+  int32_t m2l_bf16;      /* the tensor-core factored M2L (lr_tensor_cores) in BF16x3: operands
+                            split once into bf16 hi / lo, hi·hi + hi·lo + lo·hi on tcgen05
+                            kind::f16 (≈ 2⁻¹⁶ relative per product) — 1 (default);
+                            0: 3xTF32 (fp32-accurate products)                             */
 } fda_options;
 
 typedef struct {

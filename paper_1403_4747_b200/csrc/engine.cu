@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <parallel/algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -170,6 +171,8 @@ struct Dev {
     int n_lrtc = 0;
     int lrtc_grid = 0;
     LrTcPlan lrtc_plan;
+    bool lrtc_bf16 = false;          // k_m2l_bf (BF16x3) instead of k_m2l_tcw (3xTF32)
+    int64_t split0 = 0, split1 = 0;  // float range of this level's out-states (bf16 split)
     double fl_lr = 0, fl_lrtc = 0;   // algorithmic flops (16·r·T per factored op) on k_m2l_lr / k_m2l_tcw
     bool any() const {
       int n = n_lrtc;
@@ -202,7 +205,9 @@ struct Dev {
   std::vector<TcLayoutJob> tc_jobs;              // its contents, laid out on the device (k_tc_layout)
   std::unordered_map<int64_t, int64_t> tc_off;   // matrix id → float offset
   std::unordered_map<int64_t, int64_t> tc_boff;  // matrix id → float offset of its k_m2l_tcw B operand
+  std::unordered_map<int64_t, int64_t> tc_bfoff; // … of its k_m2l_bf (bf16) B operand
   float* tcpool = nullptr;
+  __nv_bfloat16 *outb_hi = nullptr, *outb_lo = nullptr;   // bf16 hi / lo planes of outb (k_m2l_bf)
   // per-kernel-family device times of a profiled (serialised) matvec: event marks
   // recorded around every launch on the one stream (fda_kernel_times)
   bool kt_on = false;
@@ -294,6 +299,18 @@ static int64_t tc_bop(Context* ctx, Dev* d, int64_t m, int nrp, int nkc) {
   return off;
 }
 
+// bf16 B operand of k_m2l_bf: as tc_bop with 32-element K chunks of bf16 hi / lo
+static int64_t tc_bop_bf(Context* ctx, Dev* d, int64_t m, int nrp, int nkc32) {
+  auto it = d->tc_bfoff.find(m);
+  if (it != d->tc_bfoff.end()) return it->second;
+  const MatInfo& mi = ctx->plan.mats[m];
+  const int64_t off = d->tc_size;
+  d->tc_size += (int64_t)nkc32 * nrp * 32;   // 2 planes × nrp × 32 bf16 = nrp × 32 floats per chunk
+  d->tc_jobs.push_back(TcLayoutJob{off, mi.offset, mi.rows, mi.cols, nrp, nkc32, 2, 0});
+  d->tc_bfoff.emplace(m, off);
+  return off;
+}
+
 // Group the ops of one stage (one level, or all M2L levels at once) by matrix
 // and cut each group into tiles of the kernel variant (rows × ops per CTA)
 // that pads the group least.  Stages with fewer CTAs than ~4 waves are split
@@ -305,7 +322,7 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   if (ops.empty()) return FDA_OK;
   std::vector<size_t> ord(ops.size());
   for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
-  std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+  __gnu_parallel::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
     return ops[a].mat != ops[b].mat ? ops[a].mat < ops[b].mat : ops[a].dof < ops[b].dof;
   });
   std::vector<int64_t> so, dof;
@@ -520,6 +537,7 @@ fda_status engine_create(Context* ctx) {
   if (d->use_tc) CK(tc_prepare());
   if (d->use_tc) CK(xlate_tcw_prepare());
   if (d->use_tc) CK(m2l_tcw_prepare());
+  if (d->use_tc) CK(m2l_bf_prepare());
   CK(m2l_lr_prepare());
 
   // leaf-local element data in wave units (fp32 k·(offset from the owning leaf
@@ -772,7 +790,7 @@ fda_status engine_create(Context* ctx) {
     for (int l = 0; l < nlev; ++l) {
       fda_status s;
       auto& F = fused[l];
-      std::stable_sort(F.begin(), F.end(), [](const LrOp& x, const LrOp& y) {
+      __gnu_parallel::stable_sort(F.begin(), F.end(), [](const LrOp& x, const LrOp& y) {
         return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
       });
       std::vector<LrTask> lt[LR_NCLS];
@@ -806,7 +824,7 @@ fda_status engine_create(Context* ctx) {
       Dev::M2LLevel& L = d->m2lv[l];
       {   // tensor-core tasks: ≤ 128 ops per factored K̃, op offsets appended to ls / ld
         auto& Ft = ftc[l];
-        std::stable_sort(Ft.begin(), Ft.end(), [](const LrOp& x, const LrOp& y) {
+        __gnu_parallel::stable_sort(Ft.begin(), Ft.end(), [](const LrOp& x, const LrOp& y) {
           return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
         });
         std::vector<LrTcTask> tt;
@@ -819,9 +837,15 @@ fda_status engine_create(Context* ctx) {
           tk.r = r;
           tk.n1 = 2 * ((r + 7) / 8) * 8;
           tk.n2 = 2 * ((T + 7) / 8) * 8;
-          tk.nk1 = (2 * T + TC_KC - 1) / TC_KC;
-          tk.b1_off = tc_bop(ctx, d, Ft[i].matV, tk.n1, tk.nk1);
-          tk.b2_off = tc_bop(ctx, d, Ft[i].matU, tk.n2, tk.n1 / TC_KC);
+          if (ctx->p.opt.m2l_bf16) {   // BF16x3: 32-element K chunks of bf16 hi / lo
+            tk.nk1 = (2 * T + 31) / 32;
+            tk.b1_off = tc_bop_bf(ctx, d, Ft[i].matV, tk.n1, tk.nk1);
+            tk.b2_off = tc_bop_bf(ctx, d, Ft[i].matU, tk.n2, (tk.n1 + 31) / 32);
+          } else {
+            tk.nk1 = (2 * T + TC_KC - 1) / TC_KC;
+            tk.b1_off = tc_bop(ctx, d, Ft[i].matV, tk.n1, tk.nk1);
+            tk.b2_off = tc_bop(ctx, d, Ft[i].matU, tk.n2, tk.n1 / TC_KC);
+          }
           tk.op_begin = (int32_t)ls.size();
           tk.op_count = (int32_t)(j - i);
           for (size_t q = i; q < j; ++q) {
@@ -840,7 +864,14 @@ fda_status engine_create(Context* ctx) {
         if (!tt.empty()) {
           int n2m = 16;
           for (const LrTcTask& tk : tt) n2m = std::max(n2m, tk.n2);
-          L.lrtc_plan = m2l_tcw_plan(n1m, n2m);
+          L.lrtc_bf16 = ctx->p.opt.m2l_bf16 != 0;
+          L.lrtc_plan = L.lrtc_bf16 ? m2l_bf_plan(n1m, n2m) : m2l_tcw_plan(n1m, n2m);
+          // this level's out-states (contiguous offsets) are split into bf16 planes after its M2M
+          const int64_t s0 = p.out_level_begin[l], s1 = p.out_level_begin[l + 1];
+          if (s1 > s0) {
+            L.split0 = 2 * p.out_offset[s0];
+            L.split1 = 2 * (s1 < (int64_t)p.out_offset.size() ? p.out_offset[s1] : p.out_size);
+          }
         }
         {
           int dev = 0, nsm = 148;
@@ -881,6 +912,12 @@ fda_status engine_create(Context* ctx) {
       cudaFree(dj);
     }
     std::vector<TcLayoutJob>().swap(d->tc_jobs);
+    bool any_bf = false;
+    for (auto& L : d->m2lv) any_bf |= L.n_lrtc > 0 && L.lrtc_bf16;
+    if (any_bf) {
+      AL(&d->outb_hi, (size_t)2 * std::max<int64_t>(1, p.out_size));
+      AL(&d->outb_lo, (size_t)2 * std::max<int64_t>(1, p.out_size));
+    }
   }
   // sharded: packed exchange lists (partition.cpp xsend / xrecv)
   d->rank = ctx->p.opt.rank;
@@ -1039,6 +1076,23 @@ void engine_destroy(Context* ctx) {
   ctx->dev = nullptr;
 }
 
+// the tensor-core factored M2L of one level: k_m2l_bf (after splitting the level's out-states
+// into bf16 hi / lo planes) or k_m2l_tcw
+static void launch_lrtc(Dev* d, const Dev::M2LLevel& L, cudaStream_t st) {
+  if (!L.n_lrtc) return;
+  if (L.lrtc_bf16) {
+    KT(KF_M2L_TCW, st, {
+      launch_split_bf16(reinterpret_cast<const float*>(d->outb) + L.split0, L.split1 - L.split0, d->outb_hi + L.split0,
+                        d->outb_lo + L.split0, st);
+      launch_m2l_bf(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb_hi, d->outb_lo, d->inb, L.lrtc_plan,
+                    L.lrtc_grid, st);
+    });
+  } else {
+    KT(KF_M2L_TCW, st,
+       launch_m2l_tcw(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_plan, L.lrtc_grid, st));
+  }
+}
+
 // the device part of one matvec: x_tree → y_near, y_far (tree order)
 static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   // profiling mode serialises the near field on the main stream so that every
@@ -1076,9 +1130,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   const int nlev = (int)d->m2m.size();
   auto m2l_level = [&](int l, cudaStream_t st) {
     const Dev::M2LLevel& L = d->m2lv[l];
-    if (L.n_lrtc)
-      KT(KF_M2L_TCW, st,
-         launch_m2l_tcw(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_plan, L.lrtc_grid, st));
+    launch_lrtc(d, L, st);
     for (int c = LR_NCLS - 1; c >= 0; --c)
       if (L.n_lr[c])
         KT(KF_M2L_LR, st, launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st));
@@ -1120,7 +1172,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
       fda_status bs;
       if (L.n_lrtc &&
           (bs = branch([&](cudaStream_t sm) {
-             launch_m2l_tcw(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_plan, L.lrtc_grid, sm);
+             launch_lrtc(d, L, sm);
            })) != FDA_OK)
         return bs;
       for (int c = LR_NCLS - 1; c >= 0; --c)
@@ -1219,7 +1271,7 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
     if (L.n_lrtc) {
       cudaStream_t sm = d->s_m2l[k++ % Dev::kM2LStreams];
       CK(cudaStreamWaitEvent(sm, d->ev_up[0], 0));
-      launch_m2l_tcw(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb, d->inb, L.lrtc_plan, L.lrtc_grid, sm);
+      launch_lrtc(d, L, sm);
       CK(cudaEventRecord(d->ev_m2l[l][nbr[l]++], sm));
     }
     for (int c = LR_NCLS - 1; c >= -1; --c) {

@@ -48,6 +48,7 @@ fda_status fda_options_default(fda_options* opt) {
   opt->hf_leaves = 0;
   opt->lr_tensor_cores = 2;
   opt->build_on_device = 1;
+  opt->m2l_bf16 = 1;
   return FDA_OK;
 }
 
@@ -137,13 +138,13 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
       int64_t off = 0;
       for (size_t s = 0; s < pl.out_states.size(); ++s) {
         pl.out_offset[s] = off;
-        off += (ctx->t.levels[ctx->t.boxes[pl.out_states[s].box].level].rank + 1) & ~1;   // 16-B aligned states
+        off += (ctx->t.levels[ctx->t.boxes[pl.out_states[s].box].level].rank + 3) & ~3;   // 32-B aligned states
       }
       pl.out_size = off;
       off = 0;
       for (size_t s = 0; s < pl.in_states.size(); ++s) {
         pl.in_offset[s] = off;
-        off += (ctx->t.levels[ctx->t.boxes[pl.in_states[s].box].level].rank + 1) & ~1;
+        off += (ctx->t.levels[ctx->t.boxes[pl.in_states[s].box].level].rank + 3) & ~3;
       }
       pl.in_size = off;
       // operator tables: the device build (fp64 on opt.device) where possible, the host for

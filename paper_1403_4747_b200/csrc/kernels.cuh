@@ -1,6 +1,7 @@
 // Device kernels of the FDA matvec (sm_100a).  See DESIGN.md §5 for the
 // roofline of each kernel and its algorithmic bytes / evaluations per unit.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -90,6 +91,14 @@ struct LrTcPlan {
 };
 LrTcPlan m2l_tcw_plan(int n1max, int n2max);
 cudaError_t m2l_tcw_prepare();
+// BF16x3 form (k_m2l_bf): same tasks with b1_off / b2_off → kind-2 (bf16) B layouts and
+// nk1 = ⌈2T / 32⌉; the source states as pre-split bf16 hi / lo planes (launch_split_bf16)
+LrTcPlan m2l_bf_plan(int n1max, int n2max);
+cudaError_t m2l_bf_prepare();
+void launch_m2l_bf(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                   const float* tcpool, const __nv_bfloat16* shi, const __nv_bfloat16* slo, float2* dst,
+                   const LrTcPlan& pl, int grid, cudaStream_t s);
+void launch_split_bf16(const float* x, int64_t n, __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t s);
 void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                     const float* tcpool, const float2* src, float2* dst, const LrTcPlan& pl, int grid,
                     cudaStream_t s);
@@ -143,7 +152,8 @@ struct TcLayoutJob {
   int32_t R, C;
   int32_t a;          // kind 0: row tiles of 128; kind 1: padded row count nrp
   int32_t nkc;        // TC_KC-float K chunks
-  int32_t kind;       // 0: A tiles [tile][chunk][hi | lo] 128 × TC_KC; 1: B operand [chunk][hi | lo] nrp × TC_KC
+  int32_t kind;       // 0: A tiles [tile][chunk][hi | lo] 128 × TC_KC; 1: B operand [chunk][hi | lo] nrp × TC_KC;
+                      // 2: bf16 B operand [32-element chunk][hi | lo] nrp × 32 (nkc = 32-element chunks)
   int32_t pad;
 };
 void launch_tc_layout(int njob, const TcLayoutJob* jobs, const float2* pool, float* tcpool, cudaStream_t s);

@@ -25,6 +25,7 @@
 // tcgen05.ld of each accumulator block into shared memory (op-major), then
 // coalesced 16-byte vector atomics into the destination states (several tasks
 // may share a destination).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -615,6 +616,342 @@ void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, co
 }
 
 // ---------------------------------------------------------------------------
+// BF16x3 form of the fused factored M2L (k_m2l_bf; opt.lr_tensor_cores with opt.m2l_bf16):
+// the roles and rings of k_m2l_tcw, with every operand split ONCE into bf16 hi / lo planes
+// (x ≈ hi + lo, hi = bf16(x), lo = bf16(x − hi): 16 significant bits) and the products
+// hi·hi + hi·lo + lo·hi on tcgen05 kind::f16 (K = 16 per MMA, fp32 accumulation in TMEM):
+//  * the source states come pre-split (engine.cu: k_split_bf16 after the level's M2M), so the
+//    row warps only issue 16-byte cp.async gathers straight into the canonical K-major bf16
+//    layout — no in-shared-memory split pass (the LSU work that paced k_m2l_tcw);
+//  * one ring job = 32 K elements (2 MMA k-steps); B1 / B2 (real forms of V̂ᵀ / Ûᵀ) are bf16
+//    hi / lo tiles laid out on the device (k_tc_layout kind 2) and streamed by the TMA engine;
+//  * phase 2's A operand is D1 read back from TMEM and split into bf16 hi / lo by the row warps.
+// Error of a product: ≈ 2⁻¹⁶ relative (the dropped lo·lo term and the bf16 rounding of lo),
+// i.e. ~1.5e-5 of the M2L contribution — below the FDA's own ε = 1e-4.
+namespace {
+constexpr int BK = 32;   // bf16 K elements per ring job
+__device__ __forceinline__ uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// bf16 hi / lo of 8 floats packed as 4 + 4 32-bit words (element order = K order)
+__device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(v[2 * q]), h1 = __float2bfloat16_rn(v[2 * q + 1]);
+    const __nv_bfloat16 l0 = __float2bfloat16_rn(v[2 * q] - __bfloat162float(h0));
+    const __nv_bfloat16 l1 = __float2bfloat16_rn(v[2 * q + 1] - __bfloat162float(h1));
+    h[q] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+    l[q] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+}  // namespace
+
+template <int S1>
+__global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict__ tasks, int ntask,
+                                                   const int64_t* __restrict__ src_off,
+                                                   const int64_t* __restrict__ dst_off,
+                                                   const float* __restrict__ tcpool,
+                                                   const __nv_bfloat16* __restrict__ shi,
+                                                   const __nv_bfloat16* __restrict__ slo, float2* __restrict__ dst,
+                                                   int stage_b, int b2_b, int n1max, uint32_t ncols) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t a_full[S1], b_full[S1], empty[S1], b2_full[2], b2_empty[2];
+  __shared__ uint64_t d1_full, a2_full, d2_full, y_free;
+  __shared__ uint32_t tmem_base_sh;
+  constexpr int LA = S1 >= 6 ? S1 - 3 : S1 - 2;
+  constexpr int A_PL = 128 * BK * 2;               // bytes of one A plane (hi or lo) per job
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x;
+  uint8_t* sB2 = sbase + S1 * stage_b;             // [2][b2_b]
+  uint8_t* sA2 = sB2 + 2 * b2_b;                   // phase-2 A: (n1max / BK) jobs × [hi | lo] 128 × BK
+  const uint8_t* pool8 = reinterpret_cast<const uint8_t*>(tcpool);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  if (tid == 0) {
+    for (int q = 0; q < S1; ++q) {
+      mbar_init(&a_full[q], 32 * TCW_RW);
+      mbar_init(&b_full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&b2_full[q], 1);
+      mbar_init(&b2_empty[q], 1);
+    }
+    mbar_init(&d1_full, 1);
+    mbar_init(&a2_full, 32 * TCW_RW);
+    mbar_init(&d2_full, 1);
+    mbar_init(&y_free, 32 * TCW_RW);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t tY = tmem + (uint32_t)n1max;      // D2 region
+
+  if (warp == TCW_RW + 1) {
+    // ---------------- TMA producer: B1 per ring job, B2 per phase-2 job
+    if (lane == 0) {
+      int j = 0, b2j = 0;
+      for (int ct = blockIdx.x; ct < ntask; ct += G) {
+        const LrTcTask t = tasks[ct];
+        const uint32_t bytes1 = (uint32_t)t.n1 * BK * 2 * 2;
+        for (int c = 0; c < t.nk1; ++c, ++j) {
+          const int st = j % S1;
+          if (j >= S1) mbar_wait(&empty[st], ((j / S1) - 1) & 1);
+          mbar_expect_tx(&b_full[st], bytes1);
+          bulk_g2s(sbase + st * stage_b + 2 * A_PL, pool8 + 4 * t.b1_off + (int64_t)c * bytes1, bytes1, &b_full[st]);
+        }
+        const int nk2 = (t.n1 + BK - 1) / BK;
+        const uint32_t bytes2 = (uint32_t)t.n2 * BK * 2 * 2;
+        for (int c2 = 0; c2 < nk2; ++c2, ++b2j) {
+          const int st = b2j & 1;
+          if (b2j >= 2) mbar_wait(&b2_empty[st], ((b2j >> 1) - 1) & 1);
+          mbar_expect_tx(&b2_full[st], bytes2);
+          bulk_g2s(sB2 + st * b2_b, pool8 + 4 * t.b2_off + (int64_t)c2 * bytes2, bytes2, &b2_full[st]);
+        }
+      }
+    }
+  } else if (warp == TCW_RW) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      int j = 0, b2j = 0, i = 0;
+      for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
+        const LrTcTask t = tasks[ct];
+        const int N1 = t.n1, N2 = t.n2, K1 = 2 * t.T, nk2 = (N1 + BK - 1) / BK;
+        const uint32_t idesc1 = idesc_bf16(N1);
+        for (int c = 0; c < t.nk1; ++c, ++j) {
+          const int st = j % S1;
+          mbar_wait(&a_full[st], (j / S1) & 1);
+          mbar_wait(&b_full[st], (j / S1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+          const uint8_t* sA = sbase + st * stage_b;
+          const uint32_t a_hi = smem_u32(sA), a_lo = a_hi + A_PL;
+          const uint32_t b_hi = smem_u32(sA + 2 * A_PL), b_lo = b_hi + N1 * BK * 2;
+#pragma unroll
+          for (int s = 0; s < BK / 16; ++s) {
+            if (c * BK + 16 * s >= K1) break;
+            const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (N1 / 8) * 128);
+            const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
+            const uint64_t Bh = make_desc(b_hi + bo, (N1 / 8) * 128, 128), Bl = make_desc(b_lo + bo, (N1 / 8) * 128, 128);
+            mma_bf16(tmem, Ah, Bh, idesc1, (c > 0 || s > 0) ? 1u : 0u);
+            mma_bf16(tmem, Ah, Bl, idesc1, 1u);
+            mma_bf16(tmem, Al, Bh, idesc1, 1u);
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           smem_u32(&empty[st]))
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&d1_full))
+                     : "memory");
+        mbar_wait(&a2_full, i & 1);                   // tmp is in shared memory (and D1 was read)
+        if (i >= 1) mbar_wait(&y_free, (i - 1) & 1);  // D2 of the previous task was drained
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        for (int c2 = 0; c2 < nk2; ++c2, ++b2j) {
+          const int st = b2j & 1;
+          mbar_wait(&b2_full[st], (b2j >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+          const uint32_t b_hi = smem_u32(sB2 + st * b2_b), b_lo = b_hi + N2 * BK * 2;
+          const uint32_t a_hi = smem_u32(sA2 + c2 * 2 * A_PL), a_lo = a_hi + A_PL;
+#pragma unroll
+          for (int s = 0; s < BK / 16; ++s) {
+            if (c2 * BK + 16 * s >= N1) break;
+            const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (N2 / 8) * 128);
+            const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
+            for (int n0 = 0; n0 < N2; n0 += 256) {
+              const int nn = min(256, N2 - n0);
+              const uint32_t idesc = idesc_bf16(nn);
+              const uint32_t no = (uint32_t)((n0 / 8) * 128);
+              const uint64_t Bh = make_desc(b_hi + bo + no, (N2 / 8) * 128, 128);
+              const uint64_t Bl = make_desc(b_lo + bo + no, (N2 / 8) * 128, 128);
+              mma_bf16(tY + n0, Ah, Bh, idesc, (c2 > 0 || s > 0) ? 1u : 0u);
+              mma_bf16(tY + n0, Ah, Bl, idesc, 1u);
+              mma_bf16(tY + n0, Al, Bh, idesc, 1u);
+            }
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           smem_u32(&b2_empty[st]))
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&d2_full))
+                     : "memory");
+      }
+    }
+  } else {
+    // ---------------- row warps: thread (row = tid & 127, half h = tid >> 7); half h gathers the
+    // k-groups {2h, 2h+1} (8 bf16 each) of each 32-element job from both planes and converts /
+    // drains the 16-column TMEM blocks b ≡ h (mod 2)
+    const int row = tid & 127, h = tid >> 7;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    int it = blockIdx.x, ic = 0, js = 0;
+    LrTcTask ti = tasks[it];
+    int64_t isp = row < ti.op_count ? 2 * src_off[ti.op_begin + row] : -1;   // bf16 element offset
+    auto issue_next = [&]() {
+      if (it < ntask) {
+        const int st = js % S1;
+        if (js >= S1) mbar_wait(&empty[st], ((js / S1) - 1) & 1);
+        uint8_t* sA = sbase + st * stage_b;
+        const int K2 = 2 * ti.T;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int kg = 2 * h + q;
+          const int k = ic * BK + 8 * kg;
+          const int nb = isp >= 0 ? 2 * min(8, max(0, K2 - k)) : 0;
+          const int so = ((kg * 16 + (row >> 3)) * 8 + (row & 7)) * 16;
+          cp16z(sA + so, nb ? (const void*)(shi + isp + k) : (const void*)shi, nb);
+          cp16z(sA + A_PL + so, nb ? (const void*)(slo + isp + k) : (const void*)slo, nb);
+        }
+        ++js;
+        if (++ic == ti.nk1) {
+          ic = 0;
+          it += G;
+          if (it < ntask) {
+            ti = tasks[it];
+            isp = row < ti.op_count ? 2 * src_off[ti.op_begin + row] : -1;
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    };
+    for (int q = 0; q < LA; ++q) issue_next();
+    int jc = 0, i = 0;
+    LrTcTask tp{};
+    auto drain = [&](const LrTcTask& t) {
+      float2* d = row < t.op_count ? dst + dst_off[t.op_begin + row] : nullptr;
+      for (int c0 = 16 * h; c0 < t.n2; c0 += 32) {
+        float w[16];
+        tmem_ld16(tY + lane_base + c0, w);
+        if (d) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = c0 / 2 + 2 * q;   // complex rows (r, r+1); r+1 = T is the padding slot
+            if (r < t.T)
+              atomicAdd(reinterpret_cast<float4*>(d + r), make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      mbar_arrive(&y_free);
+    };
+    for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
+      const LrTcTask t = tasks[ct];
+      for (int c = 0; c < t.nk1; ++c, ++jc) {
+        issue_next();
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(LA) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive(&a_full[jc % S1]);
+      }
+      if (i >= 1) {                                // D2 of the previous task → destination states
+        mbar_wait(&d2_full, (i - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        drain(tp);
+      }
+      mbar_wait(&d1_full, i & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      // D1 (fp32, row = op, columns = 2r interleaved) → bf16 hi / lo phase-2 A operand
+      for (int c0 = 16 * h; c0 < t.n1; c0 += 32) {
+        float w[16];
+        tmem_ld16(tmem + lane_base + c0, w);
+        uint8_t* ch = sA2 + (c0 / BK) * 2 * A_PL;
+#pragma unroll
+        for (int g8 = 0; g8 < 2; ++g8) {
+          const int kg = ((c0 % BK) >> 3) + g8;
+          uint4 hi, lo;
+          split8(w + 8 * g8, hi, lo);
+          const int so = ((kg * 16 + (row >> 3)) * 8 + (row & 7)) * 16;
+          *reinterpret_cast<uint4*>(ch + so) = hi;
+          *reinterpret_cast<uint4*>(ch + A_PL + so) = lo;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      mbar_arrive(&a2_full);
+      tp = t;
+    }
+    if (i >= 1) {
+      mbar_wait(&d2_full, (i - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      drain(tp);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
+}
+
+// plan of one k_m2l_bf launch: ring stages of one 32-element job (A hi|lo 16 KB + B1 hi|lo),
+// a 2-stage B2 ring and the phase-2 A region, ≤ 220 KB
+LrTcPlan m2l_bf_plan(int n1max, int n2max) {
+  LrTcPlan pl;
+  pl.stage_fl = (2 * 128 * BK * 2 + n1max * BK * 2 * 2) / 4;   // (in floats)
+  pl.b2_fl = (n2max * BK * 2 * 2) / 4;
+  const size_t a2 = (size_t)((n1max + BK - 1) / BK) * 2 * 128 * BK * 2 / 4;
+  const size_t cap = (220 * 1024 - 1024) / 4 - 2 * (size_t)pl.b2_fl - a2;
+  const int s = (int)(cap / pl.stage_fl);
+  pl.stages = s >= 8 ? 8 : (s >= 6 ? 6 : (s >= 5 ? 5 : (s >= 4 ? 4 : 3)));
+  pl.smem = ((size_t)pl.stages * pl.stage_fl + 2 * (size_t)pl.b2_fl + a2) * 4 + 1024;
+  pl.ncols = tmem_cols(n1max + n2max);
+  pl.n1max = n1max;
+  return pl;
+}
+cudaError_t m2l_bf_prepare() {
+  cudaError_t e = cudaFuncSetAttribute(k_m2l_bf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_bf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_bf<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_bf<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_bf<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  return e;
+}
+void launch_m2l_bf(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                   const float* tcpool, const __nv_bfloat16* shi, const __nv_bfloat16* slo, float2* dst,
+                   const LrTcPlan& pl, int grid, cudaStream_t s) {
+  if (ntask <= 0) return;
+#define TBF(S)                                                                                                   \
+  k_m2l_bf<S><<<grid, TCW_NT, pl.smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, shi, slo, dst, pl.stage_fl * 4, \
+                                         pl.b2_fl * 4, pl.n1max, pl.ncols)
+  switch (pl.stages) {
+    case 8: TBF(8); break;
+    case 6: TBF(6); break;
+    case 5: TBF(5); break;
+    case 4: TBF(4); break;
+    default: TBF(3); break;
+  }
+#undef TBF
+}
+
+// states → bf16 hi / lo planes (one thread per float; the planes share the states' offsets ×2)
+__global__ void k_split_bf16(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ hi,
+                             __nv_bfloat16* __restrict__ lo) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float v = x[i];
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  hi[i] = h;
+  lo[i] = __float2bfloat16_rn(v - __bfloat162float(h));
+}
+void launch_split_bf16(const float* x, int64_t n, __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t s) {
+  if (n > 0) k_split_bf16<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, n, hi, lo);
+}
+
+// ---------------------------------------------------------------------------
 // Warp-specialised persistent form of the translation kernel (k_xlate_tcw):
 // the same product (dst[:, op] += M · src[:, op] in interleaved real form,
 // 3xTF32, N = 128 ops per task, TILES ≤ 2 row tiles) with the roles of
@@ -866,6 +1203,24 @@ __global__ void k_tc_layout(const TcLayoutJob* __restrict__ jobs, const float2* 
       const int idx = (((k >> 2) * 16 + (r >> 3)) * 8 + (r & 7)) * 4 + (k & 3);
       hi[idx] = h;
       hi[128 * TC_KC + idx] = l;
+    }
+  } else if (jb.kind == 2) {
+    // bf16 B operand: per 32-element K chunk [hi: nrp × 32 | lo: nrp × 32] (canonical K-major,
+    // core matrices of 8 rows × 16 B = 8 bf16)
+    const int nrp = jb.a;
+    __nv_bfloat16* b16 = reinterpret_cast<__nv_bfloat16*>(base);
+    const int64_t total = (int64_t)jb.nkc * nrp * 32;
+    for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+      const int k = (int)(e % 32), gr = (int)((e / 32) % nrp), kc = (int)(e / ((int64_t)32 * nrp));
+      const int i = gr >> 1, gk = kc * 32 + k, j = gk >> 1;
+      if (gr >= 2 * jb.R || j >= jb.C) continue;
+      const float2 v = M[(int64_t)j * jb.R + i];
+      const float x = (gr & 1) == 0 ? ((gk & 1) == 0 ? v.x : -v.y) : ((gk & 1) == 0 ? v.y : v.x);
+      const __nv_bfloat16 h = __float2bfloat16_rn(x), l = __float2bfloat16_rn(x - __bfloat162float(h));
+      __nv_bfloat16* hi = b16 + (int64_t)kc * 2 * nrp * 32;
+      const int64_t idx = ((int64_t)((k >> 3) * (nrp / 8) + (gr >> 3)) * 8 + (gr & 7)) * 8 + (k & 7);
+      hi[idx] = h;
+      hi[(int64_t)nrp * 32 + idx] = l;
     }
   } else {
     const int nrp = jb.a;

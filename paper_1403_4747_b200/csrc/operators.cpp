@@ -98,7 +98,7 @@ static void store(Plan& plan, int64_t id, int rows, int cols, const std::vector<
 void operator_layout(const Tree& t, Plan& plan, const std::vector<char>& needed) {
   const int64_t nm = (int64_t)plan.specs.size();
   plan.mats.resize(nm);
-  int64_t off = 0;
+  int64_t off = 0, lr_bound = 0;
   for (int64_t id = 0; id < nm; ++id) {
     const MatSpec& s = plan.specs[id];
     int rows = 0, cols = 0;
@@ -119,7 +119,10 @@ void operator_layout(const Tree& t, Plan& plan, const std::vector<char>& needed)
     if (!needed.empty() && !needed[id]) rows = cols = 0;   // another rank's matrix (sharded build)
     plan.mats[id] = {off, rows, cols};
     off += (int64_t)rows * cols;
+    if (s.kind == MK_M2L) lr_bound += (int64_t)rows * cols;   // §4.2 factors: 2·r·T < T² entries
   }
+  plan.pool.clear();
+  plan.pool.reserve(off + lr_bound);   // the factors are appended without reallocating
   plan.pool.assign(off, cf(0, 0));
 }
 
@@ -142,7 +145,7 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan, co
   std::vector<int>& lrR = lr.R;
   std::vector<std::vector<cd>>& lrU = lr.U;
   std::vector<std::vector<cd>>& lrV = lr.V;
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 16)
   for (int64_t id = 0; id < nm; ++id) {
     if (!done.empty() && done[id]) continue;
     if (plan.mats[id].rows == 0) continue;   // not needed on this rank
@@ -270,18 +273,27 @@ void build_operators(const Geometry& g, const Params& p, Tree& t, Plan& plan, co
   // append the §4.2 factors as new matrices: V̂ (r × T) then Û (T × r)
   plan.lr_V.assign(nm, -1);
   plan.lr_U.assign(nm, -1);
+  int64_t off = (int64_t)plan.pool.size();
+  std::vector<std::pair<int64_t, const std::vector<cd>*>> fill;   // (pool offset, factor)
   for (int64_t id = 0; id < nm; ++id) {
     if (lrR[id] < 0) continue;
     const int r = lrR[id], T = plan.mats[id].rows;
     for (int w = 0; w < 2; ++w) {
       const int64_t nid = (int64_t)plan.mats.size();
-      MatInfo mi{(int64_t)plan.pool.size(), w == 0 ? r : T, w == 0 ? T : r};
+      MatInfo mi{off, w == 0 ? r : T, w == 0 ? T : r};
       plan.mats.push_back(mi);
       plan.specs.push_back(plan.specs[id]);
-      const std::vector<cd>& src = w == 0 ? lrV[id] : lrU[id];
-      for (const cd& v : src) plan.pool.push_back(cf((float)v.real(), (float)v.imag()));
+      fill.push_back({off, w == 0 ? &lrV[id] : &lrU[id]});
+      off += (int64_t)r * T;
       (w == 0 ? plan.lr_V : plan.lr_U)[id] = nid;
     }
+  }
+  plan.pool.resize(off);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t f = 0; f < (int64_t)fill.size(); ++f) {
+    const std::vector<cd>& src = *fill[f].second;
+    cf* dst = plan.pool.data() + fill[f].first;
+    for (size_t e = 0; e < src.size(); ++e) dst[e] = cf((float)src[e].real(), (float)src[e].imag());
   }
 }
 

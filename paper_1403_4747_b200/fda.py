@@ -58,7 +58,7 @@ class fda_options(ctypes.Structure):
                 ("verbose", ctypes.c_int32), ("m2l_lowrank", ctypes.c_int32),
                 ("rhs_operator", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("tensor_cores", ctypes.c_int32), ("hf_leaves", ctypes.c_int32), ("lr_tensor_cores", ctypes.c_int32),
-                ("build_on_device", ctypes.c_int32)]
+                ("build_on_device", ctypes.c_int32), ("m2l_bf16", ctypes.c_int32)]
 
 
 class fda_solve_info(ctypes.Structure):
