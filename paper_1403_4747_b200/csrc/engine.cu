@@ -191,7 +191,7 @@ struct Dev {
   float2* tmpb = nullptr;
   int64_t tmp_size = 0;
   cudaStream_t s_cap = nullptr;
-  cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};
+  cudaGraphExec_t graph_exec[6] = {};   // [kind]: unsharded matvec; [2 + kind] / [4 + kind]: sharded UP / DOWN
   bool use_graph = false;
   float2 *x_tree = nullptr, *y_near = nullptr, *y_far = nullptr;
   double2 *xh = nullptr, *yh = nullptr;
@@ -943,7 +943,6 @@ fda_status engine_create(Context* ctx) {
     AL(&d->sendb, (size_t)std::max<int64_t>(1, d->n_send));
     AL(&d->recvb, (size_t)std::max<int64_t>(1, d->n_recv));
     CK(cudaMemset(d->recvb, 0, sizeof(float2) * std::max<int64_t>(1, d->n_recv)));
-    d->use_graph = false;   // the NCCL exchange sits between the passes: eager launches
   }
   // kernels per matvec: gather, near, s2m, every non-empty translation launch, l2t, scatter
   int64_t nl = 4 + (d->n_s2m > 0) + (d->n_l2t_add > 0);  // gather, near, l2t, scatter (+ s2m, HF-leaf L2T)
@@ -1204,26 +1203,31 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
 // ---- sharded matvec (nranks > 1): partial upward pass →
 // exchange of partial outgoing states → downward pass for the owned targets.
 // Eager launches; the near field runs on its own stream across the exchange.
-static fda_status run_sharded_up(Context* ctx, Dev* d, cudaStream_t s, int kind) {
+// the near field of the owned leaves, forked onto its own stream (joined by the caller
+// through ev_join): eager, so that it overlaps the exchange between the two graph halves
+static fda_status launch_sharded_near(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   // profiling mode serialises the near field on the main stream (stage times as in run_core)
   const bool prof = ctx->profiling;
   cudaStream_t sn = prof ? s : d->s_near;
   CK(cudaEventRecord(d->ev_fork, s));
   CK(cudaStreamWaitEvent(sn, d->ev_fork, 0));
   if (prof) CK(cudaEventRecord(d->ev_n0, sn));
-  // near-kernel timing events: external event nodes when captured (so every graph replay
-  // re-timestamps them), plain records in eager runs (the flag is only valid under capture)
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  CK(cudaStreamIsCapturing(sn, &cap));
-  const unsigned evf = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
-  CK(cudaEventRecordWithFlags(d->ev_l0, sn, evf));
+  CK(cudaEventRecord(d->ev_l0, sn));
   launch_near(d->n_near, d->near_tasks, d->near_slots, d->near_off, d->tgt_pos, d->tgt_nrm, d->src, d->src_w,
               kind ? d->corr_ptr_rhs : d->corr_ptr, kind ? d->corr_col_rhs : d->corr_col,
               kind ? d->corr_val_rhs : d->corr_val, d->x_tree, d->y_near, d->kp, d->alpha_pure_imag, kind, d->near_wide, sn);
-  CK(cudaEventRecordWithFlags(d->ev_l1, sn, evf));
+  CK(cudaEventRecord(d->ev_l1, sn));
   d->live = true;
   if (prof) CK(cudaEventRecord(d->ev_n1, sn));
   CK(cudaEventRecord(d->ev_join, sn));
+  CK(cudaGetLastError());
+  return FDA_OK;
+}
+
+// the partial upward pass (S2M of own leaves, M2M into boxes holding own elements) and the
+// packing of the partials other ranks need: one stream, captured as a graph
+static fda_status run_sharded_up(Context* ctx, Dev* d, cudaStream_t s, int kind) {
+  const bool prof = ctx->profiling;
   if (prof) CK(cudaEventRecord(d->ev[1], s));
   if (d->out_size) CK(cudaMemsetAsync(d->outb, 0, sizeof(float2) * d->out_size, s));
   if (d->in_size) CK(cudaMemsetAsync(d->inb, 0, sizeof(float2) * d->in_size, s));
@@ -1302,30 +1306,19 @@ static fda_status run_sharded_down(Context* ctx, Dev* d, cudaStream_t s) {
   launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s);
   launch_l2t(d->n_l2t_add, d->l2t_add, d->pool, d->inb, d->y_far, s, /*accumulate=*/true);
   if (prof) CK(cudaEventRecord(d->ev[6], s));
-  CK(cudaStreamWaitEvent(s, d->ev_join, 0));
   CK(cudaGetLastError());
   return FDA_OK;
 }
 
-// run_core through a CUDA graph (captured once: all its buffers are internal,
-// so the same graph serves every call); profiled calls run it eagerly.
-// phase (sharded contexts only): 0 = whole matvec with the NCCL exchange,
-// FDA_PHASE_UP / FDA_PHASE_DOWN = the halves around an external exchange
-// (fda_exchange_local, the one-GPU test transport)
-static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind, int phase = 0) {
-  if (d->nranks > 1) {
-    fda_status st = FDA_OK;
-    if (phase != FDA_PHASE_DOWN && (st = run_sharded_up(ctx, d, s, kind)) != FDA_OK) return st;
-    if (phase == 0 && (st = exchange_nccl(ctx, d, s)) != FDA_OK) return st;
-    if (phase != FDA_PHASE_UP) st = run_sharded_down(ctx, d, s);
-    return st;
-  }
-  if (ctx->profiling || !d->use_graph) return run_core(ctx, d, s, kind);
-  cudaGraphExec_t& ge = d->graph_exec[kind];
+// capture fn(stream) once into d->graph_exec[slot] (all buffers are internal, so the graph
+// serves every call) and launch it on s
+template <class Fn>
+static fda_status launch_captured(Context* ctx, Dev* d, cudaStream_t s, int slot, Fn&& fn) {
+  cudaGraphExec_t& ge = d->graph_exec[slot];
   if (!ge) {
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(d->s_cap, cudaStreamCaptureModeThreadLocal));
-    fda_status st = run_core(ctx, d, d->s_cap, kind);
+    fda_status st = fn(d->s_cap);
     cudaError_t e = cudaStreamEndCapture(d->s_cap, &g);
     if (st != FDA_OK) return st;
     if (e != cudaSuccess) {
@@ -1342,6 +1335,36 @@ static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind, int phase
   }
   CK(cudaGraphLaunch(ge, s));
   return FDA_OK;
+}
+
+// run_core through a CUDA graph (captured once: all its buffers are internal,
+// so the same graph serves every call); profiled calls run it eagerly.
+// phase (sharded contexts only): 0 = whole matvec with the NCCL exchange,
+// FDA_PHASE_UP / FDA_PHASE_DOWN = the halves around an external exchange
+// (fda_exchange_local, the one-GPU test transport)
+static fda_status core(Context* ctx, Dev* d, cudaStream_t s, int kind, int phase = 0) {
+  if (d->nranks > 1) {
+    // sharded: near field (eager, own stream) ∥ [UP graph → NCCL exchange →
+    // DOWN graph]; the halves are CUDA graphs (graph_exec[2 + kind] / [4 + kind]) unless profiling
+    fda_status st = FDA_OK;
+    const bool graphs = !ctx->profiling && ctx->p.opt.use_graph != 0;
+    if (phase != FDA_PHASE_DOWN) {
+      if ((st = launch_sharded_near(ctx, d, s, kind)) != FDA_OK) return st;
+      st = graphs ? launch_captured(ctx, d, s, 2 + kind, [&](cudaStream_t cs) { return run_sharded_up(ctx, d, cs, kind); })
+                  : run_sharded_up(ctx, d, s, kind);
+      if (st != FDA_OK) return st;
+    }
+    if (phase == 0 && (st = exchange_nccl(ctx, d, s)) != FDA_OK) return st;
+    if (phase != FDA_PHASE_UP) {
+      st = graphs ? launch_captured(ctx, d, s, 4 + kind, [&](cudaStream_t cs) { return run_sharded_down(ctx, d, cs); })
+                  : run_sharded_down(ctx, d, s);
+      if (st != FDA_OK) return st;
+      CK(cudaStreamWaitEvent(s, d->ev_join, 0));   // the near field of this matvec
+    }
+    return st;
+  }
+  if (ctx->profiling || !d->use_graph) return run_core(ctx, d, s, kind);
+  return launch_captured(ctx, d, s, kind, [&](cudaStream_t cs) { return run_core(ctx, d, cs, kind); });
 }
 
 // device-pointer matvec in caller order (float2 in, float2 out)
