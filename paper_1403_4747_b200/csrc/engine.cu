@@ -957,7 +957,9 @@ fda_status engine_create(Context* ctx) {
     cnt(L.dense); cnt(L.a); cnt(L.b);
     for (int c = 0; c < LR_NCLS; ++c) nl += L.n_lr[c] > 0;
     nl += L.n_lrtc > 0;
+    nl += L.n_lrtc > 0 && L.lrtc_bf16;   // k_split_bf16 before k_m2l_bf
   }
+  if (d->nranks > 1) nl += 2;            // k_pack, k_unpack_add
   ctx->launches_per_matvec = nl;
   // CTA tasks per translation kernel family (fda_debug_table "kernel_tasks"; lets the tests
   // assert where the translations were routed): [k_xlate, k_xlate_tc, k_xlate_tcw, k_m2l_lr,

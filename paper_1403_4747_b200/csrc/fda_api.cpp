@@ -173,17 +173,9 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
         // levels where a factored K̃ is shared by fewer than 16 ops on average (the
         // coarse HF levels: ~10 at config 2 L2) keep the dense K̃ — the grouped dense
         // translation kernel tiles 16 ops per CTA, the fused factored one 64
-        bool use_lr = !pl.lr_V.empty();
-        if (use_lr) {
-          std::unordered_map<int64_t, int> nm;
-          int64_t nf = 0;
-          for (const Op& op : pl.m2l[l])
-            if (pl.lr_V[op.mat] >= 0) {
-              ++nf;
-              nm[op.mat] = 1;
-            }
-          use_lr = nf >= 16 * (int64_t)nm.size();
-        }
+        // (the share is counted on the GLOBAL op list before any sharding, so every rank of a
+        // sharded build routes a level the same way)
+        const bool use_lr = !pl.lr_V.empty() && l < pl.m2l_share.size() && pl.m2l_share[l] >= 16.0;
         for (const Op& op : pl.m2l[l]) {
           ++pl.n_m2l_total;
           if (use_lr && pl.lr_V[op.mat] >= 0) {

@@ -148,6 +148,7 @@ struct Plan {
   std::vector<std::vector<Op>> m2m, m2l, l2l;
   // §4.2 factored M2L ops (plan.m2l keeps the dense ones)
   std::vector<LrOp> m2l_lr;
+  std::vector<double> m2l_share;     // per level: global M2L ops per distinct K̃ (before sharding)
   int64_t tmp_size = 0;
   std::vector<int64_t> lr_V, lr_U;   // per matrix id: factor ids (-1 = dense)
   int64_t n_m2l_total = 0;

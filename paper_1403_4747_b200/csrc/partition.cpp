@@ -30,6 +30,16 @@ void apply_partition(const Params& p, const Tree& t, Plan& plan, std::vector<cha
   const int R = std::max(1, p.opt.nranks), r = p.opt.rank;
   const int64_t nleaf = (int64_t)plan.leaf_box.size();
   needed.assign(plan.specs.size(), 1);
+  // per level: M2L ops per distinct K̃ over the whole tree (the §4.2 routing rule, fda_api.cpp)
+  plan.m2l_share.assign(plan.m2l.size(), 0.0);
+  for (size_t l = 0; l < plan.m2l.size(); ++l) {
+    std::vector<int64_t> mats;
+    mats.reserve(plan.m2l[l].size());
+    for (const Op& o : plan.m2l[l]) mats.push_back(o.mat);
+    std::sort(mats.begin(), mats.end());
+    const int64_t nd = (int64_t)(std::unique(mats.begin(), mats.end()) - mats.begin());
+    plan.m2l_share[l] = nd ? (double)plan.m2l[l].size() / (double)nd : 0.0;
+  }
   if (R <= 1) {
     plan.own_leaf0 = 0; plan.own_leaf1 = nleaf;
     plan.own_e0 = 0; plan.own_e1 = nleaf ? t.boxes[plan.leaf_box[nleaf - 1]].end : 0;

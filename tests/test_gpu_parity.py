@@ -375,6 +375,8 @@ def test_sharded_exchange_one_gpu(lib, R, lrtc, tc):
     err = _rel(acc, full)
     print(f"sharded R={R}: rel-L2 vs unsharded {err:.3e}")
     assert err < 1e-5
+    el = O.element_geometry(V, F)
+    assert _rel(acc, fast.matvec_rows(el, np.arange(len(F)), x, k, 1j / k)) <= MATVEC_TOL
     with pytest.raises(Exception):
         ranks[0].matvec(x)
     # without the exchange the result is wrong (the partial states alone are not enough)
@@ -607,4 +609,6 @@ def test_sharded_config3_eight_ranks_one_gpu(lib):
     print(f"config3 R=8: rel-L2 vs unsharded {err:.3e}; table bytes / unsharded {np.round(tb, 3).tolist()}; "
           f"build s {bt}")
     assert err < 1e-5
-    assert tb.max() < 0.3 and tb.sum() < 2.0
+    # per rank: 1/8 of the leaf operators and correction rows, plus the M2L / M2M / L2L
+    # matrices its boxes use (most K̃ of a level are shared by every rank)
+    assert tb.max() < 0.4 and tb.sum() < 3.0
