@@ -61,6 +61,7 @@ def _peaks():
     fp32 = SMS * FP32_LANES * 2 * clk * 1e6 / 1e12    # TFLOP/s, derived from unit counts × max clock
     bf16 = mp.get("bf16_tflops", 2250.0)
     tf32x3 = bf16 * TF32_OVER_BF16 / 3.0               # 3xTF32: three TF32 MMA passes per fp32-accurate product
+    bf16x3 = bf16 / 3.0                                # BF16x3: three BF16 MMA passes (hi·hi + hi·lo + lo·hi)
     ub = None
     try:
         rows = [json.loads(l) for l in open(os.path.join(ROOT, "profiles", "r01_ubench_ffma2.jsonl")) if l.strip()]
@@ -71,8 +72,9 @@ def _peaks():
                    f"({'MEASURED_PEAKS.json sm_max_mhz' if 'sm_max_mhz' in mp else 'fallback clock'})",
            "fp32_measured_ubench_tflops": ub,
            "hbm": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in mp else "fallback 6650 GB/s",
-           "tf32x3": f"MEASURED_PEAKS.json bf16_tflops ({bf16}) x nominal TF32/BF16 (1.1/2.25) / 3 passes"}
-    return hbm, fp32, tf32x3, src
+           "tf32x3": f"MEASURED_PEAKS.json bf16_tflops ({bf16}) x nominal TF32/BF16 (1.1/2.25) / 3 passes",
+           "bf16x3": f"MEASURED_PEAKS.json bf16_tflops ({bf16}) / 3 passes"}
+    return hbm, fp32, {"tensor": tf32x3, "tensor_bf16": bf16x3}, src
 
 
 def _dist():
@@ -176,7 +178,10 @@ def _family_work(f, work):
         fam[k] = ("alu", fl, "complex-equivalent flops, 8·rows·cols per op (16·r·T per factored M2L op)")
     for k in ("k_xlate_tc", "k_xlate_tcw", "k_m2l_tcw"):
         fl = sum(v for n, v in kf.items() if n.startswith(k + "/"))
-        fam[k] = ("tensor", fl, "complex-equivalent flops on tcgen05 3xTF32 (8·rows·cols per op)")
+        if k == "k_m2l_tcw" and f.opt.m2l_bf16:
+            fam[k] = ("tensor_bf16", fl, "complex-equivalent flops on tcgen05 BF16x3 (k_m2l_bf: 16·r·T per factored op)")
+        else:
+            fam[k] = ("tensor", fl, "complex-equivalent flops on tcgen05 3xTF32 (8·rows·cols per op)")
     fam["k_s2m"] = ("hbm", work["s2m"]["bytes"], "8 B per stored S̃ entry + 16 B per element")
     fam["k_l2t"] = ("hbm", work["l2t"]["bytes"], "8 B per stored T̃ entry + 16 B per element")
     return fam
@@ -259,7 +264,7 @@ def run_config(cfg, args, ws, rank, local, primary):
     stage_ms = {k: float(np.mean(v)) for k, v in acc.items()}
     kern_ms = {k: float(np.mean(v)) for k, v in kacc.items()}
 
-    hbm, fp32, tf32x3, psrc = _peaks()
+    hbm, fp32, tpk, psrc = _peaks()
     work = _stage_work(f, N)
     stages = {}
     for sname, t in stage_ms.items():
@@ -290,7 +295,7 @@ def run_config(cfg, args, ws, rank, local, primary):
                 if bound == "hbm":
                     a, p, u = amount / (t * 1e-3) / 1e9, hbm, "GB/s"
                 else:
-                    a, p, u = amount / (t * 1e-3) / 1e12, (fp32 if bound == "alu" else tf32x3), "TFLOP/s"
+                    a, p, u = amount / (t * 1e-3) / 1e12, (fp32 if bound == "alu" else tpk[bound]), "TFLOP/s"
                 e.update({"bound": bound, "achieved": a, "peak": p, "unit": u, "frac": a / p, "work": unit})
             kernels[k] = e
         dom = max((k for k in kern_ms if k in fam), key=lambda k: kern_ms[k])
@@ -303,11 +308,13 @@ def run_config(cfg, args, ws, rank, local, primary):
         if bound == "hbm":
             a, p, u = amount / (t_dom * 1e-3) / 1e9, hbm, "GB/s"
         else:
-            a, p, u = amount / (t_dom * 1e-3) / 1e12, (fp32 if bound == "alu" else tf32x3), "TFLOP/s"
-        roof = {"bound": "alu" if bound == "alu" else bound, "achieved": a, "peak": p, "unit": u, "frac": a / p,
+            a, p, u = amount / (t_dom * 1e-3) / 1e12, (fp32 if bound == "alu" else tpk[bound]), "TFLOP/s"
+        roof = {"bound": "alu" if bound == "alu" else ("tensor" if bound.startswith("tensor") else bound),
+                "achieved": a, "peak": p, "unit": u, "frac": a / p,
                 "traffic": _traffic(cfg, dom), "kernel": dom, "ms_per_matvec": round(t_dom, 4),
                 "share_of_kernel_time": round(kern_ms[dom] / tot, 4), "timing": timing, "unit_of_work": unit,
-                "peak_source": psrc["fp32"] if bound == "alu" else (psrc["hbm"] if bound == "hbm" else psrc["tf32x3"]),
+                "peak_source": psrc["fp32"] if bound == "alu" else (psrc["hbm"] if bound == "hbm" else
+                                                                  psrc["bf16x3" if bound == "tensor_bf16" else "tf32x3"]),
                 "fp32_measured_ubench_tflops": psrc["fp32_measured_ubench_tflops"]}
     launches = int(f.table("launches")[0])   # exact count of our kernels per matvec (engine.cu)
     out = {"cfg": cfg, "N": N, "ms": ms, "per_step_ms": [round(p, 4) for p in per[:5]], "build_s": build_s,

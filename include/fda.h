@@ -94,11 +94,11 @@ typedef struct {
                             directional S2M / L2T per used wedge (PAPER.md P:344-346,
                             P:449-454)                                                     */
   int32_t lr_tensor_cores;  /* §4.2 factored M2L (r ≤ 32, T ≤ 160) on the fused tcgen05 kernel
-                            (both products on the tensor cores, 3xTF32, tmp kept on chip):
-                            (persistent, warp-specialised k_m2l_tcw): 0 never (fused CUDA-core
-                            kernel), 1 always, 2 (default) on levels with ≥ 64 ops per factored
-                            K̃ and ≥ 3 GFLOP of factored work; needs
-                            tensor_cores ≠ 0                                               */
+                            (both products on the tensor cores, tmp kept on chip; persistent,
+                            warp-specialised k_m2l_bf / k_m2l_tcw): 0 never (fused CUDA-core
+                            kernel), 1 always, 2 (default) every level with m2l_bf16 = 1, with
+                            3xTF32 only levels with ≥ 64 ops per factored K̃ and ≥ 3 GFLOP
+                            (DESIGN.md §5); needs tensor_cores ≠ 0                          */
   int32_t build_on_device;  /* 1 (default): the fp64 operator and correction tables of
                             fda_build are computed on opt.device (build_dev.cu: kernel-matrix
                             generation, batched fp64 complex GEMMs, tier quadrature), the

@@ -765,9 +765,14 @@ fda_status engine_create(Context* ctx) {
         fl[o.level] += 16.0 * p.mats[o.matV].rows * p.mats[o.matV].cols;
         nm[o.level][o.matV] = 1;
       }
+      // auto (2): BF16x3 (default) on every eligible level — measured faster than the fused
+      // CUDA-core kernel on configs 2 / 3 / 4 (matvec 0.475 → 0.427, 1.634 → 1.549,
+      // 5.116 → 5.047 ms, profiles/r02_ab_routing.jsonl); 3xTF32 only on levels with ≥ 64 ops
+      // per factored K̃ and ≥ 3 GFLOP (round 1)
+      const bool bf = ctx->p.opt.m2l_bf16 != 0;
       for (int l = 0; l < nlev; ++l)
         lr_f[l] = nops[l] > 0 && !lr_tc[l] &&
-                  (ctx->p.opt.lr_tensor_cores == 1 ||
+                  (ctx->p.opt.lr_tensor_cores == 1 || bf ||
                    ((double)nops[l] >= 64.0 * (double)nm[l].size() && fl[l] >= 3e9));
     }
     std::vector<std::vector<LrOp>> ftc(nlev);
