@@ -187,7 +187,12 @@ fda_status fda_rhs_apply(fda_ctx* ctx, const void* v, void* b, int32_t flags, vo
 
 /* Solve A u = rhs by GMRES (§5: tolerance on the relative
  * residual, no preconditioner; reading C20).  restart = 0: no restart.
- * Returns FDA_E_NOT_CONVERGED (u = last iterate, info filled) at max_iter. */
+ * Returns FDA_E_NOT_CONVERGED (u = last iterate, info filled) at max_iter.
+ * Sharded contexts (opt.nranks > 1, collective over the ranks, after
+ * fda_comm_init): every Krylov vector holds only the rank's own rows; the inner
+ * products are all-reduced (ncclAllReduce of j + 1 complex values per CGS
+ * pass), each matvec all-gathers its input (ncclBroadcast of every rank's
+ * slice) and keeps its output local; rhs and u are full-length on every rank. */
 fda_status bm_solve(fda_ctx* ctx, const void* rhs, void* u, double tol, int32_t max_iter,
                     int32_t restart, fda_solve_info* info, int32_t flags);
 

@@ -52,6 +52,7 @@ struct NcclApi {
   ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*groupStart)() = nullptr;
   ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
 };
 NcclApi& nccl(std::string& err) {
   static NcclApi api;
@@ -72,8 +73,9 @@ NcclApi& nccl(std::string& err) {
     api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
     api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
     api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
+    api.bcast = (decltype(api.bcast))dlsym(h, "ncclBroadcast");
     api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.errStr && api.send &&
-             api.recv && api.groupStart && api.groupEnd;
+             api.recv && api.groupStart && api.groupEnd && api.bcast;
     if (!api.ok) err = "libnccl.so.2 lacks a required symbol";
   }
   return api;
@@ -110,6 +112,7 @@ struct XStage {
 // GMRES workspace (engine_solve; cached per context)
 struct Gm {
   float2 *V = nullptr, *w = nullptr, *b = nullptr, *x = nullptr;
+  float2* full = nullptr;                         // sharded: one full-length tree-order vector
   double2 *partial = nullptr, *hbuf = nullptr;   // hbuf: [h1 (m+1) | h2 (m+1) | y (m+1)]
   double *np = nullptr, *nrm = nullptr;
   int m = 0;
@@ -300,13 +303,14 @@ static int64_t tc_bop(Context* ctx, Dev* d, int64_t m, int nrp, int nkc) {
 }
 
 // bf16 B operand of k_m2l_bf: as tc_bop with 32-element K chunks of bf16 hi / lo
-static int64_t tc_bop_bf(Context* ctx, Dev* d, int64_t m, int nrp, int nkc32) {
+// (row blocks of rb rows per chunk, rb = 0: one block; k_m2l_bf streams B2 in two N-halves)
+static int64_t tc_bop_bf(Context* ctx, Dev* d, int64_t m, int nrp, int nkc32, int rb = 0) {
   auto it = d->tc_bfoff.find(m);
   if (it != d->tc_bfoff.end()) return it->second;
   const MatInfo& mi = ctx->plan.mats[m];
   const int64_t off = d->tc_size;
   d->tc_size += (int64_t)nkc32 * nrp * 32;   // 2 planes × nrp × 32 bf16 = nrp × 32 floats per chunk
-  d->tc_jobs.push_back(TcLayoutJob{off, mi.offset, mi.rows, mi.cols, nrp, nkc32, 2, 0});
+  d->tc_jobs.push_back(TcLayoutJob{off, mi.offset, mi.rows, mi.cols, nrp, nkc32, 2, rb});
   d->tc_bfoff.emplace(m, off);
   return off;
 }
@@ -638,7 +642,13 @@ fda_status engine_create(Context* ctx) {
     UP(&d->corr_col_rhs, rc.data(), rc.size());
     UP(&d->corr_val_rhs, reinterpret_cast<const float2*>(p.corr_val_rhs.data()), p.corr_val_rhs.size());
   }
-  UP(&d->pool, reinterpret_cast<const float2*>(p.pool.data()), p.pool.size());
+  if (ctx->pool_dev) {   // device build: adopt the pool it left on the device
+    d->pool = static_cast<float2*>(ctx->pool_dev);
+    d->allocs.push_back(d->pool);
+    ctx->pool_dev = nullptr;
+  } else {
+    UP(&d->pool, reinterpret_cast<const float2*>(p.pool.data()), p.pool.size());
+  }
   UP(&d->cen, cen.data(), cen.size());
   UP(&d->nrm, nrm.data(), nrm.size());
   d->out_size = p.out_size;
@@ -845,7 +855,7 @@ fda_status engine_create(Context* ctx) {
           if (ctx->p.opt.m2l_bf16) {   // BF16x3: 32-element K chunks of bf16 hi / lo
             tk.nk1 = (2 * T + 31) / 32;
             tk.b1_off = tc_bop_bf(ctx, d, Ft[i].matV, tk.n1, tk.nk1);
-            tk.b2_off = tc_bop_bf(ctx, d, Ft[i].matU, tk.n2, (tk.n1 + 31) / 32);
+            tk.b2_off = tc_bop_bf(ctx, d, Ft[i].matU, tk.n2, (tk.n1 + 31) / 32, ((tk.n2 / 2 + 15) / 16) * 16);
           } else {
             tk.nk1 = (2 * T + TC_KC - 1) / TC_KC;
             tk.b1_off = tc_bop(ctx, d, Ft[i].matV, tk.n1, tk.nk1);
@@ -1548,15 +1558,71 @@ fda_status engine_rhs_point_source(Context* ctx, const double src[3], void* b, i
 
 static const int kChunks = 128;
 
+// ---- sharded GMRES (nranks > 1): every Krylov vector holds only this rank's rows
+// (tree order, the contiguous element range [e0, e1)); inner products are local partial sums
+// all-reduced over the ranks (one ncclAllReduce of j + 1 complex values per CGS pass), the
+// matvec input is all-gathered (one ncclBroadcast per rank's slice, grouped) and the matvec
+// returns the LOCAL rows (no all-reduce of y)
+static fda_status allgather_tree(Context* ctx, Dev* d, float2* full, cudaStream_t s) {
+  NcclApi& a = nccl(ctx->err);
+  if (!a.ok) return FDA_E_NCCL;
+  const Plan& p = ctx->plan;
+  ncclResult_t r = a.groupStart();
+  for (int q = 0; q < d->nranks && r == ncclSuccess; ++q) {
+    const int64_t n0 = p.rank_e0[q], nq = p.rank_e1[q] - p.rank_e0[q];
+    if (nq > 0) r = a.bcast(full + n0, full + n0, (size_t)(2 * nq), ncclFloat, q, d->comm, s);
+  }
+  ncclResult_t r2 = a.groupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) {
+    ctx->err = std::string("NCCL all-gather of the Krylov vector: ") + a.errStr(r);
+    return FDA_E_NCCL;
+  }
+  return FDA_OK;
+}
+static fda_status allreduce_d(Context* ctx, Dev* d, double* v, size_t count, cudaStream_t s) {
+  NcclApi& a = nccl(ctx->err);
+  if (!a.ok) return FDA_E_NCCL;
+  const ncclResult_t r = a.allReduce(v, v, count, ncclDouble, ncclSum, d->comm, s);
+  if (r != ncclSuccess) {
+    ctx->err = std::string("NCCL all-reduce of GMRES dot products: ") + a.errStr(r);
+    return FDA_E_NCCL;
+  }
+  return FDA_OK;
+}
+static fda_status matvec_own(Context* ctx, Dev* d, const float2* x_own, float2* y_own, cudaStream_t s) {
+  const int64_t e0 = d->e0, nl = d->e1 - d->e0;
+  if (nl > 0) CK(cudaMemcpyAsync(d->x_tree + e0, x_own, sizeof(float2) * nl, cudaMemcpyDeviceToDevice, s));
+  fda_status st = allgather_tree(ctx, d, d->x_tree, s);
+  if (st != FDA_OK) return st;
+  if ((st = core(ctx, d, s, 0, 0)) != FDA_OK) return st;
+  launch_add_slice(d->y_near, d->y_far, e0, nl, y_own, s);
+  CK(cudaGetLastError());
+  return FDA_OK;
+}
+
 // h[0..nv) = V[0..nv)^H w  → device
 static void dots_dev(Gm& gm, int nv, const float2* w, int64_t n, double2* h) {
   launch_dots(gm.V, n, nv, w, n, gm.partial, kChunks, 0);
   launch_reduce_partials(gm.partial, nv, kChunks, h, 0);
 }
 
-static fda_status norm_host(Context* ctx, Gm& gm, const float2* w, int64_t n, double& out) {
+// ‖w‖ into gm.nrm (device) — over the ranks' slices when sharded
+static fda_status norm_dev(Context* ctx, Dev* d, Gm& gm, const float2* w, int64_t n) {
   launch_norm2(w, n, gm.np, kChunks, 0);
-  launch_reduce_norm(gm.np, kChunks, gm.nrm, 0);
+  if (d->nranks > 1) {
+    launch_reduce_sum(gm.np, kChunks, gm.nrm, 0);
+    fda_status st = allreduce_d(ctx, d, gm.nrm, 1, 0);
+    if (st != FDA_OK) return st;
+    launch_sqrt1(gm.nrm, 0);
+  } else {
+    launch_reduce_norm(gm.np, kChunks, gm.nrm, 0);
+  }
+  return FDA_OK;
+}
+static fda_status norm_host(Context* ctx, Dev* d, Gm& gm, const float2* w, int64_t n, double& out) {
+  fda_status st = norm_dev(ctx, d, gm, w, n);
+  if (st != FDA_OK) return st;
   CK(cudaMemcpy(&out, gm.nrm, sizeof(double), cudaMemcpyDeviceToHost));
   return FDA_OK;
 }
@@ -1567,8 +1633,19 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
   CK(cudaSetDevice(d->device));
   CK(cudaDeviceSynchronize());
   auto t0 = std::chrono::steady_clock::now();
-  const int64_t n = d->n;
+  // sharded (nranks > 1): the Krylov vectors hold this rank's rows only (tree order)
+  const bool sh = d->nranks > 1;
+  if (sh && !d->comm) { ctx->err = "sharded context: call fda_comm_init before bm_solve"; return FDA_E_STATE; }
+  const int64_t n = sh ? (int64_t)(d->e1 - d->e0) : d->n;
   const int m = restart > 0 ? std::min(restart, max_iter) : max_iter;
+  auto mv = [&](const float2* xv, float2* yv) -> fda_status {
+    return sh ? matvec_own(ctx, d, xv, yv, 0) : matvec_dev(ctx, d, xv, yv, 0);
+  };
+  // h[0..nv) = V^H w over all ranks
+  auto dots = [&](Gm& g, int nv, const float2* w, double2* h) -> fda_status {
+    dots_dev(g, nv, w, n, h);
+    return sh ? allreduce_d(ctx, d, reinterpret_cast<double*>(h), (size_t)2 * nv, 0) : FDA_OK;
+  };
   // workspace cached in the context (allocated on the first solve, grown on demand)
   if (d->gm_cap < m + 1) {
     for (void* q : d->gm_allocs) cudaFree(q);
@@ -1583,8 +1660,9 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
       return true;
     };
     Gm& w = d->gm;
-    if (!A((void**)&w.V, sizeof(float2) * n * (m + 1)) || !A((void**)&w.w, sizeof(float2) * n) ||
-        !A((void**)&w.b, sizeof(float2) * n) || !A((void**)&w.x, sizeof(float2) * n) ||
+    if (!A((void**)&w.V, sizeof(float2) * std::max<int64_t>(1, n) * (m + 1)) || !A((void**)&w.w, sizeof(float2) * std::max<int64_t>(1, n)) ||
+        !A((void**)&w.full, sizeof(float2) * d->n) ||
+        !A((void**)&w.b, sizeof(float2) * std::max<int64_t>(1, n)) || !A((void**)&w.x, sizeof(float2) * std::max<int64_t>(1, n)) ||
         !A((void**)&w.partial, sizeof(double2) * kChunks * (m + 1)) ||
         !A((void**)&w.hbuf, sizeof(double2) * 3 * (m + 1)) || !A((void**)&w.np, sizeof(double) * kChunks) ||
         !A((void**)&w.nrm, sizeof(double))) {
@@ -1619,15 +1697,23 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
   double2* h1 = gm.hbuf;
   double2* h2 = gm.hbuf + (m + 1);
   double2* yd = gm.hbuf + 2 * (m + 1);
-  if (flags & FDA_DEVICE) {
+  if (sh) {   // caller order → tree order (full), then this rank's slice
+    if (flags & FDA_DEVICE) {
+      launch_gather_f32(static_cast<const float2*>(rhs), d->perm, gm.full, d->n, 0);
+    } else {
+      GCU(cudaMemcpy(d->xh, rhs, sizeof(double2) * d->n, cudaMemcpyHostToDevice));
+      launch_gather_f64(d->xh, d->perm, gm.full, d->n, 0);
+    }
+    if (n > 0) GCU(cudaMemcpy(gm.b, gm.full + d->e0, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+  } else if (flags & FDA_DEVICE) {
     GCU(cudaMemcpy(gm.b, rhs, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
   } else {
     GCU(cudaMemcpy(d->xh, rhs, sizeof(double2) * n, cudaMemcpyHostToDevice));
     launch_f64_to_f32(d->xh, gm.b, n, 0);
   }
-  GCU(cudaMemset(gm.x, 0, sizeof(float2) * n));
+  if (n > 0) GCU(cudaMemset(gm.x, 0, sizeof(float2) * n));
   double bnorm = 0;
-  GCK(norm_host(ctx, gm, gm.b, n, bnorm));
+  GCK(norm_host(ctx, d, gm, gm.b, n, bnorm));
   int it = 0;
   double res = 1.0;
   bool conv = bnorm == 0.0;
@@ -1637,13 +1723,13 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
     float2* v0 = gm.V;
     double beta;
     if (it == 0) {
-      GCU(cudaMemcpy(v0, gm.b, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+      if (n > 0) GCU(cudaMemcpy(v0, gm.b, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
       beta = bnorm;
     } else {  // restart: r = b - A x
-      GCK(matvec_dev(ctx, d, gm.x, gm.w, 0));
-      GCU(cudaMemcpy(v0, gm.b, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+      GCK(mv(gm.x, gm.w));
+      if (n > 0) GCU(cudaMemcpy(v0, gm.b, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
       launch_axpby(v0, gm.w, -1.0, 1.0, n, 0);
-      GCK(norm_host(ctx, gm, v0, n, beta));
+      GCK(norm_host(ctx, d, gm, v0, n, beta));
     }
     launch_scale(v0, v0, 1.0 / beta, 0.0, n, 0);
     std::fill(H.begin(), H.end(), cd(0));
@@ -1652,13 +1738,12 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
     int jd = 0;
     for (int j = 0; j < m && it < max_iter; ++j) {
       float2* vj = gm.V + (int64_t)j * n;
-      GCK(matvec_dev(ctx, d, vj, gm.w, 0));
-      dots_dev(gm, j + 1, gm.w, n, h1);
+      GCK(mv(vj, gm.w));
+      GCK(dots(gm, j + 1, gm.w, h1));
       launch_update(gm.w, gm.V, n, j + 1, h1, n, -1.0, 0);
-      dots_dev(gm, j + 1, gm.w, n, h2);
+      GCK(dots(gm, j + 1, gm.w, h2));
       launch_update(gm.w, gm.V, n, j + 1, h2, n, -1.0, 0);
-      launch_norm2(gm.w, n, gm.np, kChunks, 0);
-      launch_reduce_norm(gm.np, kChunks, gm.nrm, 0);
+      GCK(norm_dev(ctx, d, gm, gm.w, n));
       launch_scale_by_inv(gm.V + (int64_t)(j + 1) * n, gm.w, gm.nrm, n, 0);
       // one copy: h1, h2 and the norm
       GCU(cudaMemcpy(hh.data(), h1, sizeof(double2) * (m + 1 + j + 1), cudaMemcpyDeviceToHost));   // h1 | h2
@@ -1704,13 +1789,23 @@ fda_status engine_solve(Context* ctx, const void* rhs, void* u, double tol, int3
   // true residual ‖b - A x‖ / ‖b‖ (one extra matvec)
   double true_res = 0;
   if (bnorm > 0) {
-    GCK(matvec_dev(ctx, d, gm.x, gm.w, 0));
+    GCK(mv(gm.x, gm.w));
     launch_axpby(gm.w, gm.b, 1.0, -1.0, n, 0);  // w = b - A x
     double rn;
-    GCK(norm_host(ctx, gm, gm.w, n, rn));
+    GCK(norm_host(ctx, d, gm, gm.w, n, rn));
     true_res = rn / bnorm;
   }
-  if (flags & FDA_DEVICE) {
+  if (sh) {   // this rank's slice → full tree-order u on every rank → caller order
+    if (n > 0) GCU(cudaMemcpy(gm.full + d->e0, gm.x, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
+    GCK(allgather_tree(ctx, d, gm.full, 0));
+    GCU(cudaMemset(d->y_far, 0, sizeof(float2) * d->n));
+    if (flags & FDA_DEVICE) {
+      launch_scatter_f32(gm.full, d->y_far, d->perm, static_cast<float2*>(u), d->n, 0, d->n, 0);
+    } else {
+      launch_scatter_f64(gm.full, d->y_far, d->perm, d->yh, d->n, 0, d->n, 0);
+      GCU(cudaMemcpy(u, d->yh, sizeof(double2) * d->n, cudaMemcpyDeviceToHost));
+    }
+  } else if (flags & FDA_DEVICE) {
     GCU(cudaMemcpy(u, gm.x, sizeof(float2) * n, cudaMemcpyDeviceToDevice));
   } else {
     launch_f32_to_f64(gm.x, d->yh, n, 0);

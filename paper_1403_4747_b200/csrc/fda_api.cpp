@@ -2,6 +2,7 @@
 // orchestration (PAPER.md Algorithm Step 1, and §4 tables) and
 // host-table export for host-logic tests.
 #include <chrono>
+#include <cuda_runtime.h>
 #include <cstdio>
 #include <cmath>
 #include <cstring>
@@ -162,7 +163,15 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
         if (st != FDA_OK) throw std::runtime_error(ctx->err);
         phase("operators (device)");
       }
+      const size_t pool_dev_size = pl.pool.size();
       build_operators(ctx->g, ctx->p, ctx->t, pl, done, lr);
+      if (ctx->pool_dev) {   // append the host-side part (the §4.2 factors) to the device pool
+        if ((int64_t)pl.pool.size() > ctx->pool_dev_cap) throw std::runtime_error("device pool capacity exceeded");
+        if (pl.pool.size() > pool_dev_size &&
+            cudaMemcpy(static_cast<float2*>(ctx->pool_dev) + pool_dev_size, pl.pool.data() + pool_dev_size,
+                       (pl.pool.size() - pool_dev_size) * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess)
+          throw std::runtime_error("upload of the §4.2 factors failed");
+      }
       phase("operators");
       // §4.2: route the M2L ops whose K̃ was factored (r < T/2) to the two-stage path
       pl.n_m2l_total = 0;
@@ -210,6 +219,7 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
   if (st != FDA_OK) {
     g_build_error = ctx->err;
     engine_destroy(ctx);
+    if (ctx->pool_dev) cudaFree(ctx->pool_dev);   // not adopted by an engine
     delete ctx;
     return st;
   }

@@ -154,6 +154,7 @@ struct Plan {
   int64_t n_m2l_total = 0;
   // sharding (nranks > 1): owned leaves [own_leaf0, own_leaf1), elements [own_e0, own_e1)
   int64_t own_leaf0 = 0, own_leaf1 = 0, own_e0 = 0, own_e1 = 0;
+  std::vector<int64_t> rank_e0, rank_e1;   // every rank's element range (tree order)
   // exchange of partial outgoing states between the passes (partition.cpp):
   // per peer rank, the sorted out-state ids this rank sends / receives
   std::vector<std::vector<int64_t>> xsend, xrecv;
@@ -265,6 +266,8 @@ struct Context {
   fda_build_info info{};
   void* dev = nullptr;   // engine-owned device state
   int64_t launches_per_matvec = 0;
+  void* pool_dev = nullptr;        // device build: the matrix pool already on the device (engine adopts it)
+  int64_t pool_dev_cap = 0;        // its capacity (complex entries)
   int64_t kernel_tasks[15] = {};   // CTA tasks per translation kernel family × (M2M, M2L, L2L)
   double kernel_flops[15] = {};    // their algorithmic flops (complex-equivalent, 8·rows·cols per op)
   bool profiling = false;

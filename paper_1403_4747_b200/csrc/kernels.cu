@@ -894,6 +894,35 @@ __global__ void k_reduce_norm(const double* __restrict__ partial, int nchunks, d
 void launch_reduce_norm(const double* partial, int nchunks, double* out, cudaStream_t s) {
   k_reduce_norm<<<1, 128, 0, s>>>(partial, nchunks, out);
 }
+// sharded GMRES helpers: Σ partial (no square root; summed over ranks before the root)
+__global__ void k_reduce_sum(const double* __restrict__ partial, int nchunks, double* __restrict__ out) {
+  __shared__ double red[128];
+  double a = 0;
+  for (int c = threadIdx.x; c < nchunks; c += blockDim.x) a += partial[c];
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+void launch_reduce_sum(const double* partial, int nchunks, double* out, cudaStream_t s) {
+  k_reduce_sum<<<1, 128, 0, s>>>(partial, nchunks, out);
+}
+__global__ void k_sqrt1(double* x) { x[0] = sqrt(x[0]); }
+void launch_sqrt1(double* x, cudaStream_t s) { k_sqrt1<<<1, 1, 0, s>>>(x); }
+// y[i] = a[off + i] + b[off + i]
+__global__ void k_add_slice(const float2* __restrict__ a, const float2* __restrict__ b, int64_t off, int64_t n,
+                            float2* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float2 u = a[off + i], v = b[off + i];
+  y[i] = make_float2(u.x + v.x, u.y + v.y);
+}
+void launch_add_slice(const float2* a, const float2* b, int64_t off, int64_t n, float2* y, cudaStream_t s) {
+  if (n > 0) k_add_slice<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, off, n, y);
+}
 
 __global__ void k_scale_by_inv(float2* dst, const float2* src, const double* __restrict__ nrm, int64_t n) {
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

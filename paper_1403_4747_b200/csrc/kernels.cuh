@@ -154,7 +154,7 @@ struct TcLayoutJob {
   int32_t nkc;        // TC_KC-float K chunks
   int32_t kind;       // 0: A tiles [tile][chunk][hi | lo] 128 × TC_KC; 1: B operand [chunk][hi | lo] nrp × TC_KC;
                       // 2: bf16 B operand [32-element chunk][hi | lo] nrp × 32 (nkc = 32-element chunks)
-  int32_t pad;
+  int32_t pad;        // kind 2: rows per block (0 = one block of nrp rows)
 };
 void launch_tc_layout(int njob, const TcLayoutJob* jobs, const float2* pool, float* tcpool, cudaStream_t s);
 // warp-specialised persistent translation kernel (N = 128 ops per task, tiles ≤ 2)
@@ -171,6 +171,9 @@ void launch_norm2(const float2* w, int64_t n, double* partial, int nchunks, cuda
 void launch_reduce_partials(const double2* partial, int nv, int nchunks, double2* out, cudaStream_t s);
 void launch_reduce_norm(const double* partial, int nchunks, double* out, cudaStream_t s);   // out = sqrt(Σ)
 void launch_scale_by_inv(float2* dst, const float2* src, const double* nrm, int64_t n, cudaStream_t s);
+void launch_reduce_sum(const double* partial, int nchunks, double* out, cudaStream_t s);   // out = Σ (no root)
+void launch_sqrt1(double* x, cudaStream_t s);
+void launch_add_slice(const float2* a, const float2* b, int64_t off, int64_t n, float2* y, cudaStream_t s);
 void launch_scale(float2* dst, const float2* src, double sre, double sim, int64_t n, cudaStream_t s);
 void launch_axpby(float2* y, const float2* x, double a, double b, int64_t n, cudaStream_t s);  // y = a*x + b*y (real)
 void launch_plane_wave(const double* cen, const double* nrm, const int32_t* perm, int n, double k, double are,

@@ -97,6 +97,8 @@ void apply_partition(const Params& p, const Tree& t, Plan& plan, std::vector<cha
     re0[k] = start[k] < nleaf ? t.boxes[plan.leaf_box[start[k]]].begin : (nleaf ? t.boxes[plan.leaf_box[nleaf - 1]].end : 0);
     re1[k] = start[k + 1] > start[k] ? t.boxes[plan.leaf_box[start[k + 1] - 1]].end : re0[k];
   }
+  plan.rank_e0 = re0;
+  plan.rank_e1 = re1;
   // ranks whose element range intersects [b, e): a contiguous run [lo, hi]
   auto ranks_of = [&](int64_t b, int64_t e, int& lo, int& hi) {
     lo = R; hi = -1;
