@@ -855,7 +855,7 @@ fda_status engine_create(Context* ctx) {
           if (ctx->p.opt.m2l_bf16) {   // BF16x3: 32-element K chunks of bf16 hi / lo
             tk.nk1 = (2 * T + 31) / 32;
             tk.b1_off = tc_bop_bf(ctx, d, Ft[i].matV, tk.n1, tk.nk1);
-            tk.b2_off = tc_bop_bf(ctx, d, Ft[i].matU, tk.n2, (tk.n1 + 31) / 32, ((tk.n2 / 2 + 15) / 16) * 16);
+            tk.b2_off = tc_bop_bf(ctx, d, Ft[i].matU, tk.n2, (tk.n1 + 31) / 32);
           } else {
             tk.nk1 = (2 * T + TC_KC - 1) / TC_KC;
             tk.b1_off = tc_bop(ctx, d, Ft[i].matV, tk.n1, tk.nk1);

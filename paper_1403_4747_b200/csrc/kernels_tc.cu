@@ -657,12 +657,6 @@ __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
 }
 }  // namespace
 
-// Shared memory: an A ring of S1 stages (one 32-element job: [hi | lo] 128 × 32 bf16 =
-// 16 KB), a separate 3-stage B1 ring (n1max × 32 × 2 planes), a 2-stage B2 ring of HALF
-// tiles (phase-2 N split in two ≤ 256-row halves, n2h × 32 × 2 planes each) and the
-// phase-2 A region — so that up to S1 − 2 jobs of gathered states (the HBM/L2 latency
-// the kernel must hide) are in flight per SM.
-constexpr int BF_SB = 3;   // B1 ring stages
 template <int S1>
 __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict__ tasks, int ntask,
                                                    const int64_t* __restrict__ src_off,
@@ -670,19 +664,17 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
                                                    const float* __restrict__ tcpool,
                                                    const __nv_bfloat16* __restrict__ shi,
                                                    const __nv_bfloat16* __restrict__ slo, float2* __restrict__ dst,
-                                                   int b1_b, int b2_b, int n1max, uint32_t ncols) {
+                                                   int stage_b, int b2_b, int n1max, uint32_t ncols) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t a_full[S1], empty[S1], b1_full[BF_SB], b1_empty[BF_SB], b2_full[2], b2_empty[2];
-  __shared__ uint64_t d1_full[2], a2_full, d2_full, y_free;
+  __shared__ uint64_t a_full[S1], b_full[S1], empty[S1], b2_full[2], b2_empty[2];
+  __shared__ uint64_t d1_full, a2_full, d2_full, y_free;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int64_t s_doff[128];                   // destination offsets of the task being drained
-  constexpr int LA = S1 - 2;                        // gather lookahead (jobs in flight per row thread)
+  constexpr int LA = S1 >= 6 ? S1 - 3 : S1 - 2;
   constexpr int A_PL = 128 * BK * 2;               // bytes of one A plane (hi or lo) per job
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x;
-  uint8_t* sB1 = sbase + S1 * 2 * A_PL;            // [BF_SB][b1_b]
-  uint8_t* sB2 = sB1 + BF_SB * b1_b;               // [2][b2_b]
+  uint8_t* sB2 = sbase + S1 * stage_b;             // [2][b2_b]
   uint8_t* sA2 = sB2 + 2 * b2_b;                   // phase-2 A: (n1max / BK) jobs × [hi | lo] 128 × BK
   const uint8_t* pool8 = reinterpret_cast<const uint8_t*>(tcpool);
   if (warp == 0) {
@@ -692,146 +684,122 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
   }
   if (tid == 0) {
     for (int q = 0; q < S1; ++q) {
-      mbar_init(&a_full[q], 128);   // the 4 gather warps
+      mbar_init(&a_full[q], 32 * TCW_RW);
+      mbar_init(&b_full[q], 1);
       mbar_init(&empty[q], 1);
-    }
-    for (int q = 0; q < BF_SB; ++q) {
-      mbar_init(&b1_full[q], 1);
-      mbar_init(&b1_empty[q], 1);
     }
     for (int q = 0; q < 2; ++q) {
       mbar_init(&b2_full[q], 1);
       mbar_init(&b2_empty[q], 1);
     }
-    mbar_init(&d1_full[0], 1);
-    mbar_init(&d1_full[1], 1);
-    mbar_init(&a2_full, 128);     // the 4 epilogue warps
+    mbar_init(&d1_full, 1);
+    mbar_init(&a2_full, 32 * TCW_RW);
     mbar_init(&d2_full, 1);
-    mbar_init(&y_free, 128);
+    mbar_init(&y_free, 32 * TCW_RW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t tY = tmem + (uint32_t)(2 * n1max);   // D2 region (after the two D1 regions)
-  auto half_rows = [](int n2) { return ((n2 / 2 + 15) / 16) * 16; };   // rows of phase-2 half 0
+  const uint32_t tY = tmem + (uint32_t)n1max;      // D2 region
 
   if (warp == TCW_RW + 1) {
-    // ---------------- TMA producer: B1 per ring job (own ring), B2 per (chunk, N-half) — in the
-    // MMA warp's consumption order: B1 of task i, then B2 of task i − 1
+    // ---------------- TMA producer: B1 per ring job, B2 per phase-2 job
     if (lane == 0) {
       int j = 0, b2j = 0;
-      LrTcTask tprev{};
-      bool have_prev = false;
-      auto load_b2 = [&](const LrTcTask& t) {
-        const int nk2 = (t.n1 + BK - 1) / BK, h0 = half_rows(t.n2);
-        for (int c2 = 0; c2 < nk2; ++c2)
-          for (int hh = 0; hh < 2; ++hh, ++b2j) {
-            const int r0 = hh ? h0 : 0, nr = hh ? t.n2 - h0 : h0;
-            const int st = b2j & 1;
-            if (b2j >= 2) mbar_wait(&b2_empty[st], ((b2j >> 1) - 1) & 1);
-            const uint32_t bytes2 = (uint32_t)nr * BK * 2 * 2;
-            mbar_expect_tx(&b2_full[st], bytes2);
-            // kind-2 layout with row blocks of h0: chunk c2 = [block 0 | block 1], block = [hi | lo] nr × 32
-            bulk_g2s(sB2 + st * b2_b, pool8 + 4 * t.b2_off + (int64_t)c2 * t.n2 * BK * 2 * 2 + (int64_t)r0 * BK * 2 * 2,
-                     bytes2, &b2_full[st]);
-          }
-      };
       for (int ct = blockIdx.x; ct < ntask; ct += G) {
         const LrTcTask t = tasks[ct];
         const uint32_t bytes1 = (uint32_t)t.n1 * BK * 2 * 2;
         for (int c = 0; c < t.nk1; ++c, ++j) {
-          const int st = j % BF_SB;
-          if (j >= BF_SB) mbar_wait(&b1_empty[st], ((j / BF_SB) - 1) & 1);
-          mbar_expect_tx(&b1_full[st], bytes1);
-          bulk_g2s(sB1 + st * b1_b, pool8 + 4 * t.b1_off + (int64_t)c * bytes1, bytes1, &b1_full[st]);
+          const int st = j % S1;
+          if (j >= S1) mbar_wait(&empty[st], ((j / S1) - 1) & 1);
+          mbar_expect_tx(&b_full[st], bytes1);
+          bulk_g2s(sbase + st * stage_b + 2 * A_PL, pool8 + 4 * t.b1_off + (int64_t)c * bytes1, bytes1, &b_full[st]);
         }
-        if (have_prev) load_b2(tprev);
-        tprev = t;
-        have_prev = true;
+        const int nk2 = (t.n1 + BK - 1) / BK;
+        const uint32_t bytes2 = (uint32_t)t.n2 * BK * 2 * 2;
+        for (int c2 = 0; c2 < nk2; ++c2, ++b2j) {
+          const int st = b2j & 1;
+          if (b2j >= 2) mbar_wait(&b2_empty[st], ((b2j >> 1) - 1) & 1);
+          mbar_expect_tx(&b2_full[st], bytes2);
+          bulk_g2s(sB2 + st * b2_b, pool8 + 4 * t.b2_off + (int64_t)c2 * bytes2, bytes2, &b2_full[st]);
+        }
       }
-      if (have_prev) load_b2(tprev);
     }
   } else if (warp == TCW_RW) {
-    // ---------------- MMA issuer: phase 1 of task i into D1[i & 1], then phase 2 of task i − 1
-    // (so the epilogue's D1 → A2 conversion of task i − 1 overlaps task i's phase-1 MMAs)
+    // ---------------- MMA issuer
     if (lane == 0) {
       int j = 0, b2j = 0, i = 0;
-      LrTcTask tprev{};
-      auto phase2 = [&](const LrTcTask& t, int ip) {   // task number ip (its A2 is ready)
-        const int N1 = t.n1, N2 = t.n2, nk2 = (N1 + BK - 1) / BK, h0 = half_rows(N2);
-        mbar_wait(&a2_full, ip & 1);
-        if (ip >= 1) mbar_wait(&y_free, (ip - 1) & 1);   // D2 of the previous task was drained
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-        for (int c2 = 0; c2 < nk2; ++c2)
-          for (int hh = 0; hh < 2; ++hh, ++b2j) {
-            const int r0 = hh ? h0 : 0, nr = hh ? N2 - h0 : h0;
-            const int st = b2j & 1;
-            mbar_wait(&b2_full[st], (b2j >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-            const uint32_t b_hi = smem_u32(sB2 + st * b2_b), b_lo = b_hi + nr * BK * 2;
-            const uint32_t a_hi = smem_u32(sA2 + c2 * 2 * A_PL), a_lo = a_hi + A_PL;
-            const uint32_t idesc = idesc_bf16(nr);
-#pragma unroll
-            for (int s = 0; s < BK / 16; ++s) {
-              if (c2 * BK + 16 * s >= N1) break;
-              const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (nr / 8) * 128);
-              const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
-              const uint64_t Bh = make_desc(b_hi + bo, (nr / 8) * 128, 128), Bl = make_desc(b_lo + bo, (nr / 8) * 128, 128);
-              mma_bf16(tY + r0, Ah, Bh, idesc, (c2 > 0 || s > 0) ? 1u : 0u);
-              mma_bf16(tY + r0, Ah, Bl, idesc, 1u);
-              mma_bf16(tY + r0, Al, Bh, idesc, 1u);
-            }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                             smem_u32(&b2_empty[st]))
-                         : "memory");
-          }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                         smem_u32(&d2_full))
-                     : "memory");
-      };
       for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
         const LrTcTask t = tasks[ct];
-        const int N1 = t.n1, K1 = 2 * t.T;
+        const int N1 = t.n1, N2 = t.n2, K1 = 2 * t.T, nk2 = (N1 + BK - 1) / BK;
         const uint32_t idesc1 = idesc_bf16(N1);
-        const uint32_t tD1 = tmem + (uint32_t)((i & 1) * n1max);
         for (int c = 0; c < t.nk1; ++c, ++j) {
-          const int st = j % S1, sb = j % BF_SB;
+          const int st = j % S1;
           mbar_wait(&a_full[st], (j / S1) & 1);
-          mbar_wait(&b1_full[sb], (j / BF_SB) & 1);
+          mbar_wait(&b_full[st], (j / S1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-          const uint32_t a_hi = smem_u32(sbase + st * 2 * A_PL), a_lo = a_hi + A_PL;
-          const uint32_t b_hi = smem_u32(sB1 + sb * b1_b), b_lo = b_hi + N1 * BK * 2;
+          const uint8_t* sA = sbase + st * stage_b;
+          const uint32_t a_hi = smem_u32(sA), a_lo = a_hi + A_PL;
+          const uint32_t b_hi = smem_u32(sA + 2 * A_PL), b_lo = b_hi + N1 * BK * 2;
 #pragma unroll
           for (int s = 0; s < BK / 16; ++s) {
             if (c * BK + 16 * s >= K1) break;
             const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (N1 / 8) * 128);
             const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
             const uint64_t Bh = make_desc(b_hi + bo, (N1 / 8) * 128, 128), Bl = make_desc(b_lo + bo, (N1 / 8) * 128, 128);
-            mma_bf16(tD1, Ah, Bh, idesc1, (c > 0 || s > 0) ? 1u : 0u);
-            mma_bf16(tD1, Ah, Bl, idesc1, 1u);
-            mma_bf16(tD1, Al, Bh, idesc1, 1u);
+            mma_bf16(tmem, Ah, Bh, idesc1, (c > 0 || s > 0) ? 1u : 0u);
+            mma_bf16(tmem, Ah, Bl, idesc1, 1u);
+            mma_bf16(tmem, Al, Bh, idesc1, 1u);
           }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                            smem_u32(&empty[st]))
                        : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&d1_full))
+                     : "memory");
+        mbar_wait(&a2_full, i & 1);                   // tmp is in shared memory (and D1 was read)
+        if (i >= 1) mbar_wait(&y_free, (i - 1) & 1);  // D2 of the previous task was drained
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        for (int c2 = 0; c2 < nk2; ++c2, ++b2j) {
+          const int st = b2j & 1;
+          mbar_wait(&b2_full[st], (b2j >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+          const uint32_t b_hi = smem_u32(sB2 + st * b2_b), b_lo = b_hi + N2 * BK * 2;
+          const uint32_t a_hi = smem_u32(sA2 + c2 * 2 * A_PL), a_lo = a_hi + A_PL;
+#pragma unroll
+          for (int s = 0; s < BK / 16; ++s) {
+            if (c2 * BK + 16 * s >= N1) break;
+            const uint32_t ao = (uint32_t)(s * 2 * 16 * 128), bo = (uint32_t)(s * 2 * (N2 / 8) * 128);
+            const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
+            for (int n0 = 0; n0 < N2; n0 += 256) {
+              const int nn = min(256, N2 - n0);
+              const uint32_t idesc = idesc_bf16(nn);
+              const uint32_t no = (uint32_t)((n0 / 8) * 128);
+              const uint64_t Bh = make_desc(b_hi + bo + no, (N2 / 8) * 128, 128);
+              const uint64_t Bl = make_desc(b_lo + bo + no, (N2 / 8) * 128, 128);
+              mma_bf16(tY + n0, Ah, Bh, idesc, (c2 > 0 || s > 0) ? 1u : 0u);
+              mma_bf16(tY + n0, Ah, Bl, idesc, 1u);
+              mma_bf16(tY + n0, Al, Bh, idesc, 1u);
+            }
+          }
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                           smem_u32(&b1_empty[sb]))
+                           smem_u32(&b2_empty[st]))
                        : "memory");
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                         smem_u32(&d1_full[i & 1]))
+                         smem_u32(&d2_full))
                      : "memory");
-        if (i >= 1) phase2(tprev, i - 1);
-        tprev = t;
       }
-      if (i >= 1) phase2(tprev, i - 1);
     }
-  } else if (warp < 4) {
-    // ---------------- gather warps 0-3 (thread = op row): 16-byte cp.async of the four k-groups of
-    // every 32-element job from both bf16 planes, S1 − 2 jobs ahead; a_full when a job has landed
-    const int row = tid;
+  } else {
+    // ---------------- row warps: thread (row = tid & 127, half h = tid >> 7); half h gathers the
+    // k-groups {2h, 2h+1} (8 bf16 each) of each 32-element job from both planes and converts /
+    // drains the 16-column TMEM blocks b ≡ h (mod 2)
+    const int row = tid & 127, h = tid >> 7;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     int it = blockIdx.x, ic = 0, js = 0;
     LrTcTask ti = tasks[it];
     int64_t isp = row < ti.op_count ? 2 * src_off[ti.op_begin + row] : -1;   // bf16 element offset
@@ -839,10 +807,11 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
       if (it < ntask) {
         const int st = js % S1;
         if (js >= S1) mbar_wait(&empty[st], ((js / S1) - 1) & 1);
-        uint8_t* sA = sbase + st * 2 * A_PL;
+        uint8_t* sA = sbase + st * stage_b;
         const int K2 = 2 * ti.T;
 #pragma unroll
-        for (int kg = 0; kg < 4; ++kg) {
+        for (int q = 0; q < 2; ++q) {
+          const int kg = 2 * h + q;
           const int k = ic * BK + 8 * kg;
           const int nb = isp >= 0 ? 2 * min(8, max(0, K2 - k)) : 0;
           const int so = ((kg * 16 + (row >> 3)) * 8 + (row & 7)) * 16;
@@ -862,32 +831,44 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
       asm volatile("cp.async.commit_group;\n" ::);
     };
     for (int q = 0; q < LA; ++q) issue_next();
-    int jc = 0;
-    for (int ct = blockIdx.x; ct < ntask; ct += G) {
-      const int nk = tasks[ct].nk1;
-      for (int c = 0; c < nk; ++c, ++jc) {
+    int jc = 0, i = 0;
+    LrTcTask tp{};
+    auto drain = [&](const LrTcTask& t) {
+      float2* d = row < t.op_count ? dst + dst_off[t.op_begin + row] : nullptr;
+      for (int c0 = 16 * h; c0 < t.n2; c0 += 32) {
+        float w[16];
+        tmem_ld16(tY + lane_base + c0, w);
+        if (d) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = c0 / 2 + 2 * q;   // complex rows (r, r+1); r+1 = T is the padding slot
+            if (r < t.T)
+              atomicAdd(reinterpret_cast<float4*>(d + r), make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      mbar_arrive(&y_free);
+    };
+    for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
+      const LrTcTask t = tasks[ct];
+      for (int c = 0; c < t.nk1; ++c, ++jc) {
         issue_next();
         asm volatile("cp.async.wait_group %0;\n" ::"n"(LA) : "memory");
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_arrive(&a_full[jc % S1]);
       }
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  } else {
-    // ---------------- epilogue warps 4-7 (thread = op row = TMEM lane): D1 → bf16 hi / lo phase-2
-    // A operand, then D2 → destination states (16-byte vector atomics), overlapping the next
-    // task's phase-1 MMAs
-    const int row = tid - 128;
-    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    int i = 0;
-    for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
-      const LrTcTask t = tasks[ct];
-      mbar_wait(&d1_full[i & 1], (i >> 1) & 1);
+      if (i >= 1) {                                // D2 of the previous task → destination states
+        mbar_wait(&d2_full, (i - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        drain(tp);
+      }
+      mbar_wait(&d1_full, i & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-      const uint32_t tD1 = tmem + (uint32_t)((i & 1) * n1max);
-      for (int c0 = 0; c0 < t.n1; c0 += 16) {
+      // D1 (fp32, row = op, columns = 2r interleaved) → bf16 hi / lo phase-2 A operand
+      for (int c0 = 16 * h; c0 < t.n1; c0 += 32) {
         float w[16];
-        tmem_ld16(tD1 + lane_base + c0, w);
+        tmem_ld16(tmem + lane_base + c0, w);
         uint8_t* ch = sA2 + (c0 / BK) * 2 * A_PL;
 #pragma unroll
         for (int g8 = 0; g8 < 2; ++g8) {
@@ -902,60 +883,41 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       mbar_arrive(&a2_full);
-      s_doff[row] = row < t.op_count ? dst_off[t.op_begin + row] : -1;
-      mbar_wait(&d2_full, i & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-      // D2 → destination states, 32 columns (16 complex = 128 B per op) at a time, transposed
-      // through shared memory (the A2 region is free until the next conversion) so that each
-      // RED.128 warp instruction covers 4 ops × 128 contiguous bytes instead of 32 scattered 16 B
-      float* buf = reinterpret_cast<float*>(sA2);   // 128 rows × 36 floats
-      for (int c0 = 0; c0 < t.n2; c0 += 32) {
-        float w[32];
-        tmem_ld16(tY + lane_base + c0, w);
-        tmem_ld16(tY + lane_base + c0 + 16, w + 16);
-        float4* br = reinterpret_cast<float4*>(buf + row * 36);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) br[q] = make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
-        const int seg = lane & 7, r = c0 / 2 + 2 * seg;   // complex rows (r, r+1); r+1 = T: padding slot
-#pragma unroll 2
-        for (int it = 0; it < 8; ++it) {
-          const int op = 32 * (warp & 3) + 4 * it + (lane >> 3);
-          const int64_t doff = s_doff[op];
-          if (doff >= 0 && r < t.T)
-            atomicAdd(reinterpret_cast<float4*>(dst + doff + r), reinterpret_cast<const float4*>(buf + op * 36)[seg]);
-        }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
-      mbar_arrive(&y_free);
+      tp = t;
     }
+    if (i >= 1) {
+      mbar_wait(&d2_full, (i - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      drain(tp);
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
 }
 
-// plan of one k_m2l_bf launch: an A ring of S1 jobs (16 KB each), the B1 ring (3 × n1max × 128 B),
-// the B2 half-tile ring (2 × ⌈n2max/2⌉₁₆ × 128 B) and the phase-2 A region, ≤ 220 KB
+// plan of one k_m2l_bf launch: ring stages of one 32-element job (A hi|lo 16 KB + B1 hi|lo),
+// a 2-stage B2 ring and the phase-2 A region, ≤ 220 KB
 LrTcPlan m2l_bf_plan(int n1max, int n2max) {
   LrTcPlan pl;
-  pl.stage_fl = n1max * BK * 2 * 2 / 4;                              // B1 stage (floats)
-  pl.b2_fl = (((n2max / 2 + 15) / 16) * 16) * BK * 2 * 2 / 4;        // B2 half-tile stage (floats)
-  // phase-2 A region, also the drain's transpose buffer (128 × 36 floats)
-  const size_t a2 = std::max((size_t)((n1max + BK - 1) / BK) * 2 * 128 * BK * 2, (size_t)128 * 36 * 4);
-  const size_t fixed = (size_t)BF_SB * pl.stage_fl * 4 + 2 * (size_t)pl.b2_fl * 4 + a2 + 1024;
-  const int s = (int)((220 * 1024 - fixed) / (2 * 128 * BK * 2));
-  pl.stages = s >= 10 ? 10 : (s >= 8 ? 8 : (s >= 6 ? 6 : (s >= 5 ? 5 : 4)));
-  pl.smem = (size_t)pl.stages * 2 * 128 * BK * 2 + fixed;
-  pl.ncols = tmem_cols(2 * n1max + n2max);   // two D1 regions + D2
+  pl.stage_fl = (2 * 128 * BK * 2 + n1max * BK * 2 * 2) / 4;   // (in floats)
+  pl.b2_fl = (n2max * BK * 2 * 2) / 4;
+  const size_t a2 = (size_t)((n1max + BK - 1) / BK) * 2 * 128 * BK * 2 / 4;
+  const size_t cap = (220 * 1024 - 1024) / 4 - 2 * (size_t)pl.b2_fl - a2;
+  const int s = (int)(cap / pl.stage_fl);
+  pl.stages = s >= 8 ? 8 : (s >= 6 ? 6 : (s >= 5 ? 5 : (s >= 4 ? 4 : 3)));
+  pl.smem = ((size_t)pl.stages * pl.stage_fl + 2 * (size_t)pl.b2_fl + a2) * 4 + 1024;
+  pl.ncols = tmem_cols(n1max + n2max);
   pl.n1max = n1max;
   return pl;
 }
 cudaError_t m2l_bf_prepare() {
-  cudaError_t e = cudaSuccess;
-  for (auto f : {k_m2l_bf<4>, k_m2l_bf<5>, k_m2l_bf<6>, k_m2l_bf<8>, k_m2l_bf<10>})
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(k_m2l_bf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_bf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_bf<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_bf<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_bf<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   return e;
 }
 void launch_m2l_bf(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
@@ -966,11 +928,11 @@ void launch_m2l_bf(int ntask, const LrTcTask* tasks, const int64_t* src_off, con
   k_m2l_bf<S><<<grid, TCW_NT, pl.smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, shi, slo, dst, pl.stage_fl * 4, \
                                          pl.b2_fl * 4, pl.n1max, pl.ncols)
   switch (pl.stages) {
-    case 10: TBF(10); break;
     case 8: TBF(8); break;
     case 6: TBF(6); break;
     case 5: TBF(5); break;
-    default: TBF(4); break;
+    case 4: TBF(4); break;
+    default: TBF(3); break;
   }
 #undef TBF
 }
