@@ -165,12 +165,18 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
       }
       const size_t pool_dev_size = pl.pool.size();
       build_operators(ctx->g, ctx->p, ctx->t, pl, done, lr);
-      if (ctx->pool_dev) {   // append the host-side part (the §4.2 factors) to the device pool
+      if (ctx->pool_dev) {   // the host-side part into the device pool: the §4.2 factors appended at the
+                             // end, and any matrix the device build left to the host (HF-leaf S2M / L2T)
         if ((int64_t)pl.pool.size() > ctx->pool_dev_cap) throw std::runtime_error("device pool capacity exceeded");
-        if (pl.pool.size() > pool_dev_size &&
-            cudaMemcpy(static_cast<float2*>(ctx->pool_dev) + pool_dev_size, pl.pool.data() + pool_dev_size,
-                       (pl.pool.size() - pool_dev_size) * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess)
-          throw std::runtime_error("upload of the §4.2 factors failed");
+        float2* dp = static_cast<float2*>(ctx->pool_dev);
+        auto up = [&](size_t off, size_t cnt) {
+          if (cnt && cudaMemcpy(dp + off, pl.pool.data() + off, cnt * sizeof(float2), cudaMemcpyHostToDevice) !=
+                         cudaSuccess)
+            throw std::runtime_error("upload of host-built matrices failed");
+        };
+        up(pool_dev_size, pl.pool.size() - pool_dev_size);
+        for (size_t id = 0; id < done.size(); ++id)
+          if (!done[id] && pl.mats[id].rows > 0) up((size_t)pl.mats[id].offset, (size_t)pl.mats[id].rows * pl.mats[id].cols);
       }
       phase("operators");
       // §4.2: route the M2L ops whose K̃ was factored (r < T/2) to the two-stage path
