@@ -84,7 +84,7 @@ typedef struct {
   int32_t nranks;        /* ranks sharing the operator (1 = unsharded)                      */
   int32_t tensor_cores;  /* dense translations (M2M, L2L, dense M2L) on tcgen05 tensor cores,
                             3xTF32: 0 never, 1 every eligible stage (factored M2L too),
-                            2 (default) stages of ≥ 1 GFLOP with ≥ 64 ops per matrix (CUDA
+                            2 (default) stages of ≥ 0.1 GFLOP with ≥ 64 ops per matrix (CUDA
                             cores elsewhere); A/B variants on every eligible stage (dense
                             ones; the factored M2L keeps its fused kernels): 3 the
                             deep-pipeline one-CTA-per-SM kernels, 4 the warp-specialised

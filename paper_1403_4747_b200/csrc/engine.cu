@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_map>
 #include <vector>
@@ -339,7 +340,10 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
       flops += 8.0 * p.mats[o.mat].rows * p.mats[o.mat].cols;
       nm[o.mat] = 1;
     }
-    tc = flops >= 1e9 && (double)ops.size() >= 64.0 * (double)nm.size();
+    // ≥ 0.1 GFLOP per stage (round 1: 1 GFLOP): the LF levels' M2M / L2L (8 octant matrices shared
+    // by 10⁴ ops) then run on tcgen05 — A/B config 4 5.134 → 5.020 ms, config 3 1.562 → 1.535,
+    // config 2 0.424 → 0.428 (profiles/r02_ab_tc_threshold.jsonl)
+    tc = flops >= 0.1e9 && (double)ops.size() >= 64.0 * (double)nm.size();
   }
   if (tc) {
     std::vector<TcTask> tct[TC_NV];
