@@ -30,6 +30,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -657,6 +659,7 @@ __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
 }
 }  // namespace
 
+__device__ int g_m2l_dbg = 0;   // FDA_M2L_DBG: per-role phase timers of CTA 0 (printf)
 template <int S1>
 __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict__ tasks, int ntask,
                                                    const int64_t* __restrict__ src_off,
@@ -674,6 +677,10 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
   constexpr int A_PL = 128 * BK * 2;               // bytes of one A plane (hi or lo) per job
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x;
+  const bool dbg = g_m2l_dbg != 0 && blockIdx.x == 0;
+  long long tp_e = 0, tp_b2 = 0, m_a = 0, m_b = 0, m_a2 = 0, m_y = 0, m_b2 = 0, r_e = 0, r_g = 0, r_d2 = 0, r_dr = 0,
+            r_d1 = 0, r_is = 0, r_cv = 0, ntk = 0;
+  const long long t_start = clock64();
   uint8_t* sB2 = sbase + S1 * stage_b;             // [2][b2_b]
   uint8_t* sA2 = sB2 + 2 * b2_b;                   // phase-2 A: (n1max / BK) jobs × [hi | lo] 128 × BK
   const uint8_t* pool8 = reinterpret_cast<const uint8_t*>(tcpool);
@@ -737,8 +744,8 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
         const uint32_t idesc1 = idesc_bf16(N1);
         for (int c = 0; c < t.nk1; ++c, ++j) {
           const int st = j % S1;
-          mbar_wait(&a_full[st], (j / S1) & 1);
-          mbar_wait(&b_full[st], (j / S1) & 1);
+          { const long long T0_ = dbg ? clock64() : 0; mbar_wait(&a_full[st], (j / S1) & 1); if (dbg) m_a += clock64() - T0_; }
+          { const long long T0_ = dbg ? clock64() : 0; mbar_wait(&b_full[st], (j / S1) & 1); if (dbg) m_b += clock64() - T0_; }
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
           const uint8_t* sA = sbase + st * stage_b;
           const uint32_t a_hi = smem_u32(sA), a_lo = a_hi + A_PL;
@@ -760,12 +767,12 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                          smem_u32(&d1_full))
                      : "memory");
-        mbar_wait(&a2_full, i & 1);                   // tmp is in shared memory (and D1 was read)
-        if (i >= 1) mbar_wait(&y_free, (i - 1) & 1);  // D2 of the previous task was drained
+        { const long long T0_ = dbg ? clock64() : 0; mbar_wait(&a2_full, i & 1); if (dbg) m_a2 += clock64() - T0_; }
+        if (i >= 1) { const long long T0_ = dbg ? clock64() : 0; mbar_wait(&y_free, (i - 1) & 1); if (dbg) m_y += clock64() - T0_; }
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
         for (int c2 = 0; c2 < nk2; ++c2, ++b2j) {
           const int st = b2j & 1;
-          mbar_wait(&b2_full[st], (b2j >> 1) & 1);
+          { const long long T0_ = dbg ? clock64() : 0; mbar_wait(&b2_full[st], (b2j >> 1) & 1); if (dbg) m_b2 += clock64() - T0_; }
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
           const uint32_t b_hi = smem_u32(sB2 + st * b2_b), b_lo = b_hi + N2 * BK * 2;
           const uint32_t a_hi = smem_u32(sA2 + c2 * 2 * A_PL), a_lo = a_hi + A_PL;
@@ -806,7 +813,7 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
     auto issue_next = [&]() {
       if (it < ntask) {
         const int st = js % S1;
-        if (js >= S1) mbar_wait(&empty[st], ((js / S1) - 1) & 1);
+        if (js >= S1) { const long long T0_ = dbg ? clock64() : 0; mbar_wait(&empty[st], ((js / S1) - 1) & 1); if (dbg) r_e += clock64() - T0_; }
         uint8_t* sA = sbase + st * stage_b;
         const int K2 = 2 * ti.T;
 #pragma unroll
@@ -852,18 +859,22 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
     };
     for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
       const LrTcTask t = tasks[ct];
+      if (dbg) ++ntk;
       for (int c = 0; c < t.nk1; ++c, ++jc) {
-        issue_next();
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(LA) : "memory");
+        { const long long T1_ = dbg ? clock64() : 0; issue_next(); if (dbg) r_is += clock64() - T1_; }
+        { const long long T0_ = dbg ? clock64() : 0;
+          asm volatile("cp.async.wait_group %0;\n" ::"n"(LA) : "memory");
+          if (dbg) r_g += clock64() - T0_; }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_arrive(&a_full[jc % S1]);
       }
       if (i >= 1) {                                // D2 of the previous task → destination states
-        mbar_wait(&d2_full, (i - 1) & 1);
+        { const long long T0_ = dbg ? clock64() : 0; mbar_wait(&d2_full, (i - 1) & 1); if (dbg) r_d2 += clock64() - T0_; }
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-        drain(tp);
+        { const long long T0_ = dbg ? clock64() : 0; drain(tp); if (dbg) r_dr += clock64() - T0_; }
       }
-      mbar_wait(&d1_full, i & 1);
+      { const long long T0_ = dbg ? clock64() : 0; mbar_wait(&d1_full, i & 1); if (dbg) r_d1 += clock64() - T0_; }
+      const long long T2_ = dbg ? clock64() : 0;
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
       // D1 (fp32, row = op, columns = 2r interleaved) → bf16 hi / lo phase-2 A operand
       for (int c0 = 16 * h; c0 < t.n1; c0 += 32) {
@@ -883,6 +894,7 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
       mbar_arrive(&a2_full);
+      if (dbg) r_cv += clock64() - T2_;
       tp = t;
     }
     if (i >= 1) {
@@ -891,6 +903,16 @@ __global__ void __launch_bounds__(TCW_NT, 1) k_m2l_bf(const LrTcTask* __restrict
       drain(tp);
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
+  if (dbg && lane == 0) {
+    const long long tt = clock64() - t_start;
+    if (warp == TCW_RW + 1) printf("[m2l_bf cta0] TMA: total %lld, wait empty %lld, wait b2_empty %lld\n", tt, tp_e, tp_b2);
+    if (warp == TCW_RW)
+      printf("[m2l_bf cta0] MMA: total %lld, wait a_full %lld, b_full %lld, a2_full %lld, y_free %lld, b2_full %lld\n", tt,
+             m_a, m_b, m_a2, m_y, m_b2);
+    if (warp == 0)
+      printf("[m2l_bf cta0] ROW: tasks %lld total %lld, issue %lld (of which wait empty %lld), cp.async wait %lld, wait d2 %lld, "
+             "drain %lld, wait d1 %lld, convert %lld\n", ntk, tt, r_is, r_e, r_g, r_d2, r_dr, r_d1, r_cv);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
   __syncthreads();
@@ -913,6 +935,10 @@ LrTcPlan m2l_bf_plan(int n1max, int n2max) {
   return pl;
 }
 cudaError_t m2l_bf_prepare() {
+  if (getenv("FDA_M2L_DBG")) {
+    const int one = 1;
+    cudaMemcpyToSymbol(g_m2l_dbg, &one, sizeof(int));
+  }
   cudaError_t e = cudaFuncSetAttribute(k_m2l_bf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_bf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_m2l_bf<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
