@@ -12,6 +12,7 @@
 // the entries are evaluated here (host build) or by build_dev.cu (device build,
 // the same definitions in fp64 on the GPU).
 #include <algorithm>
+#include <parallel/algorithm>
 #include <cmath>
 #include <unordered_map>
 
@@ -37,45 +38,62 @@ void correction_pairs(const Geometry& g, const Params& p, std::vector<int64_t>& 
   auto hkey = [](int64_t a, int64_t b, int64_t d) {
     return (uint64_t)((a & 0x1fffff) | ((b & 0x1fffff) << 21) | ((d & 0x1fffff) << 42));
   };
-  std::unordered_map<uint64_t, std::vector<int64_t>> grid;
+  // uniform grid: elements sorted by cell key (parallel sort), cell → [begin, end) in that order
+  std::vector<std::pair<uint64_t, int64_t>> ce(n);
+#pragma omp parallel for schedule(static)
   for (int64_t j = 0; j < n; ++j) {
     int64_t a, b, d;
     cidx(g.centroid[j], a, b, d);
-    grid[hkey(a, b, d)].push_back(j);
+    ce[j] = {hkey(a, b, d), j};
   }
-  std::vector<std::vector<std::pair<int64_t, int8_t>>> rows(n);
-#pragma omp parallel for schedule(dynamic, 256)
-  for (int64_t i = 0; i < n; ++i) {
-    if (i < row0 || i >= row1) continue;   // another rank's row (sharded build)
+  __gnu_parallel::sort(ce.begin(), ce.end());
+  std::unordered_map<uint64_t, std::pair<int64_t, int64_t>> grid;
+  for (int64_t q = 0; q < n;) {
+    int64_t r = q;
+    while (r < n && ce[r].first == ce[q].first) ++r;
+    grid.emplace(ce[q].first, std::make_pair(q, r));
+    q = r;
+  }
+  // two passes over the rows: count, then fill the CSR in place (no per-row vectors)
+  auto scan = [&](int64_t i, auto&& emit) {
     const Vec3& x = g.centroid[i];
     int64_t a, b, d;
     cidx(x, a, b, d);
-    auto& row = rows[i];
     for (int64_t da = -1; da <= 1; ++da)
       for (int64_t db = -1; db <= 1; ++db)
         for (int64_t dd = -1; dd <= 1; ++dd) {
           auto it = grid.find(hkey(a + da, b + db, d + dd));
           if (it == grid.end()) continue;
-          for (int64_t j : it->second) {
+          for (int64_t q = it->second.first; q < it->second.second; ++q) {
+            const int64_t j = ce[q].second;
             const double rho = (x - g.centroid[j]).norm() / g.hmax[j];
             if (!(rho < t2)) continue;
-            row.push_back({j, (int8_t)(j == i ? 0 : (rho < t1 ? 1 : 2))});
+            emit(j, (int8_t)(j == i ? 0 : (rho < t1 ? 1 : 2)));
           }
         }
-    std::sort(row.begin(), row.end(), [](const auto& u, const auto& v) { return u.first < v.first; });
-  }
+  };
   ptr.assign(n + 1, 0);
-  for (int64_t i = 0; i < n; ++i) ptr[i + 1] = ptr[i] + (int64_t)rows[i].size();
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t i = 0; i < n; ++i) {
+    if (i < row0 || i >= row1) continue;   // another rank's row (sharded build)
+    int64_t c = 0;
+    scan(i, [&](int64_t, int8_t) { ++c; });
+    ptr[i + 1] = c;
+  }
+  for (int64_t i = 0; i < n; ++i) ptr[i + 1] += ptr[i];
   col.resize(ptr[n]);
   tier.resize(ptr[n]);
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(dynamic, 256)
   for (int64_t i = 0; i < n; ++i) {
-    int64_t o = ptr[i];
-    for (size_t e = 0; e < rows[i].size(); ++e) {
-      col[o + e] = rows[i][e].first;
-      tier[o + e] = rows[i][e].second;
+    if (i < row0 || i >= row1) continue;
+    std::vector<std::pair<int64_t, int8_t>> row;
+    row.reserve(ptr[i + 1] - ptr[i]);
+    scan(i, [&](int64_t j, int8_t tr) { row.push_back({j, tr}); });
+    std::sort(row.begin(), row.end(), [](const auto& u, const auto& v) { return u.first < v.first; });
+    for (size_t e = 0; e < row.size(); ++e) {
+      col[ptr[i] + e] = row[e].first;
+      tier[ptr[i] + e] = row[e].second;
     }
-    std::vector<std::pair<int64_t, int8_t>>().swap(rows[i]);
   }
 }
 

@@ -591,9 +591,14 @@ fda_status engine_create(Context* ctx) {
     ctx->err = "table too large for 32-bit indices";
     return FDA_E_INTERNAL;
   }
-  std::vector<int32_t> cptr(p.corr_ptr.begin(), p.corr_ptr.end()), ccol(p.corr_col.begin(), p.corr_col.end());
+  std::vector<int32_t> cptr(p.corr_ptr.size()), ccol(p.corr_col.size());
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)cptr.size(); ++i) cptr[i] = (int32_t)p.corr_ptr[i];
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)ccol.size(); ++i) ccol[i] = (int32_t)p.corr_col[i];
   // LPT order of the near-field CTAs: estimated work = targets × (3·sources + corrections)
   std::vector<int64_t> work(nleaf, 0), nsrc(nleaf, 0);
+#pragma omp parallel for schedule(static)
   for (int i = 0; i < nleaf; ++i) {
     const Box& B = t.boxes[t.leaves[i]];
     for (int64_t e = p.near_ptr[i]; e < p.near_ptr[i + 1]; ++e) {
@@ -606,18 +611,23 @@ fda_status engine_create(Context* ctx) {
   for (int i = 0; i < nleaf; ++i)   // sharded: this rank evaluates the near field of its own leaves only
     if (i >= p.own_leaf0 && i < p.own_leaf1) order.push_back(i);
   std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return work[a] > work[b]; });
-  std::vector<NearTask> ntask;
-  std::vector<int2> slots;
-  for (int32_t i : order) {
+  // slot table: per task (LPT order) the source elements of all its direct leaves (prefix sums,
+  // then filled in parallel)
+  std::vector<NearTask> ntask(order.size());
+  std::vector<int64_t> sbeg(order.size() + 1, 0);
+  for (size_t q = 0; q < order.size(); ++q) sbeg[q + 1] = sbeg[q] + nsrc[order[q]];
+  if (sbeg.back() >= (int64_t)INT32_MAX) { ctx->err = "near-field slot table too large"; return FDA_E_INTERNAL; }
+  std::vector<int2> slots((size_t)sbeg.back());
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t q = 0; q < (int64_t)order.size(); ++q) {
+    const int32_t i = order[q];
     const Box& B = t.boxes[t.leaves[i]];
-    NearTask nt{(int32_t)B.begin, (int32_t)(B.end - B.begin), (int32_t)slots.size(), 0};
+    int64_t o = sbeg[q];
     for (int64_t e = p.near_ptr[i]; e < p.near_ptr[i + 1]; ++e) {
       const Box& C = t.boxes[t.leaves[p.near_idx[e]]];
-      for (int64_t el = C.begin; el < C.end; ++el) slots.push_back(make_int2((int)el, (int)e));
+      for (int64_t el = C.begin; el < C.end; ++el) slots[o++] = make_int2((int)el, (int)e);
     }
-    if (slots.size() >= (size_t)INT32_MAX) { ctx->err = "near-field slot table too large"; return FDA_E_INTERNAL; }
-    nt.s1 = (int32_t)slots.size();
-    ntask.push_back(nt);
+    ntask[q] = NearTask{(int32_t)B.begin, (int32_t)(B.end - B.begin), (int32_t)sbeg[q], (int32_t)sbeg[q + 1]};
   }
   d->n_near = (int)order.size();
   // 256-thread near CTAs pay when a target leaf sees many direct sources (kernels.cu)

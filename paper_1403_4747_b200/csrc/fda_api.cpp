@@ -14,8 +14,8 @@
 
 using namespace fda;
 
-template <class T>
-static fda_status put(const std::vector<T>& v, void* dst, int64_t* count, int32_t* eb) {
+template <class T, class A>
+static fda_status put(const std::vector<T, A>& v, void* dst, int64_t* count, int32_t* eb) {
   *count = (int64_t)v.size();
   *eb = (int32_t)sizeof(T);
   if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(T));

@@ -5,6 +5,7 @@
 #include <complex>
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 #include <unordered_map>
 
@@ -15,6 +16,22 @@ namespace fda {
 struct Context;
 using cd = std::complex<double>;
 using cf = std::complex<float>;
+
+// allocator that leaves new elements uninitialised (the 20+ GB matrix pool is fully overwritten by
+// the operator build; zero-filling it cost seconds at config 5)
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind { using other = NoInitAlloc<U>; };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) {}
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    if constexpr (sizeof...(Args) > 0) ::new ((void*)p) U(std::forward<Args>(args)...);
+  }
+};
+using PoolVec = std::vector<cf, NoInitAlloc<cf>>;
 
 struct Vec3 {
   double x, y, z;
@@ -171,7 +188,7 @@ struct Plan {
   // matrices
   std::vector<MatInfo> mats;
   std::vector<MatSpec> specs;    // parallel to mats
-  std::vector<cf> pool;          // complex64 matrix pool (column-major per matrix)
+  PoolVec pool;                  // complex64 matrix pool (column-major per matrix), uninitialised until built
 };
 
 struct Params {

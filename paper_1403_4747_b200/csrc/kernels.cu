@@ -319,7 +319,7 @@ void launch_near(int ntask, const NearTask* tasks, const int2* slots, const floa
 // groups split the columns (column c handled by group c mod G), so one warp
 // reads consecutive entries of the column-major matrix; each thread keeps
 // LEAF_U independent loads in flight; the G partial sums meet in shared memory.
-constexpr int LEAF_NT = 256;   // ≥ 2 thread groups per row: twice the loads in flight per CTA
+constexpr int LEAF_NT = 128;
 constexpr int LEAF_U = 8;
 constexpr int LEAF_MAXR = 320;
 

@@ -18,6 +18,7 @@
 //  C18 R_u = minimal rotation taking the wedge centre u to +z; the incoming
 //      state of D is keyed by the antipodal wedge of C's outgoing wedge.
 #include <algorithm>
+#include <parallel/algorithm>
 #include <cmath>
 #include <map>
 #include <numeric>
@@ -69,7 +70,7 @@ void build_tree(Geometry& g, const Params& p, Tree& t) {
   }
   std::vector<int64_t> order(n);
   std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+  __gnu_parallel::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
   // permute geometry into tree order
   auto permute = [&](auto& vec) {
     auto tmp = vec;

@@ -123,7 +123,7 @@ void operator_layout(const Tree& t, Plan& plan, const std::vector<char>& needed)
   }
   plan.pool.clear();
   plan.pool.reserve(off + lr_bound);   // the factors are appended without reallocating
-  plan.pool.assign(off, cf(0, 0));
+  plan.pool.resize(off);               // (uninitialised: every stored matrix is written in full)
 }
 
 // §4.2: K̃ ≈ Û V̂ of one T × T M2L matrix, kept when r < T/2

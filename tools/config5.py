@@ -78,6 +78,7 @@ def main():
     f.matvec(xd, yd)
     torch.cuda.synchronize()
     stages = f.stage_times()
+    kernels = f.kernel_times()
     f.set_profiling(False)
     y = yd.cpu().numpy().astype(np.complex128)
     import oracle as O
@@ -108,6 +109,7 @@ def main():
     print(json.dumps({"config": a.cfg, "N": N, "k": c.k, "mesh_s": round(t_mesh, 1), "build_s": round(t_build, 1),
                       "solve": solve,
                       "matvec_ms": round(mv_ms, 3), "stages_ms": {k: round(v, 3) for k, v in stages.items()},
+                      "kernels_ms": {k: round(v, 3) for k, v in kernels.items()},
                       "sampled_rows": len(rows), "rel_l2_sampled": err, "oracle_rows_s": t_or, "tensor_cores": a.tc,
                       "lr_tensor_cores": a.lrtc, "alpha": str(c.alpha),
                       "oracle_cores": fast.num_threads(), "levels": levels,
