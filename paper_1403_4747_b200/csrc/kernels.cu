@@ -114,12 +114,14 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 //   4π r² e^{-iq} ∂G/∂n_y          = (iq - 1) b
 //   4π r² e^{-iq} ∂²G/∂n_x∂n_y     = (1/r) [ u1 - iq g ]
 // so for α = i α_i (PURE_IMAG; α = i/k):  P = -b + α_i k g,  Q = q b + α_i k (1/q) u1.
-// d = X - Y (wave units), s = d·n_x, t = Y·n_y - X·n_y = -(d·n_y) (Y.w = Y·n_y), ι = 1/q:
+// d = X - Y (wave units), s = d·n_x, t = Y·n_y - X·n_y = -(d·n_y), ι = 1/q; t is the same for
+// the three Q3 points of a (flat) source element — they lie in its plane — so the caller computes
+// it once per element from the plane constant Y·n_y:
 // a = sι, b = tι, ab = st ι², q²ab = st, qb = t — so u1 = g - st and Q = t + α_i k ι u1.
 // The source point Y is the same for both lanes (a broadcast operand); MUFU
 // work (rsqrt, sin, cos) stays per lane.
 template <bool PURE_IMAG>
-__device__ __forceinline__ void lhs_eval2(const f2x* X, const f2x* nx, float4 Y, f2x xny, f2x cn,
+__device__ __forceinline__ void lhs_eval2(const f2x* X, const f2x* nx, float4 Y, f2x t, f2x cn,
                                           const KernelParams& kp, f2x& kr, f2x& ki) {
   const f2x dx = sub2(X[0], bcast2(Y.x)), dy = sub2(X[1], bcast2(Y.y)), dz = sub2(X[2], bcast2(Y.z));
   const f2x q2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
@@ -132,7 +134,6 @@ __device__ __forceinline__ void lhs_eval2(const f2x* X, const f2x* nx, float4 Y,
   __sincosf(qa, &sa, &ca);  // MUFU sin/cos; argument error ≤ ulp(q/2π)
   __sincosf(qb, &sb, &cb);
   const f2x sd = fma2(dx, nx[0], fma2(dy, nx[1], mul2(dz, nx[2])));   // s = d·n_x
-  const f2x t = sub2(bcast2(Y.w), xny);                              // t = -(d·n_y)
   const f2x iq2 = mul2(iq, iq);
   const f2x st = mul2(sd, t);
   const f2x g = fma2(bcast2(3.0f), mul2(st, iq2), cn);   // 3ab + c
@@ -185,8 +186,8 @@ __device__ __forceinline__ void rhs_eval2(const f2x* X, const f2x* nx, float4 Y,
 // coalesced table load per slot.  Each thread owns a PAIR of targets (the two
 // lanes of its packed fp32 registers); P = ⌊NT/⌈n_B/2⌉⌋ threads share one
 // pair and split the sources; partial sums are reduced in shared memory.
-// Staged per source element: the three Q3 points with Y_q·n_y in .w (wave
-// units, shifted into the target leaf's frame), the normal, and
+// Staged per source element: the three Q3 points (wave units, shifted into the
+// target leaf's frame), the normal with the plane constant Y·n_y in .w, and
 // w_j = x_j·k²A_j/(12π).
 // KIND 0: LHS operator A (Eq. 5); KIND 1: RHS operator B (G sources).
 template <int KIND, bool PURE_IMAG, int NEAR_NT, int NEAR_MAXS>
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
     const float4* __restrict__ tgt_pos, const float4* __restrict__ tgt_nrm, const SrcElem* __restrict__ src,
     const float* __restrict__ src_w, const int32_t* __restrict__ corr_ptr, const int32_t* __restrict__ corr_col,
     const float2* __restrict__ corr_val, const float2* __restrict__ x, float2* __restrict__ y, KernelParams kp) {
-  // staged source element s: st[5s..5s+4] = Y0, Y1, Y2 (with Y_q·n_y in .w), (n_y, -), (w_j, -, -)
+  // staged source element s: st[5s..5s+4] = Y0, Y1, Y2, (n_y, Y·n_y), (w_j, -, -)
   __shared__ float4 st[NEAR_MAXS * 5];
   __shared__ float4 sred[NEAR_NT];
   const NearTask t = tasks[blockIdx.x];
@@ -224,13 +225,12 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
       SrcElem se = src[el];
       const float2 xv = x[el];
       const float wv = src_w[el];
-      const float4 n4 = make_float4(se.a.w, se.b.w, se.c.w, 0.f);
-      float4 A = make_float4(se.a.x - off.x, se.a.y - off.y, se.a.z - off.z, 0.f);
-      float4 B = make_float4(se.b.x - off.x, se.b.y - off.y, se.b.z - off.z, 0.f);
-      float4 C = make_float4(se.c.x - off.x, se.c.y - off.y, se.c.z - off.z, 0.f);
-      A.w = fmaf(A.x, n4.x, fmaf(A.y, n4.y, A.z * n4.z));
-      B.w = fmaf(B.x, n4.x, fmaf(B.y, n4.y, B.z * n4.z));
-      C.w = fmaf(C.x, n4.x, fmaf(C.y, n4.y, C.z * n4.z));
+      float4 n4 = make_float4(se.a.w, se.b.w, se.c.w, 0.f);
+      const float4 A = make_float4(se.a.x - off.x, se.a.y - off.y, se.a.z - off.z, 0.f);
+      const float4 B = make_float4(se.b.x - off.x, se.b.y - off.y, se.b.z - off.z, 0.f);
+      const float4 C = make_float4(se.c.x - off.x, se.c.y - off.y, se.c.z - off.z, 0.f);
+      // plane constant Y·n_y of the element, from its centroid (the mean of the Q3 points)
+      n4.w = fmaf(A.x + B.x + C.x, n4.x, fmaf(A.y + B.y + C.y, n4.y, (A.z + B.z + C.z) * n4.z)) * (1.0f / 3.0f);
       float4* d = st + 5 * slot;
       d[0] = A; d[1] = B; d[2] = C; d[3] = n4;
       d[4] = make_float4(xv.x * wv, xv.y * wv, 0.f, 0.f);
@@ -247,9 +247,10 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
           const float4 ny = e[3];
           const f2x cn = fma2(N[0], bcast2(ny.x), fma2(N[1], bcast2(ny.y), mul2(N[2], bcast2(ny.z))));
           const f2x xny = fma2(X[0], bcast2(ny.x), fma2(X[1], bcast2(ny.y), mul2(X[2], bcast2(ny.z))));
-          lhs_eval2<PURE_IMAG>(X, N, A, xny, cn, kp, kr, ki);
-          lhs_eval2<PURE_IMAG>(X, N, B, xny, cn, kp, kr, ki);
-          lhs_eval2<PURE_IMAG>(X, N, C, xny, cn, kp, kr, ki);
+          const f2x tp = sub2(bcast2(ny.w), xny);   // t = Y·n_y − X·n_y (plane constant in ny.w)
+          lhs_eval2<PURE_IMAG>(X, N, A, tp, cn, kp, kr, ki);
+          lhs_eval2<PURE_IMAG>(X, N, B, tp, cn, kp, kr, ki);
+          lhs_eval2<PURE_IMAG>(X, N, C, tp, cn, kp, kr, ki);
         } else {
           rhs_eval2(X, N, A, kp, kr, ki);
           rhs_eval2(X, N, B, kp, kr, ki);
@@ -297,11 +298,13 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
 void launch_near(int ntask, const NearTask* tasks, const int2* slots, const float4* near_off, const float4* tgt_pos,
                  const float4* tgt_nrm, const SrcElem* src, const float* src_w, const int32_t* corr_ptr,
                  const int32_t* corr_col, const float2* corr_val, const float2* x, float2* y, KernelParams kp,
-                 bool alpha_pure_imag, int kind, bool wide, cudaStream_t s) {
+                 bool alpha_pure_imag, int kind, bool wide, cudaStream_t s, int* ctr, int grid, bool reset_ctr) {
   if (ntask <= 0) return;
+  if (!ctr) grid = ntask;
+  else if (reset_ctr) cudaMemsetAsync(ctr, 0, sizeof(int), s);
 #define NEAR(K, PI, NT, MS)                                                                                       \
-  k_near<K, PI, NT, MS><<<ntask, NT, 0, s>>>(tasks, slots, near_off, tgt_pos, tgt_nrm, src, src_w, corr_ptr,     \
-                                             corr_col, corr_val, x, y, kp)
+  k_near<K, PI, NT, MS><<<grid, NT, 0, s>>>(tasks, ntask, ctr, slots, near_off, tgt_pos, tgt_nrm, src, src_w,      \
+                                            corr_ptr, corr_col, corr_val, x, y, kp)
   if (wide) {
     if (kind == 1) NEAR(1, false, NEAR_NT_WIDE, NEAR_MAXS_WIDE);
     else if (alpha_pure_imag) NEAR(0, true, NEAR_NT_WIDE, NEAR_MAXS_WIDE);

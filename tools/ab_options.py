@@ -3,6 +3,7 @@
 
     python tools/ab_options.py --config 4 --variants '{}' '{"lr_tensor_cores": 1}' ...
 
+A variant may carry "_env": {...} (environment set before its build).
 One JSON line per variant: matvec ms (mean of --steps), per-kernel-family ms of a
 profiled pass, relative difference of y against the first variant.
 """
@@ -30,8 +31,14 @@ def main():
     x = torch.from_numpy(random_density(len(F), c.x_seed).astype(np.complex64)).cuda()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     y_ref = None
+    prev_env = []
     for vs in a.variants:
         opts = json.loads(vs)
+        env = opts.pop("_env", {})          # build-time environment knobs (engine experiments)
+        for k in prev_env:
+            os.environ.pop(k, None)
+        os.environ.update({k: str(v) for k, v in env.items()})
+        prev_env = list(env)
         f = FDA(V, F, c.k, c.alpha, c.eps, **opts)
         y = torch.empty_like(x)
         for _ in range(5):
@@ -46,6 +53,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
+        near_live = f.near_time()
         f.set_profiling(True)
         f.matvec(x, y)
         torch.cuda.synchronize()
@@ -54,7 +62,7 @@ def main():
         yn = y.cpu().numpy().astype(np.complex128)
         if y_ref is None:
             y_ref = yn
-        print(json.dumps({"config": a.config, "options": opts, "matvec_ms": round(float(np.mean(ts)), 4),
+        print(json.dumps({"config": a.config, "options": opts, "env": env, "near_live_ms": round(near_live, 4), "matvec_ms": round(float(np.mean(ts)), 4),
                           "kernels_ms": kt, "rel_vs_first": float(np.linalg.norm(yn - y_ref) / np.linalg.norm(y_ref)),
                           "build_s": round(f.stats()["t_build_s"], 2)}), flush=True)
         f.close()
