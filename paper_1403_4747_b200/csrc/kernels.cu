@@ -298,13 +298,11 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
 void launch_near(int ntask, const NearTask* tasks, const int2* slots, const float4* near_off, const float4* tgt_pos,
                  const float4* tgt_nrm, const SrcElem* src, const float* src_w, const int32_t* corr_ptr,
                  const int32_t* corr_col, const float2* corr_val, const float2* x, float2* y, KernelParams kp,
-                 bool alpha_pure_imag, int kind, bool wide, cudaStream_t s, int* ctr, int grid, bool reset_ctr) {
+                 bool alpha_pure_imag, int kind, bool wide, cudaStream_t s) {
   if (ntask <= 0) return;
-  if (!ctr) grid = ntask;
-  else if (reset_ctr) cudaMemsetAsync(ctr, 0, sizeof(int), s);
 #define NEAR(K, PI, NT, MS)                                                                                       \
-  k_near<K, PI, NT, MS><<<grid, NT, 0, s>>>(tasks, ntask, ctr, slots, near_off, tgt_pos, tgt_nrm, src, src_w,      \
-                                            corr_ptr, corr_col, corr_val, x, y, kp)
+  k_near<K, PI, NT, MS><<<ntask, NT, 0, s>>>(tasks, slots, near_off, tgt_pos, tgt_nrm, src, src_w, corr_ptr,     \
+                                             corr_col, corr_val, x, y, kp)
   if (wide) {
     if (kind == 1) NEAR(1, false, NEAR_NT_WIDE, NEAR_MAXS_WIDE);
     else if (alpha_pure_imag) NEAR(0, true, NEAR_NT_WIDE, NEAR_MAXS_WIDE);
