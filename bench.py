@@ -48,7 +48,7 @@ SMS, FP32_LANES = 148, 128
 # B200_PROFILING.md nominal dense peaks: TF32 1.1 PFLOP/s vs BF16 2.25 PFLOP/s
 TF32_OVER_BF16 = 1.1 / 2.25
 KERNELS = ["k_gather", "k_near", "k_s2m", "k_xlate", "k_xlate_tc", "k_xlate_tcw", "k_m2l_lr", "k_m2l_tcw", "k_l2t",
-           "k_scatter", "memset"]
+           "k_scatter", "memset", "k_xlate_bf"]
 
 
 def _peaks():
@@ -182,6 +182,8 @@ def _family_work(f, work):
             fam[k] = ("tensor_bf16", fl, "complex-equivalent flops on tcgen05 BF16x3 (k_m2l_bf: 16·r·T per factored op)")
         else:
             fam[k] = ("tensor", fl, "complex-equivalent flops on tcgen05 3xTF32 (8·rows·cols per op)")
+    fl = sum(v for n, v in kf.items() if n.startswith("k_xlate_bf/"))
+    fam["k_xlate_bf"] = ("tensor_bf16", fl, "complex-equivalent flops on tcgen05 BF16x3 (k_xlate_bf: 8·rows·cols per op)")
     fam["k_s2m"] = ("hbm", work["s2m"]["bytes"], "8 B per stored S̃ entry + 16 B per element")
     fam["k_l2t"] = ("hbm", work["l2t"]["bytes"], "8 B per stored T̃ entry + 16 B per element")
     return fam

@@ -88,7 +88,8 @@ typedef struct {
                             cores elsewhere); A/B variants on every eligible stage (dense
                             ones; the factored M2L keeps its fused kernels): 3 the
                             deep-pipeline one-CTA-per-SM kernels, 4 the warp-specialised
-                            persistent kernel for ≤ 2 row tiles                            */
+                            persistent kernel for ≤ 2 row tiles, 5 the BF16x3 persistent
+                            kernel k_xlate_bf (matrices with ≤ 128 rows; unsharded)        */
   int32_t hf_leaves;     /* 0 (default): HF cubes are always split, all leaves are LF (reading
                             C9); 1: the count rule at every level, leaves may be HF, with
                             directional S2M / L2T per used wedge (PAPER.md P:344-346,
@@ -242,7 +243,7 @@ fda_status fda_stage_times(fda_ctx* ctx, double* ms, int32_t* n);
  * one stream of a profiled, serialised matvec: fda_set_profiling(ctx, 1) then
  * fda_matvec(..., FDA_DEVICE, ...) on an unsharded context), summed over the
  * family's launches, in the order [k_gather, k_near, k_s2m, k_xlate,
- * k_xlate_tc, k_xlate_tcw, k_m2l_lr, k_m2l_tcw, k_l2t, k_scatter, memset] —
+ * k_xlate_tc, k_xlate_tcw, k_m2l_lr, k_m2l_tcw, k_l2t, k_scatter, memset, k_xlate_bf] —
  * the launch-list share of each __global__ function.  n = capacity; returns
  * the count written in *n.  FDA_E_STATE before such a matvec. */
 fda_status fda_kernel_times(fda_ctx* ctx, double* ms, int32_t* n);

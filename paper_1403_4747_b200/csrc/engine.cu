@@ -108,6 +108,10 @@ struct XStage {
   int64_t* src = nullptr;
   int64_t* dst = nullptr;
   double fl[3] = {0, 0, 0};        // algorithmic flops (8·rows·cols per op) on k_xlate / k_xlate_tc / k_xlate_tcw
+  XbfTask* bf = nullptr;           // BF16x3 persistent kernel (k_xlate_bf): tasks, CTAs, ring plan
+  int n_bf = 0, grid_bf = 0;
+  LrTcPlan bf_plan;
+  double fl_bf = 0;
 };
 
 // GMRES workspace (engine_solve; cached per context)
@@ -179,7 +183,7 @@ struct Dev {
     int64_t split0 = 0, split1 = 0;  // float range of this level's out-states (bf16 split)
     double fl_lr = 0, fl_lrtc = 0;   // algorithmic flops (16·r·T per factored op) on k_m2l_lr / k_m2l_tcw
     bool any() const {
-      int n = n_lrtc;
+      int n = n_lrtc + dense.n_bf + a.n_bf + b.n_bf;
       for (int c = 0; c < LR_NCLS; ++c) n += n_lr[c];
       for (int v = 0; v < TC_NV; ++v) n += dense.n_tc[v] + a.n_tc[v] + b.n_tc[v];
       for (int q = 0; q < 2; ++q) n += dense.n_tcw[q] + a.n_tcw[q] + b.n_tcw[q];
@@ -210,8 +214,12 @@ struct Dev {
   std::unordered_map<int64_t, int64_t> tc_off;   // matrix id → float offset
   std::unordered_map<int64_t, int64_t> tc_boff;  // matrix id → float offset of its k_m2l_tcw B operand
   std::unordered_map<int64_t, int64_t> tc_bfoff; // … of its k_m2l_bf (bf16) B operand
+  std::unordered_map<int64_t, int64_t> tc_xbfoff; // … of its k_xlate_bf (bf16) B operand
   float* tcpool = nullptr;
-  __nv_bfloat16 *outb_hi = nullptr, *outb_lo = nullptr;   // bf16 hi / lo planes of outb (k_m2l_bf)
+  __nv_bfloat16 *outb_hi = nullptr, *outb_lo = nullptr;   // bf16 hi / lo planes of outb (k_m2l_bf, k_xlate_bf)
+  __nv_bfloat16 *inb_hi = nullptr, *inb_lo = nullptr;     // bf16 hi / lo planes of inb (k_xlate_bf L2L)
+  bool use_xbf = false;            // dense translations on k_xlate_bf (BF16x3)
+  std::vector<char> split_out, split_in;   // per level: split its out- / in-states into bf16 planes on the main stream
   // per-kernel-family device times of a profiled (serialised) matvec: event marks
   // recorded around every launch on the one stream (fda_kernel_times)
   bool kt_on = false;
@@ -222,7 +230,7 @@ struct Dev {
 
 // kernel families of fda_kernel_times (include/fda.h)
 enum KFam { KF_GATHER = 0, KF_NEAR, KF_S2M, KF_XLATE, KF_XLATE_TC, KF_XLATE_TCW, KF_M2L_LR, KF_M2L_TCW, KF_L2T,
-            KF_SCATTER, KF_MEMSET, KF_COUNT };
+            KF_SCATTER, KF_MEMSET, KF_XLATE_BF, KF_COUNT };
 
 static void kt_mark(Dev* d, cudaStream_t s, int fam) {
   if (!d->kt_on) return;
@@ -316,21 +324,125 @@ static int64_t tc_bop_bf(Context* ctx, Dev* d, int64_t m, int nrp, int nkc32, in
   return off;
 }
 
+// bf16 B operand of k_xlate_bf: the real 2R × 2C form of a translation matrix, nrp = 2R padded to 16
+static int64_t tc_xbf(Context* ctx, Dev* d, int64_t m, int nrp, int nkc32) {
+  auto it = d->tc_xbfoff.find(m);
+  if (it != d->tc_xbfoff.end()) return it->second;
+  const MatInfo& mi = ctx->plan.mats[m];
+  const int64_t off = d->tc_size;
+  d->tc_size += (int64_t)nkc32 * nrp * 32;
+  d->tc_jobs.push_back(TcLayoutJob{off, mi.offset, mi.rows, mi.cols, nrp, nkc32, 2, 0});
+  d->tc_xbfoff.emplace(m, off);
+  return off;
+}
+
 // Group the ops of one stage (one level, or all M2L levels at once) by matrix
 // and cut each group into tiles of the kernel variant (rows × ops per CTA)
 // that pads the group least.  Stages with fewer CTAs than ~4 waves are split
 // along K (cols) so that small, latency-bound stages still fill the GPU.
 static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops, bool atomic, XStage& st,
-                               bool tc_ok = true, bool force_tc = false) {
+                               bool tc_ok = true, bool force_tc = false, bool bf_ok = false) {
+
   const Plan& p = ctx->plan;
   st.atomic = atomic;
   if (ops.empty()) return FDA_OK;
+  // BF16x3 persistent kernel (k_xlate_bf, d->use_xbf): ≤ 128 ops per task, every matrix R ≤ 128
+  // (N = 2R ≤ 256); stages with taller matrices keep the 3xTF32 / CUDA-core kernels
+  bool use_bf = false;
+  if (bf_ok && d->use_xbf && atomic) {
+    bool fits = true;
+    for (const XOp& o : ops) fits &= p.mats[o.mat].rows <= 128;
+    use_bf = fits;
+  }
   std::vector<size_t> ord(ops.size());
   for (size_t i = 0; i < ord.size(); ++i) ord[i] = i;
-  __gnu_parallel::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
-    return ops[a].mat != ops[b].mat ? ops[a].mat < ops[b].mat : ops[a].dof < ops[b].dof;
-  });
+  // Locality order for k_xlate_bf on large stages whose matrices are each shared by many ops:
+  // ops sorted by (block of destination offsets, matrix, destination) instead of (matrix,
+  // destination), so that the tasks running at any time touch one block of destination states
+  // and the sources they read instead of streaming the level's states once per matrix (config 5
+  // M2M L7 in matrix order: 7.0 GB of DRAM traffic per launch, ncu).  A block holds ≈ 2·128 ops
+  // per matrix on average (A/B, config 5: k_xlate_bf 23.6 → 22.5 ms; 1·128: 24.9 ms; the
+  // non-persistent k_xlate_tc is slower in this order, 24.7 → 28.2 ms, and keeps matrix order).
+  bool blocked = false;
+  {
+    const double mult = 2.0;
+    if (use_bf && ops.size() >= 200000) {
+      std::vector<int64_t> mv;
+      mv.reserve(ops.size());
+      int64_t dmin = ops[0].dof, dmax = ops[0].dof;
+      for (const XOp& o : ops) {
+        mv.push_back(o.mat);
+        dmin = std::min(dmin, o.dof);
+        dmax = std::max(dmax, o.dof);
+      }
+      __gnu_parallel::sort(mv.begin(), mv.end());
+      const double nm = (double)(std::unique(mv.begin(), mv.end()) - mv.begin());
+      if ((double)ops.size() / nm >= 256) {
+        blocked = true;
+        const int64_t bspan =
+            std::max<int64_t>(1, (int64_t)(mult * 128.0 * (double)(dmax - dmin + 1) * nm / (double)ops.size()));
+        __gnu_parallel::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+          const int64_t ba = (ops[a].dof - dmin) / bspan, bb = (ops[b].dof - dmin) / bspan;
+          if (ba != bb) return ba < bb;
+          return ops[a].mat != ops[b].mat ? ops[a].mat < ops[b].mat : ops[a].dof < ops[b].dof;
+        });
+      }
+    }
+  }
+  if (!blocked)
+    __gnu_parallel::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) {
+      return ops[a].mat != ops[b].mat ? ops[a].mat < ops[b].mat : ops[a].dof < ops[b].dof;
+    });
   std::vector<int64_t> so, dof;
+  if (use_bf) {
+    {
+      std::vector<XbfTask> bt;
+      int nmax = 16;
+      for (size_t i = 0; i < ord.size();) {
+        const int64_t m = ops[ord[i]].mat;
+        size_t j = i;
+        while (j < ord.size() && ops[ord[j]].mat == m) ++j;
+        const int R = p.mats[m].rows, C = p.mats[m].cols;
+        const int n = ((2 * R + 15) / 16) * 16, nk = (2 * C + 31) / 32;
+        nmax = std::max(nmax, n);
+        const int64_t off = tc_xbf(ctx, d, m, n, nk);
+        const int32_t base = (int32_t)so.size();
+        for (size_t q = i; q < j; ++q) {
+          so.push_back(ops[ord[q]].so);
+          dof.push_back(ops[ord[q]].dof);
+        }
+        const int64_t nops = (int64_t)(j - i);
+        for (int64_t c0 = 0; c0 < nops; c0 += 128) {
+          XbfTask t;
+          t.b_off = off;
+          t.R = R;
+          t.C = C;
+          t.n = n;
+          t.nk = nk;
+          t.op_begin = base + (int32_t)c0;
+          t.op_count = (int32_t)std::min<int64_t>(128, nops - c0);
+          bt.push_back(t);
+          st.fl_bf += 8.0 * R * C * t.op_count;
+        }
+        i = j;
+      }
+      // longest tasks first (the persistent CTAs stride over them), unless in locality order
+      if (!blocked)
+        std::stable_sort(bt.begin(), bt.end(), [](const XbfTask& x, const XbfTask& y) {
+        return (int64_t)x.nk * x.n * x.op_count > (int64_t)y.nk * y.n * y.op_count;
+      });
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      st.n_bf = (int)bt.size();
+      st.grid_bf = std::min(st.n_bf, nsm);
+      st.bf_plan = xlate_bf_plan(nmax);
+      UP(&st.bf, bt.data(), bt.size());
+      UP(&st.src, so.data(), so.size());
+      UP(&st.dst, dof.data(), dof.size());
+      return FDA_OK;
+    }
+  }
   std::vector<XTask> tasks[XV];
   bool tc = d->use_tc && atomic && tc_ok;
   if (tc && ctx->p.opt.tensor_cores == 2 && !force_tc) {   // auto: large, well-shared stages only
@@ -496,9 +608,12 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
 }
 
 // one translation stage: its tensor-core tasks read the context's own operand pool (d->tcpool)
-static void launch_stage(Dev* d, const XStage& st, const float2* src, float2* dst, cudaStream_t s) {
+static void launch_stage(Dev* d, const XStage& st, const float2* src, float2* dst, cudaStream_t s,
+                         const __nv_bfloat16* shi = nullptr, const __nv_bfloat16* slo = nullptr) {
   const float2* pool = d->pool;
   const float* tcpool = d->tcpool;
+  if (st.n_bf)
+    KT(KF_XLATE_BF, s, launch_xlate_bf(st.n_bf, st.bf, st.src, st.dst, tcpool, shi, slo, dst, st.bf_plan, st.grid_bf, s));
   for (int q = 0; q < 2; ++q)
     if (st.n_tcw[q])
       KT(KF_XLATE_TCW, s, launch_xlate_tcw(q + 1, st.n_tcw[q], st.tcw[q], st.src, st.dst, tcpool, src, dst, st.grid_tcw[q], s));
@@ -542,7 +657,22 @@ fda_status engine_create(Context* ctx) {
   d->kp.ak_im = (float)(ctx->p.k * ctx->p.alpha.imag());
   d->kp.inv_k = (float)(1.0 / ctx->p.k);
   d->use_tc = ctx->p.opt.tensor_cores != 0;
+  // opt.tensor_cores = 5: dense translations on the BF16x3 persistent kernel (unsharded contexts)
+  // k_xlate_bf for the dense translations: opt.tensor_cores = 5 always; auto mode (2) on problems
+  // with ≥ 10 GFLOP of dense translations per matvec (A/B, one B200: config 4 (17 GFLOP) 4.99 →
+  // 4.92 ms, config 5 (2.2 TFLOP) 60.0 → 57 ms; configs 2 (1.1) and 3 (6.4) are faster on the
+  // CUDA-core / 3xTF32 kernels, whose smaller CTAs fill the short levels better)
+  {
+    double xf = 0;
+    for (const auto* lv : {&ctx->plan.m2m, &ctx->plan.l2l, &ctx->plan.m2l})
+      for (const auto& ops : *lv)
+        for (const Op& o : ops) xf += 8.0 * ctx->plan.mats[o.mat].rows * ctx->plan.mats[o.mat].cols;
+    d->use_xbf = ctx->p.opt.nranks <= 1 &&
+                 (ctx->p.opt.tensor_cores == 5 || (ctx->p.opt.tensor_cores == 2 && ctx->p.opt.m2l_bf16 != 0 && xf >= 10e9));
+  }
+  if (d->use_xbf) CK(xlate_bf_prepare());
   if (d->use_tc) CK(tc_prepare());
+
   if (d->use_tc) CK(xlate_tcw_prepare());
   if (d->use_tc) CK(m2l_tcw_prepare());
   if (d->use_tc) CK(m2l_bf_prepare());
@@ -742,12 +872,14 @@ fda_status engine_create(Context* ctx) {
   d->m2lv.resize(nlev);
   for (int l = 0; l < nlev; ++l) {
     fda_status s;
-    if ((s = build_xstage(ctx, d, xops(p.m2m[l], p.out_offset, p.out_offset, false), true, d->m2m[l])) != FDA_OK)
+    if ((s = build_xstage(ctx, d, xops(p.m2m[l], p.out_offset, p.out_offset, false), true, d->m2m[l], true, false,
+                          true)) != FDA_OK)
       return s;
-    if ((s = build_xstage(ctx, d, xops(p.l2l[l], p.in_offset, p.in_offset, true), true, d->l2l[l])) != FDA_OK)
+    if ((s = build_xstage(ctx, d, xops(p.l2l[l], p.in_offset, p.in_offset, true), true, d->l2l[l], true, false,
+                          true)) != FDA_OK)
       return s;
-    if ((s = build_xstage(ctx, d, xops(p.m2l[l], p.out_offset, p.in_offset, false), true, d->m2lv[l].dense)) !=
-        FDA_OK)
+    if ((s = build_xstage(ctx, d, xops(p.m2l[l], p.out_offset, p.in_offset, false), true, d->m2lv[l].dense, true,
+                          false, true)) != FDA_OK)
       return s;
   }
   {
@@ -943,6 +1075,23 @@ fda_status engine_create(Context* ctx) {
     std::vector<TcLayoutJob>().swap(d->tc_jobs);
     bool any_bf = false;
     for (auto& L : d->m2lv) any_bf |= L.n_lrtc > 0 && L.lrtc_bf16;
+    // k_xlate_bf sources: which levels' out- / in-states the main stream splits into bf16 planes
+    // (k_m2l_bf's branch then skips its own split of that level; other levels keep the split in
+    // the branch, off the M2M chain)
+    d->split_out.assign(nlev, 0);
+    d->split_in.assign(nlev, 0);
+    bool any_in = false;
+    if (d->use_xbf)
+      for (int l = 0; l < nlev; ++l) {
+        if (l + 1 < nlev && d->m2m[l].n_bf) d->split_out[l + 1] = 1;
+        if (d->m2lv[l].dense.n_bf) d->split_out[l] = 1;
+        if (d->l2l[l].n_bf) d->split_in[l] = 1, any_in = true;
+        any_bf |= d->split_out[l] != 0;
+      }
+    if (any_in) {
+      AL(&d->inb_hi, (size_t)2 * std::max<int64_t>(1, p.in_size));
+      AL(&d->inb_lo, (size_t)2 * std::max<int64_t>(1, p.in_size));
+    }
     if (any_bf) {
       AL(&d->outb_hi, (size_t)2 * std::max<int64_t>(1, p.out_size));
       AL(&d->outb_lo, (size_t)2 * std::max<int64_t>(1, p.out_size));
@@ -976,6 +1125,7 @@ fda_status engine_create(Context* ctx) {
   // kernels per matvec: gather, near, s2m, every non-empty translation launch, l2t, scatter
   int64_t nl = 4 + (d->n_s2m > 0) + (d->n_l2t_add > 0);  // gather, near, l2t, scatter (+ s2m, HF-leaf L2T)
   auto cnt = [&](const XStage& st) {
+    nl += st.n_bf > 0;
     for (int q = 0; q < 2; ++q) nl += st.n_tcw[q] > 0;
     for (int v = 0; v < TC_NV; ++v) nl += st.n_tc[v] > 0;
     for (int v = 0; v < XV; ++v) nl += st.ntask[v] > 0;
@@ -988,6 +1138,7 @@ fda_status engine_create(Context* ctx) {
     nl += L.n_lrtc > 0;
     nl += L.n_lrtc > 0 && L.lrtc_bf16;   // k_split_bf16 before k_m2l_bf
   }
+  for (size_t l = 0; l < d->split_out.size(); ++l) nl += d->split_out[l] + d->split_in[l];   // k_split_bf16
   if (d->nranks > 1) nl += 2;            // k_pack, k_unpack_add
   ctx->launches_per_matvec = nl;
   // CTA tasks per translation kernel family (fda_debug_table "kernel_tasks"; lets the tests
@@ -995,10 +1146,12 @@ fda_status engine_create(Context* ctx) {
   // k_m2l_tcw], each split into M2M | M2L | L2L
   {
     int64_t* kt = ctx->kernel_tasks;
-    for (int i = 0; i < 15; ++i) kt[i] = 0;
+    for (int i = 0; i < 18; ++i) kt[i] = 0;
     double* kf = ctx->kernel_flops;
-    for (int i = 0; i < 15; ++i) kf[i] = 0;
+    for (int i = 0; i < 18; ++i) kf[i] = 0;
     auto add = [&](const XStage& st, int which) {
+      kt[5 * 3 + which] += st.n_bf;
+      kf[5 * 3 + which] += st.fl_bf;
       for (int v = 0; v < XV; ++v) kt[0 * 3 + which] += st.ntask[v];
       for (int v = 0; v < TC_NV; ++v) kt[1 * 3 + which] += st.n_tc[v];
       for (int q = 0; q < 2; ++q) kt[2 * 3 + which] += st.n_tcw[q];
@@ -1106,14 +1259,29 @@ void engine_destroy(Context* ctx) {
   ctx->dev = nullptr;
 }
 
+// bf16 hi / lo planes of level l's out-states (in = false) or in-states (in = true), on stream s
+static void split_level(Context* ctx, Dev* d, int l, bool in, cudaStream_t s) {
+  const Plan& p = ctx->plan;
+  const auto& lb = in ? p.in_level_begin : p.out_level_begin;
+  const auto& off = in ? p.in_offset : p.out_offset;
+  const int64_t s0 = lb[l], s1 = lb[l + 1];
+  if (s1 <= s0) return;
+  const int64_t f0 = 2 * off[s0], f1 = 2 * (s1 < (int64_t)off.size() ? off[s1] : (in ? p.in_size : p.out_size));
+  const float* x = reinterpret_cast<const float*>(in ? d->inb : d->outb);
+  __nv_bfloat16* hi = in ? d->inb_hi : d->outb_hi;
+  __nv_bfloat16* lo = in ? d->inb_lo : d->outb_lo;
+  KT(KF_XLATE_BF, s, launch_split_bf16(x + f0, f1 - f0, hi + f0, lo + f0, s));
+}
+
 // the tensor-core factored M2L of one level: k_m2l_bf (after splitting the level's out-states
-// into bf16 hi / lo planes) or k_m2l_tcw
-static void launch_lrtc(Dev* d, const Dev::M2LLevel& L, cudaStream_t st) {
+// into bf16 hi / lo planes, unless the main stream did: d->split_out) or k_m2l_tcw
+static void launch_lrtc(Dev* d, const Dev::M2LLevel& L, cudaStream_t st, bool split = true) {
   if (!L.n_lrtc) return;
   if (L.lrtc_bf16) {
     KT(KF_M2L_TCW, st, {
-      launch_split_bf16(reinterpret_cast<const float*>(d->outb) + L.split0, L.split1 - L.split0, d->outb_hi + L.split0,
-                        d->outb_lo + L.split0, st);
+      if (split)
+        launch_split_bf16(reinterpret_cast<const float*>(d->outb) + L.split0, L.split1 - L.split0,
+                          d->outb_hi + L.split0, d->outb_lo + L.split0, st);
       launch_m2l_bf(L.n_lrtc, L.lrtc, L.lr_src, L.lr_dst, d->tcpool, d->outb_hi, d->outb_lo, d->inb, L.lrtc_plan,
                     L.lrtc_grid, st);
     });
@@ -1158,26 +1326,31 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
   else KT(KF_S2M, s, launch_s2m(d->n_s2m, d->s2m, d->pool, d->x_tree, d->outb, d->max_T, s));
   if (prof) CK(cudaEventRecord(d->ev[2], s));
   const int nlev = (int)d->m2m.size();
+  const bool xbf = !d->split_out.empty();
+  auto split_out = [&](int l) { if (xbf && d->split_out[l]) split_level(ctx, d, l, false, s); };
+  auto split_in = [&](int l) { if (xbf && d->split_in[l]) split_level(ctx, d, l, true, s); };
   auto m2l_level = [&](int l, cudaStream_t st) {
     const Dev::M2LLevel& L = d->m2lv[l];
-    launch_lrtc(d, L, st);
+    launch_lrtc(d, L, st, !(xbf && d->split_out[l]));
     for (int c = LR_NCLS - 1; c >= 0; --c)
       if (L.n_lr[c])
         KT(KF_M2L_LR, st, launch_m2l_lr(c, L.n_lr[c], L.lr_tasks[c], L.lr_src, L.lr_dst, d->pool, d->outb, d->inb, st));
-    launch_stage(d, L.dense, d->outb, d->inb, st);
+    launch_stage(d, L.dense, d->outb, d->inb, st, d->outb_hi, d->outb_lo);
     launch_stage(d, L.a, d->outb, d->tmpb, st);
     launch_stage(d, L.b, d->tmpb, d->inb, st);
   };
   if (prof) {
     // serialised: every stage time is the isolated duration of its kernels
     for (int l = nlev - 1; l >= 0; --l) {
-      launch_stage(d, d->m2m[l], d->outb, d->outb, s);
+      launch_stage(d, d->m2m[l], d->outb, d->outb, s, d->outb_hi, d->outb_lo);
+      split_out(l);
     }
     CK(cudaEventRecord(d->ev[3], s));
     for (int l = 0; l < nlev; ++l) m2l_level(l, s);
     CK(cudaEventRecord(d->ev[4], s));
     for (int l = 0; l < nlev; ++l) {
-      launch_stage(d, d->l2l[l], d->inb, d->inb, s);
+      split_in(l);
+      launch_stage(d, d->l2l[l], d->inb, d->inb, s, d->inb_hi, d->inb_lo);
     }
     CK(cudaEventRecord(d->ev[5], s));
   } else {
@@ -1188,7 +1361,8 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
     int k = 0;
     std::vector<int> nbr(nlev, 0);
     for (int l = nlev - 1; l >= 0; --l) {
-      launch_stage(d, d->m2m[l], d->outb, d->outb, s);   // writes level-l out-states
+      launch_stage(d, d->m2m[l], d->outb, d->outb, s, d->outb_hi, d->outb_lo);   // writes level-l out-states
+      split_out(l);
       if (!d->m2lv[l].any()) continue;
       const Dev::M2LLevel& L = d->m2lv[l];
       CK(cudaEventRecord(d->ev_up[l], s));
@@ -1202,7 +1376,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
       fda_status bs;
       if (L.n_lrtc &&
           (bs = branch([&](cudaStream_t sm) {
-             launch_lrtc(d, L, sm);
+             launch_lrtc(d, L, sm, !(xbf && d->split_out[l]));
            })) != FDA_OK)
         return bs;
       for (int c = LR_NCLS - 1; c >= 0; --c)
@@ -1212,7 +1386,7 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
              })) != FDA_OK)
           return bs;
       if ((bs = branch([&](cudaStream_t sm) {
-             launch_stage(d, L.dense, d->outb, d->inb, sm);
+             launch_stage(d, L.dense, d->outb, d->inb, sm, d->outb_hi, d->outb_lo);
              launch_stage(d, L.a, d->outb, d->tmpb, sm);
              launch_stage(d, L.b, d->tmpb, d->inb, sm);
            })) != FDA_OK)
@@ -1220,7 +1394,8 @@ static fda_status run_core(Context* ctx, Dev* d, cudaStream_t s, int kind) {
     }
     for (int l = 0; l < nlev; ++l) {
       for (int b = 0; b < nbr[l]; ++b) CK(cudaStreamWaitEvent(s, d->ev_m2l[l][b], 0));
-      launch_stage(d, d->l2l[l], d->inb, d->inb, s);
+      split_in(l);
+      launch_stage(d, d->l2l[l], d->inb, d->inb, s, d->inb_hi, d->inb_lo);
     }
   }
   KT(KF_L2T, s, launch_l2t(d->n_l2t, d->l2t, d->pool, d->inb, d->y_far, s));

@@ -103,7 +103,7 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
   }
   if (o.max_leaf < 1 || o.max_leaf > 128 || o.p_eq < 2 || o.p_chk_lf < 2 || o.p_chk_hf < 2 || !(o.eq_scale > 0) ||
       !(o.chk_scale_lf > o.eq_scale) || !(o.tier1_rho >= 0) || !(o.tier2_rho >= o.tier1_rho) ||
-      o.tensor_cores < 0 || o.tensor_cores > 4 || o.hf_leaves < 0 || o.hf_leaves > 1 ||
+      o.tensor_cores < 0 || o.tensor_cores > 5 || o.hf_leaves < 0 || o.hf_leaves > 1 ||
       o.lr_tensor_cores < 0 || o.lr_tensor_cores > 2) {
     g_build_error = "invalid fda_options";
     delete ctx;
@@ -468,9 +468,9 @@ fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int6
     return put(std::vector<int64_t>{p.own_leaf0, p.own_leaf1, p.own_e0, p.own_e1}, dst, count, eb);
   if (nm == "launches") return put(std::vector<int64_t>{ctx->launches_per_matvec}, dst, count, eb);
   if (nm == "kernel_tasks")
-    return put(std::vector<int64_t>(ctx->kernel_tasks, ctx->kernel_tasks + 15), dst, count, eb);
+    return put(std::vector<int64_t>(ctx->kernel_tasks, ctx->kernel_tasks + 18), dst, count, eb);
   if (nm == "kernel_flops")
-    return put(std::vector<double>(ctx->kernel_flops, ctx->kernel_flops + 15), dst, count, eb);
+    return put(std::vector<double>(ctx->kernel_flops, ctx->kernel_flops + 18), dst, count, eb);
   if (nm == "root") {
     return put(std::vector<double>{t.root_center.x, t.root_center.y, t.root_center.z, t.root_width, t.lambda},
                dst, count, eb);

@@ -285,8 +285,8 @@ struct Context {
   int64_t launches_per_matvec = 0;
   void* pool_dev = nullptr;        // device build: the matrix pool already on the device (engine adopts it)
   int64_t pool_dev_cap = 0;        // its capacity (complex entries)
-  int64_t kernel_tasks[15] = {};   // CTA tasks per translation kernel family × (M2M, M2L, L2L)
-  double kernel_flops[15] = {};    // their algorithmic flops (complex-equivalent, 8·rows·cols per op)
+  int64_t kernel_tasks[18] = {};   // CTA tasks per translation kernel family × (M2M, M2L, L2L)
+  double kernel_flops[18] = {};    // their algorithmic flops (complex-equivalent, 8·rows·cols per op)
   bool profiling = false;
 };
 

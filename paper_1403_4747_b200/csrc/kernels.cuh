@@ -98,6 +98,20 @@ cudaError_t m2l_bf_prepare();
 void launch_m2l_bf(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                    const float* tcpool, const __nv_bfloat16* shi, const __nv_bfloat16* slo, float2* dst,
                    const LrTcPlan& pl, int grid, cudaStream_t s);
+// dense translations in BF16x3 (k_xlate_bf): ≤ 128 ops sharing one matrix M (R × C, R ≤ 128);
+// B = real 2R × 2C form of M as a bf16 B operand (k_tc_layout kind 2: n rows, nk 32-element chunks)
+struct XbfTask {
+  int64_t b_off;      // float offset of the bf16 B operand in the tensor-core pool
+  int32_t R, C;       // matrix shape (complex)
+  int32_t n;          // B rows = MMA N: 2R padded to a multiple of 16 (≤ 256)
+  int32_t nk;         // ⌈2C / 32⌉
+  int32_t op_begin, op_count;
+};
+LrTcPlan xlate_bf_plan(int nmax);
+cudaError_t xlate_bf_prepare();
+void launch_xlate_bf(int ntask, const XbfTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                     const float* tcpool, const __nv_bfloat16* shi, const __nv_bfloat16* slo, float2* dst,
+                     const LrTcPlan& pl, int grid, cudaStream_t s);
 void launch_split_bf16(const float* x, int64_t n, __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t s);
 void launch_m2l_tcw(int ntask, const LrTcTask* tasks, const int64_t* src_off, const int64_t* dst_off,
                     const float* tcpool, const float2* src, float2* dst, const LrTcPlan& pl, int grid,

@@ -978,6 +978,227 @@ void launch_split_bf16(const float* x, int64_t n, __nv_bfloat16* hi, __nv_bfloat
 }
 
 // ---------------------------------------------------------------------------
+// Dense translations in BF16x3 on tcgen05 (k_xlate_bf; SURVEY §8(a) a3-a5, M2M / L2L / dense
+// M2L, Steps 2-3 P:458-499):  dst[:, op] += M · src[:, op]  for ≤ 128 ops sharing M (R × C).
+// The ops are the M = 128 rows (TMEM lanes) and the matrix is the B operand, as in phase 1 of
+// k_m2l_bf: D (128 × N) = S (128 × 2C) · A_Mᵀ, A_M = real interleaved 2R × 2C form of M (N =
+// 2R padded to 16 ≤ 256), so each row of D is one op's interleaved complex result.
+//  * A: the source states, pre-split into bf16 hi / lo planes (engine.cu: k_split_bf16 once per
+//    level), gathered by the row warps with 16-byte cp.async straight into the canonical K-major
+//    layout, S − 2 ring jobs (32 K elements each) ahead;
+//  * B: A_Mᵀ as bf16 hi / lo tiles (k_tc_layout kind 2), streamed by the TMA engine (warp 9);
+//  * MMA warp (8): per job 2 k-steps × (hi·hi + hi·lo + lo·hi), kind::f16, fp32 accumulation;
+//  * two TMEM accumulator sets: the MMAs of task i+1 run while the row warps drain task i
+//    (tcgen05.ld of the op's row → 16-byte vector atomics into the destination state).
+// No phase 2 and no in-shared-memory split: the row warps only gather and drain.
+template <int S>
+__global__ void __launch_bounds__(TCW_NT, 1) k_xlate_bf(const XbfTask* __restrict__ tasks, int ntask,
+                                                     const int64_t* __restrict__ src_off,
+                                                     const int64_t* __restrict__ dst_off,
+                                                     const float* __restrict__ tcpool,
+                                                     const __nv_bfloat16* __restrict__ shi,
+                                                     const __nv_bfloat16* __restrict__ slo, float2* __restrict__ dst,
+                                                     int stage_b, int nmax, uint32_t ncols) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t a_full[S], b_full[S], empty[S], d_full[2], d_free[2];
+  __shared__ uint32_t tmem_base_sh;
+  constexpr int LA = S >= 6 ? S - 3 : S - 2;
+  constexpr int A_PL = 128 * BK * 2;               // bytes of one A plane (hi or lo) per job
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x;
+  const uint8_t* pool8 = reinterpret_cast<const uint8_t*>(tcpool);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+  }
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) {
+      mbar_init(&a_full[q], 32 * TCW_RW);
+      mbar_init(&b_full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&d_full[q], 1);
+      mbar_init(&d_free[q], 32 * TCW_RW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == TCW_RW + 1) {
+    // ---------------- TMA producer: the B tile of every ring job
+    if (lane == 0) {
+      int j = 0;
+      for (int ct = blockIdx.x; ct < ntask; ct += G) {
+        const XbfTask t = tasks[ct];
+        const uint32_t bytes = (uint32_t)t.n * BK * 2 * 2;
+        for (int c = 0; c < t.nk; ++c, ++j) {
+          const int st = j % S;
+          if (j >= S) mbar_wait(&empty[st], ((j / S) - 1) & 1);
+          mbar_expect_tx(&b_full[st], bytes);
+          bulk_g2s(sbase + st * stage_b + 2 * A_PL, pool8 + 4 * t.b_off + (int64_t)c * bytes, bytes, &b_full[st]);
+        }
+      }
+    }
+  } else if (warp == TCW_RW) {
+    // ---------------- MMA issuer: task i accumulates into TMEM set i & 1
+    if (lane == 0) {
+      int j = 0, i = 0;
+      for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
+        const XbfTask t = tasks[ct];
+        const int N = t.n, K2 = 2 * t.C;
+        const uint32_t idesc = idesc_bf16(N);
+        const uint32_t td = tmem + (uint32_t)((i & 1) * nmax);
+        if (i >= 2) mbar_wait(&d_free[i & 1], ((i - 2) >> 1) & 1);   // task i-2 drained
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+        for (int c = 0; c < t.nk; ++c, ++j) {
+          const int st = j % S;
+          mbar_wait(&a_full[st], (j / S) & 1);
+          mbar_wait(&b_full[st], (j / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+          const uint8_t* sA = sbase + st * stage_b;
+          const uint32_t a_hi = smem_u32(sA), a_lo = a_hi + A_PL;
+          const uint32_t b_hi = smem_u32(sA + 2 * A_PL), b_lo = b_hi + N * BK * 2;
+#pragma unroll
+          for (int s2 = 0; s2 < BK / 16; ++s2) {
+            if (c * BK + 16 * s2 >= K2) break;
+            const uint32_t ao = (uint32_t)(s2 * 2 * 16 * 128), bo = (uint32_t)(s2 * 2 * (N / 8) * 128);
+            const uint64_t Ah = make_desc(a_hi + ao, 16 * 128, 128), Al = make_desc(a_lo + ao, 16 * 128, 128);
+            const uint64_t Bh = make_desc(b_hi + bo, (N / 8) * 128, 128), Bl = make_desc(b_lo + bo, (N / 8) * 128, 128);
+            mma_bf16(td, Ah, Bh, idesc, (c > 0 || s2 > 0) ? 1u : 0u);
+            mma_bf16(td, Ah, Bl, idesc, 1u);
+            mma_bf16(td, Al, Bh, idesc, 1u);
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           smem_u32(&empty[st]))
+                       : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&d_full[i & 1]))
+                     : "memory");
+      }
+    }
+  } else {
+    // ---------------- row warps: thread (row = tid & 127, half h = tid >> 7); half h gathers the
+    // k-groups {2h, 2h+1} of each job from both planes and drains the 16-column TMEM blocks ≡ h (mod 2)
+    const int row = tid & 127, h = tid >> 7;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    int it = blockIdx.x, ic = 0, js = 0;
+    XbfTask ti = tasks[it];
+    int64_t isp = row < ti.op_count ? 2 * src_off[ti.op_begin + row] : -1;   // bf16 element offset
+    auto issue_next = [&]() {
+      if (it < ntask) {
+        const int st = js % S;
+        if (js >= S) mbar_wait(&empty[st], ((js / S) - 1) & 1);
+        uint8_t* sA = sbase + st * stage_b;
+        const int K2 = 2 * ti.C;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int kg = 2 * h + q;
+          const int k = ic * BK + 8 * kg;
+          const int nb = isp >= 0 ? 2 * min(8, max(0, K2 - k)) : 0;
+          const int so = ((kg * 16 + (row >> 3)) * 8 + (row & 7)) * 16;
+          cp16z(sA + so, nb ? (const void*)(shi + isp + k) : (const void*)shi, nb);
+          cp16z(sA + A_PL + so, nb ? (const void*)(slo + isp + k) : (const void*)slo, nb);
+        }
+        ++js;
+        if (++ic == ti.nk) {
+          ic = 0;
+          it += G;
+          if (it < ntask) {
+            ti = tasks[it];
+            isp = row < ti.op_count ? 2 * src_off[ti.op_begin + row] : -1;
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    };
+    auto drain = [&](const XbfTask& t, int i) {
+      mbar_wait(&d_full[i & 1], (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+      const uint32_t td = tmem + (uint32_t)((i & 1) * nmax);
+      float2* d = row < t.op_count ? dst + dst_off[t.op_begin + row] : nullptr;
+      for (int c0 = 16 * h; c0 < t.n; c0 += 32) {
+        float w[16];
+        tmem_ld16(td + lane_base + c0, w);
+        if (d) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = c0 / 2 + 2 * q;   // complex rows (r, r+1); r+1 = R is the padding slot
+            if (r < t.R)
+              atomicAdd(reinterpret_cast<float4*>(d + r), make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]));
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+      mbar_arrive(&d_free[i & 1]);
+    };
+    for (int q = 0; q < LA; ++q) issue_next();
+    int jc = 0, i = 0;
+    XbfTask tp{};
+    for (int ct = blockIdx.x; ct < ntask; ct += G, ++i) {
+      const XbfTask t = tasks[ct];
+      for (int c = 0; c < t.nk; ++c, ++jc) {
+        issue_next();
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(LA) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive(&a_full[jc % S]);
+      }
+      if (i >= 1) drain(tp, i - 1);   // task i-1's accumulators while task i's MMAs run
+      tp = t;
+    }
+    if (i >= 1) drain(tp, i - 1);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
+}
+
+// plan of one k_xlate_bf launch: S ring stages of one 32-element job (A hi|lo 16 KB + B hi|lo),
+// ≤ 220 KB; two TMEM accumulator sets of nmax columns
+LrTcPlan xlate_bf_plan(int nmax) {
+  LrTcPlan pl;
+  pl.stage_fl = (2 * 128 * BK * 2 + nmax * BK * 2 * 2) / 4;   // (in floats)
+  const size_t cap = (220 * 1024 - 1024) / 4;
+  const int s = (int)(cap / pl.stage_fl);
+  pl.stages = s >= 8 ? 8 : (s >= 6 ? 6 : (s >= 5 ? 5 : (s >= 4 ? 4 : 3)));
+  pl.smem = (size_t)pl.stages * pl.stage_fl * 4 + 1024;
+  pl.ncols = tmem_cols(2 * nmax);
+  pl.n1max = nmax;
+  return pl;
+}
+cudaError_t xlate_bf_prepare() {
+  cudaError_t e = cudaFuncSetAttribute(k_xlate_bf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_xlate_bf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_xlate_bf<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_xlate_bf<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_xlate_bf<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  return e;
+}
+void launch_xlate_bf(int ntask, const XbfTask* tasks, const int64_t* src_off, const int64_t* dst_off,
+                     const float* tcpool, const __nv_bfloat16* shi, const __nv_bfloat16* slo, float2* dst,
+                     const LrTcPlan& pl, int grid, cudaStream_t s) {
+  if (ntask <= 0) return;
+#define XBF(S)                                                                                                  \
+  k_xlate_bf<S><<<grid, TCW_NT, pl.smem, s>>>(tasks, ntask, src_off, dst_off, tcpool, shi, slo, dst,            \
+                                           pl.stage_fl * 4, pl.n1max, pl.ncols)
+  switch (pl.stages) {
+    case 8: XBF(8); break;
+    case 6: XBF(6); break;
+    case 5: XBF(5); break;
+    case 4: XBF(4); break;
+    default: XBF(3); break;
+  }
+#undef XBF
+}
+
+// ---------------------------------------------------------------------------
 // Warp-specialised persistent form of the translation kernel (k_xlate_tcw):
 // the same product (dst[:, op] += M · src[:, op] in interleaved real form,
 // 3xTF32, N = 128 ops per task, TILES ≤ 2 row tiles) with the roles of

@@ -37,7 +37,7 @@ EXPORTS = ["fda_options_default", "fda_build", "fda_matvec", "fda_rhs_plane_wave
 
 STAGES = ["gather", "near", "s2m", "m2m", "m2l", "l2l", "l2t", "scatter"]
 KERNELS = ["k_gather", "k_near", "k_s2m", "k_xlate", "k_xlate_tc", "k_xlate_tcw", "k_m2l_lr", "k_m2l_tcw", "k_l2t",
-           "k_scatter", "memset"]
+           "k_scatter", "memset", "k_xlate_bf"]
 
 
 class FdaError(RuntimeError):
@@ -337,19 +337,19 @@ class FDA:
                "xsend": np.int64, "xrecv": np.int64, "hf_s2m": np.int64, "hf_s2m_rhs": np.int64,
                "hf_l2t": np.int64, "kernel_tasks": np.int64, "kernel_flops": np.float64}
 
-    KERNEL_FAMILIES = ("k_xlate", "k_xlate_tc", "k_xlate_tcw", "k_m2l_lr", "k_m2l_tcw")
+    KERNEL_FAMILIES = ("k_xlate", "k_xlate_tc", "k_xlate_tcw", "k_m2l_lr", "k_m2l_tcw", "k_xlate_bf")
 
     def kernel_tasks(self) -> dict:
         """CTA tasks per translation kernel family and stage ("k_xlate_tc/m2m", …):
         where the build routed the translations (fda_debug_table "kernel_tasks")."""
-        t = self.table("kernel_tasks").reshape(5, 3)
+        t = self.table("kernel_tasks").reshape(len(self.KERNEL_FAMILIES), 3)
         return {f"{f}/{s}": int(t[i, j]) for i, f in enumerate(self.KERNEL_FAMILIES)
                 for j, s in enumerate(("m2m", "m2l", "l2l"))}
 
     def kernel_flops(self) -> dict:
         """Algorithmic flops per translation kernel family and stage (complex-equivalent,
         8·rows·cols per op; 16·r·T per factored M2L op)."""
-        t = self.table("kernel_flops").reshape(5, 3)
+        t = self.table("kernel_flops").reshape(len(self.KERNEL_FAMILIES), 3)
         return {f"{f}/{s}": float(t[i, j]) for i, f in enumerate(self.KERNEL_FAMILIES)
                 for j, s in enumerate(("m2m", "m2l", "l2l"))}
 

@@ -416,6 +416,34 @@ def test_tensor_core_translations(lib, lowrank, tc):
     assert _rel(y1, yo) <= MATVEC_TOL
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("mesh_s,k,ml,repeat", [(4, 40.0, 32, 1), (5, 30.0, 32, 3)])
+def test_tensor_core_translations_bf16(lib, mesh_s, k, ml, repeat):
+    """BF16x3 persistent translation kernel (opt.tensor_cores = 5, k_xlate_bf): every dense
+    M2M / L2L / M2L stage routed to it, the same operator as the CUDA-core translations to the
+    BF16x3 product error (≈ 2⁻¹⁶ per product; ≤ 1e-5 on y, measured ≈ 1e-6), on the captured
+    graph (concurrent M2L branches, bf16 planes split on the main stream) and on repeated
+    applications (cross-task TMEM double buffering, ≥ 2 tasks per persistent CTA on mesh 5)."""
+    V, F = icosphere(mesh_s, 0.5)
+    x = random_density(len(F), 8)
+    y0 = lib(V, F, k, 1j / k, 1e-4, max_leaf=ml, tensor_cores=0).matvec(x)
+    f1 = lib(V, F, k, 1j / k, 1e-4, max_leaf=ml, tensor_cores=5)
+    kt = f1.kernel_tasks()
+    print(f"tensor_cores=5: {kt}")
+    assert kt["k_xlate_bf/m2m"] > 0 and kt["k_xlate_bf/l2l"] > 0
+    assert kt["k_xlate/m2m"] == 0 and kt["k_xlate/l2l"] == 0
+    if mesh_s == 4:
+        assert kt["k_xlate_bf/m2l"] > 0            # dense HF M2L branch on k_xlate_bf too
+    for _ in range(repeat):
+        y1 = f1.matvec(x)
+        print(f"k_xlate_bf vs CUDA-core translations: {_rel(y1, y0):.2e}")
+        assert _rel(y1, y0) < 1e-5
+    el = O.element_geometry(V, F)
+    rows = np.arange(len(F)) if mesh_s == 4 else sampled_rows(len(F), 600, 9)
+    yo = fast.matvec_rows(el, rows, x, k, 1j / k)
+    assert _rel(y1[rows], yo) <= MATVEC_TOL
+
+
 @pytest.mark.parametrize("mesh_s,k,ml,bf16", [(4, 40.0, 16, 0), (5, 30.0, 32, 0), (4, 40.0, 16, 1), (5, 30.0, 32, 1)])
 def test_tensor_core_fused_m2l(lib, mesh_s, k, ml, bf16):
     """Fused tcgen05 §4.2 M2L (opt.lr_tensor_cores = 1: both factors on the
