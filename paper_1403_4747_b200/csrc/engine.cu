@@ -777,14 +777,26 @@ fda_status engine_create(Context* ctx) {
   UP(&d->near_off, noff.data(), noff.size());
   UP(&d->corr_ptr, cptr.data(), cptr.size());
   UP(&d->corr_col, ccol.data(), ccol.size());
-  UP(&d->corr_val, reinterpret_cast<const float2*>(p.corr_val.data()), p.corr_val.size());
+  if (ctx->corr_dev[0]) {   // device build: adopt the correction values it left on the device
+    d->corr_val = static_cast<float2*>(ctx->corr_dev[0]);
+    d->allocs.push_back(d->corr_val);
+    ctx->corr_dev[0] = nullptr;
+  } else {
+    UP(&d->corr_val, reinterpret_cast<const float2*>(p.corr_val.data()), p.corr_val.size());
+  }
   if (ctx->p.opt.rhs_operator) {
     if (p.corr_col_rhs.size() >= (size_t)INT32_MAX) { ctx->err = "RHS table too large"; return FDA_E_INTERNAL; }
     std::vector<int32_t> rp(p.corr_ptr_rhs.begin(), p.corr_ptr_rhs.end()),
         rc(p.corr_col_rhs.begin(), p.corr_col_rhs.end());
     UP(&d->corr_ptr_rhs, rp.data(), rp.size());
     UP(&d->corr_col_rhs, rc.data(), rc.size());
-    UP(&d->corr_val_rhs, reinterpret_cast<const float2*>(p.corr_val_rhs.data()), p.corr_val_rhs.size());
+    if (ctx->corr_dev[1]) {
+      d->corr_val_rhs = static_cast<float2*>(ctx->corr_dev[1]);
+      d->allocs.push_back(d->corr_val_rhs);
+      ctx->corr_dev[1] = nullptr;
+    } else {
+      UP(&d->corr_val_rhs, reinterpret_cast<const float2*>(p.corr_val_rhs.data()), p.corr_val_rhs.size());
+    }
   }
   if (ctx->pool_dev) {   // device build: adopt the pool it left on the device
     d->pool = static_cast<float2*>(ctx->pool_dev);
@@ -1193,6 +1205,17 @@ fda_status engine_create(Context* ctx) {
   CK(cudaEventCreate(&d->ev_l1));
   CK(cudaEventCreate(&d->ev_n1));
   CK(cudaDeviceSynchronize());
+  return FDA_OK;
+}
+
+// device → host copy of the adopted matrix pool or correction values (fda_debug_table)
+fda_status engine_read_table(Context* ctx, int which, void* dst, int64_t count) {
+  Dev* d = static_cast<Dev*>(ctx->dev);
+  if (!d) return FDA_E_STATE;
+  CK(cudaSetDevice(d->device));
+  const void* src = which == 0 ? (const void*)d->pool : (which == 1 ? (const void*)d->corr_val : (const void*)d->corr_val_rhs);
+  if (!src) return FDA_E_STATE;
+  CK(cudaMemcpy(dst, src, (size_t)count * sizeof(float2), cudaMemcpyDeviceToHost));
   return FDA_OK;
 }
 

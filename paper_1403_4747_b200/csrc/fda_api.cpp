@@ -226,6 +226,8 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
     g_build_error = ctx->err;
     engine_destroy(ctx);
     if (ctx->pool_dev) cudaFree(ctx->pool_dev);   // not adopted by an engine
+    for (void* c : ctx->corr_dev)
+      if (c) cudaFree(c);
     delete ctx;
     return st;
   }
@@ -259,7 +261,7 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
   }
   I.n_corrections = (int64_t)pl.corr_col.size();
   I.n_matrices = (int64_t)pl.mats.size();
-  I.table_bytes = (int64_t)pl.pool.size() * 8 + (int64_t)(pl.corr_val.size() + pl.corr_val_rhs.size()) * 12;
+  I.table_bytes = (int64_t)pl.pool.size() * 8 + (int64_t)pl.corr_col.size() * 12 + (int64_t)pl.corr_col_rhs.size() * 12;
   I.t_build_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = ctx;
   return FDA_OK;
@@ -431,6 +433,19 @@ fda_status fda_debug_table(const fda_ctx* ctx, const char* name, void* dst, int6
       for (int64_t x : {(int64_t)s.kind, (int64_t)s.level, (int64_t)s.octant, (int64_t)s.dir, s.leaf, s.dx, s.dy, s.dz}) v.push_back(x);
     }
     return put(v, dst, count, eb);
+  }
+  if (nm == "pool" || nm == "corr_val" || nm == "corr_val_rhs") {
+    // device build: the device-built values were never downloaded; read them from the engine
+    const int which = nm == "pool" ? 0 : (nm == "corr_val" ? 1 : 2);
+    const bool on_dev = which == 0 ? ctx->pool_partial : (which == 1 ? p.corr_val.empty() && !p.corr_col.empty()
+                                                                      : p.corr_val_rhs.empty() && !p.corr_col_rhs.empty());
+    if (on_dev && ctx->dev) {
+      const int64_t n = which == 0 ? (int64_t)p.pool.size() : (int64_t)(which == 1 ? p.corr_col : p.corr_col_rhs).size();
+      if (count) *count = n;
+      if (eb) *eb = (int32_t)sizeof(cf);
+      if (!dst) return FDA_OK;
+      return engine_read_table(const_cast<fda_ctx*>(ctx), which, dst, n);
+    }
   }
   if (nm == "pool") return put(p.pool, dst, count, eb);
   if (nm == "near_ptr") return put(p.near_ptr, dst, count, eb);

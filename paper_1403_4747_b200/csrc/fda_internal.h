@@ -270,6 +270,7 @@ fda_status engine_stage_times(Context* ctx, double* ms, int32_t* n);
 fda_status engine_kernel_times(Context* ctx, double* ms, int32_t* n);
 fda_status engine_near_time(Context* ctx, double* ms);
 fda_status engine_comm_init(Context* ctx, const void* id128);
+fda_status engine_read_table(Context* ctx, int which, void* dst, int64_t count);   // 0 pool, 1 / 2 corr_val (LHS / RHS)
 fda_status engine_exchange_local(Context** ctxs, int n);
 fda_status nccl_unique_id(void* id128, std::string& err);
 void engine_destroy(Context* ctx);
@@ -285,6 +286,10 @@ struct Context {
   int64_t launches_per_matvec = 0;
   void* pool_dev = nullptr;        // device build: the matrix pool already on the device (engine adopts it)
   int64_t pool_dev_cap = 0;        // its capacity (complex entries)
+  bool pool_partial = false;       // device build: the host plan.pool lacks the device-built matrices
+                                   // (never downloaded; fda_debug_table reads them from the device)
+  void* corr_dev[2] = {nullptr, nullptr};   // device build: correction values (LHS, RHS) left on the
+  int64_t corr_dev_n[2] = {0, 0};           // device for the engine (plan.corr_val[_rhs] stays empty)
   int64_t kernel_tasks[18] = {};   // CTA tasks per translation kernel family × (M2M, M2L, L2L)
   double kernel_flops[18] = {};    // their algorithmic flops (complex-equivalent, 8·rows·cols per op)
   bool profiling = false;
