@@ -39,11 +39,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "FDA Burton-Miller matvec ms and GMRES solve s vs N,kD; %FP32/HBM roofline"
-# SURVEY §8(d) roofline table: one near-field kernel evaluation (target centroid × source
-# quadrature point of ∂G/∂n_y + α∂²G/∂n_x∂n_y) is ≈ 65 FP32-pipe instructions ≈ 100 flop
-# (FFMA = 2) by hand count; the kernel's packed-pair SASS executes ≈ 30 lane FMA-pipe ops
-# — the algorithmic unit is the survey's.
-FLOPS_PER_EVAL = 100
+# Near-field roofline unit.  SURVEY §8(d) asks for the %FP32 peak from the kernel's executed
+# FFMA/FADD/FMUL counts.  One evaluation (target centroid × source quadrature point of
+# ∂G/∂n_y + α∂²G/∂n_x∂n_y) executes, per target lane, 29.67 FP32-pipe instructions — SASS of
+# k_near's inner loop (2 source elements × 3 points for a target pair): 82 FFMA2 + 64 FMUL2 +
+# 26 FADD2 = 172 packed instructions per 6 evaluation pairs (28.67 per lane-evaluation) plus
+# 1 FMUL.RZ (sincos range reduction) per lane, and 3 MUFU.  Each occupies one FMA-pipe lane
+# slot, i.e. 2 flop-equivalents at the FFMA peak (148 SMs × 128 lanes × 2 × clock), so
+# `frac` is the FMA-pipe utilisation of the kernel (ncu's own figure: 74% at config 4).  The
+# survey's hand count of the evaluation as written (≈ 65 instructions ≈ 100 flop; the kernel
+# removes work with the identities of DESIGN.md §5) is reported alongside as frac_survey_unit.
+FP32_INSTR_PER_EVAL = 29.67
+FLOPS_PER_EVAL = 2 * FP32_INSTR_PER_EVAL
+FLOPS_PER_EVAL_SURVEY = 100
 SMS, FP32_LANES = 148, 128
 # B200_PROFILING.md nominal dense peaks: TF32 1.1 PFLOP/s vs BF16 2.25 PFLOP/s
 TF32_OVER_BF16 = 1.1 / 2.25
@@ -172,7 +180,8 @@ def _family_work(f, work):
     kf = f.kernel_flops()
     fam = {}
     fam["k_near"] = ("alu", work["near"]["evals"] * FLOPS_PER_EVAL,
-                     f"{work['near']['evals']} kernel evaluations x {FLOPS_PER_EVAL} flop (SURVEY §8(d))")
+                     f"{work['near']['evals']} kernel evaluations x {FP32_INSTR_PER_EVAL} executed FP32-pipe "
+                     f"instructions (SASS count) x 2 flop-equivalents (FMA-pipe slot at the FFMA peak)")
     for k in ("k_xlate", "k_m2l_lr"):
         fl = sum(v for n, v in kf.items() if n.startswith(k + "/"))
         fam[k] = ("alu", fl, "complex-equivalent flops, 8·rows·cols per op (16·r·T per factored M2L op)")
@@ -275,7 +284,8 @@ def run_config(cfg, args, ws, rank, local, primary):
         if sname == "near" and t > 0:
             ach = w["evals"] * FLOPS_PER_EVAL / (t * 1e-3) / 1e12
             e.update({"bound": "alu", "achieved": ach, "peak": fp32, "unit": "TFLOP/s", "frac": ach / fp32,
-                      "evals_per_s": w["evals"] / (t * 1e-3)})
+                      "evals_per_s": w["evals"] / (t * 1e-3),
+                      "frac_survey_unit": w["evals"] * FLOPS_PER_EVAL_SURVEY / (t * 1e-3) / 1e12 / fp32})
         elif sname in ("m2m", "m2l", "l2l") and t > 0 and w["flops"] > 0:
             ach = w["flops"] / (t * 1e-3) / 1e12
             e.update({"flops": w["flops"], "achieved_tflops": ach, "translation_gbs": w["bytes"] / (t * 1e-3) / 1e9,
@@ -318,6 +328,8 @@ def run_config(cfg, args, ws, rank, local, primary):
                 "peak_source": psrc["fp32"] if bound == "alu" else (psrc["hbm"] if bound == "hbm" else
                                                                   psrc["bf16x3" if bound == "tensor_bf16" else "tf32x3"]),
                 "fp32_measured_ubench_tflops": psrc["fp32_measured_ubench_tflops"]}
+        if dom == "k_near":
+            roof["frac_survey_unit"] = work["near"]["evals"] * FLOPS_PER_EVAL_SURVEY / (t_dom * 1e-3) / 1e12 / fp32
     launches = int(f.table("launches")[0])   # exact count of our kernels per matvec (engine.cu)
     out = {"cfg": cfg, "N": N, "ms": ms, "per_step_ms": [round(p, 4) for p in per[:5]], "build_s": build_s,
            "stages": stages, "kernels": kernels, "roofline": roof, "launches": launches, "clocks": ck,
