@@ -9,8 +9,18 @@
 #include <new>
 #include <stdexcept>
 #include <omp.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "fda_internal.h"
+
+namespace {
+// NVTX ranges around the public calls and the build phases (header-only NVTX v3: no-ops
+// unless a profiler such as Nsight Systems is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 using namespace fda;
 
@@ -77,6 +87,7 @@ const char* fda_last_error(const fda_ctx* ctx) {
 
 fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangles, int64_t nt, double k,
                      fda_cplx alpha, double eps, const fda_options* opt, fda_ctx** out) {
+  NvtxRange nvtx_range("fda_build");
   g_build_error.clear();
   if (!out || !vertices || !triangles) { g_build_error = "null pointer argument"; return FDA_E_INVALID_ARG; }
   *out = nullptr;
@@ -117,6 +128,7 @@ fda_status fda_build(const double* vertices, int64_t nv, const int32_t* triangle
     auto phase = [&](const char* name) {
       auto now = std::chrono::steady_clock::now();
       if (o.verbose) fprintf(stderr, "[fda_build] %-12s %8.3f s\n", name, std::chrono::duration<double>(now - tp).count());
+      nvtxMarkA(name);   // end of a build phase on the profiler timeline
       tp = now;
     };
     st = build_geometry(vertices, nv, triangles, nt, ctx->g, ctx->err);
@@ -271,6 +283,7 @@ fda_status fda_matvec(fda_ctx* ctx, const void* x, void* y, int32_t flags, void*
   if (!ctx) return FDA_E_INVALID_ARG;
   if (!x || !y || x == y) { ctx->err = "x and y must be non-null and must not alias"; return FDA_E_INVALID_ARG; }
   if (!ctx->dev) { ctx->err = "context was built host-only (opt.device = -1): no device matvec"; return FDA_E_STATE; }
+  NvtxRange nvtx_range("fda_matvec");
   return engine_apply(ctx, x, y, flags, stream, 0);
 }
 
@@ -313,6 +326,7 @@ fda_status fda_rhs_apply(fda_ctx* ctx, const void* v, void* b, int32_t flags, vo
   if (!v || !b || v == b) { ctx->err = "v and b must be non-null and must not alias"; return FDA_E_INVALID_ARG; }
   if (!ctx->dev) { ctx->err = "context was built host-only (opt.device = -1)"; return FDA_E_STATE; }
   if (!ctx->p.opt.rhs_operator) { ctx->err = "context was built without opt.rhs_operator"; return FDA_E_STATE; }
+  NvtxRange nvtx_range("fda_rhs_apply");
   return engine_apply(ctx, v, b, flags, stream, 1);
 }
 
@@ -322,6 +336,7 @@ fda_status bm_solve(fda_ctx* ctx, const void* rhs, void* u, double tol, int32_t 
   if (!rhs || !u || rhs == u) { ctx->err = "rhs and u must be non-null and must not alias"; return FDA_E_INVALID_ARG; }
   if (!(tol > 0) || max_iter < 1 || restart < 0) { ctx->err = "tol > 0, max_iter >= 1, restart >= 0"; return FDA_E_INVALID_ARG; }
   if (!ctx->dev) { ctx->err = "context was built host-only"; return FDA_E_STATE; }
+  NvtxRange nvtx_range("bm_solve");
   return engine_solve(ctx, rhs, u, tol, max_iter, restart, info, flags);
 }
 
