@@ -997,13 +997,49 @@ fda_status engine_create(Context* ctx) {
       Dev::M2LLevel& L = d->m2lv[l];
       {   // tensor-core tasks: ≤ 128 ops per factored K̃, op offsets appended to ls / ld
         auto& Ft = ftc[l];
-        __gnu_parallel::stable_sort(Ft.begin(), Ft.end(), [](const LrOp& x, const LrOp& y) {
-          return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
-        });
+        // Locality order on levels whose states exceed the L2 (config 5: 0.2-0.6 GB per level):
+        // ops sorted by (block of destination states, K̃, destination), so that the tasks running
+        // at any time touch one block of destination states and their sources instead of half
+        // the level (one K̃'s ops span every box of the level).  A block holds ≈ 4·128 ops per K̃
+        // on average; tasks keep this order (no longest-first sort).  A/B, config 5: k_m2l_bf
+        // 26.7 → 25.1 ms; on L2-resident levels (config 4) the LPT order is faster (1.18 vs 1.33).
+        bool blocked = false;
+        int64_t dmin = 0, bspan = 1;
+        if (!Ft.empty()) {
+          int64_t dmax = Ft[0].dst;
+          dmin = Ft[0].dst;
+          for (const LrOp& o : Ft) {
+            dmin = std::min(dmin, o.dst);
+            dmax = std::max(dmax, o.dst);
+          }
+          const int64_t lev_bytes = 8 * (p.in_offset[dmax] - p.in_offset[dmin] + p.mats[Ft[0].matV].cols);
+          if (lev_bytes > ((int64_t)64 << 20)) {
+            std::vector<int64_t> mv(Ft.size());
+            for (size_t q = 0; q < Ft.size(); ++q) mv[q] = Ft[q].matV;
+            __gnu_parallel::sort(mv.begin(), mv.end());
+            const double nm = (double)(std::unique(mv.begin(), mv.end()) - mv.begin());
+            if ((double)Ft.size() / nm >= 512) {
+              blocked = true;
+              bspan = std::max<int64_t>(1, (int64_t)(4.0 * 128.0 * (double)(dmax - dmin + 1) * nm / (double)Ft.size()));
+            }
+          }
+        }
+        if (blocked)
+          __gnu_parallel::stable_sort(Ft.begin(), Ft.end(), [dmin, bspan](const LrOp& x, const LrOp& y) {
+            const int64_t bx = (x.dst - dmin) / bspan, by = (y.dst - dmin) / bspan;
+            if (bx != by) return bx < by;
+            return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
+          });
+        else
+          __gnu_parallel::stable_sort(Ft.begin(), Ft.end(), [](const LrOp& x, const LrOp& y) {
+            return x.matV != y.matV ? x.matV < y.matV : x.dst < y.dst;
+          });
         std::vector<LrTcTask> tt;
         for (size_t i = 0; i < Ft.size();) {
           size_t j = i;
-          while (j < Ft.size() && Ft[j].matV == Ft[i].matV && j - i < 128) ++j;
+          while (j < Ft.size() && Ft[j].matV == Ft[i].matV && j - i < 128 &&
+                 (!blocked || (Ft[j].dst - dmin) / bspan == (Ft[i].dst - dmin) / bspan))
+            ++j;
           const int r = p.mats[Ft[i].matV].rows, T = p.mats[Ft[i].matV].cols;
           LrTcTask tk;
           tk.T = T;
@@ -1031,9 +1067,10 @@ fda_status engine_create(Context* ctx) {
         // one ring layout per launch; tasks longest first (the persistent CTAs stride over them)
         int n1m = 16;
         for (const LrTcTask& tk : tt) n1m = std::max(n1m, tk.n1);
-        std::stable_sort(tt.begin(), tt.end(), [](const LrTcTask& x, const LrTcTask& y) {
-          return (int64_t)(x.nk1 + x.n1 / TC_KC) * x.n2 > (int64_t)(y.nk1 + y.n1 / TC_KC) * y.n2;
-        });
+        if (!blocked)
+          std::stable_sort(tt.begin(), tt.end(), [](const LrTcTask& x, const LrTcTask& y) {
+            return (int64_t)(x.nk1 + x.n1 / TC_KC) * x.n2 > (int64_t)(y.nk1 + y.n1 / TC_KC) * y.n2;
+          });
         if (!tt.empty()) {
           int n2m = 16;
           for (const LrTcTask& tk : tt) n2m = std::max(n2m, tk.n2);
