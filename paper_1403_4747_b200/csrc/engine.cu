@@ -350,6 +350,8 @@ static fda_status build_xstage(Context* ctx, Dev* d, const std::vector<XOp>& ops
   // (N = 2R ≤ 256); stages with taller matrices keep the 3xTF32 / CUDA-core kernels
   bool use_bf = false;
   if (bf_ok && d->use_xbf && atomic) {
+    // every eligible stage (A/B at config 4: routing only stages with ≥ 64 / 256 / 1000 ops per
+    // matrix to k_xlate_bf, the rest to k_xlate / k_xlate_tc, is slower: 4.985-5.010 vs 4.920 ms)
     bool fits = true;
     for (const XOp& o : ops) fits &= p.mats[o.mat].rows <= 128;
     use_bf = fits;
