@@ -925,12 +925,13 @@ fda_status engine_create(Context* ctx) {
     // share the GPU with the near field inside the graph (config 2, largest level 1.6 GFLOP:
     // matvec 0.473 vs 0.471 ms at a 1.5 GFLOP threshold)
     std::vector<char> lr_f(nlev, 0);
+    const int lrtc_max_r = ctx->p.opt.m2l_bf16 != 0 ? LRBF_MAX_R : LRTC_MAX_R;
     if (d->use_tc && ctx->p.opt.lr_tensor_cores != 0) {
       std::vector<int64_t> nops(nlev, 0);
       std::vector<double> fl(nlev, 0.0);
       std::vector<std::unordered_map<int64_t, int>> nm(nlev);
       for (const LrOp& o : p.m2l_lr) {
-        if (p.mats[o.matV].rows > LRTC_MAX_R || p.mats[o.matV].cols > LRTC_MAX_T) continue;
+        if (p.mats[o.matV].rows > lrtc_max_r || p.mats[o.matV].cols > LRTC_MAX_T) continue;
         ++nops[o.level];
         fl[o.level] += 16.0 * p.mats[o.matV].rows * p.mats[o.matV].cols;
         nm[o.level][o.matV] = 1;
@@ -948,7 +949,7 @@ fda_status engine_create(Context* ctx) {
     std::vector<std::vector<LrOp>> ftc(nlev);
     int64_t tmp_off = 0;
     for (const LrOp& o : p.m2l_lr) {
-      if (lr_f[o.level] && p.mats[o.matV].rows <= LRTC_MAX_R && p.mats[o.matV].cols <= LRTC_MAX_T) {
+      if (lr_f[o.level] && p.mats[o.matV].rows <= lrtc_max_r && p.mats[o.matV].cols <= LRTC_MAX_T) {
         ftc[o.level].push_back(o);
         continue;
       }

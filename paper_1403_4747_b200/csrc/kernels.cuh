@@ -82,6 +82,7 @@ struct LrTcTask {
   int32_t op_begin, op_count;
 };
 constexpr int LRTC_MAX_R = 32;
+constexpr int LRBF_MAX_R = 48;    // BF16x3 form (k_m2l_bf): n1 ≤ 96, phase-2 A region ≤ 48 KB
 constexpr int LRTC_MAX_T = 160;   // keeps 3 ring stages + the phase-2 A region ≤ 220 KB (n1 ≤ 64, n2 ≤ 320)
 // warp-specialised persistent variant (k_m2l_tcw): launch plan from the level's max n1 / n2
 struct LrTcPlan {
