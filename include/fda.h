@@ -63,6 +63,10 @@ typedef struct { double re, im; } fda_cplx;
  * transport; fda_matvec without these flags does UP, NCCL, DOWN. */
 #define FDA_PHASE_UP   4
 #define FDA_PHASE_DOWN 8
+/* with FDA_HOST: the host x and y of fda_matvec / fda_rhs_apply are complex64 (float re,im)
+ * instead of complex128 — the device computes in fp32 anyway, so this halves the H2D / D2H
+ * bytes of a host-buffer call (pinned buffers recommended).  Not accepted by bm_solve. */
+#define FDA_HOST_C64   16
 
 typedef struct {
   int32_t max_leaf;      /* split an octree cube while it owns more elements (64)        */

@@ -1674,22 +1674,26 @@ fda_status engine_apply(Context* ctx, const void* x, void* y, int32_t flags, voi
   }
   if (flags & FDA_DEVICE)
     return matvec_dev(ctx, d, static_cast<const float2*>(x), static_cast<float2*>(y), s, kind, local, phase);
-  // host complex128 in/out
+  // host complex128 (or, with FDA_HOST_C64, complex64) in/out; the device buffers xh / yh hold
+  // n complex128, which also fit n complex64
+  const bool c64 = (flags & FDA_HOST_C64) != 0;
   const bool prof = ctx->profiling && (d->nranks <= 1 || phase == 0);
-  CK(cudaMemcpyAsync(d->xh, x, sizeof(double2) * d->n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d->xh, x, (c64 ? sizeof(float2) : sizeof(double2)) * d->n, cudaMemcpyHostToDevice, s));
   if (prof) CK(cudaEventRecord(d->ev[0], s));
-  launch_gather_f64(d->xh, d->perm, d->x_tree, d->n, s);
+  if (c64) launch_gather_f32(reinterpret_cast<const float2*>(d->xh), d->perm, d->x_tree, d->n, s);
+  else launch_gather_f64(d->xh, d->perm, d->x_tree, d->n, s);
   if (prof) CK(cudaEventRecord(d->ev[1], s));
   fda_status st = core(ctx, d, s, kind);
   if (st != FDA_OK) return st;
-  launch_scatter_f64(d->y_near, d->y_far, d->perm, d->yh, d->n, d->e0, d->e1, s);
+  if (c64) launch_scatter_f32(d->y_near, d->y_far, d->perm, reinterpret_cast<float2*>(d->yh), d->n, d->e0, d->e1, s);
+  else launch_scatter_f64(d->y_near, d->y_far, d->perm, d->yh, d->n, d->e0, d->e1, s);
   if (prof) CK(cudaEventRecord(d->ev[7], s));
   d->timed = prof;
   if (!local) {
-    fda_status r = reduce_y(ctx, d, d->yh, true, s);
+    fda_status r = reduce_y(ctx, d, d->yh, !c64, s);
     if (r != FDA_OK) return r;
   }
-  CK(cudaMemcpyAsync(y, d->yh, sizeof(double2) * d->n, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(y, d->yh, (c64 ? sizeof(float2) : sizeof(double2)) * d->n, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return FDA_OK;
 }

@@ -335,6 +335,7 @@ fda_status bm_solve(fda_ctx* ctx, const void* rhs, void* u, double tol, int32_t 
   if (!ctx) return FDA_E_INVALID_ARG;
   if (!rhs || !u || rhs == u) { ctx->err = "rhs and u must be non-null and must not alias"; return FDA_E_INVALID_ARG; }
   if (!(tol > 0) || max_iter < 1 || restart < 0) { ctx->err = "tol > 0, max_iter >= 1, restart >= 0"; return FDA_E_INVALID_ARG; }
+  if (flags & FDA_HOST_C64) { ctx->err = "bm_solve takes complex128 host vectors (FDA_HOST_C64 is for fda_matvec)"; return FDA_E_INVALID_ARG; }
   if (!ctx->dev) { ctx->err = "context was built host-only"; return FDA_E_STATE; }
   NvtxRange nvtx_range("bm_solve");
   return engine_solve(ctx, rhs, u, tol, max_iter, restart, info, flags);

@@ -24,6 +24,7 @@ FDA_DEVICE = 1
 FDA_LOCAL = 2
 FDA_PHASE_UP = 4
 FDA_PHASE_DOWN = 8
+FDA_HOST_C64 = 16
 
 STATUS = {0: "FDA_OK", 1: "FDA_E_INVALID_ARG", 2: "FDA_E_MESH", 3: "FDA_E_NOMEM", 4: "FDA_E_CUDA",
           5: "FDA_E_NCCL", 6: "FDA_E_NOT_CONVERGED", 7: "FDA_E_STATE", 8: "FDA_E_INTERNAL"}
@@ -228,13 +229,16 @@ class FDA:
 
     def _apply(self, fn, x, y=None, stream=None, extra: int = 0):
         if _is_torch(x) and not x.is_cuda:
-            # host tensors (e.g. pinned complex128): host path with raw pointers
+            # host tensors (e.g. pinned complex128, or complex64 → FDA_HOST_C64): host path with raw pointers
             import torch
-            if not (x.dtype == torch.complex128 and x.is_contiguous() and x.numel() == self.n):
-                raise ValueError("host x must be a contiguous complex128 tensor of length n")
+            if not (x.dtype in (torch.complex128, torch.complex64) and x.is_contiguous() and x.numel() == self.n):
+                raise ValueError("host x must be a contiguous complex128 or complex64 tensor of length n")
             if y is None:
                 y = torch.empty_like(x)
-            self._check(fn(self.ctx, x.data_ptr(), y.data_ptr(), FDA_HOST | extra, None))
+            if y.dtype != x.dtype:
+                raise ValueError("host y must have the dtype of x")
+            c64 = FDA_HOST_C64 if x.dtype == torch.complex64 else 0
+            self._check(fn(self.ctx, x.data_ptr(), y.data_ptr(), FDA_HOST | c64 | extra, None))
             return y
         if _is_torch(x):
             import torch

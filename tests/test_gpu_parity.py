@@ -65,6 +65,23 @@ def test_device_path_equals_host_path(cfg1):
     assert _rel(yd.cpu().numpy().astype(np.complex128), yh) < 1e-6
 
 
+def test_host_complex64_path(cfg1):
+    """fda_matvec with host complex64 buffers (FDA_HOST_C64, the bench's e2e path) equals the
+    device path (same kernels; the far field's float atomics sum in a run-to-run varying order,
+    hence a tolerance instead of bit equality) and the complex128 host path to the fp32
+    rounding of the input."""
+    import torch
+    V, F, c, el, A, f = cfg1
+    x = random_density(len(F), c.x_seed)
+    x32 = x.astype(np.complex64)
+    yd = f.matvec(torch.from_numpy(x32).cuda()).cpu().numpy()
+    yh = f.matvec(torch.from_numpy(x32).pin_memory()).numpy()
+    assert yh.dtype == np.complex64
+    assert _rel(yh.astype(np.complex128), yd.astype(np.complex128)) < 1e-6
+    y128 = f.matvec(x)
+    assert _rel(yh.astype(np.complex128), y128) < 1e-6
+
+
 def test_linearity_and_zero(cfg1):
     V, F, c, el, A, f = cfg1
     z = f.matvec(np.zeros(len(F), complex))
