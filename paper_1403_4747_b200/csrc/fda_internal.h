@@ -256,6 +256,8 @@ void svd_jacobi(int m, int n, std::vector<cd>& A /*col-major m×n, overwritten*/
 void zgemm_cm(int m, int n, int kk, const cd* A, int lda, const cd* B, int ldb, cd* C, int ldc,
               bool conjA_T = false);
 int lowrank_factor(int m, int n, const cd* A, double eps, std::vector<cd>& Uh, std::vector<cd>& Vh);
+int svd_range(int m, int n, const std::vector<cd>& A, double eps, std::vector<double>& S, std::vector<cd>& U,
+              std::vector<cd>& V);
 
 // engine.cu (device side)
 struct Context;

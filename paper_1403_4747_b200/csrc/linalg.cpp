@@ -210,3 +210,110 @@ int lowrank_factor(int m, int n, const cd* A, double eps, std::vector<cd>& Uh, s
 }
 
 }  // namespace fda
+
+namespace fda {
+
+// Truncated SVD of a check/equivalent-cloud kernel matrix (the level SVDs of P:679-705):
+// A (m×n, column-major) = U diag(S) V^H restricted to the T triplets with σ_i ≥ ε σ_0.
+// Same result as svd_jacobi + truncation up to the range finder's residual (≤ 1e-3 ε σ_0 in
+// each singular value): a pivoted, twice-orthogonalised Gram–Schmidt range finder (OpenMP over
+// the residual columns) stops once the largest residual column norm × √(remaining columns)
+// < 1e-3 ε ‖A col‖_max; then R = Q^H A (k × n, k ≈ 1.3 T ≪ n) and the one-sided Jacobi SVD of
+// R^H = W S Z^H give U = Q Z, V = W.  ~10× less work than Jacobi on the whole m×n matrix
+// (whose rank at ε is ≈ T ≪ n).  Returns T.
+int svd_range(int m, int n, const std::vector<cd>& A, double eps, std::vector<double>& S, std::vector<cd>& U,
+              std::vector<cd>& V) {
+  std::vector<cd> W(A);   // residual columns
+  std::vector<double> nrm(n);
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < n; ++j) {
+    double s = 0;
+    for (int i = 0; i < m; ++i) s += std::norm(W[(size_t)j * m + i]);
+    nrm[j] = s;
+  }
+  double cmax = 0;
+  for (int j = 0; j < n; ++j) cmax = std::max(cmax, nrm[j]);
+  S.clear(); U.clear(); V.clear();
+  if (cmax == 0) return 0;
+  const double c0 = std::sqrt(cmax), tol = 1e-3 * eps * c0;
+  std::vector<cd> Q;   // m × k
+  std::vector<char> used(n, 0);
+  int k = 0;
+  const int kmax = std::min(m, n);
+  std::vector<cd> q(m), hc;
+  while (k < kmax) {
+    int jp = -1;
+    double best = -1;
+    for (int j = 0; j < n; ++j)
+      if (!used[j] && nrm[j] > best) { best = nrm[j]; jp = j; }
+    if (jp < 0 || std::sqrt(std::max(best, 0.0)) * std::sqrt((double)(n - k)) < tol) break;
+    used[jp] = 1;
+    std::copy(W.begin() + (size_t)jp * m, W.begin() + (size_t)(jp + 1) * m, q.begin());
+    for (int pass = 0; pass < 2; ++pass) {   // reorthogonalise against Q (classical GS, twice)
+      hc.assign(k, 0.0);
+#pragma omp parallel for schedule(static)
+      for (int c = 0; c < k; ++c) {
+        const cd* qc = Q.data() + (size_t)c * m;
+        cd h = 0;
+        for (int i = 0; i < m; ++i) h += std::conj(qc[i]) * q[i];
+        hc[c] = h;
+      }
+      for (int c = 0; c < k; ++c) {
+        const cd* qc = Q.data() + (size_t)c * m;
+        for (int i = 0; i < m; ++i) q[i] -= hc[c] * qc[i];
+      }
+    }
+    double qn = 0;
+    for (int i = 0; i < m; ++i) qn += std::norm(q[i]);
+    qn = std::sqrt(qn);
+    if (qn == 0) continue;
+    for (int i = 0; i < m; ++i) q[i] /= qn;
+    Q.insert(Q.end(), q.begin(), q.end());
+    ++k;
+    // remove q from the remaining residual columns
+#pragma omp parallel for schedule(static)
+    for (int j = 0; j < n; ++j) {
+      if (used[j]) { nrm[j] = 0; continue; }
+      cd* w = W.data() + (size_t)j * m;
+      cd h = 0;
+      for (int i = 0; i < m; ++i) h += std::conj(q[i]) * w[i];
+      double s = 0;
+      for (int i = 0; i < m; ++i) {
+        w[i] -= h * q[i];
+        s += std::norm(w[i]);
+      }
+      nrm[j] = s;
+    }
+  }
+  // R^H (n × k): column c = conj(row c of Q^H A)
+  std::vector<cd> RH((size_t)n * k);
+#pragma omp parallel for schedule(static)
+  for (int cj = 0; cj < k * n; ++cj) {
+    const int c = cj / n, j = cj % n;
+    const cd* qc = Q.data() + (size_t)c * m;
+    const cd* a = A.data() + (size_t)j * m;
+    cd h = 0;
+    for (int i = 0; i < m; ++i) h += std::conj(qc[i]) * a[i];
+    RH[(size_t)c * n + j] = std::conj(h);
+  }
+  std::vector<double> Sk;
+  std::vector<cd> Z;   // k × k
+  svd_jacobi(n, k, RH, Sk, Z);   // R^H = W Sk Z^H (RH now W, n × k)  →  A ≈ Q R = (Q Z) Sk W^H
+  int T = 0;
+  while (T < k && Sk[T] >= eps * Sk[0]) ++T;
+  S.assign(Sk.begin(), Sk.begin() + T);
+  U.assign((size_t)m * T, 0.0);
+#pragma omp parallel for schedule(static)
+  for (int c = 0; c < T; ++c) {
+    cd* u = U.data() + (size_t)c * m;
+    for (int a = 0; a < k; ++a) {
+      const cd z = Z[(size_t)c * k + a];
+      const cd* qa = Q.data() + (size_t)a * m;
+      for (int i = 0; i < m; ++i) u[i] += qa[i] * z;
+    }
+  }
+  V.assign(RH.begin(), RH.begin() + (size_t)n * T);
+  return T;
+}
+
+}  // namespace fda

@@ -65,15 +65,7 @@ void build_clouds_and_svd(const Params& p, Tree& t, const std::vector<bool>& nee
     std::vector<cd> A((size_t)m * n);
     for (int j = 0; j < n; ++j)
       for (int i = 0; i < m; ++i) A[(size_t)j * m + i] = G(L.chk[i], L.eq[j], p.k);
-    std::vector<double> S;
-    std::vector<cd> V;
-    svd_jacobi(m, n, A, S, V);
-    int T = 0;
-    while (T < n && S[T] >= p.eps * S[0]) ++T;
-    L.rank = T;
-    L.S.assign(S.begin(), S.begin() + T);
-    L.U.assign(A.begin(), A.begin() + (size_t)T * m);
-    L.V.assign(V.begin(), V.begin() + (size_t)T * n);
+    L.rank = svd_range(m, n, A, p.eps, L.S, L.U, L.V);   // σ_i ≥ ε σ_0
   }
 }
 
