@@ -220,3 +220,31 @@ def test_m2l_routing_dense_on_low_sharing_levels():
     for l in lr_levels:
         o = lr[lr[:, 0] == l]
         assert len(o) >= 16 * len(set(o[:, 3].tolist()))
+
+
+def test_correction_pairs_brute_force_graded():
+    """The correction pair list (every pair with ρ_ij = |x_i − c_j|/h_j < 3, reading C6; the
+    size-class hash grids of corrections.cpp) equals the brute-force O(N²) search on a graded
+    spheroid whose element size varies 8× (the case the per-class grids exist for), including
+    the tier of each pair (self / ρ < 1.5 / ρ < 3)."""
+    from fda_inputs.meshes import graded_spheroid
+    V, F = graded_spheroid(h_eq=0.03)
+    n = len(F)
+    assert 3000 < n < 30000
+    f = FDA(V, F, 20.0, -1j / 20.0, 1e-3, device=-1)
+    perm = f.table("perm")                              # tree position → caller index
+    ptr, col = f.table("corr_ptr"), f.table("corr_col")
+    P = V[F]
+    cen = P.mean(axis=1)
+    h = np.max(np.linalg.norm(P - np.roll(P, 1, axis=1), axis=2), axis=1)
+    assert h.max() / h.min() > 4.0                      # several size classes
+    got = {}
+    for ti in range(n):
+        i = perm[ti]
+        got[i] = np.sort(perm[col[ptr[ti]:ptr[ti + 1]]])
+    for i0 in range(0, n, 512):
+        rows = np.arange(i0, min(n, i0 + 512))
+        rho = np.linalg.norm(cen[rows, None, :] - cen[None, :, :], axis=2) / h[None, :]
+        for a, i in enumerate(rows):
+            want = np.nonzero(rho[a] < 3.0)[0]
+            assert np.array_equal(got[i], want), i
