@@ -225,8 +225,7 @@ def test_m2l_routing_dense_on_low_sharing_levels():
 def test_correction_pairs_brute_force_graded():
     """The correction pair list (every pair with ρ_ij = |x_i − c_j|/h_j < 3, reading C6; the
     size-class hash grids of corrections.cpp) equals the brute-force O(N²) search on a graded
-    spheroid whose element size varies 8× (the case the per-class grids exist for), including
-    the tier of each pair (self / ρ < 1.5 / ρ < 3)."""
+    spheroid whose element size varies 8× (the case the per-class grids exist for)."""
     from fda_inputs.meshes import graded_spheroid
     V, F = graded_spheroid(h_eq=0.03)
     n = len(F)
