@@ -658,6 +658,7 @@ fda_status engine_create(Context* ctx) {
   d->kp.ak_re = (float)(ctx->p.k * ctx->p.alpha.real());
   d->kp.ak_im = (float)(ctx->p.k * ctx->p.alpha.imag());
   d->kp.inv_k = (float)(1.0 / ctx->p.k);
+  d->kp.skip_corr = getenv("FDA_NEAR_NOCORR") && atoi(getenv("FDA_NEAR_NOCORR")) != 0;
   d->use_tc = ctx->p.opt.tensor_cores != 0;
   // opt.tensor_cores = 5: dense translations on the BF16x3 persistent kernel (unsharded contexts)
   // k_xlate_bf for the dense translations: opt.tensor_cores = 5 always; auto mode (2) on problems

@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(NEAR_NT) k_near(
   unpack2(ar, acc.x, acc.z);
   unpack2(ai, acc.y, acc.w);
   // correction SpMV, rows split over the P parts
-  if (active) {
+  if (active && !kp.skip_corr) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       if (j0 + h >= nt) break;

@@ -26,6 +26,7 @@ struct KernelParams {
   float ak_re;      // k·Re α (near kernel in wave units)
   float ak_im;      // k·Im α
   float inv_k;      // 1/k
+  int skip_corr;    // FDA_NEAR_NOCORR=1 (measurement only): the near kernel skips the correction SpMV
 };
 
 // one CTA of the grouped translation kernel: a tile of XR rows × ≤ XO ops of
