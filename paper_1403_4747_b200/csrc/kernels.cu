@@ -364,26 +364,38 @@ constexpr int LEAF_MAXR = 320;
 __device__ __forceinline__ float2 leaf_colsum(const float2* __restrict__ M, int64_t ld, int row, int c0, int cstep,
                                               int ncol, const float2* __restrict__ v) {
   float2 acc = make_float2(0.f, 0.f);
-  for (int c = c0; c < ncol; c += LEAF_U * cstep) {
+  // pointer increments instead of per-load index products (ncu round 4: the ALU pipe was at 44%)
+  const float2* p = M + (int64_t)c0 * ld + row;
+  const float2* x = v + c0;
+  const int64_t step = (int64_t)cstep * ld;
+  int c = c0;
+  for (; c + (LEAF_U - 1) * cstep < ncol; c += LEAF_U * cstep, p += LEAF_U * step, x += LEAF_U * cstep) {
     float2 m[LEAF_U];
 #pragma unroll
-    for (int u = 0; u < LEAF_U; ++u) {
-      const int cc = c + u * cstep;
-      m[u] = cc < ncol ? __ldg(M + (int64_t)cc * ld + row) : make_float2(0.f, 0.f);
-    }
+    for (int u = 0; u < LEAF_U; ++u) m[u] = __ldg(p + u * step);
 #pragma unroll
     for (int u = 0; u < LEAF_U; ++u) {
-      const int cc = min(c + u * cstep, ncol - 1);
-      const float2 x = v[cc];
-      acc.x = fmaf(m[u].x, x.x, fmaf(-m[u].y, x.y, acc.x));
-      acc.y = fmaf(m[u].x, x.y, fmaf(m[u].y, x.x, acc.y));
+      const float2 xv = x[u * cstep];
+      acc.x = fmaf(m[u].x, xv.x, fmaf(-m[u].y, xv.y, acc.x));
+      acc.y = fmaf(m[u].x, xv.y, fmaf(m[u].y, xv.x, acc.y));
+    }
+  }
+  if (c < ncol) {   // last, partial batch
+    float2 m[LEAF_U];
+#pragma unroll
+    for (int u = 0; u < LEAF_U; ++u) m[u] = c + u * cstep < ncol ? __ldg(p + u * step) : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < LEAF_U; ++u) {
+      const float2 xv = x[c + u * cstep < ncol ? u * cstep : 0];
+      acc.x = fmaf(m[u].x, xv.x, fmaf(-m[u].y, xv.y, acc.x));
+      acc.y = fmaf(m[u].x, xv.y, fmaf(m[u].y, xv.x, acc.y));
     }
   }
   return acc;
 }
 
 // S2M: m̃_B = S̃_B x_B (T × n_B, column-major)   (Eq. 10; compressed S̃)
-__global__ void __launch_bounds__(LEAF_MAXR) k_s2m(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
+__global__ void __launch_bounds__(LEAF_MAXR, 6) k_s2m(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
                                                    const float2* __restrict__ x, float2* __restrict__ out) {
   __shared__ float2 sx[128];
   __shared__ float2 red[LEAF_MAXR];
@@ -414,7 +426,7 @@ __global__ void __launch_bounds__(LEAF_MAXR) k_s2m(const LeafTask* __restrict__ 
 // L2T: y_B = T̃_B ℓ̃_B (n_B × T column-major)   (Eq. 12; compressed T̃)
 // ADD: accumulate (HF leaves have one task per incoming wedge); else overwrite.
 template <bool ADD>
-__global__ void __launch_bounds__(LEAF_NT) k_l2t(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
+__global__ void __launch_bounds__(LEAF_NT, 16) k_l2t(const LeafTask* __restrict__ tasks, const float2* __restrict__ pool,
                                                  const float2* __restrict__ in, float2* __restrict__ y) {
   __shared__ float2 sl[LEAF_MAXR];
   __shared__ float2 red[LEAF_NT];
